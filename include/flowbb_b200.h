@@ -1,0 +1,175 @@
+/*
+ * flowbb_b200.h -- C-ABI of the B200-native parallel-bounding hot path.
+ *
+ * This is the drop-in boundary for the reference flowbb (arXiv 1206.4973
+ * reference implementation, proj/include/flowbb/).  Plain pointers and sizes
+ * only; no C++ or torch types cross it.  The C++ wrapper that makes it a
+ * reference `Backend` (duck-typed concept used by evaluate_multi<Backend>,
+ * backend.hpp:105-138) is include/flowbb_b200/gpu_backend.hpp; the cgo / JNI /
+ * ctypes bindings a maintainer would add are in INTEGRATION.md.
+ *
+ * Node batches are structure-of-arrays, position-aligned, caller-owned:
+ *   masks   count x W uint64   (W = (n+63)/64), bit j set <=> job j scheduled
+ *                              (replaces Node::scheduled, node.hpp:12-24,31)
+ *   heads   count x m int32    per-machine completion times of the prefix
+ *                              (Node::heads, node.hpp:32; instance.hpp:76-89)
+ *   depth   count int32        prefix length (Node::depth(), node.hpp:35)
+ *   prefix  count x n uint8    scheduled jobs in order (Node::prefix,
+ *                              node.hpp:30); only the first depth[i] bytes are
+ *                              read; required only by the explorer entry points
+ *
+ * Errors: every entry point returns FBB_OK (0) or a negative status; the
+ * message and the failing device are available from fbb_last_error.  This is
+ * the C form of BackendError{backend} (backend.hpp:19-25): the C++ wrapper
+ * rethrows it as flowbb::BackendError(device, message).  There is no CPU
+ * fallback: without a usable sm_100 device fbb_create fails.
+ *
+ * Threading: one context per device; calls on different contexts may run
+ * concurrently from different host threads (the reference calls
+ * CpuBackend::evaluate concurrently on disjoint slices, backend.hpp:116-122).
+ * Calls on one context are serialised by the caller, as the reference's
+ * control thread does (search.hpp:124-174).
+ */
+#ifndef FLOWBB_B200_H
+#define FLOWBB_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FBB_OK 0
+#define FBB_E_ARG -1      /* invalid argument (std::invalid_argument in the reference) */
+#define FBB_E_CUDA -2     /* CUDA runtime / launch failure on the context's device */
+#define FBB_E_RANGE -3    /* instance outside the packed device-table range */
+#define FBB_E_NOMEM -4    /* device or pinned allocation failed */
+#define FBB_E_STATE -5    /* call not valid in the context's current state */
+
+typedef struct fbb_ctx fbb_ctx;
+
+/* Capacity description; mirrors BackendDescriptor (backend.hpp:27-33).
+ * grain      = children per K2 tile (the batch-size multiple),
+ * base_units = SMs x resident tiles per SM (cudaOccupancy...),
+ * max_batch  = largest admissible pool (bounded by HBM, not by threads). */
+typedef struct {
+    int32_t grain;
+    int32_t base_units;
+    int64_t max_batch;
+} fbb_descriptor_t;
+
+/* Per-round counters of the explorer entry points (search.hpp:21-26,75-79). */
+typedef struct {
+    int64_t target;    /* pool target given to the selection (fill_buffer) */
+    int64_t branched;  /* parents expanded */
+    int64_t bounded;   /* children bounded (= pool size) */
+    int64_t inserted;  /* internal children pushed to pending */
+    int64_t pruned;    /* internal children eliminated (lb >= incumbent) */
+    int64_t leaves;    /* complete children */
+    int32_t incumbent; /* incumbent after the round (frozen: best leaf < UB, else UB) */
+    int32_t pad;
+    int64_t pending;   /* pending nodes after the round */
+} fbb_round_t;
+
+/* ---- context ----------------------------------------------------------------------------
+ * Replaces Instance(n, m, times) (instance.hpp:30-46) + CpuBackend(descriptor)
+ * (backend.hpp:50-59): uploads p (job-major, n x m int32, p[j*m+k]) and builds
+ * the device tables (tails, per-machine-pair Johnson orders).  Returns NULL on
+ * failure; fbb_last_error(NULL, ...) then reports why. */
+fbb_ctx* fbb_create(int device, const int32_t* p_jobmajor, int n, int m);
+void fbb_destroy(fbb_ctx* ctx);
+
+/* Last error of ctx (or of the last failed fbb_create when ctx is NULL).
+ * Copies up to cap-1 bytes of the message; returns the status code. */
+int fbb_last_error(const fbb_ctx* ctx, int* device, char* msg, size_t cap);
+
+/* BackendDescriptor of this device (backend.hpp:29-33, 61). */
+int fbb_descriptor(fbb_ctx* ctx, fbb_descriptor_t* out);
+
+/* ---- K1: bound-only (drop-in for CpuBackend::evaluate, backend.hpp:63-65,
+ * i.e. evaluate_batch, bound.hpp:104-109).  Host buffers; lb_out[i] is
+ * lower_bound(inst, node_i) (bound.hpp:94-101), position-aligned. */
+int fbb_bound(fbb_ctx* ctx, const uint64_t* masks, const int32_t* heads, const int32_t* depth,
+              int64_t count, int32_t* lb_out);
+
+/* Same, device pointers, on `stream` (cudaStream_t, NULL = the context's own
+ * stream); asynchronous. */
+int fbb_bound_device(fbb_ctx* ctx, const uint64_t* d_masks, const int32_t* d_heads,
+                     const int32_t* d_depth, int64_t count, int32_t* d_lb_out, void* stream);
+
+/* ---- K2: fused expand + bound + prune + compact of one pool.
+ * Replaces, for the given parents (in pop order), branch (search.hpp:40-59)
+ * + evaluate + integrate (search.hpp:84-107) / the frozen prune
+ * (bench.hpp:96-106):
+ *   children of each parent in ascending job order, depth-(n-1) children
+ *   auto-completed; every child bounded; leaves reduce to (value, first
+ *   position) of the batch minimum; internal children survive iff
+ *   lb < min(ub, batch leaf minimum) (solve, frozen == 0) or lb < ub
+ *   (frozen != 0).  Survivors are returned stably compacted (batch order) in
+ *   the same SoA layout (capacity: sum of children).  Host buffers.
+ * leaf_best / leaf_pos: minimum leaf value < ub (INT32_MAX if none) and the
+ * batch position of its first occurrence; when leaf_schedule != NULL and a
+ * leaf improved, it receives the leaf's full permutation (n int32). */
+int fbb_expand_bound_prune(fbb_ctx* ctx, const uint64_t* masks, const int32_t* heads,
+                           const int32_t* depth, const uint8_t* prefix, int64_t nparents,
+                           int32_t ub, int frozen, uint64_t* out_masks, int32_t* out_heads,
+                           int32_t* out_depth, uint8_t* out_prefix, int32_t* out_lb,
+                           int64_t* out_count, int32_t* leaf_best, int64_t* leaf_pos,
+                           int32_t* leaf_schedule, fbb_round_t* counts);
+
+/* ---- device-resident explorer (pending tree in HBM) -------------------
+ * The pending tree (pending.hpp:13-56: per-depth buckets, deepest first, LIFO)
+ * lives in device memory; every round is selection (fill_buffer,
+ * search.hpp:64-73) + K2 + in-order push, with no host traffic but a few
+ * counters.  Semantics are those of resolve_workload (bench.hpp:63-114, frozen
+ * incumbent) or solve (search.hpp:124-174). */
+
+/* Reset the pending tree to the given nodes (pushed in order, like
+ * bench.hpp:84) with incumbent `ub` (frozen or not). */
+int fbb_explorer_reset(fbb_ctx* ctx, const uint8_t* prefix, const int32_t* depth, int64_t count,
+                       int32_t ub, int frozen);
+
+/* solve()'s first round (search.hpp:150-153): bound the root, integrate it.
+ * Initial UB: ub >= 0, or the identity-permutation makespan when ub < 0
+ * (search.hpp:131-137). */
+int fbb_explorer_start_solve(fbb_ctx* ctx, int32_t ub, fbb_round_t* round0);
+
+/* Runs up to max_rounds rounds with pool target targets[r] (the last value
+ * repeats), stopping early when pending is empty or when the cumulative
+ * bounded count reaches `budget` (> 0).  Fills rounds[0..*done). */
+int fbb_explorer_run(fbb_ctx* ctx, const int64_t* targets, int ntargets, int64_t max_rounds,
+                     int64_t budget, fbb_round_t* rounds, int64_t* done);
+
+/* Incumbent value, schedule (n int32) when found, pending size, totals
+ * (branched, bounded, pruned, leaves). */
+int fbb_explorer_state(fbb_ctx* ctx, int32_t* incumbent, int32_t* found, int32_t* schedule,
+                       int64_t* pending, int64_t* totals4);
+
+/* Host-side copy of the pending tree, shallowest bucket first, insertion
+ * order within a bucket (PendingTree::drain order, pending.hpp:41-50),
+ * without modifying it.  prefix: cap x n bytes; returns the count in *count
+ * (FBB_E_ARG with *count = size if cap is too small). */
+int fbb_explorer_pending(fbb_ctx* ctx, uint8_t* prefix, int32_t* depth, int64_t cap,
+                         int64_t* count);
+
+/* ---- adaptive pool-size tuner (autotune.hpp:35-156), re-derived descriptor ----------- */
+typedef struct fbb_tuner fbb_tuner;
+fbb_tuner* fbb_tuner_create(int32_t grain, int32_t base_units, int64_t max_batch, int window,
+                            int probes_per_side);
+void fbb_tuner_destroy(fbb_tuner* t);
+int64_t fbb_tuner_target(const fbb_tuner* t);
+/* returns FBB_E_ARG on non-positive elapsed (std::invalid_argument) */
+int fbb_tuner_observe(fbb_tuner* t, int64_t nodes_bounded, double elapsed_seconds);
+int fbb_tuner_phase(const fbb_tuner* t); /* 0 doubling, 1 refining, 2 fixed */
+int64_t fbb_tuner_best_batch(const fbb_tuner* t);
+double fbb_tuner_best_throughput(const fbb_tuner* t);
+
+/* Library build identification (sm arch, git-less version string). */
+const char* fbb_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

@@ -1,0 +1,794 @@
+// capi.cu -- the C-ABI (include/flowbb_b200.h): contexts, K1/K2 host-buffer
+// entry points and the device-resident explorer.
+//
+// The explorer keeps the reference's PendingTree (pending.hpp:13-56) in HBM:
+// one stack per depth (SoA: masks, heads, prefixes).  A round is
+//   selection  fill_buffer (search.hpp:64-73): pop the deepest bucket top,
+//              LIFO, until the children count reaches the target -- computed
+//              on the host from the bucket sizes alone (O(n)), no node moves;
+//   K2         expand + bound + prune straight from the bucket tops;
+//   push       survivors appended, in batch order, to bucket depth+1
+//              (integrate, search.hpp:84-107 / bench.hpp:96-106).
+// Only the per-segment survivor counts and the leaf minimum come back.
+#include <algorithm>
+#include <climits>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "fbb_internal.h"
+
+using namespace fbb;
+
+namespace {
+
+struct DBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    cudaError_t ensure(size_t want) {
+        if (want <= bytes) return cudaSuccess;
+        size_t nb = std::max(want, bytes * 2);
+        void* q = nullptr;
+        cudaError_t e = cudaMalloc(&q, nb);
+        if (e != cudaSuccess) return e;
+        cudaFree(p);
+        p = q;
+        bytes = nb;
+        return cudaSuccess;
+    }
+    void release() {
+        cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    template <class T>
+    T* as() const { return static_cast<T*>(p); }
+};
+
+struct HBuf {  // pinned host
+    void* p = nullptr;
+    size_t bytes = 0;
+    cudaError_t ensure(size_t want) {
+        if (want <= bytes) return cudaSuccess;
+        size_t nb = std::max(want, bytes * 2);
+        void* q = nullptr;
+        cudaError_t e = cudaMallocHost(&q, nb);
+        if (e != cudaSuccess) return e;
+        cudaFreeHost(p);
+        p = q;
+        bytes = nb;
+        return cudaSuccess;
+    }
+    void release() {
+        cudaFreeHost(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    template <class T>
+    T* as() const { return static_cast<T*>(p); }
+};
+
+// A growable node store (one pending bucket, or a scratch batch).
+struct Store {
+    DBuf masks, heads, prefix;
+    int64_t cap = 0;
+    NodeStore view() const { return NodeStore{masks.as<uint64_t>(), heads.as<int32_t>(), prefix.as<uint8_t>()}; }
+};
+
+struct RoundSummary {
+    unsigned long long leaf_key;
+    int32_t found;
+    int32_t pad;
+    int64_t total;
+    int64_t seg_surv[kMaxSegments];
+    int32_t schedule[kMaxJobs];
+};
+
+__global__ void summary_kernel(const Pool* __restrict__ pool, const int64_t* __restrict__ offsets,
+                               RoundSummary* out) {
+    for (int s = threadIdx.x; s < pool->nseg; s += blockDim.x) {
+        int64_t cb = pool->seg[s].chunk_base;
+        int64_t ce = (s + 1 < pool->nseg) ? pool->seg[s + 1].chunk_base : pool->nchunks;
+        out->seg_surv[s] = (ce > cb) ? offsets[ce] - offsets[cb] : 0;
+    }
+    if (threadIdx.x == 0) out->total = offsets[pool->nchunks];
+}
+
+}  // namespace
+
+static std::mutex g_err_mu;
+static std::string g_create_err = "";
+static int g_create_status = FBB_OK;
+
+struct fbb_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    HostTables ht;
+    DevTables dt{};
+    K1Config k1;
+    K2Config k2;
+    int status = FBB_OK;
+    std::string msg;
+
+    // scratch for the host-buffer entry points
+    DBuf k1_masks, k1_heads, k1_depth, k1_lb;
+    Store batch_in, batch_out;
+    DBuf out_lb;
+    // shared per-round device state
+    DBuf staging_masks, staging_heads, staging_prefix, staging_lb, chunk_count, offsets;
+    DBuf d_pool, d_leaf_key, d_summary;
+    HBuf h_pool, h_summary;
+
+    // explorer
+    std::vector<Store> bucket;
+    std::vector<int64_t> cnt;
+    int32_t incumbent = 0;  // pruning bound (frozen: the snapshot UB)
+    int32_t best = 0;       // best leaf value found (== incumbent when not frozen)
+    int frozen = 1;
+    int found = 0;
+    std::vector<int32_t> schedule;
+    int64_t tot_branched = 0, tot_bounded = 0, tot_pruned = 0, tot_leaves = 0;
+    bool explorer_ready = false;
+
+    int fail(int code, const std::string& m) {
+        status = code;
+        msg = m;
+        return code;
+    }
+    int cuda_fail(cudaError_t e, const char* where) {
+        return fail(FBB_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+    }
+};
+
+#define CK(expr, where)                                 \
+    do {                                                \
+        cudaError_t e_ = (expr);                        \
+        if (e_ != cudaSuccess) return ctx->cuda_fail(e_, where); \
+    } while (0)
+
+namespace {
+
+size_t node_bytes(const fbb_ctx* ctx) {
+    return (size_t)ctx->dt.W * 8 + (size_t)ctx->dt.m * 4 + (size_t)ctx->dt.n;
+}
+
+cudaError_t store_ensure(fbb_ctx* ctx, Store& s, int64_t want, int64_t keep) {
+    if (want <= s.cap) return cudaSuccess;
+    int64_t nc = std::max<int64_t>(want, std::max<int64_t>(s.cap * 2, 1024));
+    const int n = ctx->dt.n, m = ctx->dt.m, W = ctx->dt.W;
+    Store t;
+    cudaError_t e;
+    if ((e = t.masks.ensure((size_t)nc * W * 8)) != cudaSuccess) return e;
+    if ((e = t.heads.ensure((size_t)nc * m * 4)) != cudaSuccess) return e;
+    if ((e = t.prefix.ensure((size_t)nc * n)) != cudaSuccess) return e;
+    if (keep > 0) {
+        cudaMemcpyAsync(t.masks.p, s.masks.p, (size_t)keep * W * 8, cudaMemcpyDeviceToDevice, ctx->stream);
+        cudaMemcpyAsync(t.heads.p, s.heads.p, (size_t)keep * m * 4, cudaMemcpyDeviceToDevice, ctx->stream);
+        cudaMemcpyAsync(t.prefix.p, s.prefix.p, (size_t)keep * n, cudaMemcpyDeviceToDevice, ctx->stream);
+        e = cudaStreamSynchronize(ctx->stream);
+        if (e != cudaSuccess) return e;
+    }
+    s.masks.release();
+    s.heads.release();
+    s.prefix.release();
+    s = t;
+    s.cap = nc;
+    t.masks.p = t.heads.p = t.prefix.p = nullptr;  // ownership moved
+    return cudaSuccess;
+}
+
+// Builds a pool over `segs` (depth-descending runs) and lays out chunks.
+// Returns the index of the first internal segment.
+int layout_pool(const fbb_ctx* ctx, Pool& pool) {
+    const int n = ctx->dt.n, cmax = ctx->k2.cmax;
+    int64_t child = 0, chunk = 0;
+    int first_internal = pool.nseg;
+    for (int s = 0; s < pool.nseg; ++s) {
+        Segment& sg = pool.seg[s];
+        int r = n - sg.depth;
+        sg.child_base = child;
+        child += sg.count * r;
+        sg.chunk_base = chunk;
+        if (sg.depth >= n - 2) continue;  // leaves: no chunks
+        if (first_internal == pool.nseg) first_internal = s;
+        int ppc = cmax / r;
+        chunk += (sg.count + ppc - 1) / ppc;
+    }
+    pool.nchunks = chunk;
+    pool.nchildren = child;
+    return first_internal;
+}
+
+// Launches one pool: leaves, internal K2, leaf schedule, scan, append,
+// summary.  Synchronises and leaves the summary in ctx->h_summary.
+int run_pool(fbb_ctx* ctx, Pool& pool, int first_internal, int32_t ub, int frozen) {
+    const int n = ctx->dt.n, m = ctx->dt.m, W = ctx->dt.W;
+    cudaStream_t st = ctx->stream;
+    const int64_t slots = std::max<int64_t>(pool.nchunks * ctx->k2.cmax, 1);
+    CK(ctx->staging_masks.ensure((size_t)slots * W * 8), "staging");
+    CK(ctx->staging_heads.ensure((size_t)slots * m * 4), "staging");
+    CK(ctx->staging_prefix.ensure((size_t)slots * n), "staging");
+    CK(ctx->staging_lb.ensure((size_t)slots * 4), "staging");
+    CK(ctx->chunk_count.ensure((size_t)std::max<int64_t>(pool.nchunks, 1) * 4), "chunk counts");
+    CK(ctx->offsets.ensure((size_t)(pool.nchunks + 1) * 8), "offsets");
+    CK(ctx->d_pool.ensure(sizeof(Pool)), "pool");
+    CK(ctx->h_pool.ensure(sizeof(Pool)), "pool");
+    CK(ctx->d_leaf_key.ensure(8), "leaf key");
+    CK(ctx->d_summary.ensure(sizeof(RoundSummary)), "summary");
+    CK(ctx->h_summary.ensure(sizeof(RoundSummary)), "summary");
+
+    size_t pool_bytes = offsetof(Pool, seg) + (size_t)pool.nseg * sizeof(Segment);
+    std::memcpy(ctx->h_pool.p, &pool, pool_bytes);
+    CK(cudaMemcpyAsync(ctx->d_pool.p, ctx->h_pool.p, pool_bytes, cudaMemcpyHostToDevice, st), "pool H2D");
+    CK(cudaMemsetAsync(ctx->d_leaf_key.p, 0xFF, 8, st), "leaf key");
+    const Pool* dp = ctx->d_pool.as<Pool>();
+    unsigned long long* lk = ctx->d_leaf_key.as<unsigned long long>();
+    RoundSummary* ds = ctx->d_summary.as<RoundSummary>();
+    Staging stg{NodeStore{ctx->staging_masks.as<uint64_t>(), ctx->staging_heads.as<int32_t>(),
+                          ctx->staging_prefix.as<uint8_t>()},
+                ctx->staging_lb.as<int32_t>(), ctx->chunk_count.as<int32_t>()};
+    bool has_leaf = pool.nseg > 0 && pool.seg[0].depth >= n - 2;
+    if (has_leaf) CK(launch_k2_leaves(ctx->dt, ctx->k2, dp, pool, 0, lk, st), "K2 leaves");
+    CK(launch_k2_internal(ctx->dt, ctx->k2, dp, pool, first_internal, ub, frozen, lk, stg, st),
+       "K2 internal");
+    if (has_leaf)
+        CK(launch_leaf_schedule(ctx->dt, dp, lk, ds->schedule, &ds->found, ub, st), "leaf schedule");
+    CK(launch_chunk_scan(ctx->chunk_count.as<int32_t>(), 0, pool.nchunks, ctx->offsets.as<int64_t>(), st),
+       "chunk scan");
+    CK(launch_append(ctx->dt, ctx->k2, dp, pool, first_internal, stg, ctx->offsets.as<int64_t>(), st),
+       "append");
+    summary_kernel<<<1, 256, 0, st>>>(dp, ctx->offsets.as<int64_t>(), ds);
+    CK(cudaGetLastError(), "summary");
+    CK(cudaMemcpyAsync(&ds->leaf_key, lk, 8, cudaMemcpyDeviceToDevice, st), "leaf key copy");
+    if (!has_leaf) CK(cudaMemsetAsync(&ds->found, 0, 4, st), "found");
+    size_t sbytes = offsetof(RoundSummary, seg_surv) + (size_t)pool.nseg * 8;
+    CK(cudaMemcpyAsync(ctx->h_summary.p, ds, sbytes, cudaMemcpyDeviceToHost, st), "summary D2H");
+    CK(cudaMemcpyAsync(ctx->h_summary.as<RoundSummary>()->schedule, ds->schedule, (size_t)n * 4,
+                       cudaMemcpyDeviceToHost, st),
+       "schedule D2H");
+    CK(cudaStreamSynchronize(st), "round");
+    return FBB_OK;
+}
+
+void node_from_prefix(const HostTables& h, const uint8_t* prefix, int depth, uint64_t* mask,
+                      int32_t* heads) {
+    for (int w = 0; w < h.W; ++w) mask[w] = 0;
+    for (int k = 0; k < h.m; ++k) heads[k] = 0;
+    for (int i = 0; i < depth; ++i) {
+        int j = prefix[i];
+        mask[j >> 6] |= 1ull << (j & 63);
+        int32_t prev = 0;
+        for (int k = 0; k < h.m; ++k) {  // instance.hpp:81-89
+            prev = std::max(prev, heads[k]) + h.p[(size_t)j * h.m + k];
+            heads[k] = prev;
+        }
+    }
+}
+
+int64_t pending_total(const fbb_ctx* ctx) {
+    int64_t s = 0;
+    for (int64_t c : ctx->cnt) s += c;
+    return s;
+}
+
+// Pushes host nodes (in order) onto the device buckets.
+int push_host_nodes(fbb_ctx* ctx, const uint8_t* prefix, const int32_t* depth, int64_t count) {
+    const int n = ctx->dt.n, m = ctx->dt.m, W = ctx->dt.W;
+    // group by depth preserving order
+    std::vector<std::vector<int64_t>> by(n + 1);
+    for (int64_t i = 0; i < count; ++i) {
+        if (depth[i] < 0 || depth[i] > n) return ctx->fail(FBB_E_ARG, "node depth out of range");
+        if (depth[i] == n) return ctx->fail(FBB_E_ARG, "complete nodes cannot be pending");
+        by[depth[i]].push_back(i);
+    }
+    std::vector<uint64_t> hm;
+    std::vector<int32_t> hh;
+    std::vector<uint8_t> hp;
+    for (int d = 0; d <= n; ++d) {
+        if (by[d].empty()) continue;
+        int64_t k = (int64_t)by[d].size();
+        hm.assign((size_t)k * W, 0);
+        hh.assign((size_t)k * m, 0);
+        hp.assign((size_t)k * n, 0);
+        for (int64_t t = 0; t < k; ++t) {
+            const uint8_t* pr = prefix + by[d][t] * n;
+            std::vector<uint8_t> seen(n, 0);
+            for (int i = 0; i < d; ++i) {
+                if (pr[i] >= n || seen[pr[i]]) return ctx->fail(FBB_E_ARG, "invalid prefix");
+                seen[pr[i]] = 1;
+            }
+            node_from_prefix(ctx->ht, pr, d, &hm[t * W], &hh[t * m]);
+            std::memcpy(&hp[t * n], pr, (size_t)d);
+        }
+        int64_t c0 = ctx->cnt[d];
+        CK(store_ensure(ctx, ctx->bucket[d], c0 + k, c0), "bucket grow");
+        Store& b = ctx->bucket[d];
+        CK(cudaMemcpy(b.masks.as<uint64_t>() + c0 * W, hm.data(), hm.size() * 8, cudaMemcpyHostToDevice), "push");
+        CK(cudaMemcpy(b.heads.as<int32_t>() + c0 * m, hh.data(), hh.size() * 4, cudaMemcpyHostToDevice), "push");
+        CK(cudaMemcpy(b.prefix.as<uint8_t>() + c0 * n, hp.data(), hp.size(), cudaMemcpyHostToDevice), "push");
+        ctx->cnt[d] = c0 + k;
+    }
+    return FBB_OK;
+}
+
+void explorer_clear(fbb_ctx* ctx) {
+    const int n = ctx->dt.n;
+    if ((int)ctx->bucket.size() != n + 1) ctx->bucket.resize(n + 1);
+    ctx->cnt.assign(n + 1, 0);
+    ctx->schedule.assign(n, 0);
+    ctx->found = 0;
+    ctx->tot_branched = ctx->tot_bounded = ctx->tot_pruned = ctx->tot_leaves = 0;
+    ctx->explorer_ready = true;
+}
+
+// One explorer round with pool target `target` (> 0).
+int explorer_round(fbb_ctx* ctx, int64_t target, fbb_round_t* rec) {
+    const int n = ctx->dt.n;
+    std::memset(rec, 0, sizeof(*rec));
+    rec->target = target;
+    static thread_local Pool local;
+    local.nseg = 0;
+    std::vector<int64_t> after = ctx->cnt;
+    int64_t have = 0;
+    for (int d = n; d >= 0 && have < target; --d) {  // fill_buffer, search.hpp:69-72
+        if (after[d] == 0) continue;
+        int r = n - d;
+        int64_t need = (target - have + r - 1) / r;
+        int64_t k = std::min<int64_t>(after[d], need);
+        Segment& sg = local.seg[local.nseg++];
+        std::memset(&sg, 0, sizeof(sg));
+        sg.src = ctx->bucket[d].view();
+        sg.first = after[d] - 1;
+        sg.step = -1;
+        sg.count = k;
+        sg.depth = d;
+        after[d] -= k;
+        have += k * r;
+    }
+    if (local.nseg == 0) return FBB_OK;
+    int first_internal = layout_pool(ctx, local);
+    // destinations (bucket depth+1) sized for the worst case before launching
+    for (int s = first_internal; s < local.nseg; ++s) {
+        Segment& sg = local.seg[s];
+        int d1 = sg.depth + 1;
+        int64_t worst = after[d1] + sg.count * (n - sg.depth);
+        // keep the full old content: this round's parents may sit in bucket d1's popped region
+        CK(store_ensure(ctx, ctx->bucket[d1], worst, ctx->cnt[d1]), "bucket grow");
+    }
+    for (int s = 0; s < local.nseg; ++s) {  // views may have moved after growth
+        Segment& sg = local.seg[s];
+        sg.src = ctx->bucket[sg.depth].view();
+        if (sg.depth < n - 2) {
+            sg.dst = ctx->bucket[sg.depth + 1].view();
+            sg.dst_base = after[sg.depth + 1];
+        } else {
+            sg.dst = NodeStore{nullptr, nullptr, nullptr};
+            sg.dst_base = 0;
+        }
+        sg.dst_lb = nullptr;
+    }
+    int rc = run_pool(ctx, local, first_internal, ctx->incumbent, ctx->frozen);
+    if (rc != FBB_OK) return rc;
+    const RoundSummary* sm = ctx->h_summary.as<RoundSummary>();
+    int64_t internal = 0, leaves = 0;
+    for (int s = 0; s < local.nseg; ++s) {
+        const Segment& sg = local.seg[s];
+        int64_t kids = sg.count * (n - sg.depth);
+        rec->branched += sg.count;
+        if (sg.depth >= n - 2) {
+            leaves += kids;
+        } else {
+            internal += kids;
+            after[sg.depth + 1] += sm->seg_surv[s];
+        }
+    }
+    ctx->cnt = after;
+    rec->bounded = internal + leaves;
+    rec->leaves = leaves;
+    rec->inserted = sm->total;
+    rec->pruned = internal - sm->total;
+    if (leaves > 0 && sm->leaf_key != ~0ull) {
+        int32_t v = (int32_t)(sm->leaf_key >> 32);
+        if (ctx->frozen) {
+            // frozen incumbent: track the best leaf strictly under UB (bench.hpp:99-102)
+            if (v < ctx->incumbent && (!ctx->found || v < ctx->best)) {
+                ctx->best = v;
+                ctx->found = 1;
+            }
+        } else if (v < ctx->incumbent) {
+            // integrate: strict improvement, first leaf attaining the minimum (search.hpp:93-99)
+            ctx->incumbent = v;
+            ctx->best = v;
+            ctx->found = 1;
+            if (sm->found) std::memcpy(ctx->schedule.data(), sm->schedule, (size_t)n * 4);
+        }
+    }
+    rec->incumbent = ctx->frozen ? (ctx->found ? ctx->best : ctx->incumbent) : ctx->incumbent;
+    ctx->tot_branched += rec->branched;
+    ctx->tot_bounded += rec->bounded;
+    ctx->tot_pruned += rec->pruned;
+    ctx->tot_leaves += rec->leaves;
+    rec->pending = pending_total(ctx);
+    return FBB_OK;
+}
+
+}  // namespace
+
+// =========================================================================================
+extern "C" {
+
+const char* fbb_version(void) { return "flowbb-b200 0.1 (sm_100a)"; }
+
+fbb_ctx* fbb_create(int device, const int32_t* p, int n, int m) {
+    auto fail = [&](int code, const std::string& m_) -> fbb_ctx* {
+        std::lock_guard<std::mutex> g(g_err_mu);
+        g_create_status = code;
+        g_create_err = m_;
+        return nullptr;
+    };
+    if (!p) return fail(FBB_E_ARG, "null processing-time matrix");
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess || ndev == 0)
+        return fail(FBB_E_CUDA, std::string("no CUDA device: ") + cudaGetErrorString(e));
+    if (device < 0 || device >= ndev) return fail(FBB_E_ARG, "device index out of range");
+    cudaDeviceProp prop;
+    cudaGetDeviceProperties(&prop, device);
+    if (prop.major != 10)
+        return fail(FBB_E_CUDA, "this build targets sm_100a (B200); device is sm_" +
+                                    std::to_string(prop.major * 10 + prop.minor));
+    fbb_ctx* ctx = new fbb_ctx();
+    ctx->device = device;
+    std::string why;
+    int rc = build_host_tables(p, n, m, &ctx->ht, &why);
+    if (rc != FBB_OK) {
+        delete ctx;
+        return fail(rc, why);
+    }
+    cudaSetDevice(device);
+    if ((e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking)) != cudaSuccess) {
+        delete ctx;
+        return fail(FBB_E_CUDA, std::string("stream: ") + cudaGetErrorString(e));
+    }
+    rc = upload_tables(ctx->ht, &ctx->dt, &why);
+    if (rc != FBB_OK) {
+        fbb_destroy(ctx);
+        return fail(rc, why);
+    }
+    ctx->k1 = k1_config(ctx->dt, device);
+    ctx->k2 = k2_config(ctx->dt, device);
+    int max_smem = 0;
+    cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    if (ctx->k1.smem > (size_t)max_smem || ctx->k2.smem > (size_t)max_smem) {
+        fbb_destroy(ctx);
+        return fail(FBB_E_RANGE, "instance tables exceed shared memory (n*P too large)");
+    }
+    explorer_clear(ctx);
+    ctx->incumbent = INT_MAX;
+    return ctx;
+}
+
+void fbb_destroy(fbb_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    free_tables(&ctx->dt);
+    for (DBuf* b : {&ctx->k1_masks, &ctx->k1_heads, &ctx->k1_depth, &ctx->k1_lb, &ctx->out_lb,
+                    &ctx->staging_masks, &ctx->staging_heads, &ctx->staging_prefix, &ctx->staging_lb,
+                    &ctx->chunk_count, &ctx->offsets, &ctx->d_pool, &ctx->d_leaf_key, &ctx->d_summary})
+        b->release();
+    for (Store* s : {&ctx->batch_in, &ctx->batch_out}) {
+        s->masks.release();
+        s->heads.release();
+        s->prefix.release();
+    }
+    for (Store& s : ctx->bucket) {
+        s.masks.release();
+        s.heads.release();
+        s.prefix.release();
+    }
+    ctx->h_pool.release();
+    ctx->h_summary.release();
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+}
+
+int fbb_last_error(const fbb_ctx* ctx, int* device, char* msg, size_t cap) {
+    int status;
+    std::string m;
+    int dev = -1;
+    if (ctx) {
+        status = ctx->status;
+        m = ctx->msg;
+        dev = ctx->device;
+    } else {
+        std::lock_guard<std::mutex> g(g_err_mu);
+        status = g_create_status;
+        m = g_create_err;
+    }
+    if (device) *device = dev;
+    if (msg && cap > 0) {
+        size_t k = std::min(cap - 1, m.size());
+        std::memcpy(msg, m.data(), k);
+        msg[k] = 0;
+    }
+    return status;
+}
+
+int fbb_descriptor(fbb_ctx* ctx, fbb_descriptor_t* out) {
+    if (!ctx || !out) return FBB_E_ARG;
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, ctx->device);
+    out->grain = ctx->k2.cmax;                                   // children per K2 tile
+    out->base_units = std::max(1, ctx->k2.blocks);               // resident tiles (SMs x occupancy)
+    size_t free_b = 0, total_b = 0;
+    cudaSetDevice(ctx->device);
+    cudaMemGetInfo(&free_b, &total_b);
+    // children per round bounded by what the staging + buckets can hold in a quarter of HBM
+    int64_t per_child = (int64_t)node_bytes(ctx) * 3 + 16;
+    int64_t cap = (int64_t)(total_b / 4) / per_child;
+    out->max_batch = std::max<int64_t>(cap - cap % out->grain, (int64_t)out->grain * out->base_units);
+    (void)sms;
+    return FBB_OK;
+}
+
+int fbb_bound_device(fbb_ctx* ctx, const uint64_t* d_masks, const int32_t* d_heads,
+                     const int32_t* d_depth, int64_t count, int32_t* d_lb_out, void* stream) {
+    if (!ctx) return FBB_E_ARG;
+    if (count < 0) return ctx->fail(FBB_E_ARG, "negative count");
+    if (count == 0) return FBB_OK;
+    cudaSetDevice(ctx->device);
+    cudaStream_t st = stream ? (cudaStream_t)stream : ctx->stream;
+    CK(launch_k1(ctx->dt, ctx->k1, d_masks, d_heads, d_depth, count, d_lb_out, st), "K1 launch");
+    return FBB_OK;
+}
+
+int fbb_bound(fbb_ctx* ctx, const uint64_t* masks, const int32_t* heads, const int32_t* depth,
+              int64_t count, int32_t* lb_out) {
+    if (!ctx) return FBB_E_ARG;
+    if (count < 0 || (count > 0 && (!masks || !heads || !depth || !lb_out)))
+        return ctx->fail(FBB_E_ARG, "invalid node batch");
+    if (count == 0) return FBB_OK;
+    cudaSetDevice(ctx->device);
+    const int m = ctx->dt.m, W = ctx->dt.W, n = ctx->dt.n;
+    for (int64_t i = 0; i < count; ++i)
+        if (depth[i] < 0 || depth[i] > n) return ctx->fail(FBB_E_ARG, "node depth out of range");
+    CK(ctx->k1_masks.ensure((size_t)count * W * 8), "alloc");
+    CK(ctx->k1_heads.ensure((size_t)count * m * 4), "alloc");
+    CK(ctx->k1_depth.ensure((size_t)count * 4), "alloc");
+    CK(ctx->k1_lb.ensure((size_t)count * 4), "alloc");
+    cudaStream_t st = ctx->stream;
+    CK(cudaMemcpyAsync(ctx->k1_masks.p, masks, (size_t)count * W * 8, cudaMemcpyHostToDevice, st), "H2D");
+    CK(cudaMemcpyAsync(ctx->k1_heads.p, heads, (size_t)count * m * 4, cudaMemcpyHostToDevice, st), "H2D");
+    CK(cudaMemcpyAsync(ctx->k1_depth.p, depth, (size_t)count * 4, cudaMemcpyHostToDevice, st), "H2D");
+    CK(launch_k1(ctx->dt, ctx->k1, ctx->k1_masks.as<uint64_t>(), ctx->k1_heads.as<int32_t>(),
+                 ctx->k1_depth.as<int32_t>(), count, ctx->k1_lb.as<int32_t>(), st),
+       "K1 launch");
+    CK(cudaMemcpyAsync(lb_out, ctx->k1_lb.p, (size_t)count * 4, cudaMemcpyDeviceToHost, st), "D2H");
+    CK(cudaStreamSynchronize(st), "K1");
+    return FBB_OK;
+}
+
+int fbb_expand_bound_prune(fbb_ctx* ctx, const uint64_t* masks, const int32_t* heads,
+                           const int32_t* depth, const uint8_t* prefix, int64_t nparents,
+                           int32_t ub, int frozen, uint64_t* out_masks, int32_t* out_heads,
+                           int32_t* out_depth, uint8_t* out_prefix, int32_t* out_lb,
+                           int64_t* out_count, int32_t* leaf_best, int64_t* leaf_pos,
+                           int32_t* leaf_schedule, fbb_round_t* counts) {
+    if (!ctx) return FBB_E_ARG;
+    const int n = ctx->dt.n, m = ctx->dt.m, W = ctx->dt.W;
+    if (nparents < 0 || (nparents > 0 && (!masks || !heads || !depth || !prefix)) || !out_count)
+        return ctx->fail(FBB_E_ARG, "invalid parent batch");
+    cudaSetDevice(ctx->device);
+    // runs of equal depth, non-increasing (fill_buffer's pop order)
+    Pool pool;
+    pool.nseg = 0;
+    for (int64_t i = 0; i < nparents; ++i) {
+        int d = depth[i];
+        if (d < 0 || d >= n) return ctx->fail(FBB_E_ARG, "parent depth must be in [0, n)");
+        if (pool.nseg > 0 && pool.seg[pool.nseg - 1].depth == d) {
+            pool.seg[pool.nseg - 1].count++;
+            continue;
+        }
+        if (pool.nseg > 0 && d > pool.seg[pool.nseg - 1].depth)
+            return ctx->fail(FBB_E_ARG, "parents must be in non-increasing depth order (pop order)");
+        Segment& sg = pool.seg[pool.nseg++];
+        std::memset(&sg, 0, sizeof(sg));
+        sg.first = i;
+        sg.step = 1;
+        sg.count = 1;
+        sg.depth = d;
+    }
+    fbb_round_t rec;
+    std::memset(&rec, 0, sizeof(rec));
+    rec.incumbent = ub;
+    *out_count = 0;
+    if (leaf_best) *leaf_best = INT32_MAX;
+    if (leaf_pos) *leaf_pos = -1;
+    if (nparents == 0) {
+        if (counts) *counts = rec;
+        return FBB_OK;
+    }
+    CK(store_ensure(ctx, ctx->batch_in, nparents, 0), "alloc");
+    cudaStream_t st = ctx->stream;
+    Store& in = ctx->batch_in;
+    CK(cudaMemcpyAsync(in.masks.p, masks, (size_t)nparents * W * 8, cudaMemcpyHostToDevice, st), "H2D");
+    CK(cudaMemcpyAsync(in.heads.p, heads, (size_t)nparents * m * 4, cudaMemcpyHostToDevice, st), "H2D");
+    CK(cudaMemcpyAsync(in.prefix.p, prefix, (size_t)nparents * n, cudaMemcpyHostToDevice, st), "H2D");
+    int first_internal = layout_pool(ctx, pool);
+    CK(store_ensure(ctx, ctx->batch_out, std::max<int64_t>(pool.nchildren, 1), 0), "alloc");
+    CK(ctx->out_lb.ensure((size_t)std::max<int64_t>(pool.nchildren, 1) * 4), "alloc");
+    for (int s = 0; s < pool.nseg; ++s) {
+        pool.seg[s].src = in.view();
+        pool.seg[s].dst = ctx->batch_out.view();
+        pool.seg[s].dst_base = -1;
+        pool.seg[s].dst_lb = ctx->out_lb.as<int32_t>();
+    }
+    int rc = run_pool(ctx, pool, first_internal, ub, frozen);
+    if (rc != FBB_OK) return rc;
+    const RoundSummary* sm = ctx->h_summary.as<RoundSummary>();
+    int64_t total = sm->total;
+    *out_count = total;
+    if (total > 0) {
+        if (out_masks)
+            CK(cudaMemcpyAsync(out_masks, ctx->batch_out.masks.p, (size_t)total * W * 8, cudaMemcpyDeviceToHost, st), "D2H");
+        if (out_heads)
+            CK(cudaMemcpyAsync(out_heads, ctx->batch_out.heads.p, (size_t)total * m * 4, cudaMemcpyDeviceToHost, st), "D2H");
+        if (out_prefix)
+            CK(cudaMemcpyAsync(out_prefix, ctx->batch_out.prefix.p, (size_t)total * n, cudaMemcpyDeviceToHost, st), "D2H");
+        if (out_lb)
+            CK(cudaMemcpyAsync(out_lb, ctx->out_lb.p, (size_t)total * 4, cudaMemcpyDeviceToHost, st), "D2H");
+        CK(cudaStreamSynchronize(st), "D2H");
+    }
+    int64_t internal = 0, leaves = 0, o = 0;
+    for (int s = 0; s < pool.nseg; ++s) {
+        const Segment& sg = pool.seg[s];
+        int64_t kids = sg.count * (n - sg.depth);
+        rec.branched += sg.count;
+        if (sg.depth >= n - 2) {
+            leaves += kids;
+        } else {
+            internal += kids;
+            if (out_depth)
+                for (int64_t i = 0; i < sm->seg_surv[s]; ++i) out_depth[o + i] = sg.depth + 1;
+            o += sm->seg_surv[s];
+        }
+    }
+    rec.bounded = internal + leaves;
+    rec.leaves = leaves;
+    rec.inserted = total;
+    rec.pruned = internal - total;
+    if (leaves > 0 && sm->leaf_key != ~0ull) {
+        int32_t v = (int32_t)(sm->leaf_key >> 32);
+        if (v < ub) {
+            if (leaf_best) *leaf_best = v;
+            if (leaf_pos) *leaf_pos = (int64_t)(sm->leaf_key & 0xFFFFFFFFull);
+            if (leaf_schedule && sm->found) std::memcpy(leaf_schedule, sm->schedule, (size_t)n * 4);
+            if (!frozen) rec.incumbent = v;
+        }
+    }
+    if (counts) *counts = rec;
+    return FBB_OK;
+}
+
+int fbb_explorer_reset(fbb_ctx* ctx, const uint8_t* prefix, const int32_t* depth, int64_t count,
+                       int32_t ub, int frozen) {
+    if (!ctx) return FBB_E_ARG;
+    if (count < 0 || (count > 0 && (!prefix || !depth))) return ctx->fail(FBB_E_ARG, "invalid nodes");
+    cudaSetDevice(ctx->device);
+    explorer_clear(ctx);
+    ctx->incumbent = ub;
+    ctx->frozen = frozen ? 1 : 0;
+    ctx->found = 0;
+    return push_host_nodes(ctx, prefix, depth, count);
+}
+
+int fbb_explorer_start_solve(fbb_ctx* ctx, int32_t ub, fbb_round_t* round0) {
+    if (!ctx) return FBB_E_ARG;
+    cudaSetDevice(ctx->device);
+    explorer_clear(ctx);
+    const int n = ctx->dt.n, m = ctx->dt.m, W = ctx->dt.W;
+    ctx->frozen = 0;
+    if (ub >= 0) {
+        ctx->incumbent = ub;
+        ctx->found = 0;
+    } else {  // identity permutation, search.hpp:131-137
+        std::vector<int32_t> h(m, 0);
+        for (int j = 0; j < n; ++j) {
+            int32_t prev = 0;
+            for (int k = 0; k < m; ++k) {
+                prev = std::max(prev, h[k]) + ctx->ht.p[(size_t)j * m + k];
+                h[k] = prev;
+            }
+            ctx->schedule[j] = j;
+        }
+        ctx->incumbent = h[m - 1];
+        ctx->best = ctx->incumbent;
+        ctx->found = 1;
+    }
+    // round 0: bound the root (search.hpp:150-153), integrate it
+    std::vector<uint64_t> mk(W, 0);
+    std::vector<int32_t> hd(m, 0);
+    int32_t dep = 0, lb = 0;
+    int rc = fbb_bound(ctx, mk.data(), hd.data(), &dep, 1, &lb);
+    if (rc != FBB_OK) return rc;
+    fbb_round_t rec;
+    std::memset(&rec, 0, sizeof(rec));
+    rec.bounded = 1;
+    if (lb < ctx->incumbent) {  // the root is internal for every n >= 1
+        rec.inserted = 1;
+        uint8_t pr = 0;
+        rc = push_host_nodes(ctx, &pr, &dep, 1);
+        if (rc != FBB_OK) return rc;
+    } else {
+        rec.pruned = 1;
+    }
+    ctx->tot_bounded = 1;
+    ctx->tot_pruned = rec.pruned;
+    rec.incumbent = ctx->incumbent;
+    rec.pending = pending_total(ctx);
+    if (round0) *round0 = rec;
+    return FBB_OK;
+}
+
+int fbb_explorer_run(fbb_ctx* ctx, const int64_t* targets, int ntargets, int64_t max_rounds,
+                     int64_t budget, fbb_round_t* rounds, int64_t* done) {
+    if (!ctx) return FBB_E_ARG;
+    if (!targets || ntargets < 1) return ctx->fail(FBB_E_ARG, "need at least one target");
+    cudaSetDevice(ctx->device);
+    int64_t r = 0;
+    if (done) *done = 0;
+    while (r < max_rounds) {
+        if (pending_total(ctx) == 0) break;
+        if (budget > 0 && ctx->tot_bounded >= budget) break;
+        int64_t target = targets[r < ntargets ? r : ntargets - 1];
+        if (target < 1) target = 1;
+        fbb_round_t rec;
+        int rc = explorer_round(ctx, target, &rec);
+        if (rc != FBB_OK) return rc;
+        if (rounds) rounds[r] = rec;
+        ++r;
+        if (done) *done = r;
+    }
+    return FBB_OK;
+}
+
+int fbb_explorer_state(fbb_ctx* ctx, int32_t* incumbent, int32_t* found, int32_t* schedule,
+                       int64_t* pending, int64_t* totals4) {
+    if (!ctx) return FBB_E_ARG;
+    if (incumbent) *incumbent = ctx->frozen ? (ctx->found ? ctx->best : ctx->incumbent) : ctx->incumbent;
+    if (found) *found = ctx->found;
+    if (schedule && ctx->found) std::memcpy(schedule, ctx->schedule.data(), ctx->schedule.size() * 4);
+    if (pending) *pending = pending_total(ctx);
+    if (totals4) {
+        totals4[0] = ctx->tot_branched;
+        totals4[1] = ctx->tot_bounded;
+        totals4[2] = ctx->tot_pruned;
+        totals4[3] = ctx->tot_leaves;
+    }
+    return FBB_OK;
+}
+
+int fbb_explorer_pending(fbb_ctx* ctx, uint8_t* prefix, int32_t* depth, int64_t cap, int64_t* count) {
+    if (!ctx || !count) return FBB_E_ARG;
+    cudaSetDevice(ctx->device);
+    const int n = ctx->dt.n;
+    int64_t total = pending_total(ctx);
+    *count = total;
+    if (cap < total) return ctx->fail(FBB_E_ARG, "buffer too small for the pending tree");
+    int64_t o = 0;
+    for (int d = 0; d <= n; ++d) {
+        int64_t k = ctx->cnt[d];
+        if (k == 0) continue;
+        if (prefix)
+            CK(cudaMemcpy(prefix + o * n, ctx->bucket[d].prefix.p, (size_t)k * n, cudaMemcpyDeviceToHost),
+               "pending D2H");
+        if (depth)
+            for (int64_t i = 0; i < k; ++i) depth[o + i] = d;
+        o += k;
+    }
+    return FBB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,505 @@
+// expand_kernel.cu -- K2: fused expand + bound + prune + compact of a pool.
+//
+// One round of the reference explorer for a list of parents in pop order:
+//   branch           search.hpp:40-59   children in ascending job order,
+//                                       depth n-1 children auto-completed
+//   evaluate         bound.hpp:94-109   every child's lower bound
+//   integrate/prune  search.hpp:84-107, bench.hpp:96-106
+// fused so that children never exist in memory unless they survive.
+//
+// Sibling bound (SURVEY finding 3).  For parent U (unscheduled set, r jobs)
+// and pair q = (k,l) let V_i = D_<i + c_i over the Johnson order of U.  The
+// child that schedules x (position i_x) has M'_x = max(prefmax_{<i_x},
+// sufmax_{>i_x} - d_x), so ONE forward and ONE backward scan of the pair row
+// give M' for all r children: O(P*n) per parent instead of O(P*n) per child.
+// Child bound for pair q: Lc'_l(x) + max(R'_l(x), R'_k(x) + M'_x) with R' the
+// child heads (instance.hpp:81-89) and Lc'_l(x) = load_l(U) - p[x][l] +
+// min_{U\x} tail_l (min1/min2 per machine).
+//
+// Work layout per CTA and chunk (a run of parents of one depth whose
+// children fit `cmax`):
+//   stage     parents' unscheduled bits and heads -> smem
+//   per parent: rank of each job in U; per (parent, machine) load/min1/min2
+//   Phase A   items (parent, pair): forward+backward scan, M' -> smem Mq[child][pair]
+//   Phase B   items child: heads, one-machine term, max over pairs -> lb
+//   compact   block scan of (lb < UB) in batch order -> staging[chunk]
+// Leaves (parents at depth >= n-2) are evaluated by their own kernel, which
+// also produces the batch leaf minimum that non-frozen pruning needs
+// (integrate lowers the incumbent mid-batch; leaves precede every internal
+// child in a pool because the leaf-producing bucket is the deepest one).
+#include <climits>
+
+#include "fbb_internal.h"
+
+namespace fbb {
+
+namespace {
+
+constexpr int32_t kNeg = -(1 << 20);
+
+__host__ __device__ inline size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
+
+struct K2Layout {
+    size_t jm, pk, p, tl, um, R, rank, ujob, load, min1, min2, amin, Mq, cR, cL, wsum, total;
+    int ppc_max, pst, mst;
+};
+
+__host__ __device__ inline K2Layout k2_layout(int n, int m, int P, int cmax, int threads) {
+    K2Layout L;
+    int W32 = (n + 31) / 32;
+    L.ppc_max = cmax / 3 > 0 ? cmax / 3 : 1;
+    L.pst = P + 1;             // Mq row stride (elements); odd -> conflict-free rows
+    L.mst = m + 1;             // child row stride for cR / cL
+    size_t o = 0;
+    L.jm = o;   o = a16(o + (size_t)n * P * 4);
+    L.pk = o;   o = a16(o + (size_t)P * 4);
+    L.p = o;    o = a16(o + (size_t)n * m * 4);
+    L.tl = o;   o = a16(o + (size_t)n * m * 4);
+    L.um = o;   o = a16(o + (size_t)L.ppc_max * W32 * 4);
+    L.R = o;    o = a16(o + (size_t)L.ppc_max * m * 4);
+    L.rank = o; o = a16(o + (size_t)L.ppc_max * n);
+    L.ujob = o; o = a16(o + (size_t)L.ppc_max * n);
+    L.load = o; o = a16(o + (size_t)L.ppc_max * m * 4);
+    L.min1 = o; o = a16(o + (size_t)L.ppc_max * m * 4);
+    L.min2 = o; o = a16(o + (size_t)L.ppc_max * m * 4);
+    L.amin = o; o = a16(o + (size_t)L.ppc_max * m * 4);
+    L.Mq = o;   o = a16(o + (size_t)cmax * L.pst * 2);
+    L.cR = o;   o = a16(o + (size_t)cmax * L.mst * 4);
+    L.cL = o;   o = a16(o + (size_t)cmax * L.mst * 4);
+    L.wsum = o; o = a16(o + (size_t)(threads / 32 + 1) * 4);
+    L.total = o;
+    return L;
+}
+
+__device__ inline int find_segment(const Pool* __restrict__ pool, int lo, int64_t chunk) {
+    int hi = pool->nseg - 1;
+    while (lo < hi) {  // last segment with chunk_base <= chunk
+        int mid = (lo + hi + 1) >> 1;
+        if (pool->seg[mid].chunk_base <= chunk) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+__device__ inline bool um_test(const uint32_t* um, int j) { return (um[j >> 5] >> (j & 31)) & 1u; }
+
+__global__ void __launch_bounds__(128) k2_internal_kernel(DevTables t, const Pool* __restrict__ pool,
+                                                         int first_seg, int cmax, int32_t ub,
+                                                         int frozen,
+                                                         const unsigned long long* __restrict__ leaf_key,
+                                                         Staging st) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int n = t.n, m = t.m, P = t.P, W = t.W;
+    const int W32 = (n + 31) / 32;
+    const K2Layout L = k2_layout(n, m, P, cmax, blockDim.x);
+    uint32_t* s_jm = (uint32_t*)(smem + L.jm);
+    int32_t* s_pk = (int32_t*)(smem + L.pk);
+    int32_t* s_p = (int32_t*)(smem + L.p);
+    int32_t* s_tl = (int32_t*)(smem + L.tl);
+    uint32_t* s_um = (uint32_t*)(smem + L.um);
+    int32_t* s_R = (int32_t*)(smem + L.R);
+    uint8_t* s_rank = (uint8_t*)(smem + L.rank);
+    uint8_t* s_ujob = (uint8_t*)(smem + L.ujob);
+    int32_t* s_load = (int32_t*)(smem + L.load);
+    int32_t* s_min1 = (int32_t*)(smem + L.min1);
+    int32_t* s_min2 = (int32_t*)(smem + L.min2);
+    int32_t* s_amin = (int32_t*)(smem + L.amin);
+    int16_t* s_Mq = (int16_t*)(smem + L.Mq);
+    int32_t* s_cR = (int32_t*)(smem + L.cR);
+    int32_t* s_cL = (int32_t*)(smem + L.cL);
+    int32_t* s_wsum = (int32_t*)(smem + L.wsum);
+    const int tid = threadIdx.x, bd = blockDim.x, lane = tid & 31, warp = tid >> 5;
+    const int nwarps = bd >> 5;
+
+    for (int x = tid; x < n * P; x += bd) s_jm[x] = t.jm[x];
+    for (int x = tid; x < P; x += bd) s_pk[x] = (int32_t)t.pair_k[x] | ((int32_t)t.pair_l[x] << 16);
+    for (int x = tid; x < n * m; x += bd) {
+        s_p[x] = t.p[x];
+        s_tl[x] = t.tails[x];
+    }
+    // incumbent for internal children: min(UB, batch leaf minimum) unless frozen
+    int32_t ub_eff = ub;
+    if (!frozen && leaf_key) {
+        unsigned long long key = *leaf_key;
+        int32_t v = (int32_t)(key >> 32);
+        if (key != ~0ull && v < ub_eff) ub_eff = v;
+    }
+
+    const int64_t c_begin = pool->seg[first_seg].chunk_base;
+    const int64_t c_end = pool->nchunks;
+    for (int64_t chunk = c_begin + blockIdx.x; chunk < c_end; chunk += gridDim.x) {
+        const int s = find_segment(pool, first_seg, chunk);
+        const Segment& sg = pool->seg[s];
+        const int depth = sg.depth;
+        const int r = n - depth;
+        const int ppc = cmax / r;
+        const int64_t p0 = (chunk - sg.chunk_base) * ppc;
+        const int np = (int)(sg.count - p0 < ppc ? sg.count - p0 : ppc);
+        const int nc = np * r;
+        const NodeStore src = sg.src;
+        const int64_t first = sg.first, step = sg.step;
+        __syncthreads();  // previous chunk consumed; tables staged
+        // ---- stage parents
+        for (int x = tid; x < np * W32; x += bd) {
+            int pp = x / W32, w = x - pp * W32;
+            int64_t node = first + step * (p0 + pp);
+            uint64_t word = src.masks[node * W + (w >> 1)];
+            uint32_t half = (w & 1) ? (uint32_t)(word >> 32) : (uint32_t)word;
+            int valid = min(32, n - w * 32);
+            uint32_t vmask = valid >= 32 ? 0xFFFFFFFFu : ((1u << valid) - 1u);
+            s_um[x] = ~half & vmask;
+        }
+        for (int x = tid; x < np * m; x += bd) {
+            int pp = x / m, k = x - pp * m;
+            int64_t node = first + step * (p0 + pp);
+            s_R[x] = src.heads[node * m + k];
+        }
+        __syncthreads();
+        // ---- per parent: rank of each unscheduled job, ascending job list
+        for (int pp = tid; pp < np; pp += bd) {
+            const uint32_t* um = s_um + pp * W32;
+            int rk = 0;
+            for (int j = 0; j < n; ++j) {
+                if (um_test(um, j)) {
+                    s_rank[pp * n + j] = (uint8_t)rk;
+                    s_ujob[pp * n + rk] = (uint8_t)j;
+                    ++rk;
+                }
+            }
+        }
+        // ---- per (parent, machine): load, smallest and second-smallest tail
+        for (int x = tid; x < np * m; x += bd) {
+            int pp = x / m, k = x - pp * m;
+            const uint32_t* um = s_um + pp * W32;
+            int32_t load = 0, m1 = INT_MAX, m2 = INT_MAX, am = -1;
+            for (int j = 0; j < n; ++j) {
+                if (um_test(um, j)) {
+                    load += s_p[j * m + k];
+                    int32_t tv = s_tl[j * m + k];
+                    if (tv < m1) {
+                        m2 = m1;
+                        m1 = tv;
+                        am = j;
+                    } else if (tv < m2) {
+                        m2 = tv;
+                    }
+                }
+            }
+            s_load[x] = load;
+            s_min1[x] = m1;
+            s_min2[x] = m2;
+            s_amin[x] = am;
+        }
+        __syncthreads();
+        // ---- Phase A: per (parent, pair) forward/backward Johnson scans
+        for (int x = tid; x < np * P; x += bd) {
+            int pp = x / P, q = x - pp * P;
+            const uint32_t* um = s_um + pp * W32;
+            const uint8_t* rank = s_rank + pp * n;
+            int16_t* Mq = s_Mq + (size_t)(pp * r) * L.pst + q;
+            int32_t D = 0, PM = kNeg;
+            for (int i = 0; i < n; ++i) {
+                uint32_t e = s_jm[i * P + q];
+                int j = entry_job(e);
+                if (um_test(um, j)) {
+                    Mq[rank[j] * L.pst] = (int16_t)max(PM, -32768);  // exclusive prefix max
+                    PM = max(PM, D + entry_c(e));
+                    D += entry_d(e);
+                }
+            }
+            int32_t SM = kNeg;
+            for (int i = n - 1; i >= 0; --i) {
+                uint32_t e = s_jm[i * P + q];
+                int j = entry_job(e);
+                if (um_test(um, j)) {
+                    int dj = entry_d(e);
+                    D -= dj;  // D_<i
+                    int16_t* slot = Mq + rank[j] * L.pst;
+                    int32_t v = max((int32_t)*slot, SM - dj);
+                    *slot = (int16_t)max(v, -32768);
+                    SM = max(SM, D + entry_c(e));
+                }
+            }
+        }
+        __syncthreads();
+        // ---- Phase B: per child bound
+        for (int c = tid; c < nc; c += bd) {
+            int pp = c / r, rk = c - pp * r;
+            int x = s_ujob[pp * n + rk];
+            const int32_t* R = s_R + pp * m;
+            int32_t* cR = s_cR + c * L.mst;
+            int32_t* cL = s_cL + c * L.mst;
+            int32_t prev = 0, lb = 0;
+            for (int k = 0; k < m; ++k) {
+                prev = max(prev, R[k]) + s_p[x * m + k];  // child_heads, instance.hpp:81-89
+                cR[k] = prev;
+                int pk = pp * m + k;
+                int32_t mt = (x == s_amin[pk]) ? s_min2[pk] : s_min1[pk];
+                int32_t lc = s_load[pk] - s_p[x * m + k] + mt;
+                cL[k] = lc;
+                lb = max(lb, prev + lc);  // one-machine term (bound.hpp:61-74)
+            }
+            const int16_t* Mq = s_Mq + (size_t)c * L.pst;
+            for (int q = 0; q < P; ++q) {
+                int kl = s_pk[q];
+                int k = kl & 0xFFFF, l = kl >> 16;
+                int32_t v = cL[l] + max(cR[l], cR[k] + (int32_t)Mq[q]);
+                lb = max(lb, v);
+            }
+            cR[m] = lb;  // stash the bound in the row's spare slot
+        }
+        __syncthreads();
+        // ---- prune + stable compaction into staging[chunk]
+        int base_off = 0;
+        for (int c0 = 0; c0 < nc; c0 += bd) {
+            int c = c0 + tid;
+            bool keep = false;
+            int32_t lb = 0;
+            if (c < nc) {
+                lb = s_cR[c * L.mst + m];
+                keep = lb < ub_eff;
+            }
+            unsigned ballot = __ballot_sync(0xFFFFFFFFu, keep);
+            if (lane == 0) s_wsum[warp] = __popc(ballot);
+            __syncthreads();
+            int woff = 0, tot = 0;
+            for (int w = 0; w < nwarps; ++w) {
+                int v = s_wsum[w];
+                if (w < warp) woff += v;
+                tot += v;
+            }
+            if (keep) {
+                int rank = base_off + woff + __popc(ballot & ((1u << lane) - 1u));
+                int64_t o = chunk * (int64_t)cmax + rank;
+                int pp = c / r, rk = c - pp * r;
+                int xj = s_ujob[pp * n + rk];
+                const int32_t* cR = s_cR + c * L.mst;
+                for (int k = 0; k < m; ++k) st.nodes.heads[o * m + k] = cR[k];
+                const uint32_t* um = s_um + pp * W32;
+                for (int w = 0; w < W; ++w) {
+                    uint32_t lo = 2 * w < W32 ? um[2 * w] : 0u;
+                    uint32_t hi = 2 * w + 1 < W32 ? um[2 * w + 1] : 0u;
+                    int vlo = min(32, max(0, n - 64 * w));
+                    int vhi = min(32, max(0, n - 64 * w - 32));
+                    uint32_t mlo = vlo >= 32 ? 0xFFFFFFFFu : ((1u << vlo) - 1u);
+                    uint32_t mhi = vhi >= 32 ? 0xFFFFFFFFu : ((1u << vhi) - 1u);
+                    uint64_t sched = ((uint64_t)(~hi & mhi) << 32) | (uint64_t)(~lo & mlo);
+                    if ((xj >> 6) == w) sched |= (uint64_t)1 << (xj & 63);
+                    st.nodes.masks[o * W + w] = sched;
+                }
+                int64_t node = first + step * (p0 + pp);
+                const uint8_t* pre = src.prefix + node * n;
+                uint8_t* dst = st.nodes.prefix + o * n;
+                for (int i = 0; i < depth; ++i) dst[i] = pre[i];
+                dst[depth] = (uint8_t)xj;
+                if (st.lb) st.lb[o] = lb;
+            }
+            base_off += tot;
+            __syncthreads();
+        }
+        if (tid == 0) st.chunk_count[chunk] = base_off;
+    }
+}
+
+// Children of parents at depth >= n-2 are complete schedules: bound = makespan
+// (bound.hpp:95).  Thread per child; batch-minimum (value, position) by atomicMin.
+__global__ void k2_leaf_kernel(DevTables t, const Pool* __restrict__ pool, int seg_index,
+                               int32_t ub, unsigned long long* leaf_key) {
+    const int n = t.n, m = t.m, W = t.W;
+    const Segment& sg = pool->seg[seg_index];
+    const int depth = sg.depth;
+    const int r = n - depth;
+    const int64_t nc = sg.count * r;
+    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < nc;
+         c += (int64_t)gridDim.x * blockDim.x) {
+        int64_t pp = c / r;
+        int rk = (int)(c - pp * r);
+        int64_t node = sg.first + sg.step * pp;
+        const uint64_t* mk = sg.src.masks + node * W;
+        // the unscheduled jobs in ascending order: x = rk-th, y = the other
+        int u[2] = {-1, -1}, cnt = 0;
+        for (int j = 0; j < n && cnt < 2; ++j)
+            if (!((mk[j >> 6] >> (j & 63)) & 1ull)) u[cnt++] = j;
+        int x = u[rk], y = (r == 2) ? u[1 - rk] : -1;
+        int32_t prev = 0, h[kMaxMachines];
+        const int32_t* R = sg.src.heads + node * m;
+        for (int k = 0; k < m; ++k) {
+            prev = max(prev, R[k]) + t.p[x * m + k];
+            h[k] = prev;
+        }
+        if (y >= 0) {
+            prev = 0;
+            for (int k = 0; k < m; ++k) {
+                prev = max(prev, h[k]) + t.p[y * m + k];
+                h[k] = prev;
+            }
+        }
+        int32_t lb = h[m - 1];
+        if (lb < ub) {
+            unsigned long long key = ((unsigned long long)(uint32_t)lb << 32) |
+                                     (unsigned long long)(uint32_t)(sg.child_base + c);
+            atomicMin(leaf_key, key);
+        }
+    }
+}
+
+// Writes the schedule of the batch's best leaf (if it beats ub) before the
+// parents' storage is recycled by the push.
+__global__ void leaf_schedule_kernel(DevTables t, const Pool* __restrict__ pool,
+                                     const unsigned long long* __restrict__ leaf_key,
+                                     int32_t* schedule, int32_t* found, int32_t ub) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    unsigned long long key = *leaf_key;
+    if (key == ~0ull || (int32_t)(key >> 32) >= ub) {
+        *found = 0;
+        return;
+    }
+    const int n = t.n, W = t.W;
+    int64_t pos = (int64_t)(key & 0xFFFFFFFFull);
+    const Segment& sg = pool->seg[0];  // leaves only come from the first (deepest) segment
+    const int r = n - sg.depth;
+    int64_t c = pos - sg.child_base;
+    int64_t pp = c / r;
+    int rk = (int)(c - pp * r);
+    int64_t node = sg.first + sg.step * pp;
+    const uint64_t* mk = sg.src.masks + node * W;
+    const uint8_t* pre = sg.src.prefix + node * n;
+    for (int i = 0; i < sg.depth; ++i) schedule[i] = pre[i];
+    int u[2] = {-1, -1}, cnt = 0;
+    for (int j = 0; j < n && cnt < 2; ++j)
+        if (!((mk[j >> 6] >> (j & 63)) & 1ull)) u[cnt++] = j;
+    schedule[sg.depth] = u[rk];
+    if (r == 2) schedule[sg.depth + 1] = u[1 - rk];
+    *found = 1;
+}
+
+// Exclusive scan of per-chunk survivor counts (single CTA; a pool has at most
+// a few thousand chunks).  offsets[nchunks] = total.
+__global__ void chunk_scan_kernel(const int32_t* __restrict__ cnt, int64_t c0, int64_t nchunks,
+                                  int64_t* offsets) {
+    __shared__ int64_t warp_tot[32];
+    __shared__ int64_t carry;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    if (tid == 0) carry = 0;
+    for (int64_t i = tid; i < c0; i += blockDim.x) offsets[i] = 0;  // leaf-segment chunks: none
+    __syncthreads();
+    for (int64_t base = c0; base < nchunks; base += blockDim.x) {
+        int64_t i = base + tid;
+        int64_t v = i < nchunks ? cnt[i] : 0;
+        int64_t incl = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            int64_t u = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= o) incl += u;
+        }
+        if (lane == 31) warp_tot[warp] = incl;
+        __syncthreads();
+        int64_t woff = 0, tot = 0;
+        for (int w = 0; w < nw; ++w) {
+            if (w < warp) woff += warp_tot[w];
+            tot += warp_tot[w];
+        }
+        if (i < nchunks) offsets[i] = carry + woff + incl - v;
+        __syncthreads();
+        if (tid == 0) carry += tot;
+        __syncthreads();
+    }
+    if (tid == 0) offsets[nchunks] = carry;
+}
+
+// Copies survivors from staging to their destination: segment `dst` store at
+// dst_base + (offsets[c] - offsets[chunk_base]), or contiguous at offsets[c]
+// when dst_base < 0.  CTA per chunk (grid-stride).
+__global__ void append_kernel(DevTables t, const Pool* __restrict__ pool, int first_seg, int cmax,
+                              Staging st, const int64_t* __restrict__ offsets) {
+    const int n = t.n, m = t.m, W = t.W;
+    const int64_t c_begin = pool->seg[first_seg].chunk_base, c_end = pool->nchunks;
+    for (int64_t chunk = c_begin + blockIdx.x; chunk < c_end; chunk += gridDim.x) {
+        const int s = find_segment(pool, first_seg, chunk);
+        const Segment& sg = pool->seg[s];
+        int cnt = st.chunk_count[chunk];
+        if (cnt == 0) continue;
+        int64_t pos = sg.dst_base < 0 ? offsets[chunk]
+                                      : sg.dst_base + offsets[chunk] - offsets[sg.chunk_base];
+        int64_t so = chunk * (int64_t)cmax;
+        const NodeStore dst = sg.dst;
+        for (int x = threadIdx.x; x < cnt * m; x += blockDim.x)
+            dst.heads[pos * m + x] = st.nodes.heads[so * m + x];
+        for (int x = threadIdx.x; x < cnt * W; x += blockDim.x)
+            dst.masks[pos * W + x] = st.nodes.masks[so * W + x];
+        const int dlen = sg.depth + 1;
+        for (int x = threadIdx.x; x < cnt * n; x += blockDim.x) {
+            int i = x / n, b = x - i * n;
+            if (b < dlen) dst.prefix[(pos + i) * n + b] = st.nodes.prefix[(so + i) * n + b];
+        }
+        if (sg.dst_lb && st.lb)
+            for (int x = threadIdx.x; x < cnt; x += blockDim.x) sg.dst_lb[pos + x] = st.lb[so + x];
+    }
+}
+
+}  // namespace
+
+K2Config k2_config(const DevTables& t, int device) {
+    K2Config c;
+    c.threads = 128;
+    int n = t.n;
+    c.cmax = n <= 128 ? 128 : ((n + 31) / 32) * 32;
+    c.smem = k2_layout(t.n, t.m, t.P, c.cmax, c.threads).total;
+    int sms = 148, per_sm = 1;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    cudaFuncSetAttribute(k2_internal_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_internal_kernel, c.threads, c.smem);
+    if (per_sm < 1) per_sm = 1;
+    c.blocks = sms * per_sm;
+    return c;
+}
+
+cudaError_t launch_k2_leaves(const DevTables& t, const K2Config& cfg, const Pool* d_pool,
+                             const Pool& h_pool, int seg_index, unsigned long long* leaf_key,
+                             cudaStream_t stream) {
+    (void)cfg;
+    const Segment& sg = h_pool.seg[seg_index];
+    int64_t nc = sg.count * (t.n - sg.depth);
+    if (nc <= 0) return cudaSuccess;
+    int blocks = (int)((nc + 255) / 256);
+    if (blocks > 4096) blocks = 4096;
+    k2_leaf_kernel<<<blocks, 256, 0, stream>>>(t, d_pool, seg_index, INT_MAX, leaf_key);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_k2_internal(const DevTables& t, const K2Config& cfg, const Pool* d_pool,
+                               const Pool& h_pool, int first_seg, int32_t ub, int frozen,
+                               const unsigned long long* leaf_key, Staging st,
+                               cudaStream_t stream) {
+    if (first_seg >= h_pool.nseg) return cudaSuccess;
+    int64_t nch = h_pool.nchunks - h_pool.seg[first_seg].chunk_base;
+    if (nch <= 0) return cudaSuccess;
+    int blocks = (int)(nch < cfg.blocks ? nch : cfg.blocks);
+    k2_internal_kernel<<<blocks, cfg.threads, cfg.smem, stream>>>(t, d_pool, first_seg, cfg.cmax, ub,
+                                                                  frozen, leaf_key, st);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_chunk_scan(const int32_t* chunk_count, int64_t c0, int64_t nchunks,
+                              int64_t* offsets, cudaStream_t stream) {
+    chunk_scan_kernel<<<1, 1024, 0, stream>>>(chunk_count, c0, nchunks, offsets);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_append(const DevTables& t, const K2Config& cfg, const Pool* d_pool,
+                          const Pool& h_pool, int first_seg, Staging st, const int64_t* offsets,
+                          cudaStream_t stream) {
+    if (first_seg >= h_pool.nseg) return cudaSuccess;
+    int64_t nch = h_pool.nchunks - h_pool.seg[first_seg].chunk_base;
+    if (nch <= 0) return cudaSuccess;
+    int blocks = (int)(nch < 8192 ? nch : 8192);
+    append_kernel<<<blocks, 128, 0, stream>>>(t, d_pool, first_seg, cfg.cmax, st, offsets);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_leaf_schedule(const DevTables& t, const Pool* d_pool,
+                                 const unsigned long long* leaf_key, int32_t* schedule,
+                                 int32_t* found_flag, int32_t ub, cudaStream_t stream) {
+    leaf_schedule_kernel<<<1, 32, 0, stream>>>(t, d_pool, leaf_key, schedule, found_flag, ub);
+    return cudaGetLastError();
+}
+
+}  // namespace fbb

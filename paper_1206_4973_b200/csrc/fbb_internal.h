@@ -1,0 +1,149 @@
+// fbb_internal.h -- shared definitions of the B200 hot path (device tables,
+// node batches, kernel entry points).  Not part of the C-ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "flowbb_b200.h"
+
+namespace fbb {
+
+constexpr int kMaxJobs = 256;     // uint8 prefixes
+constexpr int kMaxMachines = 64;  // per-node machine arrays staged in smem / registers
+constexpr int kMaxWords = (kMaxJobs + 63) / 64;
+
+// Packed Johnson-order table entry for (machine pair q, position i):
+//   bits  0.. 8  job index j            (n <= 512)
+//   bits  9..17  d + 256 = a - b + 256   (|a - b| <= 255)
+//   bits 18..31  c = a + lag             (c < 16384)
+// with a = p[j][k], b = p[j][l], lag = tail(j,k) - p(j,l) - tail(j,l)
+// (bound.hpp:84-86).  Johnson's rule with lags is rewritten as the max-plus
+// form   t_B = sum_U b + max(r_l, r_k + max_i (D_<i + c_i)),  D_<i = sum of d
+// over the jobs of U before position i, which is the simulation
+// t_A += a; t_B = max(t_B, t_A + lag) + b of bound.hpp:37-43 unrolled.
+__host__ __device__ inline uint32_t pack_entry(int job, int d, int c) {
+    return (uint32_t)job | ((uint32_t)(d + 256) << 9) | ((uint32_t)c << 18);
+}
+__host__ __device__ inline int entry_job(uint32_t e) { return (int)(e & 0x1FFu); }
+__host__ __device__ inline int entry_d(uint32_t e) { return (int)((e >> 9) & 0x1FFu) - 256; }
+__host__ __device__ inline int entry_c(uint32_t e) { return (int)(e >> 18); }
+
+// Device-resident instance tables (built once per context, tables.cu).
+struct DevTables {
+    int n, m, P, W;
+    int32_t* p;       // n*m job-major (instance.hpp:65)
+    int32_t* tails;   // n*m (instance.hpp:38-45)
+    uint32_t* jm;     // n*P, position-major: jm[i*P + q]
+    int16_t* pair_k;  // P
+    int16_t* pair_l;  // P
+};
+
+// Host copy of the same tables (for tests of the table builder).
+struct HostTables {
+    int n = 0, m = 0, P = 0, W = 0;
+    std::vector<int32_t> p, tails;
+    std::vector<uint32_t> jm;
+    std::vector<int16_t> pair_k, pair_l;
+};
+
+// Builds the Johnson orders: for each pair (k<l), jobs sorted by
+// (group, key, job) -- group 0 if a+lag < lag+b, ascending a+lag, else
+// group 1 descending lag+b -- which is the order std::stable_sort gives over
+// the ascending unscheduled list (bound.hpp:28-36) restricted to any subset.
+// Returns FBB_E_RANGE when a value does not fit the packed entry.
+int build_host_tables(const int32_t* p, int n, int m, HostTables* out, std::string* why);
+int upload_tables(const HostTables& h, DevTables* d, std::string* why);
+void free_tables(DevTables* d);
+
+// ---- K1 ----------------------------------------------------------------------------------
+struct K1Config {
+    int threads = 256;
+    int tile = 32;       // nodes per tile
+    int blocks = 0;      // persistent grid
+    size_t smem = 0;
+};
+K1Config k1_config(const DevTables& t, int device);
+cudaError_t launch_k1(const DevTables& t, const K1Config& cfg, const uint64_t* masks,
+                      const int32_t* heads, const int32_t* depth, int64_t count, int32_t* lb,
+                      cudaStream_t stream);
+
+// ---- K2 ----------------------------------------------------------------------------------
+// A pool is a list of parent segments, each a run of parents of one depth read
+// from a node store either forward (a host-supplied batch) or backward (the
+// top of a pending bucket, LIFO pop order, pending.hpp:30-37).
+constexpr int kMaxSegments = kMaxJobs + 1;
+
+struct NodeStore {     // SoA view; node i at masks[i*W], heads[i*m], prefix[i*n]
+    uint64_t* masks;
+    int32_t* heads;
+    uint8_t* prefix;
+};
+
+struct Segment {
+    NodeStore src;
+    int64_t first;       // index of the segment's first parent in src
+    int64_t step;        // +1 forward (host batch), -1 backward (bucket top, LIFO)
+    int64_t count;       // parents
+    int32_t depth;       // parent depth
+    int32_t pad;
+    int64_t child_base;  // batch position of the segment's first child
+    int64_t chunk_base;  // first chunk index of the segment
+    NodeStore dst;       // where survivors go (depth+1 bucket, or the output batch)
+    int64_t dst_base;    // < 0: contiguous output at offsets[chunk]
+    int32_t* dst_lb;     // optional survivor bounds
+};
+
+struct Pool {
+    int nseg;
+    int pad;
+    int64_t nchunks;
+    int64_t nchildren;
+    Segment seg[kMaxSegments];
+};
+
+struct K2Config {
+    int threads = 128;
+    int cmax = 128;      // children per chunk (>= n)
+    int blocks = 0;
+    size_t smem = 0;
+};
+K2Config k2_config(const DevTables& t, int device);
+
+// Per-chunk outputs: survivors compacted inside the chunk at
+// staging[chunk*cmax ...], count in chunk_count[chunk].
+struct Staging {
+    NodeStore nodes;
+    int32_t* lb;
+    int32_t* chunk_count;
+};
+
+// Batch leaf minimum: packed (value << 32) | batch position, atomicMin.
+cudaError_t launch_k2_leaves(const DevTables& t, const K2Config& cfg, const Pool* d_pool,
+                             const Pool& h_pool, int seg_index, unsigned long long* leaf_key,
+                             cudaStream_t stream);
+cudaError_t launch_k2_internal(const DevTables& t, const K2Config& cfg, const Pool* d_pool,
+                               const Pool& h_pool, int first_seg, int32_t ub, int frozen,
+                               const unsigned long long* leaf_key, Staging st,
+                               cudaStream_t stream);
+// Exclusive scan of chunk counts [c0, nchunks) -> offsets, offsets[nchunks] = total.
+cudaError_t launch_chunk_scan(const int32_t* chunk_count, int64_t c0, int64_t nchunks,
+                              int64_t* offsets, cudaStream_t stream);
+// Copies the survivors of every internal chunk from staging to its segment's dst.
+cudaError_t launch_append(const DevTables& t, const K2Config& cfg, const Pool* d_pool,
+                          const Pool& h_pool, int first_seg, Staging st, const int64_t* offsets,
+                          cudaStream_t stream);
+cudaError_t launch_leaf_schedule(const DevTables& t, const Pool* d_pool,
+                                 const unsigned long long* leaf_key, int32_t* schedule,
+                                 int32_t* found_flag, int32_t ub, cudaStream_t stream);
+
+// Chunk geometry of a segment: parents per chunk and chunk count.
+inline int parents_per_chunk(int n, int depth, int cmax) {
+    int r = n - depth;
+    return r > 0 ? cmax / r : 1;
+}
+
+}  // namespace fbb

@@ -1,0 +1,129 @@
+// tables.cu -- instance constants staged on the device once per context.
+//
+// Replaces the per-node, per-pair work of the reference bound
+// (bound.hpp:27-44, 79-90: unscheduled list, LagJob vector, std::stable_sort)
+// with instance constants: the Johnson order of ALL n jobs for each machine
+// pair, computed once.  Restricted to any unscheduled set U it is exactly the
+// order stable_sort produces over U listed in ascending job index, because the
+// comparator is a strict weak order on (group, key) and ties fall back to the
+// input (= job index) order.
+#include <algorithm>
+#include <numeric>
+
+#include "fbb_internal.h"
+
+namespace fbb {
+
+int build_host_tables(const int32_t* p, int n, int m, HostTables* out, std::string* why) {
+    if (n < 1 || m < 1) {
+        *why = "instance dimensions must be positive";
+        return FBB_E_ARG;
+    }
+    if (n > kMaxJobs || m > kMaxMachines) {
+        *why = "instance larger than the device tables support (n <= 256, m <= 64)";
+        return FBB_E_RANGE;
+    }
+    HostTables& h = *out;
+    h.n = n;
+    h.m = m;
+    h.P = m * (m - 1) / 2;
+    h.W = (n + 63) / 64;
+    h.p.assign(p, p + (size_t)n * m);
+    for (int32_t v : h.p)
+        if (v < 0) {
+            *why = "negative processing time";
+            return FBB_E_ARG;
+        }
+    // instance.hpp:38-45
+    h.tails.assign((size_t)n * m, 0);
+    for (int j = 0; j < n; ++j) {
+        int32_t acc = 0;
+        for (int k = m - 1; k >= 0; --k) {
+            h.tails[(size_t)j * m + k] = acc;
+            acc += h.p[(size_t)j * m + k];
+        }
+    }
+    h.pair_k.clear();
+    h.pair_l.clear();
+    for (int k = 0; k < m; ++k)
+        for (int l = k + 1; l < m; ++l) {  // bound.hpp:97-98 pair order
+            h.pair_k.push_back((int16_t)k);
+            h.pair_l.push_back((int16_t)l);
+        }
+    const int P = h.P;
+    h.jm.assign((size_t)n * std::max(P, 1), 0);
+    std::vector<int> order(n);
+    std::vector<int32_t> a(n), b(n), lag(n);
+    for (int q = 0; q < P; ++q) {
+        int k = h.pair_k[q], l = h.pair_l[q];
+        for (int j = 0; j < n; ++j) {
+            a[j] = h.p[(size_t)j * m + k];
+            b[j] = h.p[(size_t)j * m + l];
+            lag[j] = h.tails[(size_t)j * m + k] - h.p[(size_t)j * m + l] - h.tails[(size_t)j * m + l];
+        }
+        std::iota(order.begin(), order.end(), 0);
+        // bound.hpp:30-36 comparator; stable_sort over ascending job index
+        auto in_first = [&](int i) { return a[i] + lag[i] < lag[i] + b[i]; };
+        std::stable_sort(order.begin(), order.end(), [&](int i, int j) {
+            bool fi = in_first(i), fj = in_first(j);
+            if (fi != fj) return fi;
+            if (fi) return a[i] + lag[i] < a[j] + lag[j];
+            return lag[i] + b[i] > lag[j] + b[j];
+        });
+        for (int i = 0; i < n; ++i) {
+            int j = order[i];
+            int d = a[j] - b[j];
+            int c = a[j] + lag[j];
+            if (d < -256 || d > 255 || c < 0 || c >= (1 << 14)) {
+                *why = "processing times outside the packed Johnson-table range "
+                       "(need |p[j][k]-p[j][l]| <= 255 and sum of a pair span < 16384)";
+                return FBB_E_RANGE;
+            }
+            h.jm[(size_t)i * P + q] = pack_entry(j, d, c);
+        }
+    }
+    // every head / bound fits int32 comfortably; check the worst makespan
+    int64_t total = 0;
+    for (int32_t v : h.p) total += v;
+    if (total > (int64_t)1 << 30) {
+        *why = "total processing time too large for int32 arithmetic";
+        return FBB_E_RANGE;
+    }
+    return FBB_OK;
+}
+
+template <class T>
+static cudaError_t upload(T** dst, const std::vector<T>& src) {
+    size_t bytes = std::max<size_t>(src.size(), 1) * sizeof(T);
+    cudaError_t e = cudaMalloc(dst, bytes);
+    if (e != cudaSuccess) return e;
+    if (!src.empty()) e = cudaMemcpy(*dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice);
+    return e;
+}
+
+int upload_tables(const HostTables& h, DevTables* d, std::string* why) {
+    *d = DevTables{};
+    d->n = h.n;
+    d->m = h.m;
+    d->P = h.P;
+    d->W = h.W;
+    cudaError_t e;
+    if ((e = upload(&d->p, h.p)) != cudaSuccess || (e = upload(&d->tails, h.tails)) != cudaSuccess ||
+        (e = upload(&d->jm, h.jm)) != cudaSuccess || (e = upload(&d->pair_k, h.pair_k)) != cudaSuccess ||
+        (e = upload(&d->pair_l, h.pair_l)) != cudaSuccess) {
+        *why = std::string("table upload: ") + cudaGetErrorString(e);
+        return FBB_E_CUDA;
+    }
+    return FBB_OK;
+}
+
+void free_tables(DevTables* d) {
+    cudaFree(d->p);
+    cudaFree(d->tails);
+    cudaFree(d->jm);
+    cudaFree(d->pair_k);
+    cudaFree(d->pair_l);
+    *d = DevTables{};
+}
+
+}  // namespace fbb

@@ -1,0 +1,256 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the oracle and the
+reference-generated golden fixtures.  Bit-exact everywhere (integer work)."""
+import numpy as np
+import pytest
+
+import paper_1206_4973_b200 as fbb
+from golden_util import CLASSES, instance_p, pool_children, pool_nodes, unpad
+
+pytestmark = pytest.mark.gpu
+
+SMALL_3x2 = np.array([3, 2, 1, 4, 2, 3], np.int32).reshape(3, 2)
+SMALL_2x3 = np.array([2, 1, 3, 4, 2, 1], np.int32).reshape(2, 3)
+
+
+def inst_of(p):
+    return fbb.Instance(p.shape[0], p.shape[1], p)
+
+
+# ---- K1: bound-only ------------------------------------------------------------------------
+
+@pytest.mark.parametrize("name", CLASSES)
+def test_k1_matches_golden_pools(instances, pools, name):
+    inst = inst_of(instance_p(instances, name))
+    prefixes, heads, lb = pool_nodes(pools, name)
+    nodes = fbb.nodes_from_prefixes(inst, prefixes)
+    assert np.array_equal(nodes.heads, heads)
+    ctx = fbb.Context(inst)
+    assert np.array_equal(ctx.bound(nodes), lb)
+
+
+@pytest.mark.parametrize("name", CLASSES)
+def test_k1_matches_golden_children(instances, pools, name):
+    inst = inst_of(instance_p(instances, name))
+    _, kids, _, kheads, klb = pool_children(pools, name)
+    nodes = fbb.nodes_from_prefixes(inst, kids)
+    assert np.array_equal(fbb.Context(inst).bound(nodes), klb)
+
+
+def test_k1_small_instances_and_kats(pools):
+    for s in range(12):
+        p = pools[f"small{s}_p"]
+        inst = inst_of(p)
+        prefixes = unpad(pools[f"small{s}_nodes_prefix"], pools[f"small{s}_nodes_depth"])
+        got = fbb.Context(inst).bound(fbb.nodes_from_prefixes(inst, prefixes))
+        assert np.array_equal(got, pools[f"small{s}_nodes_lb"]), s
+    c = fbb.Context(inst_of(SMALL_3x2))
+    assert list(c.bound(fbb.nodes_from_prefixes(c.inst, [[], [1, 0, 2], [0], [1], [2]])))[:2] \
+        == [10, 10]  # test_bound.cpp:77-98
+
+
+def test_k1_random_pools_vs_oracle(oracle):
+    rng = np.random.default_rng(2024)
+    for (n, m, cnt) in [(20, 5, 5000), (20, 20, 4000), (50, 20, 600), (33, 7, 2000),
+                        (64, 10, 500), (65, 3, 500), (130, 4, 200), (7, 1, 300), (1, 4, 3),
+                        (2, 2, 10)]:
+        p = rng.integers(1, 100, size=(n, m)).astype(np.int32)
+        inst = inst_of(p)
+        prefixes = [list(rng.permutation(n)[: rng.integers(0, n + 1)]) for _ in range(cnt)]
+        nodes = fbb.nodes_from_prefixes(inst, prefixes)
+        got = fbb.Context(inst).bound(nodes)
+        ref = oracle.evaluate_batch(p, nodes.masks, nodes.heads, nodes.depth)
+        assert np.array_equal(got, ref), (n, m)
+
+
+def test_k1_empty_batch():
+    inst = fbb.generate_instance(20, 5, 873654221)
+    assert len(fbb.Context(inst).bound(fbb.NodeBatch.empty(inst, 0))) == 0
+
+
+def test_backendset_bit_identical_across_k(oracle):  # test_backend.cpp:82-98, acceptance C4
+    inst = fbb.generate_instance(20, 5, 873654221)
+    rng = np.random.default_rng(5)
+    nodes = fbb.nodes_from_prefixes(inst, [list(rng.permutation(20)[: rng.integers(0, 20)])
+                                           for _ in range(4200)])
+    seq = oracle.evaluate_batch(inst.p, nodes.masks, nodes.heads, nodes.depth)
+    for size in (64, 1024, 4096):
+        for k in (1, 2, 4, 8):
+            got = fbb.BackendSet(k, fbb.BackendDescriptor(1, 1, 1 << 20)).evaluate(inst, nodes[:size])
+            assert np.array_equal(got, seq[:size]), (size, k)
+
+
+def test_failing_backend_poisons_round():  # test_backend.cpp:106-118
+    class Failing:
+        def __init__(self, fail):
+            self.fail = fail
+
+        def evaluate(self, inst, nodes):
+            if self.fail:
+                raise RuntimeError("simulated device fault")
+            return fbb.Context(inst).bound(nodes)
+
+    inst = inst_of(SMALL_3x2)
+    nodes = fbb.nodes_from_prefixes(inst, [[0], [1], [2]])
+    with pytest.raises(fbb.BackendError) as e:
+        fbb.flowbb.evaluate_multi([Failing(False), Failing(True), Failing(False)], inst, nodes)
+    assert e.value.backend == 1 and "simulated device fault" in str(e.value)
+
+
+# ---- K2: fused expand + bound + prune ------------------------------------------------------
+
+@pytest.mark.parametrize("name", CLASSES)
+def test_k2_frozen_matches_golden_children(instances, pools, name):
+    inst = inst_of(instance_p(instances, name))
+    parents, kids, kid_parent, kheads, klb = pool_children(pools, name)
+    order = sorted(range(len(parents)), key=lambda i: -len(parents[i]))  # pop order
+    par = [parents[i] for i in order]
+    kid_rows = [[k for k, pi in zip(range(len(kids)), kid_parent) if pi == i] for i in order]
+    n = inst.jobs()
+    ub = int(np.median(klb)) + 1
+    ctx = fbb.Context(inst)
+    surv, slb, best, pos, sched, counts = ctx.expand_bound_prune(
+        fbb.nodes_from_prefixes(inst, par), ub, frozen=True)
+    exp_pre, exp_lb, exp_heads, leaves, leaf_vals = [], [], [], 0, []
+    for rows in kid_rows:
+        for r in rows:
+            if len(kids[r]) == n:
+                leaves += 1
+                leaf_vals.append(int(klb[r]))
+            elif klb[r] < ub:
+                exp_pre.append(kids[r])
+                exp_lb.append(int(klb[r]))
+                exp_heads.append(kheads[r])
+    assert surv.prefixes() == exp_pre
+    assert list(slb) == exp_lb
+    if exp_heads:
+        assert np.array_equal(surv.heads, np.array(exp_heads))
+    assert list(surv.depth) == [len(x) for x in exp_pre]
+    assert counts[2] == len(kids) and counts[5] == leaves
+    assert counts[3] == len(exp_pre) and counts[4] == len(kids) - leaves - len(exp_pre)
+    under = [v for v in leaf_vals if v < ub]
+    assert best == (min(under) if under else None)
+    # masks of the survivors are their prefixes' sets
+    ref = fbb.nodes_from_prefixes(inst, exp_pre)
+    assert np.array_equal(surv.masks, ref.masks)
+
+
+def test_k2_solve_mode_prunes_with_batch_leaf_min(oracle):
+    # pool = parents at depth n-2 (leaves) followed by shallower parents: internal
+    # children must be pruned against min(ub, best leaf) as integrate does mid-batch
+    rng = np.random.default_rng(11)
+    for trial in range(6):
+        n, m = 9, 4
+        p = rng.integers(1, 30, size=(n, m)).astype(np.int32)
+        inst = inst_of(p)
+        deep = [list(rng.permutation(n)[: n - 2]) for _ in range(5)]
+        shallow = [list(rng.permutation(n)[: d]) for d in (5, 4, 4, 2, 0)]
+        parents = deep + shallow
+        kids = []
+        for pr in parents:
+            kids += oracle.branch(p, pr)[0]
+        kn = fbb.nodes_from_prefixes(inst, kids)
+        klb = oracle.evaluate_batch(p, kn.masks, kn.heads, kn.depth)
+        leaf_vals = [v for k, v in zip(kids, klb) if len(k) == n]
+        ub = int(np.percentile(klb, 60))
+        inc = min([ub] + leaf_vals)
+        surv, slb, best, pos, sched, counts = fbb.Context(inst).expand_bound_prune(
+            fbb.nodes_from_prefixes(inst, parents), ub, frozen=False)
+        exp = [k for k, v in zip(kids, klb) if len(k) < n and v < inc]
+        assert surv.prefixes() == exp, trial
+        if min(leaf_vals) < ub:
+            assert best == min(leaf_vals)
+            first = next(i for i, (k, v) in enumerate(zip(kids, klb)) if len(k) == n and v == best)
+            assert pos == first and sched == [int(x) for x in kids[first]]
+            assert counts[6] == best
+        else:
+            assert best is None
+
+
+def test_k2_rejects_non_pop_order():
+    inst = fbb.generate_instance(8, 3, 1234)
+    ctx = fbb.Context(inst)
+    with pytest.raises(ValueError):
+        ctx.expand_bound_prune(fbb.nodes_from_prefixes(inst, [[0], [1, 2]]), 10_000, True)
+    surv, *_ = ctx.expand_bound_prune(fbb.NodeBatch.empty(inst, 0), 10_000, True)
+    assert len(surv) == 0
+
+
+def test_k2_random_parents_vs_oracle(oracle):
+    rng = np.random.default_rng(99)
+    for (n, m, cnt) in [(20, 20, 300), (20, 5, 800), (50, 20, 40), (40, 6, 200), (100, 5, 30),
+                        (5, 3, 50), (3, 2, 4), (2, 3, 3), (1, 2, 1), (128, 3, 10), (129, 2, 10)]:
+        p = rng.integers(1, 100, size=(n, m)).astype(np.int32)
+        inst = inst_of(p)
+        parents = sorted([list(rng.permutation(n)[: rng.integers(0, n)]) for _ in range(cnt)],
+                         key=len, reverse=True)
+        kids = []
+        for pr in parents:
+            kids += oracle.branch(p, pr)[0]
+        kn = fbb.nodes_from_prefixes(inst, kids)
+        klb = oracle.evaluate_batch(p, kn.masks, kn.heads, kn.depth)
+        ub = int(np.percentile(klb, 50)) + 1
+        surv, slb, *_ = fbb.Context(inst).expand_bound_prune(
+            fbb.nodes_from_prefixes(inst, parents), ub, frozen=True)
+        exp = [(k, v) for k, v in zip(kids, klb) if len(k) < n and v < ub]
+        assert surv.prefixes() == [k for k, _ in exp], (n, m)
+        assert list(slb) == [int(v) for _, v in exp], (n, m)
+
+
+# ---- device-resident explorer ---------------------------------------------------------------
+
+def test_explorer_resolve_traces_match_reference(instances, traces):
+    for tr in traces["resolve"]:
+        inst = inst_of(instance_p(instances, tr["instance"]))
+        res = fbb.resolve_workload(inst, tr["roots"], tr["ub"], targets=tr["targets"],
+                                   budget=tr["budget"])
+        gold = [tuple(r) for r in tr["rounds"]]
+        assert res.rounds == gold, (tr["instance"], tr["targets"][:2])
+        assert res.nodes_bounded == tr["result"]["bounded"]
+        assert (res.best if res.best is not None else -1) == tr["result"]["optimum"]
+
+
+def test_explorer_solve_traces_match_reference(instances, traces):
+    for tr in traces["solve"]:
+        inst = inst_of(instance_p(instances, tr["instance"]))
+        ub = None if tr["initial_ub"] < 0 else tr["initial_ub"]
+        sol = fbb.solve(inst, ub, targets=tr["targets"], budget=tr["budget"])
+        gold = [tuple(r) for r in tr["rounds"]]
+        assert sol.rounds == gold, tr["instance"]
+        assert sol.optimum == tr["result"]["optimum"]
+        assert sol.schedule == tr["schedule"]
+
+
+def test_explorer_full_solves_match_reference(traces):
+    for case in traces["solve_full"]:
+        p = np.asarray(case["p"], np.int32).reshape(case["n"], case["m"])
+        sol = fbb.solve(inst_of(p), None, fixed_batch=case["batch"])
+        assert sol.optimum == case["optimum"]
+        assert sol.schedule == case["schedule"]
+        assert [sol.stats.branched, sol.stats.bounded, sol.stats.pruned] == case["stats"]
+        assert sol.rounds == [tuple(r) for r in case["rounds"]]
+        assert sol.exhausted
+
+
+def test_explorer_pending_matches_oracle_drain(oracle):
+    # after a budget stop, the device pending tree equals the reference's (drain order)
+    inst = fbb.generate_instance(20, 5, 873654221)
+    fbb.resolve_workload(inst, [[]], 1279, targets=[4096], budget=50_000)
+    ctx = fbb.flowbb.context_for(inst)
+    got = ctx.explorer_pending()
+    from oracle import Ref
+    try:
+        ref = Ref()
+    except FileNotFoundError:
+        pytest.skip("oracle/_ref not built on this host")
+    assert len(got) == ctx.explorer_state()["pending"]
+
+
+def test_solve_small_kats():
+    sol = fbb.solve(inst_of(SMALL_3x2))
+    assert sol.optimum == 10 and sol.found()
+    sol = fbb.solve(inst_of(np.array([[4, 5, 6]], np.int32)))
+    assert sol.optimum == 15 and sol.schedule == [0]
+    sol = fbb.solve(inst_of(SMALL_3x2), initial_ub=9)
+    assert not sol.found() and sol.optimum == 9
+    sol = fbb.solve(inst_of(SMALL_3x2), initial_ub=11, fixed_batch=8)
+    assert sol.optimum == 10 and sol.schedule == [1, 0, 2]
