@@ -1,0 +1,352 @@
+"""bench.py -- bounded subproblems/s of the B200 explorer on Taillard Ta021 (20x20),
+frozen optimal UB 2297 (BASELINE.json configs[1]).
+
+A step is one explorer round: select the pool (fill_buffer) at the target size,
+expand + bound + prune + compact every child on the GPU (K2), push the survivors.
+  value   device-resident explorer (pending tree in HBM), rounds timed with CUDA
+          events inside the library; L2 flushed (256 MiB write) between rounds.
+  e2e     same rounds through the reference-facing C-ABI with HOST buffers: host
+          pending tree, parents H2D, K2, survivors D2H, host push; wall clock.
+  --impl reference: the reference CPU explorer (oracle/_ref: the reference headers
+          compiled in place; BackendSet over all host cores) on the same rounds.
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--target T] [--impl ours|reference]
+Multi-GPU (torchrun): each rank explores its own contiguous slice of the frontier
+(split_slices, backend.hpp:73-84); frozen UB means no data-path collective
+(scaling "weak"); the max over ranks of the device time is reported.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+INSTANCES = {"ta021": (20, 20, 479340445, 2297), "ta022": (20, 20, 268827376, 2099),
+             "ta051": (50, 20, 1539989115, 3847), "ta081": (100, 20, 450926852, 6202),
+             "ta001": (20, 5, 873654221, 1279)}
+METRIC = "bounded subproblems/sec & explore time, Taillard 20x20/50x20, 1/2/4/8 B200"
+INT32_LANES_PER_SM = 128  # ALU pipe 64 + FMA pipe 64 integer lanes / clk / SM (B300_MICROARCH)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--target", type=int, default=262144)
+    ap.add_argument("--instance", default="ta021")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=1_000_000,
+                    help="bounded-node budget of the CPU baseline sample")
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def sample_clocks_start():
+    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+    try:
+        f = open(os.path.join(ROOT, "gpurun_out", f"clocks_{os.getpid()}.csv"), "w")
+        p = subprocess.Popen(
+            ["nvidia-smi", "--query-gpu=index,clocks.sm,clocks.max.sm,power.draw,"
+             "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "100"],
+            stdout=f, stderr=subprocess.DEVNULL)
+        return p, f
+    except Exception:
+        return None, None
+
+
+def sample_clocks_stop(handle, device):
+    p, f = handle
+    if p is None:
+        return None
+    p.terminate()
+    p.wait()
+    f.close()
+    sm, mx, reasons = [], 0, set()
+    names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+    for line in open(f.name):
+        parts = [x.strip() for x in line.split(",")]
+        if len(parts) < 9 or parts[0] != str(device):
+            continue
+        try:
+            sm.append(float(parts[1]))
+            mx = max(mx, float(parts[2]))
+        except ValueError:
+            continue
+        for nm, v in zip(names, parts[5:9]):
+            if v.lower() in ("active", "1", "yes"):
+                reasons.add(nm)
+    if not sm:
+        return None
+    return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+            "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+def reference_arm(args, inst_name):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import REF_SO, Oracle, Ref
+
+    n, m, seed, ub = INSTANCES[inst_name]
+    cfg = {"workload": f"{inst_name} {n}x{m} frozen UB {ub}, root pushed, pool target "
+                       f"{args.target}, step = one explorer round",
+           "instance": inst_name, "pool_target": args.target, "ub": ub,
+           "parallelism": "host threads"}
+    if os.path.exists(REF_SO):
+        ref = Ref()
+        cores = ref.detect_units()
+        p = ref.generate_instance(n, m, seed)
+        pre, rounds, secs = ref.bench_rounds(p, ub, args.target, args.warmup, args.steps, cores)
+        kind = "reference"
+    else:  # the C restatement, single thread (reference not compiled on this host)
+        orc = Oracle()
+        p = orc.generate_instance(n, m, seed)
+        t0 = time.perf_counter()
+        res, rounds = orc.resolve(p, ub, [[]], targets=[args.target],
+                                  budget=args.cpu_sample, max_trace=1 << 16)
+        secs = [time.perf_counter() - t0]
+        rounds = [tuple(r) for r in rounds]
+        cores, kind, pre = 1, "port", 0
+    bounded = sum(r[2] for r in rounds)
+    total = sum(secs)
+    value = bounded / total if total > 0 else 0.0
+    line = {"metric": METRIC, "value": value, "unit": "bounded subproblems/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / max(1, len(secs)),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic (Taillard generator, published seed)", "config": cfg,
+            "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": "bounded subproblems/s", "cores": cores,
+                             "kind": kind,
+                             "sample": f"{len(secs)} rounds after {pre} prefill + {args.warmup} "
+                                       f"warm-up rounds, {bounded} bounded nodes"},
+            "e2e": {"value": value, "unit": "bounded subproblems/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "rounds": [list(r) for r in rounds]}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(inst_name, target, sample_nodes):
+    """The reference CPU explorer (oracle/_ref) on a bounded sample of the same workload."""
+    from oracle import REF_SO, Oracle, Ref
+
+    n, m, seed, ub = INSTANCES[inst_name]
+    if os.path.exists(REF_SO):
+        ref = Ref()
+        cores = ref.detect_units()
+        p = ref.generate_instance(n, m, seed)
+        res, rounds, secs = ref.resolve(p, ub, [[]], targets=[target], budget=sample_nodes,
+                                        backends=cores, max_trace=1)
+        kind = "reference"
+    else:
+        orc = Oracle()
+        p = orc.generate_instance(n, m, seed)
+        t0 = time.perf_counter()
+        res, _ = orc.resolve(p, ub, [[]], targets=[target], budget=sample_nodes // 20)
+        secs = time.perf_counter() - t0
+        cores, kind = 1, "port"
+    return {"value": res["bounded"] / secs, "unit": "bounded subproblems/s", "cores": cores,
+            "kind": kind, "sample": f"resolve from the root, target {target}, first "
+                                    f"{res['bounded']} bounded nodes ({res['rounds']} rounds, "
+                                    f"{secs:.1f} s)"}
+
+
+def main():
+    args = parse()
+    inst_name = args.instance
+    if args.impl == "reference":
+        reference_arm(args, inst_name)
+        return
+    rank, world, local = dist_env()
+    import torch
+
+    dev = local if world > 1 else 0
+    torch.cuda.set_device(dev)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+    import paper_1206_4973_b200 as fbb
+    from paper_1206_4973_b200.host_explorer import HostExplorer
+
+    n, m, seed, ub = INSTANCES[inst_name]
+    inst = fbb.generate_instance(n, m, seed)
+    ctx = fbb.Context(inst, dev)
+    T = args.target
+    P = m * (m - 1) // 2
+
+    # ---- prefill: rounds from the root until one reaches the pool target ------------------
+    ctx.explorer_reset(fbb.NodeBatch.root(inst), ub, frozen=True)
+    prefill = []
+    while len(prefill) < 64:
+        r = ctx.explorer_run([T], 1)
+        if not r:
+            break
+        prefill.append(r[0])
+        if r[0][2] >= T:
+            break
+    frontier = ctx.explorer_pending()
+    if world > 1:  # each rank keeps its contiguous slice (split_slices, backend.hpp:73-84)
+        off, ln = fbb.split_slices(len(frontier), world)[rank]
+        mine = frontier[off:off + ln]
+        ctx.explorer_reset(fbb.nodes_from_prefixes(inst, mine), ub, frozen=True)
+        frontier = mine
+        while True:  # regrow to full pools on this rank's subtree
+            r = ctx.explorer_run([T], 1)
+            if not r or r[0][2] >= T:
+                break
+        frontier = ctx.explorer_pending()
+    snapshot = fbb.nodes_from_prefixes(inst, frontier)
+
+    # ---- device-resident explorer: W warm-up rounds, K timed rounds -------------------------
+    for _ in range(args.warmup):
+        ctx.explorer_run([T], 1)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{dev}")
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clocks_h = sample_clocks_start() if rank == 0 else (None, None)
+    rounds, timing = [], []
+    wall0 = time.perf_counter()
+    for _ in range(args.steps):
+        flush.fill_(rank + len(rounds) % 7)  # L2 flush (> 126 MB) between timed rounds
+        torch.cuda.synchronize()
+        r, t = ctx.explorer_run([T], 1, timing=True)
+        if not r:
+            break
+        rounds += r
+        timing += t
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - wall0
+    clocks = sample_clocks_stop(clocks_h, dev) if rank == 0 else None
+    dev_ms = sum(t["round_ms"] for t in timing)
+    k2_ms = sum(t["k2_ms"] for t in timing)
+    bounded = sum(r[2] for r in rounds)
+    branched = sum(r[1] for r in rounds)
+    leaves = sum(r[5] for r in rounds)
+    survivors = sum(r[3] for r in rounds)
+    launches = sum(t["launches"] for t in timing)
+    stats = torch.tensor([dev_ms, k2_ms, wall, bounded, branched, leaves, survivors, launches,
+                          len(rounds)], dtype=torch.float64, device=f"cuda:{dev}")
+    if world > 1:
+        import torch.distributed as dist
+
+        mx = stats.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = stats.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        dev_ms_max, wall_max = float(mx[0]), float(mx[2])
+        bounded_all, launches_all = float(sm[3]), float(sm[7])
+    else:
+        dev_ms_max, wall_max, bounded_all, launches_all = dev_ms, wall, bounded, launches
+
+    # ---- e2e: same rounds, host pending tree + host buffers through the C-ABI ----------------
+    e2e = None
+    if not args.no_e2e:
+        hx = HostExplorer(ctx, max_pool=T)
+        hx.reset(snapshot, ub, frozen=True)
+        for _ in range(args.warmup):
+            hx.round(T)
+        e_rounds, e_secs, h2d, d2h = [], 0.0, 0, 0
+        for _ in range(args.steps):
+            out = hx.round(T)
+            if out is None:
+                break
+            tup, s, hb, db = out
+            e_rounds.append(tup)
+            e_secs += s
+            h2d += hb
+            d2h += db
+        stepsd = max(1, len(e_rounds))
+        e2e = {"value": sum(r[2] for r in e_rounds) / e_secs * (world if world > 1 else 1)
+               if e_secs > 0 else 0.0,
+               "unit": "bounded subproblems/s", "h2d_bytes_per_step": h2d // stepsd,
+               "d2h_bytes_per_step": d2h // stepsd,
+               "rounds_match_device_explorer": [tuple(r) for r in e_rounds] == [
+                   tuple(r) for r in rounds[: len(e_rounds)]],
+               "timing": "wall clock per round (host selection + H2D + K2 + D2H + host push)"}
+
+    if rank != 0:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return
+    peaks = measured_peaks()
+    hbm_peak = peaks.get("hbm_gbs", 6528.7)
+    clock_mhz = (clocks or {}).get("sm_max_mhz") or peaks.get("sm_max_mhz", 1965.0)
+    int_peak = 148 * INT32_LANES_PER_SM * clock_mhz * 1e6 / 1e9  # Gop/s
+    internal = bounded - leaves
+    # algorithmic int32 ops: per parent scan P*n, per child P*15 + 6m
+    ops = P * (n * max(0, branched - leaves // 2) + 15 * internal) + 6 * m * bounded
+    node_b = ((n + 63) // 64) * 8 + m * 4 + n
+    alg_bytes = (branched * node_b) + survivors * (2 * node_b + 4)  # parents in, survivors staged+pushed
+    k2_s = k2_ms / 1e3
+    roofline = {
+        "bound": "int32-alu", "kernel": "k2_internal_kernel (fused expand+bound+prune)",
+        "achieved": ops / k2_s / 1e9 if k2_s > 0 else 0.0, "peak": int_peak, "unit": "Gop/s",
+        "frac": (ops / k2_s / 1e9) / int_peak if k2_s > 0 else 0.0, "traffic": None,
+        "ops_per_child": ops / max(1, bounded),
+        "peak_note": "148 SMs x 128 int32 lanes/clk (alu+fma pipes) x max SM clock; derived, "
+                     "not measured (MEASURED_PEAKS has no integer figure)",
+        "hbm": {"achieved": alg_bytes / k2_s / 1e9 if k2_s > 0 else 0.0, "peak": hbm_peak,
+                "unit": "GB/s", "frac": (alg_bytes / k2_s / 1e9) / hbm_peak if k2_s > 0 else 0.0},
+        "k2_share_of_round": k2_ms / dev_ms if dev_ms > 0 else 0.0,
+    }
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        try:
+            cpu = cpu_baseline(inst_name, T, args.cpu_sample)
+        except Exception as e:  # noqa: BLE001
+            cpu = {"value": None, "error": str(e)}
+    steps_done = len(rounds)
+    line = {
+        "metric": METRIC,
+        "value": bounded_all / (dev_ms_max / 1e3) if dev_ms_max > 0 else 0.0,
+        "unit": "bounded subproblems/s",
+        "n_gpus": world, "steps": steps_done, "warmup": args.warmup,
+        "ms_per_step": dev_ms_max / max(1, steps_done),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic (Taillard generator, published seed; no dataset)",
+        "config": {"workload": f"{inst_name} {n}x{m} frozen UB {ub}, root pushed, prefill to a "
+                               f"full pool, then rounds at pool target {T}; step = one explorer "
+                               f"round (select + K2 expand/bound/prune/compact + push)",
+                   "instance": inst_name, "pool_target": T, "ub": ub,
+                   "parallelism": f"dp{world} (frontier slices)",
+                   "l2": "flushed between timed rounds (256 MiB write)"},
+        "wall_value": bounded_all / wall_max if wall_max > 0 else 0.0,
+        "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,
+        "gpu_launches": int(launches_all),
+        "rounds": [list(r) for r in rounds],
+        "prefill_rounds": len(prefill),
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

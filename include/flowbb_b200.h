@@ -68,8 +68,10 @@ typedef struct {
     int64_t pruned;    /* internal children eliminated (lb >= incumbent) */
     int64_t leaves;    /* complete children */
     int32_t incumbent; /* incumbent after the round (frozen: best leaf < UB, else UB) */
-    int32_t pad;
+    float k2_ms;       /* device time of the internal-children K2 launch (CUDA events) */
     int64_t pending;   /* pending nodes after the round */
+    float round_ms;    /* device time of the round, pool upload .. summary download */
+    int32_t launches;  /* kernels this library launched for the round */
 } fbb_round_t;
 
 /* ---- context ----------------------------------------------------------------------------

@@ -292,6 +292,27 @@ class Ref:
                                 C.POINTER(C.c_int32), C.POINTER(C.c_int32), _i32p, _i64p]
         L.ref_brute_force.argtypes = [C.c_int, C.c_int, _i32p, C.POINTER(C.c_int32), _i32p]
         L.ref_detect_units.restype = C.c_int
+        L.ref_bench_rounds.argtypes = [C.c_int, C.c_int, _i32p, C.c_int32, C.c_int64, C.c_int,
+                                       C.c_int, C.c_int, C.POINTER(C.c_int64), C.c_void_p,
+                                       np.ctypeslib.ndpointer(dtype=np.float64,
+                                                              flags="C_CONTIGUOUS")]
+
+    def bench_rounds(self, p, ub, target, warm, steps, backends):
+        """Prefill-until-full, `warm` untimed rounds, `steps` timed rounds of the reference
+        resolve loop; returns (prefill_rounds, [round tuples], [seconds])."""
+        n, m = p.shape
+        pre = C.c_int64(0)
+        trace = (Round * max(steps, 1))()
+        secs = np.zeros(max(steps, 1), np.float64)
+        rc = self.lib.ref_bench_rounds(n, m, np.ascontiguousarray(p, np.int32).ravel(), ub, target,
+                                       warm, steps, backends, C.byref(pre),
+                                       C.cast(trace, C.c_void_p), secs)
+        if rc != 0:
+            raise RuntimeError("ref_bench_rounds failed")
+        return pre.value, [trace[i].as_tuple() for i in range(steps)], list(secs[:steps])
+
+    def detect_units(self):
+        return int(self.lib.ref_detect_units())
 
     def generate_instance(self, n, m, seed):
         p = np.zeros(n * m, np.int32)

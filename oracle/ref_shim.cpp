@@ -297,4 +297,69 @@ int ref_brute_force(int n, int m, const int32_t* p, int32_t* optimum, int32_t* s
 
 int ref_detect_units() { return detect_units(); }
 
+// The bench.py reference arm: the resolve_workload loop (bench.hpp:88-109,
+// reference fill_buffer + BackendSet(k).evaluate + frozen prune) from the root,
+//   prefill: rounds until one reaches the pool target (max 64 rounds),
+//   warm:    `warm` more rounds,
+//   timed:   `steps` rounds, each timed whole (selection, bounding, prune).
+// Per timed round the counts go to trace[0..steps) and the seconds to secs[].
+int ref_bench_rounds(int n, int m, const int32_t* p, int32_t ub, int64_t target, int warm,
+                     int steps, int backends, int64_t* prefill_rounds, orc_round* trace,
+                     double* secs) {
+    try {
+        Instance inst = make_instance(n, m, p);
+        BackendSet set(backends, wide_descriptor());
+        PendingTree pending(inst.jobs());
+        pending.push(Node::root(inst));
+        std::optional<int> best;
+        auto round = [&](orc_round* rec) -> bool {
+            if (pending.empty()) return false;
+            std::int64_t branched = 0;
+            std::vector<Node> batch =
+                fill_buffer(inst, pending, static_cast<std::size_t>(target), &branched);
+            std::vector<int> bounds = set.evaluate(inst, batch);
+            orc_round r{};
+            r.target = target;
+            r.branched = branched;
+            r.bounded = static_cast<int64_t>(batch.size());
+            for (std::size_t i = 0; i < batch.size(); ++i) {
+                Node& node = batch[i];
+                node.lb = bounds[i];
+                if (node.depth() == inst.jobs()) {
+                    ++r.leaves;
+                    if (node.lb < ub && (!best || node.lb < *best)) best = node.lb;
+                } else if (node.lb < ub) {
+                    ++r.inserted;
+                    pending.push(std::move(node));
+                } else {
+                    ++r.pruned;
+                }
+            }
+            r.incumbent = best ? *best : ub;
+            r.pending = static_cast<int64_t>(pending.size());
+            if (rec) *rec = r;
+            return true;
+        };
+        orc_round rec{};
+        int64_t pre = 0;
+        while (pre < 64 && round(&rec)) {
+            ++pre;
+            if (rec.bounded >= target) break;
+        }
+        *prefill_rounds = pre;
+        for (int i = 0; i < warm; ++i) round(nullptr);
+        for (int i = 0; i < steps; ++i) {
+            auto t0 = std::chrono::steady_clock::now();
+            orc_round r{};
+            bool ok = round(&r);
+            secs[i] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            trace[i] = r;
+            if (!ok) secs[i] = 0.0;
+        }
+        return 0;
+    } catch (const std::exception&) {
+        return -1;
+    }
+}
+
 }  // extern "C"

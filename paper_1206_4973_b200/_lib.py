@@ -50,9 +50,14 @@ class RoundRec(C.Structure):
         ("pruned", C.c_int64),
         ("leaves", C.c_int64),
         ("incumbent", C.c_int32),
-        ("pad", C.c_int32),
+        ("k2_ms", C.c_float),
         ("pending", C.c_int64),
+        ("round_ms", C.c_float),
+        ("launches", C.c_int32),
     ]
+
+    def timing(self):
+        return {"k2_ms": self.k2_ms, "round_ms": self.round_ms, "launches": self.launches}
 
     def as_tuple(self):
         return (self.target, self.branched, self.bounded, self.inserted, self.pruned,

@@ -120,6 +120,9 @@ struct fbb_ctx {
     DBuf staging_masks, staging_heads, staging_prefix, staging_lb, chunk_count, offsets;
     DBuf d_pool, d_leaf_key, d_summary;
     HBuf h_pool, h_summary;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    float last_k2_ms = 0.f, last_round_ms = 0.f;
+    int last_launches = 0;
 
     // explorer
     std::vector<Store> bucket;
@@ -221,6 +224,8 @@ int run_pool(fbb_ctx* ctx, Pool& pool, int first_internal, int32_t ub, int froze
 
     size_t pool_bytes = offsetof(Pool, seg) + (size_t)pool.nseg * sizeof(Segment);
     std::memcpy(ctx->h_pool.p, &pool, pool_bytes);
+    int launches = 0;
+    CK(cudaEventRecord(ctx->ev[0], st), "event");
     CK(cudaMemcpyAsync(ctx->d_pool.p, ctx->h_pool.p, pool_bytes, cudaMemcpyHostToDevice, st), "pool H2D");
     CK(cudaMemsetAsync(ctx->d_leaf_key.p, 0xFF, 8, st), "leaf key");
     const Pool* dp = ctx->d_pool.as<Pool>();
@@ -230,17 +235,27 @@ int run_pool(fbb_ctx* ctx, Pool& pool, int first_internal, int32_t ub, int froze
                           ctx->staging_prefix.as<uint8_t>()},
                 ctx->staging_lb.as<int32_t>(), ctx->chunk_count.as<int32_t>()};
     bool has_leaf = pool.nseg > 0 && pool.seg[0].depth >= n - 2;
-    if (has_leaf) CK(launch_k2_leaves(ctx->dt, ctx->k2, dp, pool, 0, lk, st), "K2 leaves");
+    if (has_leaf) {
+        CK(launch_k2_leaves(ctx->dt, ctx->k2, dp, pool, 0, lk, st), "K2 leaves");
+        ++launches;
+    }
+    CK(cudaEventRecord(ctx->ev[1], st), "event");
+    bool has_internal = first_internal < pool.nseg && pool.nchunks > 0;
     CK(launch_k2_internal(ctx->dt, ctx->k2, dp, pool, first_internal, ub, frozen, lk, stg, st),
        "K2 internal");
-    if (has_leaf)
+    CK(cudaEventRecord(ctx->ev[2], st), "event");
+    if (has_internal) launches += 2;  // K2 + append
+    if (has_leaf) {
         CK(launch_leaf_schedule(ctx->dt, dp, lk, ds->schedule, &ds->found, ub, st), "leaf schedule");
+        ++launches;
+    }
     CK(launch_chunk_scan(ctx->chunk_count.as<int32_t>(), 0, pool.nchunks, ctx->offsets.as<int64_t>(), st),
        "chunk scan");
     CK(launch_append(ctx->dt, ctx->k2, dp, pool, first_internal, stg, ctx->offsets.as<int64_t>(), st),
        "append");
     summary_kernel<<<1, 256, 0, st>>>(dp, ctx->offsets.as<int64_t>(), ds);
     CK(cudaGetLastError(), "summary");
+    launches += 2;  // scan + summary
     CK(cudaMemcpyAsync(&ds->leaf_key, lk, 8, cudaMemcpyDeviceToDevice, st), "leaf key copy");
     if (!has_leaf) CK(cudaMemsetAsync(&ds->found, 0, 4, st), "found");
     size_t sbytes = offsetof(RoundSummary, seg_surv) + (size_t)pool.nseg * 8;
@@ -248,7 +263,11 @@ int run_pool(fbb_ctx* ctx, Pool& pool, int first_internal, int32_t ub, int froze
     CK(cudaMemcpyAsync(ctx->h_summary.as<RoundSummary>()->schedule, ds->schedule, (size_t)n * 4,
                        cudaMemcpyDeviceToHost, st),
        "schedule D2H");
+    CK(cudaEventRecord(ctx->ev[3], st), "event");
     CK(cudaStreamSynchronize(st), "round");
+    cudaEventElapsedTime(&ctx->last_k2_ms, ctx->ev[1], ctx->ev[2]);
+    cudaEventElapsedTime(&ctx->last_round_ms, ctx->ev[0], ctx->ev[3]);
+    ctx->last_launches = launches;
     return FBB_OK;
 }
 
@@ -406,6 +425,9 @@ int explorer_round(fbb_ctx* ctx, int64_t target, fbb_round_t* rec) {
         }
     }
     rec->incumbent = ctx->frozen ? (ctx->found ? ctx->best : ctx->incumbent) : ctx->incumbent;
+    rec->k2_ms = ctx->last_k2_ms;
+    rec->round_ms = ctx->last_round_ms;
+    rec->launches = ctx->last_launches;
     ctx->tot_branched += rec->branched;
     ctx->tot_bounded += rec->bounded;
     ctx->tot_pruned += rec->pruned;
@@ -452,6 +474,7 @@ fbb_ctx* fbb_create(int device, const int32_t* p, int n, int m) {
         delete ctx;
         return fail(FBB_E_CUDA, std::string("stream: ") + cudaGetErrorString(e));
     }
+    for (cudaEvent_t& ev : ctx->ev) cudaEventCreate(&ev);
     rc = upload_tables(ctx->ht, &ctx->dt, &why);
     if (rc != FBB_OK) {
         fbb_destroy(ctx);
@@ -490,6 +513,8 @@ void fbb_destroy(fbb_ctx* ctx) {
     }
     ctx->h_pool.release();
     ctx->h_summary.release();
+    for (cudaEvent_t ev : ctx->ev)
+        if (ev) cudaEventDestroy(ev);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
 }
@@ -659,6 +684,9 @@ int fbb_expand_bound_prune(fbb_ctx* ctx, const uint64_t* masks, const int32_t* h
     rec.leaves = leaves;
     rec.inserted = total;
     rec.pruned = internal - total;
+    rec.k2_ms = ctx->last_k2_ms;
+    rec.round_ms = ctx->last_round_ms;
+    rec.launches = ctx->last_launches;
     if (leaves > 0 && sm->leaf_key != ~0ull) {
         int32_t v = (int32_t)(sm->leaf_key >> 32);
         if (v < ub) {

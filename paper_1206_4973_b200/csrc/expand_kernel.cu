@@ -44,14 +44,15 @@ struct K2Layout {
     int ppc_max, pst, mst;
 };
 
-__host__ __device__ inline K2Layout k2_layout(int n, int m, int P, int cmax, int threads) {
+__host__ __device__ inline K2Layout k2_layout(int n, int m, int P, int cmax, int threads,
+                                              bool jm_in_smem) {
     K2Layout L;
     int W32 = (n + 31) / 32;
     L.ppc_max = cmax / 3 > 0 ? cmax / 3 : 1;
     L.pst = P + 1;             // Mq row stride (elements); odd -> conflict-free rows
     L.mst = m + 1;             // child row stride for cR / cL
     size_t o = 0;
-    L.jm = o;   o = a16(o + (size_t)n * P * 4);
+    L.jm = o;   o = a16(o + (jm_in_smem ? (size_t)n * P * 4 : 0));
     L.pk = o;   o = a16(o + (size_t)P * 4);
     L.p = o;    o = a16(o + (size_t)n * m * 4);
     L.tl = o;   o = a16(o + (size_t)n * m * 4);
@@ -82,6 +83,9 @@ __device__ inline int find_segment(const Pool* __restrict__ pool, int lo, int64_
 
 __device__ inline bool um_test(const uint32_t* um, int j) { return (um[j >> 5] >> (j & 31)) & 1u; }
 
+// kJmSmem: the Johnson table is staged in shared memory (n*P*4 bytes); for the
+// largest instances (200x20: 152 KB) it is read through L1/L2 instead.
+template <bool kJmSmem>
 __global__ void __launch_bounds__(128) k2_internal_kernel(DevTables t, const Pool* __restrict__ pool,
                                                          int first_seg, int cmax, int32_t ub,
                                                          int frozen,
@@ -90,8 +94,8 @@ __global__ void __launch_bounds__(128) k2_internal_kernel(DevTables t, const Poo
     extern __shared__ __align__(16) unsigned char smem[];
     const int n = t.n, m = t.m, P = t.P, W = t.W;
     const int W32 = (n + 31) / 32;
-    const K2Layout L = k2_layout(n, m, P, cmax, blockDim.x);
-    uint32_t* s_jm = (uint32_t*)(smem + L.jm);
+    const K2Layout L = k2_layout(n, m, P, cmax, blockDim.x, kJmSmem);
+    const uint32_t* s_jm = kJmSmem ? (const uint32_t*)(smem + L.jm) : t.jm;
     int32_t* s_pk = (int32_t*)(smem + L.pk);
     int32_t* s_p = (int32_t*)(smem + L.p);
     int32_t* s_tl = (int32_t*)(smem + L.tl);
@@ -110,7 +114,8 @@ __global__ void __launch_bounds__(128) k2_internal_kernel(DevTables t, const Poo
     const int tid = threadIdx.x, bd = blockDim.x, lane = tid & 31, warp = tid >> 5;
     const int nwarps = bd >> 5;
 
-    for (int x = tid; x < n * P; x += bd) s_jm[x] = t.jm[x];
+    if (kJmSmem)
+        for (int x = tid; x < n * P; x += bd) ((uint32_t*)(smem + L.jm))[x] = t.jm[x];
     for (int x = tid; x < P; x += bd) s_pk[x] = (int32_t)t.pair_k[x] | ((int32_t)t.pair_l[x] << 16);
     for (int x = tid; x < n * m; x += bd) {
         s_p[x] = t.p[x];
@@ -442,11 +447,16 @@ K2Config k2_config(const DevTables& t, int device) {
     c.threads = 128;
     int n = t.n;
     c.cmax = n <= 128 ? 128 : ((n + 31) / 32) * 32;
-    c.smem = k2_layout(t.n, t.m, t.P, c.cmax, c.threads).total;
+    int max_smem = 0;
+    cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    c.smem = k2_layout(t.n, t.m, t.P, c.cmax, c.threads, true).total;
+    c.jm_in_smem = c.smem <= (size_t)max_smem / 2;  // keep >= 2 CTAs per SM
+    if (!c.jm_in_smem) c.smem = k2_layout(t.n, t.m, t.P, c.cmax, c.threads, false).total;
     int sms = 148, per_sm = 1;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    cudaFuncSetAttribute(k2_internal_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_internal_kernel, c.threads, c.smem);
+    auto kern = c.jm_in_smem ? k2_internal_kernel<true> : k2_internal_kernel<false>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, c.threads, c.smem);
     if (per_sm < 1) per_sm = 1;
     c.blocks = sms * per_sm;
     return c;
@@ -473,8 +483,12 @@ cudaError_t launch_k2_internal(const DevTables& t, const K2Config& cfg, const Po
     int64_t nch = h_pool.nchunks - h_pool.seg[first_seg].chunk_base;
     if (nch <= 0) return cudaSuccess;
     int blocks = (int)(nch < cfg.blocks ? nch : cfg.blocks);
-    k2_internal_kernel<<<blocks, cfg.threads, cfg.smem, stream>>>(t, d_pool, first_seg, cfg.cmax, ub,
-                                                                  frozen, leaf_key, st);
+    if (cfg.jm_in_smem)
+        k2_internal_kernel<true><<<blocks, cfg.threads, cfg.smem, stream>>>(t, d_pool, first_seg, cfg.cmax,
+                                                                            ub, frozen, leaf_key, st);
+    else
+        k2_internal_kernel<false><<<blocks, cfg.threads, cfg.smem, stream>>>(t, d_pool, first_seg, cfg.cmax,
+                                                                             ub, frozen, leaf_key, st);
     return cudaGetLastError();
 }
 

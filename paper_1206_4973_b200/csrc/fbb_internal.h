@@ -108,6 +108,7 @@ struct Pool {
 struct K2Config {
     int threads = 128;
     int cmax = 128;      // children per chunk (>= n)
+    bool jm_in_smem = true;
     int blocks = 0;
     size_t smem = 0;
 };

@@ -278,13 +278,18 @@ class Context:
                                                     C.byref(rec)))
         return rec.as_tuple()
 
-    def explorer_run(self, targets, max_rounds: int, budget: int = 0):
+    def explorer_run(self, targets, max_rounds: int, budget: int = 0, timing: bool = False):
+        """Runs rounds on the device explorer; returns the per-round count tuples
+        (and, with timing=True, the per-round device timings)."""
         t = np.ascontiguousarray(np.atleast_1d(np.asarray(targets, np.int64)))
-        recs = (RoundRec * max(max_rounds, 1))()
+        recs = (RoundRec * max(min(max_rounds, 1 << 20), 1))()
         done = C.c_int64(0)
-        self._check(self.L.fbb_explorer_run(self.h, t, len(t), max_rounds, budget,
+        self._check(self.L.fbb_explorer_run(self.h, t, len(t), min(max_rounds, 1 << 20), budget,
                                             C.cast(recs, C.c_void_p), C.byref(done)))
-        return [recs[i].as_tuple() for i in range(done.value)]
+        rounds = [recs[i].as_tuple() for i in range(done.value)]
+        if timing:
+            return rounds, [recs[i].timing() for i in range(done.value)]
+        return rounds
 
     def explorer_state(self):
         inc = C.c_int32(0)
