@@ -1,0 +1,230 @@
+// gpu_backend.hpp -- header-only C++ drop-in for the reference flowbb API.
+//
+// Include AFTER the reference headers are on the include path (-I proj/include)
+// and link libflowbb_b200.so.  Provides:
+//
+//   flowbb_b200::GpuBackend      models the reference's duck-typed Backend concept
+//                                (descriptor() + evaluate(inst, span<const Node>),
+//                                backend.hpp:50-69, used by evaluate_multi<Backend>,
+//                                backend.hpp:105-138) over fbb_bound (K1);
+//   flowbb_b200::GpuBackendSet   BackendSet (backend.hpp:140-158) over GPUs;
+//   flowbb_b200::gpu_round       the fused replacement of one reference round
+//                                fill_buffer -> evaluate -> integrate / frozen
+//                                prune (search.hpp:64-107, bench.hpp:88-106)
+//                                over fbb_expand_bound_prune (K2), operating on
+//                                the reference's own PendingTree and Incumbent.
+//
+// Errors surface as flowbb::BackendError(device, message), like a failing
+// CpuBackend slice (backend.hpp:124-136).
+#ifndef FLOWBB_B200_GPU_BACKEND_HPP
+#define FLOWBB_B200_GPU_BACKEND_HPP
+
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <optional>
+#include <span>
+#include <string>
+#include <vector>
+
+#include "flowbb/backend.hpp"
+#include "flowbb/pending.hpp"
+#include "flowbb/search.hpp"
+#include "flowbb_b200.h"
+
+namespace flowbb_b200 {
+
+namespace detail {
+
+inline std::string last_error(const fbb_ctx* ctx, int* device) {
+    char buf[512];
+    fbb_last_error(ctx, device, buf, sizeof(buf));
+    return buf;
+}
+
+// One device context per (device, instance); created on first use.
+class ContextCache {
+public:
+    explicit ContextCache(int device) : device_(device) {}
+    ~ContextCache() {
+        if (ctx_) fbb_destroy(ctx_);
+    }
+    fbb_ctx* get(const flowbb::Instance& inst) {
+        std::lock_guard<std::mutex> g(mu_);
+        std::vector<int32_t> p(static_cast<std::size_t>(inst.jobs()) * inst.machines());
+        for (int j = 0; j < inst.jobs(); ++j)
+            for (int k = 0; k < inst.machines(); ++k) p[j * inst.machines() + k] = inst.p(j, k);
+        if (ctx_ && p == p_) return ctx_;
+        if (ctx_) fbb_destroy(ctx_);
+        ctx_ = fbb_create(device_, p.data(), inst.jobs(), inst.machines());
+        if (!ctx_) {
+            int dev = device_;
+            throw flowbb::BackendError(device_, last_error(nullptr, &dev));
+        }
+        p_ = std::move(p);
+        return ctx_;
+    }
+    std::mutex& call_mutex() { return call_mu_; }
+
+private:
+    int device_;
+    std::mutex mu_, call_mu_;
+    fbb_ctx* ctx_ = nullptr;
+    std::vector<int32_t> p_;
+};
+
+// Node (node.hpp:28-53) -> SoA row
+inline void pack(const flowbb::Instance& inst, const flowbb::Node& node, uint64_t* mask,
+                 int32_t* heads, uint8_t* prefix) {
+    const int n = inst.jobs(), W = (n + 63) / 64;
+    for (int w = 0; w < W; ++w) mask[w] = 0;
+    for (int j = 0; j < n; ++j)
+        if (node.scheduled.test(j)) mask[j >> 6] |= uint64_t{1} << (j & 63);
+    for (int k = 0; k < inst.machines(); ++k) heads[k] = node.heads[k];
+    if (prefix)
+        for (int i = 0; i < node.depth(); ++i) prefix[i] = static_cast<uint8_t>(node.prefix[i]);
+}
+
+}  // namespace detail
+
+class GpuBackend {
+public:
+    explicit GpuBackend(int device = 0,
+                        flowbb::BackendDescriptor descriptor = flowbb::BackendDescriptor{256, 148, 1 << 24})
+        : device_(device), descriptor_(descriptor),
+          cache_(std::make_shared<detail::ContextCache>(device)) {}
+
+    const flowbb::BackendDescriptor& descriptor() const { return descriptor_; }
+    int device() const { return device_; }
+
+    // CpuBackend::evaluate (backend.hpp:63-65): position-aligned lower_bound of every node.
+    std::vector<int> evaluate(const flowbb::Instance& inst, std::span<const flowbb::Node> nodes) const {
+        std::vector<int> out(nodes.size());
+        if (nodes.empty()) return out;
+        fbb_ctx* ctx = cache_->get(inst);
+        const int n = inst.jobs(), m = inst.machines(), W = (n + 63) / 64;
+        std::vector<uint64_t> masks(nodes.size() * W);
+        std::vector<int32_t> heads(nodes.size() * m), depth(nodes.size());
+        for (std::size_t i = 0; i < nodes.size(); ++i) {
+            detail::pack(inst, nodes[i], &masks[i * W], &heads[i * m], nullptr);
+            depth[i] = nodes[i].depth();
+        }
+        std::lock_guard<std::mutex> g(cache_->call_mutex());
+        int rc = fbb_bound(ctx, masks.data(), heads.data(), depth.data(),
+                           static_cast<int64_t>(nodes.size()), out.data());
+        if (rc != FBB_OK) {
+            int dev = device_;
+            throw flowbb::BackendError(device_, detail::last_error(ctx, &dev));
+        }
+        return out;
+    }
+
+    fbb_ctx* context(const flowbb::Instance& inst) const { return cache_->get(inst); }
+    std::mutex& call_mutex() const { return cache_->call_mutex(); }
+
+private:
+    int device_;
+    flowbb::BackendDescriptor descriptor_;
+    std::shared_ptr<detail::ContextCache> cache_;
+};
+
+// BackendSet (backend.hpp:140-158) with backend i on device devices[i % size].
+class GpuBackendSet {
+public:
+    GpuBackendSet(int count, std::vector<int> devices = {0},
+                  flowbb::BackendDescriptor descriptor = flowbb::BackendDescriptor{256, 148, 1 << 24}) {
+        if (count < 1) throw std::invalid_argument("backend count must be positive");
+        for (int i = 0; i < count; ++i)
+            backends_.emplace_back(devices[static_cast<std::size_t>(i) % devices.size()], descriptor);
+    }
+    int size() const { return static_cast<int>(backends_.size()); }
+    const flowbb::BackendDescriptor& descriptor() const { return backends_.front().descriptor(); }
+    std::vector<int> evaluate(const flowbb::Instance& inst, std::span<const flowbb::Node> batch) const {
+        return flowbb::evaluate_multi<GpuBackend>(backends_, inst, batch);
+    }
+    const GpuBackend& front() const { return backends_.front(); }
+
+private:
+    std::vector<GpuBackend> backends_;
+};
+
+struct RoundCounts {
+    std::int64_t branched = 0, bounded = 0, inserted = 0, pruned = 0, leaves = 0;
+};
+
+// One fused round on the reference's own PendingTree: pops exactly the parents
+// fill_buffer would (search.hpp:64-73), expands/bounds/prunes their children on
+// the GPU (K2), pushes the survivors in batch order.  frozen == false follows
+// integrate (search.hpp:84-107: strict improvement, mid-batch incumbent);
+// frozen == true the resolve loop (bench.hpp:96-106; `best` tracks the leaf
+// minimum under the frozen incumbent).
+inline RoundCounts gpu_round(const GpuBackend& backend, const flowbb::Instance& inst,
+                             flowbb::PendingTree& pending, flowbb::Incumbent& incumbent,
+                             std::size_t target, bool frozen, std::optional<int>* best = nullptr) {
+    RoundCounts rc;
+    const int n = inst.jobs(), m = inst.machines(), W = (n + 63) / 64;
+    std::vector<uint64_t> masks;
+    std::vector<int32_t> heads, depth;
+    std::vector<uint8_t> prefix;
+    std::size_t children = 0;
+    while (children < target && !pending.empty()) {
+        flowbb::Node node = pending.pop();
+        ++rc.branched;
+        std::size_t i = depth.size();
+        masks.resize((i + 1) * W);
+        heads.resize((i + 1) * m);
+        prefix.resize((i + 1) * n);
+        detail::pack(inst, node, &masks[i * W], &heads[i * m], &prefix[i * n]);
+        depth.push_back(node.depth());
+        children += static_cast<std::size_t>(n - node.depth());
+    }
+    if (depth.empty()) return rc;
+    std::vector<uint64_t> omask(children * W);
+    std::vector<int32_t> oheads(children * m), odepth(children), olb(children), sched(n);
+    std::vector<uint8_t> oprefix(children * n);
+    int64_t count = 0, pos = 0;
+    int32_t leaf_best = 0;
+    fbb_round_t rec;
+    fbb_ctx* ctx = backend.context(inst);
+    {
+        std::lock_guard<std::mutex> g(backend.call_mutex());
+        int st = fbb_expand_bound_prune(ctx, masks.data(), heads.data(), depth.data(), prefix.data(),
+                                        static_cast<int64_t>(depth.size()), incumbent.value,
+                                        frozen ? 1 : 0, omask.data(), oheads.data(), odepth.data(),
+                                        oprefix.data(), olb.data(), &count, &leaf_best, &pos,
+                                        sched.data(), &rec);
+        if (st != FBB_OK) {
+            int dev = backend.device();
+            throw flowbb::BackendError(backend.device(), detail::last_error(ctx, &dev));
+        }
+    }
+    for (int64_t i = 0; i < count; ++i) {
+        flowbb::Node node = flowbb::Node::root(inst);
+        for (int d = 0; d < odepth[i]; ++d) {
+            int j = oprefix[i * n + d];
+            node.prefix.push_back(j);
+            node.scheduled.set(j);
+        }
+        for (int k = 0; k < m; ++k) node.heads[k] = oheads[i * m + k];
+        node.lb = olb[i];
+        pending.push(std::move(node));
+    }
+    if (leaf_best != INT32_MAX) {
+        if (frozen) {
+            if (best && leaf_best < incumbent.value && (!*best || leaf_best < **best)) *best = leaf_best;
+        } else if (leaf_best < incumbent.value) {
+            incumbent.value = leaf_best;
+            incumbent.schedule = flowbb::Permutation(sched.begin(), sched.end());
+        }
+    }
+    rc.bounded = rec.bounded;
+    rc.inserted = rec.inserted;
+    rc.pruned = rec.pruned;
+    rc.leaves = rec.leaves;
+    return rc;
+}
+
+}  // namespace flowbb_b200
+
+#endif  // FLOWBB_B200_GPU_BACKEND_HPP

@@ -155,7 +155,10 @@ K1Config k1_config(const DevTables& t, int device) {
     int sms = 148, per_sm = 1;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     auto kern = (t.n <= 32) ? k1_bound_kernel<true> : k1_bound_kernel<false>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
+    // the attribute is per kernel, not per context: allow the device maximum once
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, c.threads, c.smem);
     if (per_sm < 1) per_sm = 1;
     c.blocks = sms * per_sm;

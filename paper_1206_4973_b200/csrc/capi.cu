@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <climits>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -482,6 +483,15 @@ fbb_ctx* fbb_create(int device, const int32_t* p, int n, int m) {
     }
     ctx->k1 = k1_config(ctx->dt, device);
     ctx->k2 = k2_config(ctx->dt, device);
+    {
+        // register-row K2 for n <= 32, m in {5,10,20}; tails packed as 16-bit there
+        int32_t max_tail = 0;
+        for (int32_t v : ctx->ht.tails) max_tail = std::max(max_tail, v);
+        K2Config v2;
+        const char* force = getenv("FBB_K2_GENERIC");
+        if (max_tail < 0x7FFF && !(force && force[0] == '1') && k2_v2_config(ctx->dt, device, &v2))
+            ctx->k2 = v2;
+    }
     int max_smem = 0;
     cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
     if (ctx->k1.smem > (size_t)max_smem || ctx->k2.smem > (size_t)max_smem) {

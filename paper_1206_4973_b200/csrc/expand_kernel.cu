@@ -455,7 +455,10 @@ K2Config k2_config(const DevTables& t, int device) {
     int sms = 148, per_sm = 1;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     auto kern = c.jm_in_smem ? k2_internal_kernel<true> : k2_internal_kernel<false>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c.smem);
+    // the attribute is per kernel, not per context: allow the device maximum once
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, c.threads, c.smem);
     if (per_sm < 1) per_sm = 1;
     c.blocks = sms * per_sm;
@@ -483,6 +486,8 @@ cudaError_t launch_k2_internal(const DevTables& t, const K2Config& cfg, const Po
     int64_t nch = h_pool.nchunks - h_pool.seg[first_seg].chunk_base;
     if (nch <= 0) return cudaSuccess;
     int blocks = (int)(nch < cfg.blocks ? nch : cfg.blocks);
+    if (cfg.variant != 0)
+        return launch_k2_v2(t, cfg, d_pool, first_seg, blocks, ub, frozen, leaf_key, st, stream);
     if (cfg.jm_in_smem)
         k2_internal_kernel<true><<<blocks, cfg.threads, cfg.smem, stream>>>(t, d_pool, first_seg, cfg.cmax,
                                                                             ub, frozen, leaf_key, st);

@@ -1,0 +1,365 @@
+// expand_v2.cu -- K2 specialised for n <= 32 jobs and m in {5, 10, 20}
+// (the Taillard 20xm classes: configs 1-2).  Same contract and output as
+// k2_internal_kernel (expand_kernel.cu); different mapping:
+//
+//  * thread (g, q) owns machine pair q for the whole kernel; its Johnson row
+//    (n entries: job bit, c, d) lives in REGISTERS, so Phase A issues no table
+//    loads.  g = 0..G-1 are parent lanes (G = threads / P).
+//  * Phase A is branch-free: per position one LOP3 (job in U?) and predicated
+//    max/add; the backward pass emits M'_x to smem Mq[child][q] (int16).
+//  * Phase B: thread per child; child heads R' and the per-machine terms Lc'
+//    are register arrays (template M), the pair loop is fully unrolled and reads
+//    the child's Mq row with 128-bit loads (row stride = odd multiple of 16 B,
+//    conflict-free).
+#include <climits>
+
+#include "fbb_internal.h"
+
+namespace fbb {
+
+namespace {
+
+constexpr int32_t kNeg2 = -(1 << 20);
+
+__host__ __device__ inline size_t b16(size_t x) { return (x + 15) & ~size_t(15); }
+
+__host__ __device__ inline int v2_row_bytes(int P) {
+    int b = (P * 2 + 15) / 16;  // 16-byte units
+    if ((b & 1) == 0) b += 1;   // odd -> 8 consecutive rows hit 8 distinct bank groups
+    return b * 16;
+}
+
+struct V2Layout {
+    size_t row, um, rank, R, load, mins, amin, Mq, p, wsum, total;
+    int ppc_max, rowb;
+};
+
+__host__ __device__ inline V2Layout v2_layout(int n, int m, int P, int cmax, int threads, int N) {
+    V2Layout L;
+    L.ppc_max = cmax / 3 > 0 ? cmax / 3 : 1;
+    L.rowb = v2_row_bytes(P);
+    size_t o = 0;
+    L.row = o;  o = b16(o + (size_t)N * P * 4);  // rows padded to N positions
+    L.um = o;   o = b16(o + (size_t)L.ppc_max * 4);
+    L.rank = o; o = b16(o + (size_t)L.ppc_max * 32);
+    L.R = o;    o = b16(o + (size_t)L.ppc_max * m * 4);
+    L.load = o; o = b16(o + (size_t)L.ppc_max * m * 4);
+    L.mins = o; o = b16(o + (size_t)L.ppc_max * m * 4);  // min1 | min2 << 16
+    L.amin = o; o = b16(o + (size_t)L.ppc_max * m);
+    L.Mq = o;   o = b16(o + (size_t)(cmax + 1) * L.rowb);  // + a dummy row for non-members
+    L.p = o;    o = b16(o + (size_t)n * m * 4);
+    L.wsum = o; o = b16(o + (size_t)(threads / 32 + 1) * 4);
+    L.total = o;
+    return L;
+}
+
+__device__ inline int v2_find_segment(const Pool* __restrict__ pool, int lo, int64_t chunk) {
+    int hi = pool->nseg - 1;
+    while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        if (pool->seg[mid].chunk_base <= chunk) lo = mid; else hi = mid - 1;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ void sts_u16(uint32_t addr, int32_t v) {
+    asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"((unsigned short)v));
+}
+
+template <int M>
+struct PairTab {  // (k, l) of pair index q in bound.hpp:97-98 order
+    int k[M * (M - 1) / 2 > 0 ? M * (M - 1) / 2 : 1];
+    int l[M * (M - 1) / 2 > 0 ? M * (M - 1) / 2 : 1];
+    constexpr PairTab() : k(), l() {
+        int q = 0;
+        for (int a = 0; a < M; ++a)
+            for (int b = a + 1; b < M; ++b) {
+                k[q] = a;
+                l[q] = b;
+                ++q;
+            }
+    }
+};
+
+template <int N, int M>
+__global__ void __launch_bounds__(192, 4) k2_v2_kernel(DevTables t, const Pool* __restrict__ pool,
+                                                   int first_seg, int cmax, int32_t ub, int frozen,
+                                                   const unsigned long long* __restrict__ leaf_key,
+                                                   Staging st) {
+    constexpr int P = M * (M - 1) / 2;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int n = t.n, W = t.W;
+    const V2Layout L = v2_layout(n, M, P, cmax, blockDim.x, N);
+    uint32_t* s_um = (uint32_t*)(smem + L.um);
+    uint8_t* s_rank = (uint8_t*)(smem + L.rank);
+    int32_t* s_R = (int32_t*)(smem + L.R);
+    int32_t* s_load = (int32_t*)(smem + L.load);
+    uint32_t* s_mins = (uint32_t*)(smem + L.mins);
+    uint8_t* s_amin = (uint8_t*)(smem + L.amin);
+    unsigned char* s_Mq = smem + L.Mq;
+    int32_t* s_p = (int32_t*)(smem + L.p);
+    int32_t* s_wsum = (int32_t*)(smem + L.wsum);
+    const int tid = threadIdx.x, bd = blockDim.x, lane = tid & 31, warp = tid >> 5;
+    const int nwarps = bd >> 5;
+    const int G = bd / P;
+    const int q = tid % P, g = tid / P;
+    const bool a_lane = g < G;
+
+    for (int x = tid; x < n * M; x += bd) s_p[x] = t.p[x];
+
+    // Johnson rows repacked for the scans, one word per (position, pair), [i][q]:
+    //   bits 0..4 job, bits 8..23 c, bits 24..31 d (int8)
+    //   padding positions i >= n carry job 31, never in U (n < 32 there)
+    uint32_t* s_row = (uint32_t*)(smem + L.row);
+    for (int x = tid; x < N * P; x += bd) {
+        uint32_t v = 31u;
+        if (x < n * P) {
+            uint32_t e = t.jm[x];
+            v = (uint32_t)entry_job(e) | ((uint32_t)entry_c(e) << 8) | ((uint32_t)entry_d(e) << 24);
+        }
+        s_row[x] = v;
+    }
+    // 32-bit shared addresses: each scan step is one LDS [reg + immediate]
+    const uint32_t row_sa = (uint32_t)__cvta_generic_to_shared(s_row + q);
+
+    int32_t ub_eff = ub;
+    if (!frozen && leaf_key) {
+        unsigned long long key = *leaf_key;
+        int32_t v = (int32_t)(key >> 32);
+        if (key != ~0ull && v < ub_eff) ub_eff = v;
+    }
+
+    const int64_t c_begin = pool->seg[first_seg].chunk_base;
+    const int64_t c_end = pool->nchunks;
+    for (int64_t chunk = c_begin + blockIdx.x; chunk < c_end; chunk += gridDim.x) {
+        const int s = v2_find_segment(pool, first_seg, chunk);
+        const Segment& sg = pool->seg[s];
+        const int depth = sg.depth;
+        const int r = n - depth;
+        const int ppc = cmax / r;
+        const int64_t p0 = (chunk - sg.chunk_base) * ppc;
+        const int np = (int)(sg.count - p0 < ppc ? sg.count - p0 : ppc);
+        const int nc = np * r;
+        const NodeStore src = sg.src;
+        const int64_t first = sg.first, step = sg.step;
+        __syncthreads();
+        for (int pp = tid; pp < np; pp += bd) {
+            int64_t node = first + step * (p0 + pp);
+            uint32_t sched = (uint32_t)src.masks[node * W];
+            s_um[pp] = ~sched & (n >= 32 ? 0xFFFFFFFFu : ((1u << n) - 1u));
+        }
+        for (int x = tid; x < np * M; x += bd) {
+            int pp = x / M, k = x - pp * M;
+            s_R[x] = src.heads[(first + step * (p0 + pp)) * M + k];
+        }
+        __syncthreads();
+        for (int x = tid; x < np * 32; x += bd) {  // rank of job j among U (ascending)
+            int pp = x >> 5, j = x & 31;
+            s_rank[x] = (uint8_t)__popc(s_um[pp] & ((1u << j) - 1u));
+        }
+        // per (parent, machine): load, two smallest tails (+ argmin)
+        for (int x = tid; x < np * M; x += bd) {
+            int pp = x / M, k = x - pp * M;
+            uint32_t um = s_um[pp];
+            int32_t load = 0, m1 = 0x7FFF, m2 = 0x7FFF, am = 0;
+            while (um) {
+                int j = __ffs(um) - 1;
+                um &= um - 1;
+                load += s_p[j * M + k];
+                int32_t tv = t.tails[j * M + k];
+                if (tv < m1) {
+                    m2 = m1;
+                    m1 = tv;
+                    am = j;
+                } else if (tv < m2) {
+                    m2 = tv;
+                }
+            }
+            s_load[x] = load;
+            s_mins[x] = (uint32_t)m1 | ((uint32_t)m2 << 16);
+            s_amin[x] = (uint8_t)am;
+        }
+        // ---- Phase A: forward / backward max-plus scans of pair q over parent pp
+        if (a_lane) {
+            for (int pp = g; pp < np; pp += G) {
+                const uint32_t um = s_um[pp];
+                const uint32_t rank_sa = (uint32_t)__cvta_generic_to_shared(s_rank + pp * 32);
+                const uint32_t out_sa =
+                    (uint32_t)__cvta_generic_to_shared(s_Mq + (size_t)(pp * r) * L.rowb + 2 * q);
+                const uint32_t dummy_sa =
+                    (uint32_t)__cvta_generic_to_shared(s_Mq + (size_t)cmax * L.rowb + 2 * q);
+                const uint32_t rowb = (uint32_t)L.rowb;
+                int32_t D = 0, PM = kNeg2;
+                int32_t pm[N];
+#pragma unroll
+                for (int i = 0; i < N; ++i) {
+                    const uint32_t e = lds_u32(row_sa + (uint32_t)(i * P * 4));
+                    const bool in = (__funnelshift_r(um, 0u, e) & 1u) != 0u;  // shift = e & 31
+                    const int32_t c = (int32_t)__byte_perm(e, 0u, 0x4421);    // bytes 1..2
+                    const int32_t d = (int32_t)e >> 24;
+                    pm[i] = PM;
+                    PM = in ? max(PM, D + c) : PM;
+                    D = in ? D + d : D;
+                }
+                int32_t SM = kNeg2;
+#pragma unroll
+                for (int i = N - 1; i >= 0; --i) {
+                    const uint32_t e = lds_u32(row_sa + (uint32_t)(i * P * 4));
+                    const bool in = (__funnelshift_r(um, 0u, e) & 1u) != 0u;
+                    const int32_t c = (int32_t)__byte_perm(e, 0u, 0x4421);
+                    const int32_t d = (int32_t)e >> 24;
+                    const int32_t Db = D - d;  // D before position i
+                    // finite for members of U with |U| >= 3 (internal children), fits int16
+                    const int32_t mp = max(pm[i], SM - d);
+                    const uint32_t rk = lds_u8(rank_sa + (e & 31u));
+                    sts_u16(in ? out_sa + rk * rowb : dummy_sa, mp);
+                    SM = in ? max(SM, Db + c) : SM;
+                    D = in ? Db : D;
+                }
+            }
+        }
+        __syncthreads();
+        // ---- Phase B: per child bound with register-resident heads
+        int32_t myR[M];
+        int32_t mylb = 0;
+        int myx = 0, mypp = 0;
+        const bool b_lane = tid < nc;  // cmax <= blockDim
+        if (b_lane) {
+            const int pp = tid / r, rk = tid - pp * r;
+            const uint32_t um = s_um[pp];
+            const int x = __fns(um, 0, rk + 1);
+            myx = x;
+            mypp = pp;
+            int32_t Lc[M];
+            int32_t prev = 0, lb = 0;
+#pragma unroll
+            for (int k = 0; k < M; ++k) {
+                const int pk = pp * M + k;
+                prev = max(prev, s_R[pk]) + s_p[x * M + k];  // child_heads, instance.hpp:81-89
+                myR[k] = prev;
+                uint32_t mins = s_mins[pk];
+                int32_t mt = (x == (int)s_amin[pk]) ? (int32_t)(mins >> 16) : (int32_t)(mins & 0xFFFFu);
+                Lc[k] = s_load[pk] - s_p[x * M + k] + mt;
+                lb = max(lb, prev + Lc[k]);  // one-machine term (bound.hpp:61-74)
+            }
+            const uint4* mrow = (const uint4*)(s_Mq + (size_t)tid * L.rowb);
+            constexpr PairTab<M> tab{};
+#pragma unroll
+            for (int q8 = 0; q8 < (P + 7) / 8; ++q8) {
+                const uint4 cur = mrow[q8];
+                const uint32_t wv[4] = {cur.x, cur.y, cur.z, cur.w};
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int qq = q8 * 8 + u;
+                    if (qq < P) {
+                        const uint32_t w = wv[u >> 1];
+                        const int32_t mq = (u & 1) ? ((int32_t)w >> 16) : (int32_t)(int16_t)(w & 0xFFFFu);
+                        const int k = tab.k[qq], l = tab.l[qq];
+                        lb = max(lb, Lc[l] + max(myR[l], myR[k] + mq));
+                    }
+                }
+            }
+            mylb = lb;
+        }
+        // ---- prune + stable compaction into staging[chunk] (one child per thread)
+        const bool keep = b_lane && mylb < ub_eff;
+        const unsigned ballot = __ballot_sync(0xFFFFFFFFu, keep);
+        if (lane == 0) s_wsum[warp] = __popc(ballot);
+        __syncthreads();
+        int woff = 0, tot = 0;
+        for (int w = 0; w < nwarps; ++w) {
+            int v = s_wsum[w];
+            if (w < warp) woff += v;
+            tot += v;
+        }
+        if (keep) {
+            const int rank = woff + __popc(ballot & ((1u << lane) - 1u));
+            const int64_t o = chunk * (int64_t)cmax + rank;
+#pragma unroll
+            for (int k = 0; k < M; ++k) st.nodes.heads[o * M + k] = myR[k];
+            const uint32_t um = s_um[mypp];
+            const uint32_t valid = n >= 32 ? 0xFFFFFFFFu : ((1u << n) - 1u);
+            st.nodes.masks[o * W] = (uint64_t)((~um & valid) | (1u << myx));
+            const int64_t node = first + step * (p0 + mypp);
+            const uint8_t* pre = src.prefix + node * n;
+            uint8_t* dst = st.nodes.prefix + o * n;
+            for (int i = 0; i < depth; ++i) dst[i] = pre[i];
+            dst[depth] = (uint8_t)myx;
+            if (st.lb) st.lb[o] = mylb;
+        }
+        if (tid == 0) st.chunk_count[chunk] = tot;
+    }
+}
+
+template <int N, int M>
+cudaError_t v2_setup(const DevTables& t, K2Config& c, int device) {
+    int optin = 0, sms = 148, per_sm = 1;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    cudaError_t e = cudaFuncSetAttribute(k2_v2_kernel<N, M>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+    if (e != cudaSuccess) return e;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_v2_kernel<N, M>, c.threads, c.smem);
+    c.blocks = sms * (per_sm < 1 ? 1 : per_sm);
+    return cudaSuccess;
+}
+
+}  // namespace
+
+bool k2_v2_config(const DevTables& t, int device, K2Config* out) {
+    int m = t.m, n = t.n;
+    if (n > 32 || !(m == 5 || m == 10 || m == 20)) return false;
+    K2Config c;
+    c.threads = 192;
+    c.cmax = 128;
+    c.variant = (n <= 20 ? 20 : 32) * 100 + m;
+    c.jm_in_smem = false;
+    c.smem = v2_layout(n, m, t.P, c.cmax, c.threads, n <= 20 ? 20 : 32).total;
+    cudaError_t e;
+    switch (c.variant) {
+        case 2005: e = v2_setup<20, 5>(t, c, device); break;
+        case 2010: e = v2_setup<20, 10>(t, c, device); break;
+        case 2020: e = v2_setup<20, 20>(t, c, device); break;
+        case 3205: e = v2_setup<32, 5>(t, c, device); break;
+        case 3210: e = v2_setup<32, 10>(t, c, device); break;
+        case 3220: e = v2_setup<32, 20>(t, c, device); break;
+        default: return false;
+    }
+    if (e != cudaSuccess) return false;
+    *out = c;
+    return true;
+}
+
+cudaError_t launch_k2_v2(const DevTables& t, const K2Config& cfg, const Pool* d_pool, int first_seg,
+                         int blocks, int32_t ub, int frozen, const unsigned long long* leaf_key,
+                         Staging st, cudaStream_t stream) {
+#define V2_CASE(NN, MM)                                                                       \
+    case NN * 100 + MM:                                                                       \
+        k2_v2_kernel<NN, MM><<<blocks, cfg.threads, cfg.smem, stream>>>(t, d_pool, first_seg,  \
+                                                                         cfg.cmax, ub, frozen, \
+                                                                         leaf_key, st);       \
+        break;
+    switch (cfg.variant) {
+        V2_CASE(20, 5)
+        V2_CASE(20, 10)
+        V2_CASE(20, 20)
+        V2_CASE(32, 5)
+        V2_CASE(32, 10)
+        V2_CASE(32, 20)
+        default: return cudaErrorInvalidValue;
+    }
+#undef V2_CASE
+    return cudaGetLastError();
+}
+
+}  // namespace fbb

@@ -109,6 +109,7 @@ struct K2Config {
     int threads = 128;
     int cmax = 128;      // children per chunk (>= n)
     bool jm_in_smem = true;
+    int variant = 0;     // 0: generic kernel; N*100+M: k2_v2_kernel<N, M> (expand_v2.cu)
     int blocks = 0;
     size_t smem = 0;
 };
@@ -121,6 +122,12 @@ struct Staging {
     int32_t* lb;
     int32_t* chunk_count;
 };
+
+// n <= 32, m in {5,10,20}: the register-row kernel; false when not applicable.
+bool k2_v2_config(const DevTables& t, int device, K2Config* out);
+cudaError_t launch_k2_v2(const DevTables& t, const K2Config& cfg, const Pool* d_pool, int first_seg,
+                         int blocks, int32_t ub, int frozen, const unsigned long long* leaf_key,
+                         Staging st, cudaStream_t stream);
 
 // Batch leaf minimum: packed (value << 32) | batch position, atomicMin.
 cudaError_t launch_k2_leaves(const DevTables& t, const K2Config& cfg, const Pool* d_pool,
