@@ -25,22 +25,27 @@ using namespace fbb;
 
 namespace {
 
+// Device buffers come from the device's stream-ordered memory pool (release
+// threshold raised at context creation), so growing a pending bucket between
+// rounds is an async alloc + D2D copy + async free on the context stream, with
+// no host synchronisation and no cudaMalloc latency.
 struct DBuf {
     void* p = nullptr;
     size_t bytes = 0;
+    cudaStream_t st = nullptr;
     cudaError_t ensure(size_t want) {
         if (want <= bytes) return cudaSuccess;
         size_t nb = std::max(want, bytes * 2);
         void* q = nullptr;
-        cudaError_t e = cudaMalloc(&q, nb);
+        cudaError_t e = cudaMallocAsync(&q, nb, st);
         if (e != cudaSuccess) return e;
-        cudaFree(p);
+        if (p) cudaFreeAsync(p, st);
         p = q;
         bytes = nb;
         return cudaSuccess;
     }
     void release() {
-        cudaFree(p);
+        if (p) cudaFreeAsync(p, st);
         p = nullptr;
         bytes = 0;
     }
@@ -78,25 +83,6 @@ struct Store {
     NodeStore view() const { return NodeStore{masks.as<uint64_t>(), heads.as<int32_t>(), prefix.as<uint8_t>()}; }
 };
 
-struct RoundSummary {
-    unsigned long long leaf_key;
-    int32_t found;
-    int32_t pad;
-    int64_t total;
-    int64_t seg_surv[kMaxSegments];
-    int32_t schedule[kMaxJobs];
-};
-
-__global__ void summary_kernel(const Pool* __restrict__ pool, const int64_t* __restrict__ offsets,
-                               RoundSummary* out) {
-    for (int s = threadIdx.x; s < pool->nseg; s += blockDim.x) {
-        int64_t cb = pool->seg[s].chunk_base;
-        int64_t ce = (s + 1 < pool->nseg) ? pool->seg[s + 1].chunk_base : pool->nchunks;
-        out->seg_surv[s] = (ce > cb) ? offsets[ce] - offsets[cb] : 0;
-    }
-    if (threadIdx.x == 0) out->total = offsets[pool->nchunks];
-}
-
 }  // namespace
 
 static std::mutex g_err_mu;
@@ -118,9 +104,10 @@ struct fbb_ctx {
     Store batch_in, batch_out;
     DBuf out_lb;
     // shared per-round device state
-    DBuf staging_masks, staging_heads, staging_prefix, staging_lb, chunk_count, offsets;
-    DBuf d_pool, d_leaf_key, d_summary;
-    HBuf h_pool, h_summary;
+    DBuf flags;             // per-chunk look-back words (epoch tagged)
+    DBuf d_pool, d_round;   // Pool, RoundState
+    HBuf h_pool, h_round;
+    uint32_t epoch = 0;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     float last_k2_ms = 0.f, last_round_ms = 0.f;
     int last_launches = 0;
@@ -135,6 +122,7 @@ struct fbb_ctx {
     std::vector<int32_t> schedule;
     int64_t tot_branched = 0, tot_bounded = 0, tot_pruned = 0, tot_leaves = 0;
     bool explorer_ready = false;
+    bool check = false;  // FBB_CHECK=1: validate the pending tree after every round
 
     int fail(int code, const std::string& m) {
         status = code;
@@ -163,16 +151,16 @@ cudaError_t store_ensure(fbb_ctx* ctx, Store& s, int64_t want, int64_t keep) {
     int64_t nc = std::max<int64_t>(want, std::max<int64_t>(s.cap * 2, 1024));
     const int n = ctx->dt.n, m = ctx->dt.m, W = ctx->dt.W;
     Store t;
+    t.masks.st = t.heads.st = t.prefix.st = ctx->stream;
+    s.masks.st = s.heads.st = s.prefix.st = ctx->stream;
     cudaError_t e;
     if ((e = t.masks.ensure((size_t)nc * W * 8)) != cudaSuccess) return e;
     if ((e = t.heads.ensure((size_t)nc * m * 4)) != cudaSuccess) return e;
     if ((e = t.prefix.ensure((size_t)nc * n)) != cudaSuccess) return e;
-    if (keep > 0) {
+    if (keep > 0) {  // stream-ordered: the copy precedes the old buffers' async free
         cudaMemcpyAsync(t.masks.p, s.masks.p, (size_t)keep * W * 8, cudaMemcpyDeviceToDevice, ctx->stream);
         cudaMemcpyAsync(t.heads.p, s.heads.p, (size_t)keep * m * 4, cudaMemcpyDeviceToDevice, ctx->stream);
         cudaMemcpyAsync(t.prefix.p, s.prefix.p, (size_t)keep * n, cudaMemcpyDeviceToDevice, ctx->stream);
-        e = cudaStreamSynchronize(ctx->stream);
-        if (e != cudaSuccess) return e;
     }
     s.masks.release();
     s.heads.release();
@@ -187,6 +175,7 @@ cudaError_t store_ensure(fbb_ctx* ctx, Store& s, int64_t want, int64_t keep) {
 // Returns the index of the first internal segment.
 int layout_pool(const fbb_ctx* ctx, Pool& pool) {
     const int n = ctx->dt.n, cmax = ctx->k2.cmax;
+    pool.pad = 0;  // read by the kernels as an opaque zero
     int64_t child = 0, chunk = 0;
     int first_internal = pool.nseg;
     for (int s = 0; s < pool.nseg; ++s) {
@@ -205,71 +194,70 @@ int layout_pool(const fbb_ctx* ctx, Pool& pool) {
     return first_internal;
 }
 
-// Launches one pool: leaves, internal K2, leaf schedule, scan, append,
-// summary.  Synchronises and leaves the summary in ctx->h_summary.
+// Launches one pool: [leaves], internal K2 (bound + prune + ordered writes),
+// [leaf schedule]; then downloads the RoundState.  Synchronises; the result is
+// in ctx->h_round.
 int run_pool(fbb_ctx* ctx, Pool& pool, int first_internal, int32_t ub, int frozen) {
-    const int n = ctx->dt.n, m = ctx->dt.m, W = ctx->dt.W;
+    const int n = ctx->dt.n;
     cudaStream_t st = ctx->stream;
-    const int64_t slots = std::max<int64_t>(pool.nchunks * ctx->k2.cmax, 1);
-    CK(ctx->staging_masks.ensure((size_t)slots * W * 8), "staging");
-    CK(ctx->staging_heads.ensure((size_t)slots * m * 4), "staging");
-    CK(ctx->staging_prefix.ensure((size_t)slots * n), "staging");
-    CK(ctx->staging_lb.ensure((size_t)slots * 4), "staging");
-    CK(ctx->chunk_count.ensure((size_t)std::max<int64_t>(pool.nchunks, 1) * 4), "chunk counts");
-    CK(ctx->offsets.ensure((size_t)(pool.nchunks + 1) * 8), "offsets");
+    const size_t fl_before = ctx->flags.bytes;
+    CK(ctx->flags.ensure((size_t)std::max<int64_t>(pool.nchunks, 1) * 8), "chunk flags");
+    ctx->epoch = (ctx->epoch + 1) & 0xFFFFu;
+    if (ctx->epoch == 0) ctx->epoch = 1;
+    if (ctx->flags.bytes != fl_before || ctx->epoch == 1)  // fresh memory / epoch wrap
+        CK(cudaMemsetAsync(ctx->flags.p, 0, ctx->flags.bytes, st), "chunk flags");
     CK(ctx->d_pool.ensure(sizeof(Pool)), "pool");
     CK(ctx->h_pool.ensure(sizeof(Pool)), "pool");
-    CK(ctx->d_leaf_key.ensure(8), "leaf key");
-    CK(ctx->d_summary.ensure(sizeof(RoundSummary)), "summary");
-    CK(ctx->h_summary.ensure(sizeof(RoundSummary)), "summary");
+    CK(ctx->d_round.ensure(sizeof(RoundState)), "round state");
+    CK(ctx->h_round.ensure(sizeof(RoundState)), "round state");
 
     size_t pool_bytes = offsetof(Pool, seg) + (size_t)pool.nseg * sizeof(Segment);
     std::memcpy(ctx->h_pool.p, &pool, pool_bytes);
     int launches = 0;
     CK(cudaEventRecord(ctx->ev[0], st), "event");
     CK(cudaMemcpyAsync(ctx->d_pool.p, ctx->h_pool.p, pool_bytes, cudaMemcpyHostToDevice, st), "pool H2D");
-    CK(cudaMemsetAsync(ctx->d_leaf_key.p, 0xFF, 8, st), "leaf key");
+    CK(cudaMemsetAsync(ctx->d_round.p, 0, kRoundStateHead, st), "round state");
     const Pool* dp = ctx->d_pool.as<Pool>();
-    unsigned long long* lk = ctx->d_leaf_key.as<unsigned long long>();
-    RoundSummary* ds = ctx->d_summary.as<RoundSummary>();
-    Staging stg{NodeStore{ctx->staging_masks.as<uint64_t>(), ctx->staging_heads.as<int32_t>(),
-                          ctx->staging_prefix.as<uint8_t>()},
-                ctx->staging_lb.as<int32_t>(), ctx->chunk_count.as<int32_t>()};
+    RoundState* rs = ctx->d_round.as<RoundState>();
     bool has_leaf = pool.nseg > 0 && pool.seg[0].depth >= n - 2;
     if (has_leaf) {
-        CK(launch_k2_leaves(ctx->dt, ctx->k2, dp, pool, 0, lk, st), "K2 leaves");
+        CK(launch_k2_leaves(ctx->dt, dp, pool, 0, rs, st), "K2 leaves");
         ++launches;
     }
     CK(cudaEventRecord(ctx->ev[1], st), "event");
     bool has_internal = first_internal < pool.nseg && pool.nchunks > 0;
-    CK(launch_k2_internal(ctx->dt, ctx->k2, dp, pool, first_internal, ub, frozen, lk, stg, st),
+    CK(launch_k2_internal(ctx->dt, ctx->k2, dp, pool, first_internal, ub, frozen, rs,
+                          ctx->flags.as<uint64_t>(), ctx->epoch, st),
        "K2 internal");
     CK(cudaEventRecord(ctx->ev[2], st), "event");
-    if (has_internal) launches += 2;  // K2 + append
+    if (has_internal) ++launches;
     if (has_leaf) {
-        CK(launch_leaf_schedule(ctx->dt, dp, lk, ds->schedule, &ds->found, ub, st), "leaf schedule");
+        CK(launch_leaf_schedule(ctx->dt, dp, rs, ub, st), "leaf schedule");
         ++launches;
     }
-    CK(launch_chunk_scan(ctx->chunk_count.as<int32_t>(), 0, pool.nchunks, ctx->offsets.as<int64_t>(), st),
-       "chunk scan");
-    CK(launch_append(ctx->dt, ctx->k2, dp, pool, first_internal, stg, ctx->offsets.as<int64_t>(), st),
-       "append");
-    summary_kernel<<<1, 256, 0, st>>>(dp, ctx->offsets.as<int64_t>(), ds);
-    CK(cudaGetLastError(), "summary");
-    launches += 2;  // scan + summary
-    CK(cudaMemcpyAsync(&ds->leaf_key, lk, 8, cudaMemcpyDeviceToDevice, st), "leaf key copy");
-    if (!has_leaf) CK(cudaMemsetAsync(&ds->found, 0, 4, st), "found");
-    size_t sbytes = offsetof(RoundSummary, seg_surv) + (size_t)pool.nseg * 8;
-    CK(cudaMemcpyAsync(ctx->h_summary.p, ds, sbytes, cudaMemcpyDeviceToHost, st), "summary D2H");
-    CK(cudaMemcpyAsync(ctx->h_summary.as<RoundSummary>()->schedule, ds->schedule, (size_t)n * 4,
-                       cudaMemcpyDeviceToHost, st),
-       "schedule D2H");
+    size_t head = offsetof(RoundState, seg_surv) + (size_t)pool.nseg * 8;
+    CK(cudaMemcpyAsync(ctx->h_round.p, rs, head, cudaMemcpyDeviceToHost, st), "round D2H");
+    if (has_leaf)
+        CK(cudaMemcpyAsync(ctx->h_round.as<RoundState>()->schedule, rs->schedule, (size_t)n * 4,
+                           cudaMemcpyDeviceToHost, st),
+           "schedule D2H");
     CK(cudaEventRecord(ctx->ev[3], st), "event");
     CK(cudaStreamSynchronize(st), "round");
+    if (ctx->h_round.as<RoundState>()->found < 0)
+        return ctx->fail(FBB_E_STATE, "corrupt pending node (unscheduled-job count mismatch)");
     cudaEventElapsedTime(&ctx->last_k2_ms, ctx->ev[1], ctx->ev[2]);
     cudaEventElapsedTime(&ctx->last_round_ms, ctx->ev[0], ctx->ev[3]);
     ctx->last_launches = launches;
     return FBB_OK;
+}
+
+// Best leaf of the round (value, position), when any.
+bool round_leaf(const RoundState* r, int32_t* value, int64_t* pos) {
+    if (r->leaf_inv == 0ull) return false;
+    unsigned long long key = ~r->leaf_inv;
+    *value = (int32_t)(key >> 32);
+    *pos = (int64_t)(key & 0xFFFFFFFFull);
+    return true;
 }
 
 void node_from_prefix(const HostTables& h, const uint8_t* prefix, int depth, uint64_t* mask,
@@ -325,10 +313,45 @@ int push_host_nodes(fbb_ctx* ctx, const uint8_t* prefix, const int32_t* depth, i
         int64_t c0 = ctx->cnt[d];
         CK(store_ensure(ctx, ctx->bucket[d], c0 + k, c0), "bucket grow");
         Store& b = ctx->bucket[d];
-        CK(cudaMemcpy(b.masks.as<uint64_t>() + c0 * W, hm.data(), hm.size() * 8, cudaMemcpyHostToDevice), "push");
-        CK(cudaMemcpy(b.heads.as<int32_t>() + c0 * m, hh.data(), hh.size() * 4, cudaMemcpyHostToDevice), "push");
-        CK(cudaMemcpy(b.prefix.as<uint8_t>() + c0 * n, hp.data(), hp.size(), cudaMemcpyHostToDevice), "push");
+        cudaStream_t st = ctx->stream;
+        CK(cudaMemcpyAsync(b.masks.as<uint64_t>() + c0 * W, hm.data(), hm.size() * 8, cudaMemcpyHostToDevice, st), "push");
+        CK(cudaMemcpyAsync(b.heads.as<int32_t>() + c0 * m, hh.data(), hh.size() * 4, cudaMemcpyHostToDevice, st), "push");
+        CK(cudaMemcpyAsync(b.prefix.as<uint8_t>() + c0 * n, hp.data(), hp.size(), cudaMemcpyHostToDevice, st), "push");
+        CK(cudaStreamSynchronize(st), "push");  // host vectors are reused
         ctx->cnt[d] = c0 + k;
+    }
+    return FBB_OK;
+}
+
+// FBB_CHECK=1: after every round, every pending node must have popcount(mask)
+// == depth == the number of prefix entries, and heads must fold from the prefix.
+int check_pending(fbb_ctx* ctx) {
+    const int n = ctx->dt.n, m = ctx->dt.m, W = ctx->dt.W;
+    for (int d = 0; d <= n; ++d) {
+        int64_t k = ctx->cnt[d];
+        if (k == 0) continue;
+        if (k > ctx->bucket[d].cap) return ctx->fail(FBB_E_STATE, "check: count exceeds capacity");
+        std::vector<uint64_t> mk((size_t)k * W);
+        std::vector<int32_t> hd((size_t)k * m);
+        std::vector<uint8_t> pr((size_t)k * n);
+        cudaStream_t st = ctx->stream;
+        CK(cudaMemcpyAsync(mk.data(), ctx->bucket[d].masks.p, mk.size() * 8, cudaMemcpyDeviceToHost, st), "check");
+        CK(cudaMemcpyAsync(hd.data(), ctx->bucket[d].heads.p, hd.size() * 4, cudaMemcpyDeviceToHost, st), "check");
+        CK(cudaMemcpyAsync(pr.data(), ctx->bucket[d].prefix.p, pr.size(), cudaMemcpyDeviceToHost, st), "check");
+        CK(cudaStreamSynchronize(st), "check");
+        std::vector<uint64_t> m2(W);
+        std::vector<int32_t> h2(m);
+        for (int64_t i = 0; i < k; ++i) {
+            node_from_prefix(ctx->ht, &pr[i * n], d, m2.data(), h2.data());
+            bool ok = std::memcmp(m2.data(), &mk[i * W], W * 8) == 0 &&
+                      std::memcmp(h2.data(), &hd[i * m], m * 4) == 0;
+            if (!ok) {
+                char buf[160];
+                std::snprintf(buf, sizeof buf, "check: bad pending node depth %d index %lld of %lld",
+                              d, (long long)i, (long long)k);
+                return ctx->fail(FBB_E_STATE, buf);
+            }
+        }
     }
     return FBB_OK;
 }
@@ -391,7 +414,7 @@ int explorer_round(fbb_ctx* ctx, int64_t target, fbb_round_t* rec) {
     }
     int rc = run_pool(ctx, local, first_internal, ctx->incumbent, ctx->frozen);
     if (rc != FBB_OK) return rc;
-    const RoundSummary* sm = ctx->h_summary.as<RoundSummary>();
+    const RoundState* sm = ctx->h_round.as<RoundState>();
     int64_t internal = 0, leaves = 0;
     for (int s = 0; s < local.nseg; ++s) {
         const Segment& sg = local.seg[s];
@@ -409,8 +432,9 @@ int explorer_round(fbb_ctx* ctx, int64_t target, fbb_round_t* rec) {
     rec->leaves = leaves;
     rec->inserted = sm->total;
     rec->pruned = internal - sm->total;
-    if (leaves > 0 && sm->leaf_key != ~0ull) {
-        int32_t v = (int32_t)(sm->leaf_key >> 32);
+    int32_t v;
+    int64_t vpos;
+    if (leaves > 0 && round_leaf(sm, &v, &vpos)) {
         if (ctx->frozen) {
             // frozen incumbent: track the best leaf strictly under UB (bench.hpp:99-102)
             if (v < ctx->incumbent && (!ctx->found || v < ctx->best)) {
@@ -429,6 +453,10 @@ int explorer_round(fbb_ctx* ctx, int64_t target, fbb_round_t* rec) {
     rec->k2_ms = ctx->last_k2_ms;
     rec->round_ms = ctx->last_round_ms;
     rec->launches = ctx->last_launches;
+    if (ctx->check) {
+        int rc2 = check_pending(ctx);
+        if (rc2 != FBB_OK) return rc2;
+    }
     ctx->tot_branched += rec->branched;
     ctx->tot_bounded += rec->bounded;
     ctx->tot_pruned += rec->pruned;
@@ -476,6 +504,18 @@ fbb_ctx* fbb_create(int device, const int32_t* p, int n, int m) {
         return fail(FBB_E_CUDA, std::string("stream: ") + cudaGetErrorString(e));
     }
     for (cudaEvent_t& ev : ctx->ev) cudaEventCreate(&ev);
+    {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t keep_all = UINT64_MAX;  // retain freed blocks for reuse
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep_all);
+        }
+        for (DBuf* b : {&ctx->k1_masks, &ctx->k1_heads, &ctx->k1_depth, &ctx->k1_lb, &ctx->out_lb,
+                        &ctx->flags, &ctx->d_pool, &ctx->d_round})
+            b->st = ctx->stream;
+        for (Store* st : {&ctx->batch_in, &ctx->batch_out})
+            st->masks.st = st->heads.st = st->prefix.st = ctx->stream;
+    }
     rc = upload_tables(ctx->ht, &ctx->dt, &why);
     if (rc != FBB_OK) {
         fbb_destroy(ctx);
@@ -500,6 +540,8 @@ fbb_ctx* fbb_create(int device, const int32_t* p, int n, int m) {
     }
     explorer_clear(ctx);
     ctx->incumbent = INT_MAX;
+    const char* chk = getenv("FBB_CHECK");
+    ctx->check = chk && chk[0] == '1';
     return ctx;
 }
 
@@ -508,8 +550,7 @@ void fbb_destroy(fbb_ctx* ctx) {
     cudaSetDevice(ctx->device);
     free_tables(&ctx->dt);
     for (DBuf* b : {&ctx->k1_masks, &ctx->k1_heads, &ctx->k1_depth, &ctx->k1_lb, &ctx->out_lb,
-                    &ctx->staging_masks, &ctx->staging_heads, &ctx->staging_prefix, &ctx->staging_lb,
-                    &ctx->chunk_count, &ctx->offsets, &ctx->d_pool, &ctx->d_leaf_key, &ctx->d_summary})
+                    &ctx->flags, &ctx->d_pool, &ctx->d_round})
         b->release();
     for (Store* s : {&ctx->batch_in, &ctx->batch_out}) {
         s->masks.release();
@@ -521,8 +562,9 @@ void fbb_destroy(fbb_ctx* ctx) {
         s.heads.release();
         s.prefix.release();
     }
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     ctx->h_pool.release();
-    ctx->h_summary.release();
+    ctx->h_round.release();
     for (cudaEvent_t ev : ctx->ev)
         if (ev) cudaEventDestroy(ev);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -662,7 +704,7 @@ int fbb_expand_bound_prune(fbb_ctx* ctx, const uint64_t* masks, const int32_t* h
     }
     int rc = run_pool(ctx, pool, first_internal, ub, frozen);
     if (rc != FBB_OK) return rc;
-    const RoundSummary* sm = ctx->h_summary.as<RoundSummary>();
+    const RoundState* sm = ctx->h_round.as<RoundState>();
     int64_t total = sm->total;
     *out_count = total;
     if (total > 0) {
@@ -697,11 +739,12 @@ int fbb_expand_bound_prune(fbb_ctx* ctx, const uint64_t* masks, const int32_t* h
     rec.k2_ms = ctx->last_k2_ms;
     rec.round_ms = ctx->last_round_ms;
     rec.launches = ctx->last_launches;
-    if (leaves > 0 && sm->leaf_key != ~0ull) {
-        int32_t v = (int32_t)(sm->leaf_key >> 32);
+    int32_t v;
+    int64_t vpos;
+    if (leaves > 0 && round_leaf(sm, &v, &vpos)) {
         if (v < ub) {
             if (leaf_best) *leaf_best = v;
-            if (leaf_pos) *leaf_pos = (int64_t)(sm->leaf_key & 0xFFFFFFFFull);
+            if (leaf_pos) *leaf_pos = vpos;
             if (leaf_schedule && sm->found) std::memcpy(leaf_schedule, sm->schedule, (size_t)n * 4);
             if (!frozen) rec.incumbent = v;
         }
@@ -819,9 +862,12 @@ int fbb_explorer_pending(fbb_ctx* ctx, uint8_t* prefix, int32_t* depth, int64_t 
     for (int d = 0; d <= n; ++d) {
         int64_t k = ctx->cnt[d];
         if (k == 0) continue;
-        if (prefix)
-            CK(cudaMemcpy(prefix + o * n, ctx->bucket[d].prefix.p, (size_t)k * n, cudaMemcpyDeviceToHost),
+        if (prefix) {
+            CK(cudaMemcpyAsync(prefix + o * n, ctx->bucket[d].prefix.p, (size_t)k * n,
+                               cudaMemcpyDeviceToHost, ctx->stream),
                "pending D2H");
+            CK(cudaStreamSynchronize(ctx->stream), "pending D2H");
+        }
         if (depth)
             for (int64_t i = 0; i < k; ++i) depth[o + i] = d;
         o += k;

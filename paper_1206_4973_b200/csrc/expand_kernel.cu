@@ -29,7 +29,7 @@
 // child in a pool because the leaf-producing bucket is the deepest one).
 #include <climits>
 
-#include "fbb_internal.h"
+#include "k2_common.cuh"
 
 namespace fbb {
 
@@ -40,7 +40,7 @@ constexpr int32_t kNeg = -(1 << 20);
 __host__ __device__ inline size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
 
 struct K2Layout {
-    size_t jm, pk, p, tl, um, R, rank, ujob, load, min1, min2, amin, Mq, cR, cL, wsum, total;
+    size_t jm, pk, p, tl, um, R, rank, ujob, load, min1, min2, amin, Mq, cR, cL, pre, wsum, total;
     int ppc_max, pst, mst;
 };
 
@@ -67,7 +67,8 @@ __host__ __device__ inline K2Layout k2_layout(int n, int m, int P, int cmax, int
     L.Mq = o;   o = a16(o + (size_t)cmax * L.pst * 2);
     L.cR = o;   o = a16(o + (size_t)cmax * L.mst * 4);
     L.cL = o;   o = a16(o + (size_t)cmax * L.mst * 4);
-    L.wsum = o; o = a16(o + (size_t)(threads / 32 + 1) * 4);
+    L.pre = o;  o = a16(o + (size_t)L.ppc_max * n);
+    L.wsum = o; o = a16(o + (size_t)(threads / 32 + 2) * 8);
     L.total = o;
     return L;
 }
@@ -88,9 +89,8 @@ __device__ inline bool um_test(const uint32_t* um, int j) { return (um[j >> 5] >
 template <bool kJmSmem>
 __global__ void __launch_bounds__(128) k2_internal_kernel(DevTables t, const Pool* __restrict__ pool,
                                                          int first_seg, int cmax, int32_t ub,
-                                                         int frozen,
-                                                         const unsigned long long* __restrict__ leaf_key,
-                                                         Staging st) {
+                                                         int frozen, RoundState* rs,
+                                                         uint64_t* flags, uint32_t epoch) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int n = t.n, m = t.m, P = t.P, W = t.W;
     const int W32 = (n + 31) / 32;
@@ -110,7 +110,9 @@ __global__ void __launch_bounds__(128) k2_internal_kernel(DevTables t, const Poo
     int16_t* s_Mq = (int16_t*)(smem + L.Mq);
     int32_t* s_cR = (int32_t*)(smem + L.cR);
     int32_t* s_cL = (int32_t*)(smem + L.cL);
-    int32_t* s_wsum = (int32_t*)(smem + L.wsum);
+    uint8_t* s_pre = (uint8_t*)(smem + L.pre);
+    int64_t* s_slot = (int64_t*)(smem + L.wsum);
+    int32_t* s_wsum = (int32_t*)(smem + L.wsum + 16);
     const int tid = threadIdx.x, bd = blockDim.x, lane = tid & 31, warp = tid >> 5;
     const int nwarps = bd >> 5;
 
@@ -123,15 +125,16 @@ __global__ void __launch_bounds__(128) k2_internal_kernel(DevTables t, const Poo
     }
     // incumbent for internal children: min(UB, batch leaf minimum) unless frozen
     int32_t ub_eff = ub;
-    if (!frozen && leaf_key) {
-        unsigned long long key = *leaf_key;
-        int32_t v = (int32_t)(key >> 32);
-        if (key != ~0ull && v < ub_eff) ub_eff = v;
+    if (!frozen) {
+        unsigned long long inv = rs->leaf_inv;
+        int32_t v = (int32_t)((~inv) >> 32);
+        if (inv != 0ull && v < ub_eff) ub_eff = v;
     }
 
     const int64_t c_begin = pool->seg[first_seg].chunk_base;
     const int64_t c_end = pool->nchunks;
-    for (int64_t chunk = c_begin + blockIdx.x; chunk < c_end; chunk += gridDim.x) {
+    for (int64_t chunk = claim_chunk(rs, c_begin, s_slot); chunk < c_end;
+         chunk = claim_chunk(rs, c_begin, s_slot)) {
         const int s = find_segment(pool, first_seg, chunk);
         const Segment& sg = pool->seg[s];
         const int depth = sg.depth;
@@ -142,8 +145,11 @@ __global__ void __launch_bounds__(128) k2_internal_kernel(DevTables t, const Poo
         const int nc = np * r;
         const NodeStore src = sg.src;
         const int64_t first = sg.first, step = sg.step;
-        __syncthreads();  // previous chunk consumed; tables staged
-        // ---- stage parents
+        // ---- stage parents (all global parent reads happen before the look-back)
+        for (int x = tid; x < np * depth; x += bd) {
+            int pp = x / depth, i = x - pp * depth;
+            s_pre[pp * n + i] = src.prefix[(first + step * (p0 + pp)) * n + i];
+        }
         for (int x = tid; x < np * W32; x += bd) {
             int pp = x / W32, w = x - pp * W32;
             int64_t node = first + step * (p0 + pp);
@@ -253,16 +259,35 @@ __global__ void __launch_bounds__(128) k2_internal_kernel(DevTables t, const Poo
             cR[m] = lb;  // stash the bound in the row's spare slot
         }
         __syncthreads();
-        // ---- prune + stable compaction into staging[chunk]
+        // ---- prune + stable compaction straight into the destination
         int base_off = 0;
+        for (int c0 = 0; c0 < nc; c0 += bd) {  // survivor count first
+            int c = c0 + tid;
+            bool keep = c < nc && s_cR[c * L.mst + m] < ub_eff;
+            unsigned ballot = __ballot_sync(0xFFFFFFFFu, keep);
+            if (lane == 0) s_wsum[warp] = __popc(ballot);
+            __syncthreads();
+            int tot = 0;
+            for (int w = 0; w < nwarps; ++w) tot += s_wsum[w];
+            base_off += tot;
+            __syncthreads();
+        }
+        if (warp == 0) {
+            const int64_t excl = lookback_warp(flags, epoch, c_begin, chunk, base_off);
+            if (lane == 0) {
+                const int64_t nch = (sg.count + ppc - 1) / ppc;
+                *s_slot = chunk_output_base(pool, s, chunk, c_begin, nch, excl, base_off, flags,
+                                            epoch, rs);
+            }
+        }
+        __syncthreads();
+        const int64_t out0 = *s_slot;
+        const NodeStore dst = sg.dst;
+        int run = 0;
         for (int c0 = 0; c0 < nc; c0 += bd) {
             int c = c0 + tid;
-            bool keep = false;
-            int32_t lb = 0;
-            if (c < nc) {
-                lb = s_cR[c * L.mst + m];
-                keep = lb < ub_eff;
-            }
+            int32_t lb = c < nc ? s_cR[c * L.mst + m] : 0;
+            bool keep = c < nc && lb < ub_eff;
             unsigned ballot = __ballot_sync(0xFFFFFFFFu, keep);
             if (lane == 0) s_wsum[warp] = __popc(ballot);
             __syncthreads();
@@ -273,12 +298,11 @@ __global__ void __launch_bounds__(128) k2_internal_kernel(DevTables t, const Poo
                 tot += v;
             }
             if (keep) {
-                int rank = base_off + woff + __popc(ballot & ((1u << lane) - 1u));
-                int64_t o = chunk * (int64_t)cmax + rank;
+                const int64_t o = out0 + run + woff + __popc(ballot & ((1u << lane) - 1u));
                 int pp = c / r, rk = c - pp * r;
                 int xj = s_ujob[pp * n + rk];
                 const int32_t* cR = s_cR + c * L.mst;
-                for (int k = 0; k < m; ++k) st.nodes.heads[o * m + k] = cR[k];
+                for (int k = 0; k < m; ++k) dst.heads[o * m + k] = cR[k];
                 const uint32_t* um = s_um + pp * W32;
                 for (int w = 0; w < W; ++w) {
                     uint32_t lo = 2 * w < W32 ? um[2 * w] : 0u;
@@ -289,26 +313,23 @@ __global__ void __launch_bounds__(128) k2_internal_kernel(DevTables t, const Poo
                     uint32_t mhi = vhi >= 32 ? 0xFFFFFFFFu : ((1u << vhi) - 1u);
                     uint64_t sched = ((uint64_t)(~hi & mhi) << 32) | (uint64_t)(~lo & mlo);
                     if ((xj >> 6) == w) sched |= (uint64_t)1 << (xj & 63);
-                    st.nodes.masks[o * W + w] = sched;
+                    dst.masks[o * W + w] = sched;
                 }
-                int64_t node = first + step * (p0 + pp);
-                const uint8_t* pre = src.prefix + node * n;
-                uint8_t* dst = st.nodes.prefix + o * n;
-                for (int i = 0; i < depth; ++i) dst[i] = pre[i];
-                dst[depth] = (uint8_t)xj;
-                if (st.lb) st.lb[o] = lb;
+                uint8_t* dp = dst.prefix + o * n;
+                for (int i = 0; i < depth; ++i) dp[i] = s_pre[pp * n + i];
+                dp[depth] = (uint8_t)xj;
+                if (sg.dst_lb) sg.dst_lb[o] = lb;
             }
-            base_off += tot;
+            run += tot;
             __syncthreads();
         }
-        if (tid == 0) st.chunk_count[chunk] = base_off;
     }
 }
 
 // Children of parents at depth >= n-2 are complete schedules: bound = makespan
 // (bound.hpp:95).  Thread per child; batch-minimum (value, position) by atomicMin.
 __global__ void k2_leaf_kernel(DevTables t, const Pool* __restrict__ pool, int seg_index,
-                               int32_t ub, unsigned long long* leaf_key) {
+                               RoundState* rs) {
     const int n = t.n, m = t.m, W = t.W;
     const Segment& sg = pool->seg[seg_index];
     const int depth = sg.depth;
@@ -324,6 +345,10 @@ __global__ void k2_leaf_kernel(DevTables t, const Pool* __restrict__ pool, int s
         int u[2] = {-1, -1}, cnt = 0;
         for (int j = 0; j < n && cnt < 2; ++j)
             if (!((mk[j >> 6] >> (j & 63)) & 1ull)) u[cnt++] = j;
+        if (cnt < r) {  // a pending node must have exactly r unscheduled jobs
+            atomicExch(&rs->found, -1);
+            continue;
+        }
         int x = u[rk], y = (r == 2) ? u[1 - rk] : -1;
         int32_t prev = 0, h[kMaxMachines];
         const int32_t* R = sg.src.heads + node * m;
@@ -338,23 +363,20 @@ __global__ void k2_leaf_kernel(DevTables t, const Pool* __restrict__ pool, int s
                 h[k] = prev;
             }
         }
-        int32_t lb = h[m - 1];
-        if (lb < ub) {
-            unsigned long long key = ((unsigned long long)(uint32_t)lb << 32) |
-                                     (unsigned long long)(uint32_t)(sg.child_base + c);
-            atomicMin(leaf_key, key);
-        }
+        leaf_offer(rs, h[m - 1], sg.child_base + c);
     }
 }
 
 // Writes the schedule of the batch's best leaf (if it beats ub) before the
 // parents' storage is recycled by the push.
-__global__ void leaf_schedule_kernel(DevTables t, const Pool* __restrict__ pool,
-                                     const unsigned long long* __restrict__ leaf_key,
-                                     int32_t* schedule, int32_t* found, int32_t ub) {
+__global__ void leaf_schedule_kernel(DevTables t, const Pool* __restrict__ pool, RoundState* rs,
+                                     int32_t ub) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    unsigned long long key = *leaf_key;
-    if (key == ~0ull || (int32_t)(key >> 32) >= ub) {
+    unsigned long long inv = rs->leaf_inv;
+    unsigned long long key = ~inv;
+    int32_t* schedule = rs->schedule;
+    int32_t* found = &rs->found;
+    if (inv == 0ull || (int32_t)(key >> 32) >= ub) {
         *found = 0;
         return;
     }
@@ -375,69 +397,6 @@ __global__ void leaf_schedule_kernel(DevTables t, const Pool* __restrict__ pool,
     schedule[sg.depth] = u[rk];
     if (r == 2) schedule[sg.depth + 1] = u[1 - rk];
     *found = 1;
-}
-
-// Exclusive scan of per-chunk survivor counts (single CTA; a pool has at most
-// a few thousand chunks).  offsets[nchunks] = total.
-__global__ void chunk_scan_kernel(const int32_t* __restrict__ cnt, int64_t c0, int64_t nchunks,
-                                  int64_t* offsets) {
-    __shared__ int64_t warp_tot[32];
-    __shared__ int64_t carry;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-    if (tid == 0) carry = 0;
-    for (int64_t i = tid; i < c0; i += blockDim.x) offsets[i] = 0;  // leaf-segment chunks: none
-    __syncthreads();
-    for (int64_t base = c0; base < nchunks; base += blockDim.x) {
-        int64_t i = base + tid;
-        int64_t v = i < nchunks ? cnt[i] : 0;
-        int64_t incl = v;
-        for (int o = 1; o < 32; o <<= 1) {
-            int64_t u = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-            if (lane >= o) incl += u;
-        }
-        if (lane == 31) warp_tot[warp] = incl;
-        __syncthreads();
-        int64_t woff = 0, tot = 0;
-        for (int w = 0; w < nw; ++w) {
-            if (w < warp) woff += warp_tot[w];
-            tot += warp_tot[w];
-        }
-        if (i < nchunks) offsets[i] = carry + woff + incl - v;
-        __syncthreads();
-        if (tid == 0) carry += tot;
-        __syncthreads();
-    }
-    if (tid == 0) offsets[nchunks] = carry;
-}
-
-// Copies survivors from staging to their destination: segment `dst` store at
-// dst_base + (offsets[c] - offsets[chunk_base]), or contiguous at offsets[c]
-// when dst_base < 0.  CTA per chunk (grid-stride).
-__global__ void append_kernel(DevTables t, const Pool* __restrict__ pool, int first_seg, int cmax,
-                              Staging st, const int64_t* __restrict__ offsets) {
-    const int n = t.n, m = t.m, W = t.W;
-    const int64_t c_begin = pool->seg[first_seg].chunk_base, c_end = pool->nchunks;
-    for (int64_t chunk = c_begin + blockIdx.x; chunk < c_end; chunk += gridDim.x) {
-        const int s = find_segment(pool, first_seg, chunk);
-        const Segment& sg = pool->seg[s];
-        int cnt = st.chunk_count[chunk];
-        if (cnt == 0) continue;
-        int64_t pos = sg.dst_base < 0 ? offsets[chunk]
-                                      : sg.dst_base + offsets[chunk] - offsets[sg.chunk_base];
-        int64_t so = chunk * (int64_t)cmax;
-        const NodeStore dst = sg.dst;
-        for (int x = threadIdx.x; x < cnt * m; x += blockDim.x)
-            dst.heads[pos * m + x] = st.nodes.heads[so * m + x];
-        for (int x = threadIdx.x; x < cnt * W; x += blockDim.x)
-            dst.masks[pos * W + x] = st.nodes.masks[so * W + x];
-        const int dlen = sg.depth + 1;
-        for (int x = threadIdx.x; x < cnt * n; x += blockDim.x) {
-            int i = x / n, b = x - i * n;
-            if (b < dlen) dst.prefix[(pos + i) * n + b] = st.nodes.prefix[(so + i) * n + b];
-        }
-        if (sg.dst_lb && st.lb)
-            for (int x = threadIdx.x; x < cnt; x += blockDim.x) sg.dst_lb[pos + x] = st.lb[so + x];
-    }
 }
 
 }  // namespace
@@ -465,59 +424,39 @@ K2Config k2_config(const DevTables& t, int device) {
     return c;
 }
 
-cudaError_t launch_k2_leaves(const DevTables& t, const K2Config& cfg, const Pool* d_pool,
-                             const Pool& h_pool, int seg_index, unsigned long long* leaf_key,
-                             cudaStream_t stream) {
-    (void)cfg;
+cudaError_t launch_k2_leaves(const DevTables& t, const Pool* d_pool, const Pool& h_pool,
+                             int seg_index, RoundState* rs, cudaStream_t stream) {
     const Segment& sg = h_pool.seg[seg_index];
     int64_t nc = sg.count * (t.n - sg.depth);
     if (nc <= 0) return cudaSuccess;
     int blocks = (int)((nc + 255) / 256);
     if (blocks > 4096) blocks = 4096;
-    k2_leaf_kernel<<<blocks, 256, 0, stream>>>(t, d_pool, seg_index, INT_MAX, leaf_key);
+    k2_leaf_kernel<<<blocks, 256, 0, stream>>>(t, d_pool, seg_index, rs);
     return cudaGetLastError();
 }
 
 cudaError_t launch_k2_internal(const DevTables& t, const K2Config& cfg, const Pool* d_pool,
                                const Pool& h_pool, int first_seg, int32_t ub, int frozen,
-                               const unsigned long long* leaf_key, Staging st,
+                               RoundState* rs, uint64_t* flags, uint32_t epoch,
                                cudaStream_t stream) {
     if (first_seg >= h_pool.nseg) return cudaSuccess;
     int64_t nch = h_pool.nchunks - h_pool.seg[first_seg].chunk_base;
     if (nch <= 0) return cudaSuccess;
     int blocks = (int)(nch < cfg.blocks ? nch : cfg.blocks);
     if (cfg.variant != 0)
-        return launch_k2_v2(t, cfg, d_pool, first_seg, blocks, ub, frozen, leaf_key, st, stream);
+        return launch_k2_v2(t, cfg, d_pool, first_seg, blocks, ub, frozen, rs, flags, epoch, stream);
     if (cfg.jm_in_smem)
         k2_internal_kernel<true><<<blocks, cfg.threads, cfg.smem, stream>>>(t, d_pool, first_seg, cfg.cmax,
-                                                                            ub, frozen, leaf_key, st);
+                                                                            ub, frozen, rs, flags, epoch);
     else
         k2_internal_kernel<false><<<blocks, cfg.threads, cfg.smem, stream>>>(t, d_pool, first_seg, cfg.cmax,
-                                                                             ub, frozen, leaf_key, st);
+                                                                             ub, frozen, rs, flags, epoch);
     return cudaGetLastError();
 }
 
-cudaError_t launch_chunk_scan(const int32_t* chunk_count, int64_t c0, int64_t nchunks,
-                              int64_t* offsets, cudaStream_t stream) {
-    chunk_scan_kernel<<<1, 1024, 0, stream>>>(chunk_count, c0, nchunks, offsets);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_append(const DevTables& t, const K2Config& cfg, const Pool* d_pool,
-                          const Pool& h_pool, int first_seg, Staging st, const int64_t* offsets,
-                          cudaStream_t stream) {
-    if (first_seg >= h_pool.nseg) return cudaSuccess;
-    int64_t nch = h_pool.nchunks - h_pool.seg[first_seg].chunk_base;
-    if (nch <= 0) return cudaSuccess;
-    int blocks = (int)(nch < 8192 ? nch : 8192);
-    append_kernel<<<blocks, 128, 0, stream>>>(t, d_pool, first_seg, cfg.cmax, st, offsets);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_leaf_schedule(const DevTables& t, const Pool* d_pool,
-                                 const unsigned long long* leaf_key, int32_t* schedule,
-                                 int32_t* found_flag, int32_t ub, cudaStream_t stream) {
-    leaf_schedule_kernel<<<1, 32, 0, stream>>>(t, d_pool, leaf_key, schedule, found_flag, ub);
+cudaError_t launch_leaf_schedule(const DevTables& t, const Pool* d_pool, RoundState* rs,
+                                 int32_t ub, cudaStream_t stream) {
+    leaf_schedule_kernel<<<1, 32, 0, stream>>>(t, d_pool, rs, ub);
     return cudaGetLastError();
 }
 

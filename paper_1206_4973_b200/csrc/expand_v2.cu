@@ -13,7 +13,7 @@
 //    conflict-free).
 #include <climits>
 
-#include "fbb_internal.h"
+#include "k2_common.cuh"
 
 namespace fbb {
 
@@ -30,7 +30,7 @@ __host__ __device__ inline int v2_row_bytes(int P) {
 }
 
 struct V2Layout {
-    size_t row, um, rank, R, load, mins, amin, Mq, p, wsum, total;
+    size_t row, um, rank, R, load, mins, amin, Mq, p, pre, wsum, total;
     int ppc_max, rowb;
 };
 
@@ -48,7 +48,8 @@ __host__ __device__ inline V2Layout v2_layout(int n, int m, int P, int cmax, int
     L.amin = o; o = b16(o + (size_t)L.ppc_max * m);
     L.Mq = o;   o = b16(o + (size_t)(cmax + 1) * L.rowb);  // + a dummy row for non-members
     L.p = o;    o = b16(o + (size_t)n * m * 4);
-    L.wsum = o; o = b16(o + (size_t)(threads / 32 + 1) * 4);
+    L.pre = o;  o = b16(o + (size_t)L.ppc_max * 32);
+    L.wsum = o; o = b16(o + (size_t)(threads / 32 + 2) * 8);
     L.total = o;
     return L;
 }
@@ -62,14 +63,16 @@ __device__ inline int v2_find_segment(const Pool* __restrict__ pool, int lo, int
     return lo;
 }
 
+// Non-volatile: ptxas may schedule these loads early (the tables are read-only
+// after staging).
 __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
     uint32_t v;
-    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
     return v;
 }
 __device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
     uint32_t v;
-    asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
+    asm("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
     return v;
 }
 __device__ __forceinline__ void sts_u16(uint32_t addr, int32_t v) {
@@ -92,10 +95,9 @@ struct PairTab {  // (k, l) of pair index q in bound.hpp:97-98 order
 };
 
 template <int N, int M>
-__global__ void __launch_bounds__(192, 4) k2_v2_kernel(DevTables t, const Pool* __restrict__ pool,
+__global__ void __launch_bounds__(192, 2) k2_v2_kernel(DevTables t, const Pool* __restrict__ pool,
                                                    int first_seg, int cmax, int32_t ub, int frozen,
-                                                   const unsigned long long* __restrict__ leaf_key,
-                                                   Staging st) {
+                                                   RoundState* rs, uint64_t* flags, uint32_t epoch) {
     constexpr int P = M * (M - 1) / 2;
     extern __shared__ __align__(16) unsigned char smem[];
     const int n = t.n, W = t.W;
@@ -108,7 +110,9 @@ __global__ void __launch_bounds__(192, 4) k2_v2_kernel(DevTables t, const Pool* 
     uint8_t* s_amin = (uint8_t*)(smem + L.amin);
     unsigned char* s_Mq = smem + L.Mq;
     int32_t* s_p = (int32_t*)(smem + L.p);
-    int32_t* s_wsum = (int32_t*)(smem + L.wsum);
+    uint8_t* s_pre = (uint8_t*)(smem + L.pre);
+    int64_t* s_slot = (int64_t*)(smem + L.wsum);
+    int32_t* s_wsum = (int32_t*)(smem + L.wsum + 16);
     const int tid = threadIdx.x, bd = blockDim.x, lane = tid & 31, warp = tid >> 5;
     const int nwarps = bd >> 5;
     const int G = bd / P;
@@ -133,15 +137,16 @@ __global__ void __launch_bounds__(192, 4) k2_v2_kernel(DevTables t, const Pool* 
     const uint32_t row_sa = (uint32_t)__cvta_generic_to_shared(s_row + q);
 
     int32_t ub_eff = ub;
-    if (!frozen && leaf_key) {
-        unsigned long long key = *leaf_key;
-        int32_t v = (int32_t)(key >> 32);
-        if (key != ~0ull && v < ub_eff) ub_eff = v;
+    if (!frozen) {
+        unsigned long long inv = rs->leaf_inv;
+        int32_t v = (int32_t)((~inv) >> 32);
+        if (inv != 0ull && v < ub_eff) ub_eff = v;
     }
 
     const int64_t c_begin = pool->seg[first_seg].chunk_base;
     const int64_t c_end = pool->nchunks;
-    for (int64_t chunk = c_begin + blockIdx.x; chunk < c_end; chunk += gridDim.x) {
+    for (int64_t chunk = claim_chunk(rs, c_begin, s_slot); chunk < c_end;
+         chunk = claim_chunk(rs, c_begin, s_slot)) {
         const int s = v2_find_segment(pool, first_seg, chunk);
         const Segment& sg = pool->seg[s];
         const int depth = sg.depth;
@@ -152,7 +157,11 @@ __global__ void __launch_bounds__(192, 4) k2_v2_kernel(DevTables t, const Pool* 
         const int nc = np * r;
         const NodeStore src = sg.src;
         const int64_t first = sg.first, step = sg.step;
-        __syncthreads();
+        // every global read of the parents happens before this chunk publishes
+        for (int x = tid; x < np * depth; x += bd) {
+            int pp = x / depth, i = x - pp * depth;
+            s_pre[pp * 32 + i] = src.prefix[(first + step * (p0 + pp)) * n + i];
+        }
         for (int pp = tid; pp < np; pp += bd) {
             int64_t node = first + step * (p0 + pp);
             uint32_t sched = (uint32_t)src.masks[node * W];
@@ -199,14 +208,21 @@ __global__ void __launch_bounds__(192, 4) k2_v2_kernel(DevTables t, const Pool* 
                 const uint32_t dummy_sa =
                     (uint32_t)__cvta_generic_to_shared(s_Mq + (size_t)cmax * L.rowb + 2 * q);
                 const uint32_t rowb = (uint32_t)L.rowb;
+                // the row once into registers (loads issued back to back), then the
+                // ranks of its jobs, so neither pass waits on shared-memory latency
+                uint32_t e[N];
+#pragma unroll
+                for (int i = 0; i < N; ++i) e[i] = lds_u32(row_sa + (uint32_t)(i * P * 4));
+                uint32_t rk[N];
+#pragma unroll
+                for (int i = 0; i < N; ++i) rk[i] = lds_u8(rank_sa + (e[i] & 31u));
                 int32_t D = 0, PM = kNeg2;
                 int32_t pm[N];
 #pragma unroll
                 for (int i = 0; i < N; ++i) {
-                    const uint32_t e = lds_u32(row_sa + (uint32_t)(i * P * 4));
-                    const bool in = (__funnelshift_r(um, 0u, e) & 1u) != 0u;  // shift = e & 31
-                    const int32_t c = (int32_t)__byte_perm(e, 0u, 0x4421);    // bytes 1..2
-                    const int32_t d = (int32_t)e >> 24;
+                    const bool in = (__funnelshift_r(um, 0u, e[i]) & 1u) != 0u;  // shift = e & 31
+                    const int32_t c = (int32_t)__byte_perm(e[i], 0u, 0x4421);    // bytes 1..2
+                    const int32_t d = (int32_t)e[i] >> 24;
                     pm[i] = PM;
                     PM = in ? max(PM, D + c) : PM;
                     D = in ? D + d : D;
@@ -214,15 +230,13 @@ __global__ void __launch_bounds__(192, 4) k2_v2_kernel(DevTables t, const Pool* 
                 int32_t SM = kNeg2;
 #pragma unroll
                 for (int i = N - 1; i >= 0; --i) {
-                    const uint32_t e = lds_u32(row_sa + (uint32_t)(i * P * 4));
-                    const bool in = (__funnelshift_r(um, 0u, e) & 1u) != 0u;
-                    const int32_t c = (int32_t)__byte_perm(e, 0u, 0x4421);
-                    const int32_t d = (int32_t)e >> 24;
+                    const bool in = (__funnelshift_r(um, 0u, e[i]) & 1u) != 0u;
+                    const int32_t c = (int32_t)__byte_perm(e[i], 0u, 0x4421);
+                    const int32_t d = (int32_t)e[i] >> 24;
                     const int32_t Db = D - d;  // D before position i
                     // finite for members of U with |U| >= 3 (internal children), fits int16
                     const int32_t mp = max(pm[i], SM - d);
-                    const uint32_t rk = lds_u8(rank_sa + (e & 31u));
-                    sts_u16(in ? out_sa + rk * rowb : dummy_sa, mp);
+                    sts_u16(in ? out_sa + rk[i] * rowb : dummy_sa, mp);
                     SM = in ? max(SM, Db + c) : SM;
                     D = in ? Db : D;
                 }
@@ -271,7 +285,7 @@ __global__ void __launch_bounds__(192, 4) k2_v2_kernel(DevTables t, const Pool* 
             }
             mylb = lb;
         }
-        // ---- prune + stable compaction into staging[chunk] (one child per thread)
+        // ---- prune + stable compaction straight into the destination (one child per thread)
         const bool keep = b_lane && mylb < ub_eff;
         const unsigned ballot = __ballot_sync(0xFFFFFFFFu, keep);
         if (lane == 0) s_wsum[warp] = __popc(ballot);
@@ -282,22 +296,27 @@ __global__ void __launch_bounds__(192, 4) k2_v2_kernel(DevTables t, const Pool* 
             if (w < warp) woff += v;
             tot += v;
         }
+        if (warp == 0) {
+            const int64_t excl = lookback_warp(flags, epoch, c_begin, chunk, tot);
+            if (lane == 0) {
+                const int64_t nch = (sg.count + ppc - 1) / ppc;
+                *s_slot = chunk_output_base(pool, s, chunk, c_begin, nch, excl, tot, flags, epoch, rs);
+            }
+        }
+        __syncthreads();
         if (keep) {
-            const int rank = woff + __popc(ballot & ((1u << lane) - 1u));
-            const int64_t o = chunk * (int64_t)cmax + rank;
+            const int64_t o = *s_slot + woff + __popc(ballot & ((1u << lane) - 1u));
+            const NodeStore dst = sg.dst;
 #pragma unroll
-            for (int k = 0; k < M; ++k) st.nodes.heads[o * M + k] = myR[k];
+            for (int k = 0; k < M; ++k) dst.heads[o * M + k] = myR[k];
             const uint32_t um = s_um[mypp];
             const uint32_t valid = n >= 32 ? 0xFFFFFFFFu : ((1u << n) - 1u);
-            st.nodes.masks[o * W] = (uint64_t)((~um & valid) | (1u << myx));
-            const int64_t node = first + step * (p0 + mypp);
-            const uint8_t* pre = src.prefix + node * n;
-            uint8_t* dst = st.nodes.prefix + o * n;
-            for (int i = 0; i < depth; ++i) dst[i] = pre[i];
-            dst[depth] = (uint8_t)myx;
-            if (st.lb) st.lb[o] = mylb;
+            dst.masks[o * W] = (uint64_t)((~um & valid) | (1u << myx));
+            uint8_t* dp = dst.prefix + o * n;
+            for (int i = 0; i < depth; ++i) dp[i] = s_pre[mypp * 32 + i];
+            dp[depth] = (uint8_t)myx;
+            if (sg.dst_lb) sg.dst_lb[o] = mylb;
         }
-        if (tid == 0) st.chunk_count[chunk] = tot;
     }
 }
 
@@ -341,13 +360,13 @@ bool k2_v2_config(const DevTables& t, int device, K2Config* out) {
 }
 
 cudaError_t launch_k2_v2(const DevTables& t, const K2Config& cfg, const Pool* d_pool, int first_seg,
-                         int blocks, int32_t ub, int frozen, const unsigned long long* leaf_key,
-                         Staging st, cudaStream_t stream) {
+                         int blocks, int32_t ub, int frozen, RoundState* rs, uint64_t* flags,
+                         uint32_t epoch, cudaStream_t stream) {
 #define V2_CASE(NN, MM)                                                                       \
     case NN * 100 + MM:                                                                       \
         k2_v2_kernel<NN, MM><<<blocks, cfg.threads, cfg.smem, stream>>>(t, d_pool, first_seg,  \
                                                                          cfg.cmax, ub, frozen, \
-                                                                         leaf_key, st);       \
+                                                                         rs, flags, epoch);   \
         break;
     switch (cfg.variant) {
         V2_CASE(20, 5)

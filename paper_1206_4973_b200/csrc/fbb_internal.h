@@ -4,6 +4,7 @@
 
 #include <cuda_runtime.h>
 
+#include <cstddef>
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -99,7 +100,7 @@ struct Segment {
 
 struct Pool {
     int nseg;
-    int pad;
+    int pad;             // always 0 (an opaque zero for the kernels)
     int64_t nchunks;
     int64_t nchildren;
     Segment seg[kMaxSegments];
@@ -115,38 +116,36 @@ struct K2Config {
 };
 K2Config k2_config(const DevTables& t, int device);
 
-// Per-chunk outputs: survivors compacted inside the chunk at
-// staging[chunk*cmax ...], count in chunk_count[chunk].
-struct Staging {
-    NodeStore nodes;
-    int32_t* lb;
-    int32_t* chunk_count;
+// Per-round device state; the head (everything before `schedule`) is zeroed by
+// one memset before the round.
+struct RoundState {
+    unsigned long long leaf_inv;  // ~((best leaf value << 32) | batch position); 0 = no leaf
+    int32_t found;                // leaf schedule written (value < ub)
+    uint32_t ticket;              // next chunk to claim
+    int64_t total;                // survivors of the pool
+    int64_t seg_surv[kMaxSegments];
+    int32_t schedule[kMaxJobs];
 };
+constexpr size_t kRoundStateHead = offsetof(RoundState, schedule);
 
-// n <= 32, m in {5,10,20}: the register-row kernel; false when not applicable.
+// n <= 32, m in {5,10,20}: the register/shared-row kernel; false when not applicable.
 bool k2_v2_config(const DevTables& t, int device, K2Config* out);
 cudaError_t launch_k2_v2(const DevTables& t, const K2Config& cfg, const Pool* d_pool, int first_seg,
-                         int blocks, int32_t ub, int frozen, const unsigned long long* leaf_key,
-                         Staging st, cudaStream_t stream);
+                         int blocks, int32_t ub, int frozen, RoundState* rs, uint64_t* flags,
+                         uint32_t epoch, cudaStream_t stream);
 
-// Batch leaf minimum: packed (value << 32) | batch position, atomicMin.
-cudaError_t launch_k2_leaves(const DevTables& t, const K2Config& cfg, const Pool* d_pool,
-                             const Pool& h_pool, int seg_index, unsigned long long* leaf_key,
-                             cudaStream_t stream);
+// Leaves (parents at depth >= n-2): batch minimum (value, first position).
+cudaError_t launch_k2_leaves(const DevTables& t, const Pool* d_pool, const Pool& h_pool,
+                             int seg_index, RoundState* rs, cudaStream_t stream);
+// Internal children: bound, prune against min(ub, leaf minimum) (frozen: ub),
+// survivors written in batch order to each segment's dst.
 cudaError_t launch_k2_internal(const DevTables& t, const K2Config& cfg, const Pool* d_pool,
                                const Pool& h_pool, int first_seg, int32_t ub, int frozen,
-                               const unsigned long long* leaf_key, Staging st,
+                               RoundState* rs, uint64_t* flags, uint32_t epoch,
                                cudaStream_t stream);
-// Exclusive scan of chunk counts [c0, nchunks) -> offsets, offsets[nchunks] = total.
-cudaError_t launch_chunk_scan(const int32_t* chunk_count, int64_t c0, int64_t nchunks,
-                              int64_t* offsets, cudaStream_t stream);
-// Copies the survivors of every internal chunk from staging to its segment's dst.
-cudaError_t launch_append(const DevTables& t, const K2Config& cfg, const Pool* d_pool,
-                          const Pool& h_pool, int first_seg, Staging st, const int64_t* offsets,
-                          cudaStream_t stream);
-cudaError_t launch_leaf_schedule(const DevTables& t, const Pool* d_pool,
-                                 const unsigned long long* leaf_key, int32_t* schedule,
-                                 int32_t* found_flag, int32_t ub, cudaStream_t stream);
+// Schedule of the best leaf when it beats ub (before the parents are recycled).
+cudaError_t launch_leaf_schedule(const DevTables& t, const Pool* d_pool, RoundState* rs,
+                                 int32_t ub, cudaStream_t stream);
 
 // Chunk geometry of a segment: parents per chunk and chunk count.
 inline int parents_per_chunk(int n, int depth, int cmax) {
