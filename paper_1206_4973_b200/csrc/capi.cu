@@ -221,8 +221,11 @@ int run_pool(fbb_ctx* ctx, Pool& pool, int first_internal, int32_t ub, int froze
     RoundState* rs = ctx->d_round.as<RoundState>();
     bool has_leaf = pool.nseg > 0 && pool.seg[0].depth >= n - 2;
     if (has_leaf) {
+        // leaves, then the best leaf's schedule -- before K2 recycles the leaf
+        // parents' slots (bucket n-2 receives the next segment's survivors)
         CK(launch_k2_leaves(ctx->dt, dp, pool, 0, rs, st), "K2 leaves");
-        ++launches;
+        CK(launch_leaf_schedule(ctx->dt, dp, rs, ub, st), "leaf schedule");
+        launches += 2;
     }
     CK(cudaEventRecord(ctx->ev[1], st), "event");
     bool has_internal = first_internal < pool.nseg && pool.nchunks > 0;
@@ -231,10 +234,6 @@ int run_pool(fbb_ctx* ctx, Pool& pool, int first_internal, int32_t ub, int froze
        "K2 internal");
     CK(cudaEventRecord(ctx->ev[2], st), "event");
     if (has_internal) ++launches;
-    if (has_leaf) {
-        CK(launch_leaf_schedule(ctx->dt, dp, rs, ub, st), "leaf schedule");
-        ++launches;
-    }
     size_t head = offsetof(RoundState, seg_surv) + (size_t)pool.nseg * 8;
     CK(cudaMemcpyAsync(ctx->h_round.p, rs, head, cudaMemcpyDeviceToHost, st), "round D2H");
     if (has_leaf)
@@ -509,6 +508,22 @@ fbb_ctx* fbb_create(int device, const int32_t* p, int n, int m) {
         if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
             uint64_t keep_all = UINT64_MAX;  // retain freed blocks for reuse
             cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep_all);
+            // once per process and device: map a working set up front so that
+            // pending-tree growth during a run is a pool hit, not a new mapping
+            static std::mutex reserve_mu;
+            static bool reserved[64] = {false};
+            std::lock_guard<std::mutex> g(reserve_mu);
+            if (device < 64 && !reserved[device]) {
+                reserved[device] = true;
+                size_t free_b = 0, total_b = 0;
+                cudaMemGetInfo(&free_b, &total_b);
+                size_t want = std::min<size_t>((size_t)4 << 30, free_b / 16);
+                void* tmp = nullptr;
+                if (cudaMallocAsync(&tmp, want, ctx->stream) == cudaSuccess) {
+                    cudaFreeAsync(tmp, ctx->stream);
+                    cudaStreamSynchronize(ctx->stream);
+                }
+            }
         }
         for (DBuf* b : {&ctx->k1_masks, &ctx->k1_heads, &ctx->k1_depth, &ctx->k1_lb, &ctx->out_lb,
                         &ctx->flags, &ctx->d_pool, &ctx->d_round})

@@ -198,6 +198,7 @@ __global__ void __launch_bounds__(192, 2) k2_v2_kernel(DevTables t, const Pool* 
             s_mins[x] = (uint32_t)m1 | ((uint32_t)m2 << 16);
             s_amin[x] = (uint8_t)am;
         }
+        __syncthreads();  // rank table and per-machine terms visible to every lane
         // ---- Phase A: forward / backward max-plus scans of pair q over parent pp
         if (a_lane) {
             for (int pp = g; pp < np; pp += G) {
