@@ -542,10 +542,11 @@ fbb_ctx* fbb_create(int device, const int32_t* p, int n, int m) {
         // register-row K2 for n <= 32, m in {5,10,20}; tails packed as 16-bit there
         int32_t max_tail = 0;
         for (int32_t v : ctx->ht.tails) max_tail = std::max(max_tail, v);
-        K2Config v2;
-        const char* force = getenv("FBB_K2_GENERIC");
-        if (max_tail < 0x7FFF && !(force && force[0] == '1') && k2_v2_config(ctx->dt, device, &v2))
-            ctx->k2 = v2;
+        // FBB_K2=generic forces the generic kernel (A/B comparisons)
+        K2Config kc;
+        const char* sel = getenv("FBB_K2");
+        bool generic = sel && std::string(sel) == "generic";
+        if (max_tail < 0x7FFF && !generic && k2_v2_config(ctx->dt, device, &kc)) ctx->k2 = kc;
     }
     int max_smem = 0;
     cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);

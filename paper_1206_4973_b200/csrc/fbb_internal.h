@@ -110,7 +110,7 @@ struct K2Config {
     int threads = 128;
     int cmax = 128;      // children per chunk (>= n)
     bool jm_in_smem = true;
-    int variant = 0;     // 0: generic kernel; N*100+M: k2_v2_kernel<N, M> (expand_v2.cu)
+    int variant = 0;     // 0: generic kernel; N*100+M: k2_v2_kernel<N,M> (expand_v2.cu)
     int blocks = 0;
     size_t smem = 0;
 };

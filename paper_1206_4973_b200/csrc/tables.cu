@@ -8,6 +8,7 @@
 // comparator is a strict weak order on (group, key) and ties fall back to the
 // input (= job index) order.
 #include <algorithm>
+#include <climits>
 #include <numeric>
 
 #include "fbb_internal.h"
