@@ -21,7 +21,6 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
 import time
 
@@ -40,7 +39,7 @@ INT32_LANES_PER_SM = 128  # ALU pipe 64 + FMA pipe 64 integer lanes / clk / SM (
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--target", type=int, default=262144)
     ap.add_argument("--instance", default="ta021")
@@ -57,46 +56,64 @@ def dist_env():
             int(os.environ.get("LOCAL_RANK", 0)))
 
 
-def sample_clocks_start():
-    os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
-    try:
-        f = open(os.path.join(ROOT, "gpurun_out", f"clocks_{os.getpid()}.csv"), "w")
-        p = subprocess.Popen(
-            ["nvidia-smi", "--query-gpu=index,clocks.sm,clocks.max.sm,power.draw,"
-             "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-             "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "100"],
-            stdout=f, stderr=subprocess.DEVNULL)
-        return p, f
-    except Exception:
-        return None, None
+class ClockSampler:
+    """SM clock and throttle reasons DURING the timed region, polled through NVML from a
+    background thread every ~1 ms (nvidia-smi's 100 ms period would miss a few-ms region);
+    the raw samples go to gpurun_out/clocks_<pid>.csv."""
 
+    REASONS = {"hw_slowdown": "nvmlClocksEventReasonHwSlowdown",
+               "hw_thermal_slowdown": "nvmlClocksEventReasonHwThermalSlowdown",
+               "sw_thermal_slowdown": "nvmlClocksEventReasonSwThermalSlowdown",
+               "sw_power_cap": "nvmlClocksEventReasonSwPowerCap",
+               "hw_power_brake": "nvmlClocksEventReasonHwPowerBrakeSlowdown"}
 
-def sample_clocks_stop(handle, device):
-    p, f = handle
-    if p is None:
-        return None
-    p.terminate()
-    p.wait()
-    f.close()
-    sm, mx, reasons = [], 0, set()
-    names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-    for line in open(f.name):
-        parts = [x.strip() for x in line.split(",")]
-        if len(parts) < 9 or parts[0] != str(device):
-            continue
+    def __init__(self, device):
+        import threading
+
+        self.samples, self.stop = [], threading.Event()
         try:
-            sm.append(float(parts[1]))
-            mx = max(mx, float(parts[2]))
-        except ValueError:
-            continue
-        for nm, v in zip(names, parts[5:9]):
-            if v.lower() in ("active", "1", "yes"):
-                reasons.add(nm)
-    if not sm:
-        return None
-    return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
-            "samples": len(sm)}
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+            return
+        self.t = threading.Thread(target=self._run, daemon=True)
+        self.t.start()
+
+    def _run(self):
+        nv = self.nv
+        while not self.stop.is_set():
+            try:
+                mhz = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.samples.append((time.perf_counter(), mhz, rs))
+            except Exception:
+                pass
+            time.sleep(0.001)
+
+    def result(self):
+        if self.nv is None:
+            return None
+        self.stop.set()
+        self.t.join()
+        if not self.samples:
+            return None
+        os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+        with open(os.path.join(ROOT, "gpurun_out", f"clocks_{os.getpid()}.csv"), "w") as f:
+            for t, mhz, rs in self.samples:
+                f.write(f"{t:.6f},{mhz},{rs:#x}\n")
+        reasons = set()
+        for _, _, rs in self.samples:
+            for name, attr in self.REASONS.items():
+                if rs & getattr(self.nv, attr, 0):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(m for _, m, _ in self.samples),
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(reasons),
+                "samples": len(self.samples), "source": "NVML, ~1 ms polling"}
 
 
 def measured_peaks():
@@ -230,20 +247,20 @@ def main():
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
-    clocks_h = sample_clocks_start() if rank == 0 else (None, None)
-    rounds, timing = [], []
-    wall0 = time.perf_counter()
+    sampler = ClockSampler(dev) if rank == 0 else None
+    rounds, timing, wall = [], [], 0.0
     for _ in range(args.steps):
         flush.fill_(rank + len(rounds) % 7)  # L2 flush (> 126 MB) between timed rounds
         torch.cuda.synchronize()
+        w0 = time.perf_counter()  # wall clock of the round itself (the flush excluded)
         r, t = ctx.explorer_run([T], 1, timing=True)
+        wall += time.perf_counter() - w0
         if not r:
             break
         rounds += r
         timing += t
     torch.cuda.synchronize()
-    wall = time.perf_counter() - wall0
-    clocks = sample_clocks_stop(clocks_h, dev) if rank == 0 else None
+    clocks = sampler.result() if sampler else None
     dev_ms = sum(t["round_ms"] for t in timing)
     k2_ms = sum(t["k2_ms"] for t in timing)
     bounded = sum(r[2] for r in rounds)

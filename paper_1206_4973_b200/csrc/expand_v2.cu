@@ -12,6 +12,7 @@
 //    the child's Mq row with 128-bit loads (row stride = odd multiple of 16 B,
 //    conflict-free).
 #include <climits>
+#include <cstdlib>
 
 #include "k2_common.cuh"
 
@@ -34,21 +35,25 @@ struct V2Layout {
     int ppc_max, rowb;
 };
 
+// Per-parent job-indexed arrays (ranks, staged prefixes) hold RW = 32 entries for
+// n <= 32 and 64 for the wide variant (32 < n <= 64).
+__host__ __device__ inline int v2_rw(int N) { return N <= 32 ? 32 : 64; }
+
 __host__ __device__ inline V2Layout v2_layout(int n, int m, int P, int cmax, int threads, int N) {
     V2Layout L;
     L.ppc_max = cmax / 3 > 0 ? cmax / 3 : 1;
     L.rowb = v2_row_bytes(P);
     size_t o = 0;
     L.row = o;  o = b16(o + (size_t)N * P * 4);  // rows padded to N positions
-    L.um = o;   o = b16(o + (size_t)L.ppc_max * 4);
-    L.rank = o; o = b16(o + (size_t)L.ppc_max * 32);
+    L.um = o;   o = b16(o + (size_t)L.ppc_max * 8);
+    L.rank = o; o = b16(o + (size_t)L.ppc_max * v2_rw(N));
     L.R = o;    o = b16(o + (size_t)L.ppc_max * m * 4);
     L.load = o; o = b16(o + (size_t)L.ppc_max * m * 4);
     L.mins = o; o = b16(o + (size_t)L.ppc_max * m * 4);  // min1 | min2 << 16
     L.amin = o; o = b16(o + (size_t)L.ppc_max * m);
     L.Mq = o;   o = b16(o + (size_t)(cmax + 1) * L.rowb);  // + a dummy row for non-members
     L.p = o;    o = b16(o + (size_t)n * m * 4);
-    L.pre = o;  o = b16(o + (size_t)L.ppc_max * 32);
+    L.pre = o;  o = b16(o + (size_t)L.ppc_max * v2_rw(N));
     L.wsum = o; o = b16(o + (size_t)(threads / 32 + 2) * 8);
     L.total = o;
     return L;
@@ -70,6 +75,11 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
     asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
     return v;
 }
+__device__ __forceinline__ uint32_t lds_u32_v(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
 __device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
     uint32_t v;
     asm("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
@@ -77,6 +87,58 @@ __device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
 }
 __device__ __forceinline__ void sts_u16(uint32_t addr, int32_t v) {
     asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"((unsigned short)v));
+}
+
+// Is the job of row entry e unscheduled?  Its U bit is moved to the sign bit by a
+// wrapped left funnel shift (shift = e & 31 = 31 - (job & 31)); bit 5 of e picks
+// the 32-bit word of U (always the low word for n <= 32).
+__device__ __forceinline__ bool member(uint32_t e, uint32_t lo, uint32_t hi) {
+    return (int32_t)__funnelshift_l(0u, (e & 32u) ? hi : lo, e) < 0;
+}
+
+// Forward + backward scan of NB consecutive row positions of one pair for one
+// parent, entering with D0 and prefix max PM0 (the block's start state) and the
+// suffix max SM0 of the positions after the block; emits M' = max(prefix max,
+// suffix max - d) of every member to its child's Mq slot (non-members to the
+// dummy row) and returns the suffix max including this block.  FULL: the scan
+// covers the whole row (n <= 32), so the U bit is always in the low word.
+template <int NB, int P, bool WIDE>
+__device__ __forceinline__ int32_t scan_block(uint32_t row_sa, uint32_t lo, uint32_t hi,
+                                              uint32_t rank_sa, uint32_t out_sa, uint32_t dummy_sa,
+                                              uint32_t rowb, int32_t D0, int32_t PM0, int32_t SM0) {
+    // the rows (loads issued back to back), then the ranks of their jobs
+    uint32_t e[NB];
+#pragma unroll
+    for (int i = 0; i < NB; ++i) e[i] = lds_u32(row_sa + (uint32_t)(i * P * 4));
+    uint32_t at[NB];
+#pragma unroll
+    for (int i = 0; i < NB; ++i) at[i] = lds_u8(rank_sa + (e[i] & (WIDE ? 63u : 31u)));
+    // forward: prefix maxima; per position the effective c (-inf for non-members),
+    // -d (0 for non-members) and the store address
+    int32_t D = D0, PM = PM0;
+    int32_t pm[NB], ce[NB], nd[NB];
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+        const bool in = WIDE ? member(e[i], lo, hi) : (int32_t)__funnelshift_l(0u, lo, e[i]) < 0;
+        const int32_t c = (int32_t)__byte_perm(e[i], 0u, 0x4421);  // bytes 1..2
+        const int32_t d = (int32_t)e[i] >> 24;
+        ce[i] = in ? c : kNeg2;
+        nd[i] = in ? -d : 0;
+        at[i] = in ? out_sa + at[i] * rowb : dummy_sa;
+        pm[i] = PM;
+        PM = max(PM, D + ce[i]);
+        D -= nd[i];
+    }
+    // backward: suffix maxima and M' = max(prefix, suffix - d), unconditional
+    int32_t SM = SM0;
+#pragma unroll
+    for (int i = NB - 1; i >= 0; --i) {
+        const int32_t Db = D + nd[i];  // D before position i
+        sts_u16(at[i], max(pm[i], SM + nd[i]));
+        SM = max(SM, Db + ce[i]);
+        D = Db;
+    }
+    return SM;
 }
 
 template <int M>
@@ -94,15 +156,17 @@ struct PairTab {  // (k, l) of pair index q in bound.hpp:97-98 order
     }
 };
 
-template <int N, int M>
-__global__ void __launch_bounds__(192, 2) k2_v2_kernel(DevTables t, const Pool* __restrict__ pool,
+// OCC = target CTAs per SM: 2 -> up to 168 registers, 3 -> 112 (smaller chunks too)
+template <int N, int M, int OCC>
+__global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool* __restrict__ pool,
                                                    int first_seg, int cmax, int32_t ub, int frozen,
                                                    RoundState* rs, uint64_t* flags, uint32_t epoch) {
     constexpr int P = M * (M - 1) / 2;
     extern __shared__ __align__(16) unsigned char smem[];
     const int n = t.n, W = t.W;
     const V2Layout L = v2_layout(n, M, P, cmax, blockDim.x, N);
-    uint32_t* s_um = (uint32_t*)(smem + L.um);
+    uint64_t* s_um = (uint64_t*)(smem + L.um);  // unscheduled jobs of each parent
+    constexpr int RW = N <= 32 ? 32 : 64;
     uint8_t* s_rank = (uint8_t*)(smem + L.rank);
     int32_t* s_R = (int32_t*)(smem + L.R);
     int32_t* s_load = (int32_t*)(smem + L.load);
@@ -122,14 +186,18 @@ __global__ void __launch_bounds__(192, 2) k2_v2_kernel(DevTables t, const Pool* 
     for (int x = tid; x < n * M; x += bd) s_p[x] = t.p[x];
 
     // Johnson rows repacked for the scans, one word per (position, pair), [i][q]:
-    //   bits 0..4 job, bits 8..23 c, bits 24..31 d (int8)
-    //   padding positions i >= n carry job 31, never in U (n < 32 there)
+    //   bits 0..4 = 31 - (job & 31) (a left funnel shift by it moves the job's U bit
+    //   to the sign bit), bit 5 = job >> 5 (which 32-bit word of U, wide variant),
+    //   bits 8..23 c, bits 24..31 d (int8).  Padding positions i >= n read the top bit
+    //   of U (bit 31, or 63 in the wide variant), which is 0 when padding exists.
     uint32_t* s_row = (uint32_t*)(smem + L.row);
     for (int x = tid; x < N * P; x += bd) {
-        uint32_t v = 31u;
+        uint32_t v = N <= 32 ? 0u : 32u;
         if (x < n * P) {
             uint32_t e = t.jm[x];
-            v = (uint32_t)entry_job(e) | ((uint32_t)entry_c(e) << 8) | ((uint32_t)entry_d(e) << 24);
+            const uint32_t j = (uint32_t)entry_job(e);
+            v = (31u - (j & 31u)) | (j & 32u) | ((uint32_t)entry_c(e) << 8) |
+                ((uint32_t)entry_d(e) << 24);
         }
         s_row[x] = v;
     }
@@ -160,29 +228,30 @@ __global__ void __launch_bounds__(192, 2) k2_v2_kernel(DevTables t, const Pool* 
         // every global read of the parents happens before this chunk publishes
         for (int x = tid; x < np * depth; x += bd) {
             int pp = x / depth, i = x - pp * depth;
-            s_pre[pp * 32 + i] = src.prefix[(first + step * (p0 + pp)) * n + i];
+            s_pre[pp * RW + i] = src.prefix[(first + step * (p0 + pp)) * n + i];
         }
+        const uint64_t valid = n >= 64 ? ~0ull : ((1ull << n) - 1ull);
         for (int pp = tid; pp < np; pp += bd) {
             int64_t node = first + step * (p0 + pp);
-            uint32_t sched = (uint32_t)src.masks[node * W];
-            s_um[pp] = ~sched & (n >= 32 ? 0xFFFFFFFFu : ((1u << n) - 1u));
+            s_um[pp] = ~src.masks[node * W] & valid;
         }
         for (int x = tid; x < np * M; x += bd) {
             int pp = x / M, k = x - pp * M;
             s_R[x] = src.heads[(first + step * (p0 + pp)) * M + k];
         }
         __syncthreads();
-        for (int x = tid; x < np * 32; x += bd) {  // rank of job j among U (ascending)
-            int pp = x >> 5, j = x & 31;
-            s_rank[x] = (uint8_t)__popc(s_um[pp] & ((1u << j) - 1u));
+        for (int x = tid; x < np * RW; x += bd) {  // rank of job j among U, at its entry code
+            const int pp = x / RW, idx = x - pp * RW;
+            const int j = (idx & 32) | (31 - (idx & 31));
+            s_rank[x] = (uint8_t)__popcll(s_um[pp] & ((1ull << j) - 1ull));
         }
         // per (parent, machine): load, two smallest tails (+ argmin)
         for (int x = tid; x < np * M; x += bd) {
             int pp = x / M, k = x - pp * M;
-            uint32_t um = s_um[pp];
+            uint64_t um = s_um[pp];
             int32_t load = 0, m1 = 0x7FFF, m2 = 0x7FFF, am = 0;
             while (um) {
-                int j = __ffs(um) - 1;
+                int j = __ffsll((long long)um) - 1;
                 um &= um - 1;
                 load += s_p[j * M + k];
                 int32_t tv = t.tails[j * M + k];
@@ -202,44 +271,43 @@ __global__ void __launch_bounds__(192, 2) k2_v2_kernel(DevTables t, const Pool* 
         // ---- Phase A: forward / backward max-plus scans of pair q over parent pp
         if (a_lane) {
             for (int pp = g; pp < np; pp += G) {
-                const uint32_t um = s_um[pp];
-                const uint32_t rank_sa = (uint32_t)__cvta_generic_to_shared(s_rank + pp * 32);
+                const uint64_t um64 = s_um[pp];
+                const uint32_t rank_sa = (uint32_t)__cvta_generic_to_shared(s_rank + pp * RW);
                 const uint32_t out_sa =
                     (uint32_t)__cvta_generic_to_shared(s_Mq + (size_t)(pp * r) * L.rowb + 2 * q);
                 const uint32_t dummy_sa =
                     (uint32_t)__cvta_generic_to_shared(s_Mq + (size_t)cmax * L.rowb + 2 * q);
                 const uint32_t rowb = (uint32_t)L.rowb;
-                // the row once into registers (loads issued back to back), then the
-                // ranks of its jobs, so neither pass waits on shared-memory latency
-                uint32_t e[N];
+                if constexpr (N <= 32) {
+                    scan_block<N, P, false>(row_sa, (uint32_t)um64, 0u, rank_sa, out_sa, dummy_sa,
+                                            rowb, 0, kNeg2, 0);
+                } else {
+                    // wide: forward pass keeps (D, prefix max) checkpoints every 16
+                    // positions; each block is then recomputed and scanned backward
+                    const uint32_t lo = (uint32_t)um64, hi = (uint32_t)(um64 >> 32);
+                    int32_t ckD[N / 16], ckP[N / 16];
+                    int32_t D = 0, PM = kNeg2;
 #pragma unroll
-                for (int i = 0; i < N; ++i) e[i] = lds_u32(row_sa + (uint32_t)(i * P * 4));
-                uint32_t rk[N];
+                    for (int b = 0; b < N / 16; ++b) {
+                        ckD[b] = D;
+                        ckP[b] = PM;
 #pragma unroll
-                for (int i = 0; i < N; ++i) rk[i] = lds_u8(rank_sa + (e[i] & 31u));
-                int32_t D = 0, PM = kNeg2;
-                int32_t pm[N];
+                        for (int i = 0; i < 16; ++i) {
+                            // volatile: keep the 64 checkpoint-pass loads from being hoisted
+                            const uint32_t e = lds_u32_v(row_sa + (uint32_t)((b * 16 + i) * P * 4));
+                            const bool in = member(e, lo, hi);
+                            const int32_t c = (int32_t)__byte_perm(e, 0u, 0x4421);
+                            const int32_t d = (int32_t)e >> 24;
+                            PM = in ? max(PM, D + c) : PM;
+                            D = in ? D + d : D;
+                        }
+                    }
+                    int32_t SM = kNeg2;
 #pragma unroll
-                for (int i = 0; i < N; ++i) {
-                    const bool in = (__funnelshift_r(um, 0u, e[i]) & 1u) != 0u;  // shift = e & 31
-                    const int32_t c = (int32_t)__byte_perm(e[i], 0u, 0x4421);    // bytes 1..2
-                    const int32_t d = (int32_t)e[i] >> 24;
-                    pm[i] = PM;
-                    PM = in ? max(PM, D + c) : PM;
-                    D = in ? D + d : D;
-                }
-                int32_t SM = kNeg2;
-#pragma unroll
-                for (int i = N - 1; i >= 0; --i) {
-                    const bool in = (__funnelshift_r(um, 0u, e[i]) & 1u) != 0u;
-                    const int32_t c = (int32_t)__byte_perm(e[i], 0u, 0x4421);
-                    const int32_t d = (int32_t)e[i] >> 24;
-                    const int32_t Db = D - d;  // D before position i
-                    // finite for members of U with |U| >= 3 (internal children), fits int16
-                    const int32_t mp = max(pm[i], SM - d);
-                    sts_u16(in ? out_sa + rk[i] * rowb : dummy_sa, mp);
-                    SM = in ? max(SM, Db + c) : SM;
-                    D = in ? Db : D;
+                    for (int b = N / 16 - 1; b >= 0; --b)
+                        SM = scan_block<16, P, true>(row_sa + (uint32_t)(b * 16 * P * 4), lo, hi,
+                                                     rank_sa, out_sa, dummy_sa, rowb, ckD[b],
+                                                     ckP[b], SM);
                 }
             }
         }
@@ -251,8 +319,11 @@ __global__ void __launch_bounds__(192, 2) k2_v2_kernel(DevTables t, const Pool* 
         const bool b_lane = tid < nc;  // cmax <= blockDim
         if (b_lane) {
             const int pp = tid / r, rk = tid - pp * r;
-            const uint32_t um = s_um[pp];
-            const int x = __fns(um, 0, rk + 1);
+            const uint64_t um = s_um[pp];
+            const uint32_t lo = (uint32_t)um;
+            const int nlo = __popc(lo);
+            const int x = rk < nlo ? (int)__fns(lo, 0, rk + 1)
+                                   : 32 + (int)__fns((uint32_t)(um >> 32), 0, rk - nlo + 1);
             myx = x;
             mypp = pp;
             int32_t Lc[M];
@@ -310,26 +381,25 @@ __global__ void __launch_bounds__(192, 2) k2_v2_kernel(DevTables t, const Pool* 
             const NodeStore dst = sg.dst;
 #pragma unroll
             for (int k = 0; k < M; ++k) dst.heads[o * M + k] = myR[k];
-            const uint32_t um = s_um[mypp];
-            const uint32_t valid = n >= 32 ? 0xFFFFFFFFu : ((1u << n) - 1u);
-            dst.masks[o * W] = (uint64_t)((~um & valid) | (1u << myx));
+            const uint64_t valid = n >= 64 ? ~0ull : ((1ull << n) - 1ull);
+            dst.masks[o * W] = (~s_um[mypp] & valid) | (1ull << myx);
             uint8_t* dp = dst.prefix + o * n;
-            for (int i = 0; i < depth; ++i) dp[i] = s_pre[mypp * 32 + i];
+            for (int i = 0; i < depth; ++i) dp[i] = s_pre[mypp * RW + i];
             dp[depth] = (uint8_t)myx;
             if (sg.dst_lb) sg.dst_lb[o] = mylb;
         }
     }
 }
 
-template <int N, int M>
+template <int N, int M, int OCC>
 cudaError_t v2_setup(const DevTables& t, K2Config& c, int device) {
     int optin = 0, sms = 148, per_sm = 1;
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    cudaError_t e = cudaFuncSetAttribute(k2_v2_kernel<N, M>,
+    cudaError_t e = cudaFuncSetAttribute(k2_v2_kernel<N, M, OCC>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
     if (e != cudaSuccess) return e;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_v2_kernel<N, M>, c.threads, c.smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_v2_kernel<N, M, OCC>, c.threads, c.smem);
     c.blocks = sms * (per_sm < 1 ? 1 : per_sm);
     return cudaSuccess;
 }
@@ -338,21 +408,36 @@ cudaError_t v2_setup(const DevTables& t, K2Config& c, int device) {
 
 bool k2_v2_config(const DevTables& t, int device, K2Config* out) {
     int m = t.m, n = t.n;
-    if (n > 32 || !(m == 5 || m == 10 || m == 20)) return false;
+    if (n > 64 || !(m == 5 || m == 10 || m == 20)) return false;
     K2Config c;
     c.threads = 192;
-    c.cmax = 128;
-    c.variant = (n <= 20 ? 20 : 32) * 100 + m;
+    const char* occ_env = getenv("FBB_K2_OCC");
+    const int occ = occ_env && occ_env[0] == '2' ? 2 : 3;
+    c.cmax = occ == 3 ? 112 : 128;
+    const int NN = n <= 20 ? 20 : (n <= 32 ? 32 : 64);
+    c.variant = occ * 10000 + NN * 100 + m;
     c.jm_in_smem = false;
-    c.smem = v2_layout(n, m, t.P, c.cmax, c.threads, n <= 20 ? 20 : 32).total;
+    c.smem = v2_layout(n, m, t.P, c.cmax, c.threads, NN).total;
     cudaError_t e;
     switch (c.variant) {
-        case 2005: e = v2_setup<20, 5>(t, c, device); break;
-        case 2010: e = v2_setup<20, 10>(t, c, device); break;
-        case 2020: e = v2_setup<20, 20>(t, c, device); break;
-        case 3205: e = v2_setup<32, 5>(t, c, device); break;
-        case 3210: e = v2_setup<32, 10>(t, c, device); break;
-        case 3220: e = v2_setup<32, 20>(t, c, device); break;
+        case 22005: e = v2_setup<20, 5, 2>(t, c, device); break;
+        case 22010: e = v2_setup<20, 10, 2>(t, c, device); break;
+        case 22020: e = v2_setup<20, 20, 2>(t, c, device); break;
+        case 23205: e = v2_setup<32, 5, 2>(t, c, device); break;
+        case 23210: e = v2_setup<32, 10, 2>(t, c, device); break;
+        case 23220: e = v2_setup<32, 20, 2>(t, c, device); break;
+        case 32005: e = v2_setup<20, 5, 3>(t, c, device); break;
+        case 32010: e = v2_setup<20, 10, 3>(t, c, device); break;
+        case 32020: e = v2_setup<20, 20, 3>(t, c, device); break;
+        case 33205: e = v2_setup<32, 5, 3>(t, c, device); break;
+        case 33210: e = v2_setup<32, 10, 3>(t, c, device); break;
+        case 33220: e = v2_setup<32, 20, 3>(t, c, device); break;
+        case 26405: e = v2_setup<64, 5, 2>(t, c, device); break;
+        case 26410: e = v2_setup<64, 10, 2>(t, c, device); break;
+        case 26420: e = v2_setup<64, 20, 2>(t, c, device); break;
+        case 36405: e = v2_setup<64, 5, 3>(t, c, device); break;
+        case 36410: e = v2_setup<64, 10, 3>(t, c, device); break;
+        case 36420: e = v2_setup<64, 20, 3>(t, c, device); break;
         default: return false;
     }
     if (e != cudaSuccess) return false;
@@ -363,19 +448,30 @@ bool k2_v2_config(const DevTables& t, int device, K2Config* out) {
 cudaError_t launch_k2_v2(const DevTables& t, const K2Config& cfg, const Pool* d_pool, int first_seg,
                          int blocks, int32_t ub, int frozen, RoundState* rs, uint64_t* flags,
                          uint32_t epoch, cudaStream_t stream) {
-#define V2_CASE(NN, MM)                                                                       \
-    case NN * 100 + MM:                                                                       \
-        k2_v2_kernel<NN, MM><<<blocks, cfg.threads, cfg.smem, stream>>>(t, d_pool, first_seg,  \
-                                                                         cfg.cmax, ub, frozen, \
-                                                                         rs, flags, epoch);   \
+#define V2_CASE(NN, MM, OO)                                                                   \
+    case OO * 10000 + NN * 100 + MM:                                                          \
+        k2_v2_kernel<NN, MM, OO><<<blocks, cfg.threads, cfg.smem, stream>>>(                   \
+            t, d_pool, first_seg, cfg.cmax, ub, frozen, rs, flags, epoch);                    \
         break;
     switch (cfg.variant) {
-        V2_CASE(20, 5)
-        V2_CASE(20, 10)
-        V2_CASE(20, 20)
-        V2_CASE(32, 5)
-        V2_CASE(32, 10)
-        V2_CASE(32, 20)
+        V2_CASE(20, 5, 2)
+        V2_CASE(20, 10, 2)
+        V2_CASE(20, 20, 2)
+        V2_CASE(32, 5, 2)
+        V2_CASE(32, 10, 2)
+        V2_CASE(32, 20, 2)
+        V2_CASE(20, 5, 3)
+        V2_CASE(20, 10, 3)
+        V2_CASE(20, 20, 3)
+        V2_CASE(32, 5, 3)
+        V2_CASE(32, 10, 3)
+        V2_CASE(32, 20, 3)
+        V2_CASE(64, 5, 2)
+        V2_CASE(64, 10, 2)
+        V2_CASE(64, 20, 2)
+        V2_CASE(64, 5, 3)
+        V2_CASE(64, 10, 3)
+        V2_CASE(64, 20, 3)
         default: return cudaErrorInvalidValue;
     }
 #undef V2_CASE
