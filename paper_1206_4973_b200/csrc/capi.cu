@@ -104,10 +104,10 @@ struct fbb_ctx {
     Store batch_in, batch_out;
     DBuf out_lb;
     // shared per-round device state
-    DBuf flags;             // per-chunk look-back words (epoch tagged)
+    Store staging;          // per-chunk compacted survivors (chunk c at c * cmax)
+    DBuf st_lb, st_count, st_offset;
     DBuf d_pool, d_round;   // Pool, RoundState
     HBuf h_pool, h_round;
-    uint32_t epoch = 0;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     float last_k2_ms = 0.f, last_round_ms = 0.f;
     int last_launches = 0;
@@ -200,12 +200,11 @@ int layout_pool(const fbb_ctx* ctx, Pool& pool) {
 int run_pool(fbb_ctx* ctx, Pool& pool, int first_internal, int32_t ub, int frozen) {
     const int n = ctx->dt.n;
     cudaStream_t st = ctx->stream;
-    const size_t fl_before = ctx->flags.bytes;
-    CK(ctx->flags.ensure((size_t)std::max<int64_t>(pool.nchunks, 1) * 8), "chunk flags");
-    ctx->epoch = (ctx->epoch + 1) & 0xFFFFu;
-    if (ctx->epoch == 0) ctx->epoch = 1;
-    if (ctx->flags.bytes != fl_before || ctx->epoch == 1)  // fresh memory / epoch wrap
-        CK(cudaMemsetAsync(ctx->flags.p, 0, ctx->flags.bytes, st), "chunk flags");
+    const int64_t slots = std::max<int64_t>(pool.nchunks * ctx->k2.cmax, 1);
+    CK(store_ensure(ctx, ctx->staging, slots, 0), "staging");
+    CK(ctx->st_lb.ensure((size_t)slots * 4), "staging");
+    CK(ctx->st_count.ensure((size_t)std::max<int64_t>(pool.nchunks, 1) * 4), "staging");
+    CK(ctx->st_offset.ensure((size_t)(pool.nchunks + 1) * 8), "staging");
     CK(ctx->d_pool.ensure(sizeof(Pool)), "pool");
     CK(ctx->h_pool.ensure(sizeof(Pool)), "pool");
     CK(ctx->d_round.ensure(sizeof(RoundState)), "round state");
@@ -229,11 +228,13 @@ int run_pool(fbb_ctx* ctx, Pool& pool, int first_internal, int32_t ub, int froze
     }
     CK(cudaEventRecord(ctx->ev[1], st), "event");
     bool has_internal = first_internal < pool.nseg && pool.nchunks > 0;
-    CK(launch_k2_internal(ctx->dt, ctx->k2, dp, pool, first_internal, ub, frozen, rs,
-                          ctx->flags.as<uint64_t>(), ctx->epoch, st),
+    ChunkOut out{ctx->staging.view(), ctx->st_lb.as<int32_t>(), ctx->st_count.as<int32_t>(),
+                 ctx->st_offset.as<int64_t>()};
+    CK(launch_k2_internal(ctx->dt, ctx->k2, dp, pool, first_internal, ub, frozen, rs, out, st),
        "K2 internal");
     CK(cudaEventRecord(ctx->ev[2], st), "event");
-    if (has_internal) ++launches;
+    CK(launch_place(ctx->dt, ctx->k2, dp, pool, rs, out, st), "place");
+    launches += has_internal ? 3 : 1;
     size_t head = offsetof(RoundState, seg_surv) + (size_t)pool.nseg * 8;
     CK(cudaMemcpyAsync(ctx->h_round.p, rs, head, cudaMemcpyDeviceToHost, st), "round D2H");
     if (has_leaf)
@@ -526,9 +527,9 @@ fbb_ctx* fbb_create(int device, const int32_t* p, int n, int m) {
             }
         }
         for (DBuf* b : {&ctx->k1_masks, &ctx->k1_heads, &ctx->k1_depth, &ctx->k1_lb, &ctx->out_lb,
-                        &ctx->flags, &ctx->d_pool, &ctx->d_round})
+                        &ctx->st_lb, &ctx->st_count, &ctx->st_offset, &ctx->d_pool, &ctx->d_round})
             b->st = ctx->stream;
-        for (Store* st : {&ctx->batch_in, &ctx->batch_out})
+        for (Store* st : {&ctx->batch_in, &ctx->batch_out, &ctx->staging})
             st->masks.st = st->heads.st = st->prefix.st = ctx->stream;
     }
     rc = upload_tables(ctx->ht, &ctx->dt, &why);
@@ -566,9 +567,9 @@ void fbb_destroy(fbb_ctx* ctx) {
     cudaSetDevice(ctx->device);
     free_tables(&ctx->dt);
     for (DBuf* b : {&ctx->k1_masks, &ctx->k1_heads, &ctx->k1_depth, &ctx->k1_lb, &ctx->out_lb,
-                    &ctx->flags, &ctx->d_pool, &ctx->d_round})
+                    &ctx->st_lb, &ctx->st_count, &ctx->st_offset, &ctx->d_pool, &ctx->d_round})
         b->release();
-    for (Store* s : {&ctx->batch_in, &ctx->batch_out}) {
+    for (Store* s : {&ctx->batch_in, &ctx->batch_out, &ctx->staging}) {
         s->masks.release();
         s->heads.release();
         s->prefix.release();

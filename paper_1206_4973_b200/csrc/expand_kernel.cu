@@ -90,7 +90,7 @@ template <bool kJmSmem>
 __global__ void __launch_bounds__(128) k2_internal_kernel(DevTables t, const Pool* __restrict__ pool,
                                                          int first_seg, int cmax, int32_t ub,
                                                          int frozen, RoundState* rs,
-                                                         uint64_t* flags, uint32_t epoch) {
+                                                         ChunkOut out) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int n = t.n, m = t.m, P = t.P, W = t.W;
     const int W32 = (n + 31) / 32;
@@ -272,17 +272,9 @@ __global__ void __launch_bounds__(128) k2_internal_kernel(DevTables t, const Poo
             base_off += tot;
             __syncthreads();
         }
-        if (warp == 0) {
-            const int64_t excl = lookback_warp(flags, epoch, c_begin, chunk, base_off);
-            if (lane == 0) {
-                const int64_t nch = (sg.count + ppc - 1) / ppc;
-                *s_slot = chunk_output_base(pool, s, chunk, c_begin, nch, excl, base_off, flags,
-                                            epoch, rs);
-            }
-        }
-        __syncthreads();
-        const int64_t out0 = *s_slot;
-        const NodeStore dst = sg.dst;
+        if (tid == 0) out.count[chunk] = base_off;
+        const int64_t out0 = chunk * (int64_t)cmax;
+        const NodeStore dst = out.nodes;
         int run = 0;
         for (int c0 = 0; c0 < nc; c0 += bd) {
             int c = c0 + tid;
@@ -318,7 +310,7 @@ __global__ void __launch_bounds__(128) k2_internal_kernel(DevTables t, const Poo
                 uint8_t* dp = dst.prefix + o * n;
                 for (int i = 0; i < depth; ++i) dp[i] = s_pre[pp * n + i];
                 dp[depth] = (uint8_t)xj;
-                if (sg.dst_lb) sg.dst_lb[o] = lb;
+                out.lb[o] = lb;
             }
             run += tot;
             __syncthreads();
@@ -399,6 +391,89 @@ __global__ void leaf_schedule_kernel(DevTables t, const Pool* __restrict__ pool,
     *found = 1;
 }
 
+// Exclusive scan of the per-chunk survivor counts (one CTA; a pool has a few
+// thousand chunks), per-segment totals and the pool total.
+__global__ void chunk_scan_kernel(const Pool* __restrict__ pool, RoundState* rs, ChunkOut out) {
+    __shared__ int64_t warp_tot[32];
+    __shared__ int64_t carry;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+    const int64_t nchunks = pool->nchunks;
+    if (tid == 0) carry = 0;
+    __syncthreads();
+    for (int64_t base = 0; base < nchunks; base += blockDim.x) {
+        const int64_t i = base + tid;
+        const int64_t v = i < nchunks ? out.count[i] : 0;
+        int64_t incl = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int64_t u = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (lane >= o) incl += u;
+        }
+        if (lane == 31) warp_tot[warp] = incl;
+        __syncthreads();
+        int64_t woff = 0, tot = 0;
+        for (int w = 0; w < nw; ++w) {
+            if (w < warp) woff += warp_tot[w];
+            tot += warp_tot[w];
+        }
+        if (i < nchunks) out.offset[i] = carry + woff + incl - v;
+        __syncthreads();
+        if (tid == 0) carry += tot;
+        __syncthreads();
+    }
+    if (tid == 0) out.offset[nchunks] = carry;
+    __syncthreads();
+    for (int s = tid; s < pool->nseg; s += blockDim.x) {
+        const int64_t cb = pool->seg[s].chunk_base;
+        const int64_t ce = s + 1 < pool->nseg ? pool->seg[s + 1].chunk_base : nchunks;
+        rs->seg_surv[s] = ce > cb ? out.offset[ce] - out.offset[cb] : 0;
+    }
+    if (tid == 0) rs->total = carry;
+}
+
+// Moves every chunk's survivors to their final place: segment dst at
+// dst_base + (offset[c] - offset[first chunk of the segment]), or the contiguous
+// output at offset[c] (dst_base < 0).  A warp per chunk; a chunk's rows are
+// contiguous in both places, so each array moves as one flat run.
+__global__ void place_kernel(DevTables t, const Pool* __restrict__ pool, int cmax, ChunkOut out) {
+    const int n = t.n, m = t.m, W = t.W;
+    const int lane = threadIdx.x & 31;
+    const int64_t nchunks = pool->nchunks;
+    const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t c = wid; c < nchunks; c += nwarps) {
+        const int cnt = out.count[c];
+        if (cnt == 0) continue;
+        const int s = find_segment_lb(pool, 0, c);
+        const Segment& sg = pool->seg[s];
+        const int64_t pos = sg.dst_base < 0 ? out.offset[c]
+                                            : sg.dst_base + out.offset[c] - out.offset[sg.chunk_base];
+        const int64_t so = c * (int64_t)cmax;
+        const NodeStore dst = sg.dst;
+        {
+            const int32_t* a = out.nodes.heads + so * m;
+            int32_t* b = dst.heads + pos * m;
+            for (int x = lane; x < cnt * m; x += 32) b[x] = a[x];
+        }
+        {
+            const uint64_t* a = out.nodes.masks + so * W;
+            uint64_t* b = dst.masks + pos * W;
+            for (int x = lane; x < cnt * W; x += 32) b[x] = a[x];
+        }
+        {  // prefixes: only the first depth + 1 bytes of a row are meaningful
+            const uint8_t* a = out.nodes.prefix + so * n;
+            uint8_t* b = dst.prefix + pos * n;
+            const int len = sg.depth + 1;
+            for (int x = lane; x < cnt * len; x += 32) {
+                const int i = x / len, k = x - i * len;
+                b[i * n + k] = a[i * n + k];
+            }
+        }
+        if (sg.dst_lb)
+            for (int x = lane; x < cnt; x += 32) sg.dst_lb[pos + x] = out.lb[so + x];
+    }
+}
+
 }  // namespace
 
 K2Config k2_config(const DevTables& t, int device) {
@@ -437,26 +512,41 @@ cudaError_t launch_k2_leaves(const DevTables& t, const Pool* d_pool, const Pool&
 
 cudaError_t launch_k2_internal(const DevTables& t, const K2Config& cfg, const Pool* d_pool,
                                const Pool& h_pool, int first_seg, int32_t ub, int frozen,
-                               RoundState* rs, uint64_t* flags, uint32_t epoch,
-                               cudaStream_t stream) {
+                               RoundState* rs, ChunkOut out, cudaStream_t stream) {
     if (first_seg >= h_pool.nseg) return cudaSuccess;
     int64_t nch = h_pool.nchunks - h_pool.seg[first_seg].chunk_base;
     if (nch <= 0) return cudaSuccess;
     int blocks = (int)(nch < cfg.blocks ? nch : cfg.blocks);
     if (cfg.variant != 0)
-        return launch_k2_v2(t, cfg, d_pool, first_seg, blocks, ub, frozen, rs, flags, epoch, stream);
+        return launch_k2_v2(t, cfg, d_pool, first_seg, blocks, ub, frozen, rs, out, stream);
     if (cfg.jm_in_smem)
         k2_internal_kernel<true><<<blocks, cfg.threads, cfg.smem, stream>>>(t, d_pool, first_seg, cfg.cmax,
-                                                                            ub, frozen, rs, flags, epoch);
+                                                                            ub, frozen, rs, out);
     else
         k2_internal_kernel<false><<<blocks, cfg.threads, cfg.smem, stream>>>(t, d_pool, first_seg, cfg.cmax,
-                                                                             ub, frozen, rs, flags, epoch);
+                                                                             ub, frozen, rs, out);
     return cudaGetLastError();
 }
 
 cudaError_t launch_leaf_schedule(const DevTables& t, const Pool* d_pool, RoundState* rs,
                                  int32_t ub, cudaStream_t stream) {
     leaf_schedule_kernel<<<1, 32, 0, stream>>>(t, d_pool, rs, ub);
+    return cudaGetLastError();
+}
+
+}  // namespace fbb
+
+namespace fbb {
+
+cudaError_t launch_place(const DevTables& t, const K2Config& cfg, const Pool* d_pool,
+                         const Pool& h_pool, RoundState* rs, ChunkOut out, cudaStream_t stream) {
+    chunk_scan_kernel<<<1, 1024, 0, stream>>>(d_pool, rs, out);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess || h_pool.nchunks == 0) return e;
+    int64_t warps = h_pool.nchunks;
+    int blocks = (int)((warps * 32 + 255) / 256);
+    if (blocks > 1184) blocks = 1184;
+    place_kernel<<<blocks, 256, 0, stream>>>(t, d_pool, cfg.cmax, out);
     return cudaGetLastError();
 }
 

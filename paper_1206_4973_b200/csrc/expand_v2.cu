@@ -160,7 +160,7 @@ struct PairTab {  // (k, l) of pair index q in bound.hpp:97-98 order
 template <int N, int M, int OCC>
 __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool* __restrict__ pool,
                                                    int first_seg, int cmax, int32_t ub, int frozen,
-                                                   RoundState* rs, uint64_t* flags, uint32_t epoch) {
+                                                   RoundState* rs, ChunkOut out) {
     constexpr int P = M * (M - 1) / 2;
     extern __shared__ __align__(16) unsigned char smem[];
     const int n = t.n, W = t.W;
@@ -368,17 +368,10 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
             if (w < warp) woff += v;
             tot += v;
         }
-        if (warp == 0) {
-            const int64_t excl = lookback_warp(flags, epoch, c_begin, chunk, tot);
-            if (lane == 0) {
-                const int64_t nch = (sg.count + ppc - 1) / ppc;
-                *s_slot = chunk_output_base(pool, s, chunk, c_begin, nch, excl, tot, flags, epoch, rs);
-            }
-        }
-        __syncthreads();
+        if (tid == 0) out.count[chunk] = tot;
         if (keep) {
-            const int64_t o = *s_slot + woff + __popc(ballot & ((1u << lane) - 1u));
-            const NodeStore dst = sg.dst;
+            const int64_t o = chunk * (int64_t)cmax + woff + __popc(ballot & ((1u << lane) - 1u));
+            const NodeStore dst = out.nodes;
 #pragma unroll
             for (int k = 0; k < M; ++k) dst.heads[o * M + k] = myR[k];
             const uint64_t valid = n >= 64 ? ~0ull : ((1ull << n) - 1ull);
@@ -386,7 +379,7 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
             uint8_t* dp = dst.prefix + o * n;
             for (int i = 0; i < depth; ++i) dp[i] = s_pre[mypp * RW + i];
             dp[depth] = (uint8_t)myx;
-            if (sg.dst_lb) sg.dst_lb[o] = mylb;
+            out.lb[o] = mylb;
         }
     }
 }
@@ -446,12 +439,12 @@ bool k2_v2_config(const DevTables& t, int device, K2Config* out) {
 }
 
 cudaError_t launch_k2_v2(const DevTables& t, const K2Config& cfg, const Pool* d_pool, int first_seg,
-                         int blocks, int32_t ub, int frozen, RoundState* rs, uint64_t* flags,
-                         uint32_t epoch, cudaStream_t stream) {
+                         int blocks, int32_t ub, int frozen, RoundState* rs, ChunkOut out,
+                         cudaStream_t stream) {
 #define V2_CASE(NN, MM, OO)                                                                   \
     case OO * 10000 + NN * 100 + MM:                                                          \
         k2_v2_kernel<NN, MM, OO><<<blocks, cfg.threads, cfg.smem, stream>>>(                   \
-            t, d_pool, first_seg, cfg.cmax, ub, frozen, rs, flags, epoch);                    \
+            t, d_pool, first_seg, cfg.cmax, ub, frozen, rs, out);                             \
         break;
     switch (cfg.variant) {
         V2_CASE(20, 5, 2)

@@ -116,6 +116,15 @@ struct K2Config {
 };
 K2Config k2_config(const DevTables& t, int device);
 
+// Per-chunk staging of survivors (compacted, batch order inside the chunk), placed
+// by place_kernel after chunk_scan_kernel computed the exclusive offsets.
+struct ChunkOut {
+    NodeStore nodes;  // capacity nchunks * cmax, chunk c at [c * cmax, c * cmax + count[c])
+    int32_t* lb;      // survivor bounds (same indexing)
+    int32_t* count;   // survivors per chunk
+    int64_t* offset;  // exclusive prefix of count
+};
+
 // Per-round device state; the head (everything before `schedule`) is zeroed by
 // one memset before the round.
 struct RoundState {
@@ -131,18 +140,21 @@ constexpr size_t kRoundStateHead = offsetof(RoundState, schedule);
 // n <= 32, m in {5,10,20}: the register/shared-row kernel; false when not applicable.
 bool k2_v2_config(const DevTables& t, int device, K2Config* out);
 cudaError_t launch_k2_v2(const DevTables& t, const K2Config& cfg, const Pool* d_pool, int first_seg,
-                         int blocks, int32_t ub, int frozen, RoundState* rs, uint64_t* flags,
-                         uint32_t epoch, cudaStream_t stream);
+                         int blocks, int32_t ub, int frozen, RoundState* rs, ChunkOut out,
+                         cudaStream_t stream);
 
 // Leaves (parents at depth >= n-2): batch minimum (value, first position).
 cudaError_t launch_k2_leaves(const DevTables& t, const Pool* d_pool, const Pool& h_pool,
                              int seg_index, RoundState* rs, cudaStream_t stream);
 // Internal children: bound, prune against min(ub, leaf minimum) (frozen: ub),
-// survivors written in batch order to each segment's dst.
+// survivors compacted per chunk into `out`.
 cudaError_t launch_k2_internal(const DevTables& t, const K2Config& cfg, const Pool* d_pool,
                                const Pool& h_pool, int first_seg, int32_t ub, int frozen,
-                               RoundState* rs, uint64_t* flags, uint32_t epoch,
-                               cudaStream_t stream);
+                               RoundState* rs, ChunkOut out, cudaStream_t stream);
+// Exclusive offsets of the chunk counts, per-segment totals and the pool total
+// into `rs`; then every chunk's survivors moved to its segment's dst.
+cudaError_t launch_place(const DevTables& t, const K2Config& cfg, const Pool* d_pool,
+                         const Pool& h_pool, RoundState* rs, ChunkOut out, cudaStream_t stream);
 // Schedule of the best leaf when it beats ub (before the parents are recycled).
 cudaError_t launch_leaf_schedule(const DevTables& t, const Pool* d_pool, RoundState* rs,
                                  int32_t ub, cudaStream_t stream);
