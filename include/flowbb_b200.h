@@ -72,6 +72,10 @@ typedef struct {
     int64_t pending;   /* pending nodes after the round */
     float round_ms;    /* device time of the round, pool upload .. summary download */
     int32_t launches;  /* kernels this library launched for the round */
+    float host_ms;     /* wall time of the round inside the library (steady clock) */
+    float sync_ms;     /* part of host_ms spent waiting for the device */
+    int64_t h2d_bytes; /* host -> device bytes of the round (host-resident explorer) */
+    int64_t d2h_bytes; /* device -> host bytes of the round (host-resident explorer) */
 } fbb_round_t;
 
 /* ---- context ----------------------------------------------------------------------------
@@ -126,6 +130,12 @@ int fbb_expand_bound_prune(fbb_ctx* ctx, const uint64_t* masks, const int32_t* h
  * search.hpp:64-73) + K2 + in-order push, with no host traffic but a few
  * counters.  Semantics are those of resolve_workload (bench.hpp:63-114, frozen
  * incumbent) or solve (search.hpp:124-174). */
+
+/* Where the pending tree lives: device memory (0, default) or pinned host
+ * memory (1: the paper's Type-1 split -- the host owns the tree, each round
+ * uploads its parents and the surviving children come back into the host
+ * buckets).  Clears the pending tree.  Same explorer semantics either way. */
+int fbb_explorer_set_residency(fbb_ctx* ctx, int pending_on_host);
 
 /* Reset the pending tree to the given nodes (pushed in order, like
  * bench.hpp:84) with incumbent `ub` (frozen or not). */

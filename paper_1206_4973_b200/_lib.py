@@ -20,7 +20,7 @@ EXPORTED = (
     "fbb_create", "fbb_destroy", "fbb_last_error", "fbb_descriptor", "fbb_bound",
     "fbb_bound_device", "fbb_expand_bound_prune", "fbb_explorer_reset",
     "fbb_explorer_start_solve", "fbb_explorer_run", "fbb_explorer_state",
-    "fbb_explorer_pending", "fbb_tuner_create", "fbb_tuner_destroy", "fbb_tuner_target",
+    "fbb_explorer_pending", "fbb_explorer_set_residency", "fbb_tuner_create", "fbb_tuner_destroy", "fbb_tuner_target",
     "fbb_tuner_observe", "fbb_tuner_phase", "fbb_tuner_best_batch",
     "fbb_tuner_best_throughput", "fbb_version",
 )
@@ -54,10 +54,16 @@ class RoundRec(C.Structure):
         ("pending", C.c_int64),
         ("round_ms", C.c_float),
         ("launches", C.c_int32),
+        ("host_ms", C.c_float),
+        ("sync_ms", C.c_float),
+        ("h2d_bytes", C.c_int64),
+        ("d2h_bytes", C.c_int64),
     ]
 
     def timing(self):
-        return {"k2_ms": self.k2_ms, "round_ms": self.round_ms, "launches": self.launches}
+        return {"k2_ms": self.k2_ms, "round_ms": self.round_ms, "launches": self.launches,
+                "host_ms": self.host_ms, "sync_ms": self.sync_ms, "h2d_bytes": self.h2d_bytes,
+                "d2h_bytes": self.d2h_bytes}
 
     def as_tuple(self):
         return (self.target, self.branched, self.bounded, self.inserted, self.pruned,
@@ -96,6 +102,7 @@ def load_library(path: str = LIB_PATH):
         _i32p, C.POINTER(C.c_int64), C.POINTER(C.c_int32), C.POINTER(C.c_int64), _i32p,
         C.POINTER(RoundRec)]
     L.fbb_explorer_reset.argtypes = [_vp, _u8p, _i32p, C.c_int64, C.c_int32, C.c_int]
+    L.fbb_explorer_set_residency.argtypes = [_vp, C.c_int]
     L.fbb_explorer_start_solve.argtypes = [_vp, C.c_int32, C.POINTER(RoundRec)]
     L.fbb_explorer_run.argtypes = [_vp, _i64p, C.c_int, C.c_int64, C.c_int64, _vp,
                                    C.POINTER(C.c_int64)]

@@ -11,6 +11,7 @@
 //              (integrate, search.hpp:84-107 / bench.hpp:96-106).
 // Only the per-segment survivor counts and the leaf minimum come back.
 #include <algorithm>
+#include <chrono>
 #include <climits>
 #include <cstdio>
 #include <cstdlib>
@@ -33,19 +34,28 @@ struct DBuf {
     void* p = nullptr;
     size_t bytes = 0;
     cudaStream_t st = nullptr;
+    bool host = false;  // pinned, device-mapped host memory (host-resident pending tree)
     cudaError_t ensure(size_t want) {
         if (want <= bytes) return cudaSuccess;
         size_t nb = std::max(want, bytes * 2);
         void* q = nullptr;
-        cudaError_t e = cudaMallocAsync(&q, nb, st);
+        cudaError_t e = host ? cudaHostAlloc(&q, nb, cudaHostAllocMapped | cudaHostAllocPortable)
+                             : cudaMallocAsync(&q, nb, st);
         if (e != cudaSuccess) return e;
-        if (p) cudaFreeAsync(p, st);
+        release();
         p = q;
         bytes = nb;
         return cudaSuccess;
     }
     void release() {
-        if (p) cudaFreeAsync(p, st);
+        if (p) {
+            if (host) {
+                cudaStreamSynchronize(st);  // no device access may still be in flight
+                cudaFreeHost(p);
+            } else {
+                cudaFreeAsync(p, st);
+            }
+        }
         p = nullptr;
         bytes = 0;
     }
@@ -80,6 +90,12 @@ struct HBuf {  // pinned host
 struct Store {
     DBuf masks, heads, prefix;
     int64_t cap = 0;
+    void set(cudaStream_t st, bool host) {
+        for (DBuf* b : {&masks, &heads, &prefix}) {
+            b->st = st;
+            b->host = host;
+        }
+    }
     NodeStore view() const { return NodeStore{masks.as<uint64_t>(), heads.as<int32_t>(), prefix.as<uint8_t>()}; }
 };
 
@@ -105,11 +121,12 @@ struct fbb_ctx {
     DBuf out_lb;
     // shared per-round device state
     Store staging;          // per-chunk compacted survivors (chunk c at c * cmax)
-    DBuf st_lb, st_count, st_offset;
+    Store parents;          // host-resident explorer: this round's parents, uploaded
+    DBuf st_lb, st_count;
     DBuf d_pool, d_round;   // Pool, RoundState
     HBuf h_pool, h_round;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
-    float last_k2_ms = 0.f, last_round_ms = 0.f;
+    float last_k2_ms = 0.f, last_round_ms = 0.f, last_sync_ms = 0.f;
     int last_launches = 0;
 
     // explorer
@@ -122,6 +139,8 @@ struct fbb_ctx {
     std::vector<int32_t> schedule;
     int64_t tot_branched = 0, tot_bounded = 0, tot_pruned = 0, tot_leaves = 0;
     bool explorer_ready = false;
+    bool host_pending = false;  // pending tree in pinned host memory (fbb_explorer_set_residency)
+    int64_t last_h2d = 0, last_d2h = 0;
     bool check = false;  // FBB_CHECK=1: validate the pending tree after every round
 
     int fail(int code, const std::string& m) {
@@ -150,17 +169,18 @@ cudaError_t store_ensure(fbb_ctx* ctx, Store& s, int64_t want, int64_t keep) {
     if (want <= s.cap) return cudaSuccess;
     int64_t nc = std::max<int64_t>(want, std::max<int64_t>(s.cap * 2, 1024));
     const int n = ctx->dt.n, m = ctx->dt.m, W = ctx->dt.W;
+    const bool host = s.masks.host;
     Store t;
-    t.masks.st = t.heads.st = t.prefix.st = ctx->stream;
-    s.masks.st = s.heads.st = s.prefix.st = ctx->stream;
+    t.set(ctx->stream, host);
+    s.set(ctx->stream, host);
     cudaError_t e;
     if ((e = t.masks.ensure((size_t)nc * W * 8)) != cudaSuccess) return e;
     if ((e = t.heads.ensure((size_t)nc * m * 4)) != cudaSuccess) return e;
     if ((e = t.prefix.ensure((size_t)nc * n)) != cudaSuccess) return e;
-    if (keep > 0) {  // stream-ordered: the copy precedes the old buffers' async free
-        cudaMemcpyAsync(t.masks.p, s.masks.p, (size_t)keep * W * 8, cudaMemcpyDeviceToDevice, ctx->stream);
-        cudaMemcpyAsync(t.heads.p, s.heads.p, (size_t)keep * m * 4, cudaMemcpyDeviceToDevice, ctx->stream);
-        cudaMemcpyAsync(t.prefix.p, s.prefix.p, (size_t)keep * n, cudaMemcpyDeviceToDevice, ctx->stream);
+    if (keep > 0) {  // stream-ordered: the copy precedes the old buffers' release
+        cudaMemcpyAsync(t.masks.p, s.masks.p, (size_t)keep * W * 8, cudaMemcpyDefault, ctx->stream);
+        cudaMemcpyAsync(t.heads.p, s.heads.p, (size_t)keep * m * 4, cudaMemcpyDefault, ctx->stream);
+        cudaMemcpyAsync(t.prefix.p, s.prefix.p, (size_t)keep * n, cudaMemcpyDefault, ctx->stream);
     }
     s.masks.release();
     s.heads.release();
@@ -204,7 +224,6 @@ int run_pool(fbb_ctx* ctx, Pool& pool, int first_internal, int32_t ub, int froze
     CK(store_ensure(ctx, ctx->staging, slots, 0), "staging");
     CK(ctx->st_lb.ensure((size_t)slots * 4), "staging");
     CK(ctx->st_count.ensure((size_t)std::max<int64_t>(pool.nchunks, 1) * 4), "staging");
-    CK(ctx->st_offset.ensure((size_t)(pool.nchunks + 1) * 8), "staging");
     CK(ctx->d_pool.ensure(sizeof(Pool)), "pool");
     CK(ctx->h_pool.ensure(sizeof(Pool)), "pool");
     CK(ctx->d_round.ensure(sizeof(RoundState)), "round state");
@@ -228,13 +247,12 @@ int run_pool(fbb_ctx* ctx, Pool& pool, int first_internal, int32_t ub, int froze
     }
     CK(cudaEventRecord(ctx->ev[1], st), "event");
     bool has_internal = first_internal < pool.nseg && pool.nchunks > 0;
-    ChunkOut out{ctx->staging.view(), ctx->st_lb.as<int32_t>(), ctx->st_count.as<int32_t>(),
-                 ctx->st_offset.as<int64_t>()};
+    ChunkOut out{ctx->staging.view(), ctx->st_lb.as<int32_t>(), ctx->st_count.as<int32_t>()};
     CK(launch_k2_internal(ctx->dt, ctx->k2, dp, pool, first_internal, ub, frozen, rs, out, st),
        "K2 internal");
     CK(cudaEventRecord(ctx->ev[2], st), "event");
     CK(launch_place(ctx->dt, ctx->k2, dp, pool, rs, out, st), "place");
-    launches += has_internal ? 3 : 1;
+    launches += has_internal ? 2 : 0;  // K2 + place
     size_t head = offsetof(RoundState, seg_surv) + (size_t)pool.nseg * 8;
     CK(cudaMemcpyAsync(ctx->h_round.p, rs, head, cudaMemcpyDeviceToHost, st), "round D2H");
     if (has_leaf)
@@ -242,7 +260,9 @@ int run_pool(fbb_ctx* ctx, Pool& pool, int first_internal, int32_t ub, int froze
                            cudaMemcpyDeviceToHost, st),
            "schedule D2H");
     CK(cudaEventRecord(ctx->ev[3], st), "event");
+    const auto t_sync = std::chrono::steady_clock::now();
     CK(cudaStreamSynchronize(st), "round");
+    ctx->last_sync_ms = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t_sync).count();
     if (ctx->h_round.as<RoundState>()->found < 0)
         return ctx->fail(FBB_E_STATE, "corrupt pending node (unscheduled-job count mismatch)");
     cudaEventElapsedTime(&ctx->last_k2_ms, ctx->ev[1], ctx->ev[2]);
@@ -314,9 +334,9 @@ int push_host_nodes(fbb_ctx* ctx, const uint8_t* prefix, const int32_t* depth, i
         CK(store_ensure(ctx, ctx->bucket[d], c0 + k, c0), "bucket grow");
         Store& b = ctx->bucket[d];
         cudaStream_t st = ctx->stream;
-        CK(cudaMemcpyAsync(b.masks.as<uint64_t>() + c0 * W, hm.data(), hm.size() * 8, cudaMemcpyHostToDevice, st), "push");
-        CK(cudaMemcpyAsync(b.heads.as<int32_t>() + c0 * m, hh.data(), hh.size() * 4, cudaMemcpyHostToDevice, st), "push");
-        CK(cudaMemcpyAsync(b.prefix.as<uint8_t>() + c0 * n, hp.data(), hp.size(), cudaMemcpyHostToDevice, st), "push");
+        CK(cudaMemcpyAsync(b.masks.as<uint64_t>() + c0 * W, hm.data(), hm.size() * 8, cudaMemcpyDefault, st), "push");
+        CK(cudaMemcpyAsync(b.heads.as<int32_t>() + c0 * m, hh.data(), hh.size() * 4, cudaMemcpyDefault, st), "push");
+        CK(cudaMemcpyAsync(b.prefix.as<uint8_t>() + c0 * n, hp.data(), hp.size(), cudaMemcpyDefault, st), "push");
         CK(cudaStreamSynchronize(st), "push");  // host vectors are reused
         ctx->cnt[d] = c0 + k;
     }
@@ -335,9 +355,9 @@ int check_pending(fbb_ctx* ctx) {
         std::vector<int32_t> hd((size_t)k * m);
         std::vector<uint8_t> pr((size_t)k * n);
         cudaStream_t st = ctx->stream;
-        CK(cudaMemcpyAsync(mk.data(), ctx->bucket[d].masks.p, mk.size() * 8, cudaMemcpyDeviceToHost, st), "check");
-        CK(cudaMemcpyAsync(hd.data(), ctx->bucket[d].heads.p, hd.size() * 4, cudaMemcpyDeviceToHost, st), "check");
-        CK(cudaMemcpyAsync(pr.data(), ctx->bucket[d].prefix.p, pr.size(), cudaMemcpyDeviceToHost, st), "check");
+        CK(cudaMemcpyAsync(mk.data(), ctx->bucket[d].masks.p, mk.size() * 8, cudaMemcpyDefault, st), "check");
+        CK(cudaMemcpyAsync(hd.data(), ctx->bucket[d].heads.p, hd.size() * 4, cudaMemcpyDefault, st), "check");
+        CK(cudaMemcpyAsync(pr.data(), ctx->bucket[d].prefix.p, pr.size(), cudaMemcpyDefault, st), "check");
         CK(cudaStreamSynchronize(st), "check");
         std::vector<uint64_t> m2(W);
         std::vector<int32_t> h2(m);
@@ -359,6 +379,15 @@ int check_pending(fbb_ctx* ctx) {
 void explorer_clear(fbb_ctx* ctx) {
     const int n = ctx->dt.n;
     if ((int)ctx->bucket.size() != n + 1) ctx->bucket.resize(n + 1);
+    for (Store& b : ctx->bucket) {
+        if (b.masks.host != ctx->host_pending) {  // residency changed: drop the old storage
+            b.masks.release();
+            b.heads.release();
+            b.prefix.release();
+            b.cap = 0;
+        }
+        b.set(ctx->stream, ctx->host_pending);
+    }
     ctx->cnt.assign(n + 1, 0);
     ctx->schedule.assign(n, 0);
     ctx->found = 0;
@@ -368,6 +397,7 @@ void explorer_clear(fbb_ctx* ctx) {
 
 // One explorer round with pool target `target` (> 0).
 int explorer_round(fbb_ctx* ctx, int64_t target, fbb_round_t* rec) {
+    const auto t0 = std::chrono::steady_clock::now();
     const int n = ctx->dt.n;
     std::memset(rec, 0, sizeof(*rec));
     rec->target = target;
@@ -400,9 +430,31 @@ int explorer_round(fbb_ctx* ctx, int64_t target, fbb_round_t* rec) {
         // keep the full old content: this round's parents may sit in bucket d1's popped region
         CK(store_ensure(ctx, ctx->bucket[d1], worst, ctx->cnt[d1]), "bucket grow");
     }
+    int64_t h2d = 0, npar = 0;
+    if (ctx->host_pending) {
+        // host-resident pending tree: this round's parents (the top rows of each
+        // selected bucket, contiguous) go host -> device; survivors are written by
+        // place_kernel straight into the (device-mapped, pinned) host buckets
+        for (int s = 0; s < local.nseg; ++s) npar += local.seg[s].count;
+        CK(store_ensure(ctx, ctx->parents, npar, 0), "parents");
+        const int m = ctx->dt.m, W = ctx->dt.W;
+        const NodeStore pv = ctx->parents.view();
+        int64_t o = 0;
+        for (int s = 0; s < local.nseg; ++s) {
+            Segment& sg = local.seg[s];
+            const NodeStore b = ctx->bucket[sg.depth].view();
+            const int64_t lo = after[sg.depth], k = sg.count;
+            CK(cudaMemcpyAsync(pv.masks + o * W, b.masks + lo * W, (size_t)k * W * 8, cudaMemcpyDefault, ctx->stream), "parents H2D");
+            CK(cudaMemcpyAsync(pv.heads + o * m, b.heads + lo * m, (size_t)k * m * 4, cudaMemcpyDefault, ctx->stream), "parents H2D");
+            CK(cudaMemcpyAsync(pv.prefix + o * n, b.prefix + lo * n, (size_t)k * n, cudaMemcpyDefault, ctx->stream), "parents H2D");
+            sg.first = o + k - 1;  // LIFO: the bucket top is popped first
+            o += k;
+        }
+        h2d = npar * (int64_t)node_bytes(ctx);
+    }
     for (int s = 0; s < local.nseg; ++s) {  // views may have moved after growth
         Segment& sg = local.seg[s];
-        sg.src = ctx->bucket[sg.depth].view();
+        sg.src = ctx->host_pending ? ctx->parents.view() : ctx->bucket[sg.depth].view();
         if (sg.depth < n - 2) {
             sg.dst = ctx->bucket[sg.depth + 1].view();
             sg.dst_base = after[sg.depth + 1];
@@ -462,6 +514,10 @@ int explorer_round(fbb_ctx* ctx, int64_t target, fbb_round_t* rec) {
     ctx->tot_pruned += rec->pruned;
     ctx->tot_leaves += rec->leaves;
     rec->pending = pending_total(ctx);
+    rec->sync_ms = ctx->last_sync_ms;
+    rec->h2d_bytes = h2d;
+    rec->d2h_bytes = ctx->host_pending ? rec->inserted * (int64_t)node_bytes(ctx) : 0;
+    rec->host_ms = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t0).count();
     return FBB_OK;
 }
 
@@ -527,10 +583,10 @@ fbb_ctx* fbb_create(int device, const int32_t* p, int n, int m) {
             }
         }
         for (DBuf* b : {&ctx->k1_masks, &ctx->k1_heads, &ctx->k1_depth, &ctx->k1_lb, &ctx->out_lb,
-                        &ctx->st_lb, &ctx->st_count, &ctx->st_offset, &ctx->d_pool, &ctx->d_round})
+                        &ctx->st_lb, &ctx->st_count, &ctx->d_pool, &ctx->d_round})
             b->st = ctx->stream;
-        for (Store* st : {&ctx->batch_in, &ctx->batch_out, &ctx->staging})
-            st->masks.st = st->heads.st = st->prefix.st = ctx->stream;
+        for (Store* st : {&ctx->batch_in, &ctx->batch_out, &ctx->staging, &ctx->parents})
+            st->set(ctx->stream, false);
     }
     rc = upload_tables(ctx->ht, &ctx->dt, &why);
     if (rc != FBB_OK) {
@@ -567,9 +623,9 @@ void fbb_destroy(fbb_ctx* ctx) {
     cudaSetDevice(ctx->device);
     free_tables(&ctx->dt);
     for (DBuf* b : {&ctx->k1_masks, &ctx->k1_heads, &ctx->k1_depth, &ctx->k1_lb, &ctx->out_lb,
-                    &ctx->st_lb, &ctx->st_count, &ctx->st_offset, &ctx->d_pool, &ctx->d_round})
+                    &ctx->st_lb, &ctx->st_count, &ctx->d_pool, &ctx->d_round})
         b->release();
-    for (Store* s : {&ctx->batch_in, &ctx->batch_out, &ctx->staging}) {
+    for (Store* s : {&ctx->batch_in, &ctx->batch_out, &ctx->staging, &ctx->parents}) {
         s->masks.release();
         s->heads.release();
         s->prefix.release();
@@ -770,6 +826,14 @@ int fbb_expand_bound_prune(fbb_ctx* ctx, const uint64_t* masks, const int32_t* h
     return FBB_OK;
 }
 
+int fbb_explorer_set_residency(fbb_ctx* ctx, int pending_on_host) {
+    if (!ctx) return FBB_E_ARG;
+    cudaSetDevice(ctx->device);
+    ctx->host_pending = pending_on_host != 0;
+    explorer_clear(ctx);
+    return FBB_OK;
+}
+
 int fbb_explorer_reset(fbb_ctx* ctx, const uint8_t* prefix, const int32_t* depth, int64_t count,
                        int32_t ub, int frozen) {
     if (!ctx) return FBB_E_ARG;
@@ -881,7 +945,7 @@ int fbb_explorer_pending(fbb_ctx* ctx, uint8_t* prefix, int32_t* depth, int64_t 
         if (k == 0) continue;
         if (prefix) {
             CK(cudaMemcpyAsync(prefix + o * n, ctx->bucket[d].prefix.p, (size_t)k * n,
-                               cudaMemcpyDeviceToHost, ctx->stream),
+                               cudaMemcpyDefault, ctx->stream),
                "pending D2H");
             CK(cudaStreamSynchronize(ctx->stream), "pending D2H");
         }

@@ -391,87 +391,112 @@ __global__ void leaf_schedule_kernel(DevTables t, const Pool* __restrict__ pool,
     *found = 1;
 }
 
-// Exclusive scan of the per-chunk survivor counts (one CTA; a pool has a few
-// thousand chunks), per-segment totals and the pool total.
-__global__ void chunk_scan_kernel(const Pool* __restrict__ pool, RoundState* rs, ChunkOut out) {
-    __shared__ int64_t warp_tot[32];
-    __shared__ int64_t carry;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-    const int64_t nchunks = pool->nchunks;
-    if (tid == 0) carry = 0;
-    __syncthreads();
-    for (int64_t base = 0; base < nchunks; base += blockDim.x) {
-        const int64_t i = base + tid;
-        const int64_t v = i < nchunks ? out.count[i] : 0;
-        int64_t incl = v;
+// Places every chunk's survivors at their final, batch-ordered position: the
+// segment's dst at dst_base + (survivors of the segment's earlier chunks), or the
+// contiguous output at (survivors of all earlier chunks) when dst_base < 0; adds
+// the per-segment and pool totals to `rs`.  One CTA per kPlaceChunks consecutive
+// chunks computes its own exclusive offsets (a block reduction over the counts of
+// all earlier chunks -- a few thousand L2-resident ints), so there is no separate
+// scan launch; rows are then copied flat (one thread per 4-byte head, mask word or
+// prefix byte), which keeps many independent loads in flight per thread.
+constexpr int kPlaceChunks = 8;
+constexpr int kPlaceThreads = 256;
+constexpr int kPlaceBatch = 8;
+
+// Copies rows x width elements: element f = (row, k) with row = f / width.
+template <int B, class Load, class Store>
+__device__ __forceinline__ void copy_rows(int rows, int width, Load load, Store store) {
+    const int total = rows * width;
+    for (int base = threadIdx.x; base < total; base += B * kPlaceThreads) {
+        decltype(load(0, 0)) v[B];
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            int64_t u = __shfl_up_sync(0xFFFFFFFFu, incl, o);
-            if (lane >= o) incl += u;
+        for (int u = 0; u < B; ++u) {
+            const int f = base + u * kPlaceThreads;
+            if (f < total) v[u] = load(f / width, f % width);
         }
-        if (lane == 31) warp_tot[warp] = incl;
-        __syncthreads();
-        int64_t woff = 0, tot = 0;
-        for (int w = 0; w < nw; ++w) {
-            if (w < warp) woff += warp_tot[w];
-            tot += warp_tot[w];
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+            const int f = base + u * kPlaceThreads;
+            if (f < total) store(f / width, f % width, v[u]);
         }
-        if (i < nchunks) out.offset[i] = carry + woff + incl - v;
-        __syncthreads();
-        if (tid == 0) carry += tot;
-        __syncthreads();
     }
-    if (tid == 0) out.offset[nchunks] = carry;
-    __syncthreads();
-    for (int s = tid; s < pool->nseg; s += blockDim.x) {
-        const int64_t cb = pool->seg[s].chunk_base;
-        const int64_t ce = s + 1 < pool->nseg ? pool->seg[s + 1].chunk_base : nchunks;
-        rs->seg_surv[s] = ce > cb ? out.offset[ce] - out.offset[cb] : 0;
-    }
-    if (tid == 0) rs->total = carry;
 }
 
-// Moves every chunk's survivors to their final place: segment dst at
-// dst_base + (offset[c] - offset[first chunk of the segment]), or the contiguous
-// output at offset[c] (dst_base < 0).  A warp per chunk; a chunk's rows are
-// contiguous in both places, so each array moves as one flat run.
-__global__ void place_kernel(DevTables t, const Pool* __restrict__ pool, int cmax, ChunkOut out) {
+__device__ __forceinline__ int64_t block_sum(int64_t v, int64_t* s_red) {
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) s_red[warp] = v;
+    __syncthreads();
+    int64_t tot = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += s_red[w];
+    return tot;
+}
+
+__global__ void __launch_bounds__(kPlaceThreads) place_kernel(DevTables t, const Pool* __restrict__ pool,
+                                                              int cmax, RoundState* rs, ChunkOut out) {
     const int n = t.n, m = t.m, W = t.W;
-    const int lane = threadIdx.x & 31;
+    __shared__ int64_t s_red[kPlaceThreads / 32];
+    __shared__ int s_row0[kPlaceChunks + 1];  // CTA-local exclusive survivor offsets
+    __shared__ int64_t s_dst[kPlaceChunks];   // destination row of each chunk's first survivor
+    __shared__ NodeStore s_store[kPlaceChunks];
+    __shared__ int32_t* s_dlb[kPlaceChunks];
+    extern __shared__ uint8_t s_rc[];          // chunk of each row (cmax * kPlaceChunks)
+    const int tid = threadIdx.x;
     const int64_t nchunks = pool->nchunks;
-    const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t c = wid; c < nchunks; c += nwarps) {
-        const int cnt = out.count[c];
-        if (cnt == 0) continue;
-        const int s = find_segment_lb(pool, 0, c);
-        const Segment& sg = pool->seg[s];
-        const int64_t pos = sg.dst_base < 0 ? out.offset[c]
-                                            : sg.dst_base + out.offset[c] - out.offset[sg.chunk_base];
-        const int64_t so = c * (int64_t)cmax;
-        const NodeStore dst = sg.dst;
-        {
-            const int32_t* a = out.nodes.heads + so * m;
-            int32_t* b = dst.heads + pos * m;
-            for (int x = lane; x < cnt * m; x += 32) b[x] = a[x];
-        }
-        {
-            const uint64_t* a = out.nodes.masks + so * W;
-            uint64_t* b = dst.masks + pos * W;
-            for (int x = lane; x < cnt * W; x += 32) b[x] = a[x];
-        }
-        {  // prefixes: only the first depth + 1 bytes of a row are meaningful
-            const uint8_t* a = out.nodes.prefix + so * n;
-            uint8_t* b = dst.prefix + pos * n;
-            const int len = sg.depth + 1;
-            for (int x = lane; x < cnt * len; x += 32) {
-                const int i = x / len, k = x - i * len;
-                b[i * n + k] = a[i * n + k];
-            }
-        }
-        if (sg.dst_lb)
-            for (int x = lane; x < cnt; x += 32) sg.dst_lb[pos + x] = out.lb[so + x];
+    const int64_t c0 = (int64_t)blockIdx.x * kPlaceChunks;
+    const int nch = (int)(nchunks - c0 < kPlaceChunks ? nchunks - c0 : kPlaceChunks);
+    const int s0 = find_segment_lb(pool, 0, c0);
+    const int64_t cb0 = pool->seg[s0].chunk_base;
+    int64_t a = 0, b = 0;  // survivors of chunks [0, cb0) and [cb0, c0)
+    for (int64_t i = tid; i < c0; i += blockDim.x) {
+        const int v = out.count[i];
+        if (i < cb0) a += v; else b += v;
     }
+    const int64_t A = block_sum(a, s_red);
+    const int64_t B = block_sum(b, s_red);
+    if (tid < 32) {
+        const int v = tid < nch ? out.count[c0 + tid] : 0;
+        int incl = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int u = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+            if (tid >= o) incl += u;
+        }
+        if (tid < nch) s_row0[tid] = incl - v;
+        if (tid == nch - 1) s_row0[nch] = incl;
+    }
+    __syncthreads();
+    if (tid < nch) {
+        const int s = find_segment_lb(pool, s0, c0 + tid);
+        const Segment& sg = pool->seg[s];
+        const int64_t glob = A + B + s_row0[tid];
+        const int64_t seg0 = s == s0 ? A : A + B + s_row0[sg.chunk_base - c0];
+        s_dst[tid] = sg.dst_base < 0 ? glob : sg.dst_base + (glob - seg0);
+        s_store[tid] = sg.dst;
+        s_dlb[tid] = sg.dst_lb;
+        const int cnt = s_row0[tid + 1] - s_row0[tid];
+        if (cnt) atomicAdd((unsigned long long*)&rs->seg_surv[s], (unsigned long long)cnt);
+    }
+    __syncthreads();
+    const int R = s_row0[nch];
+    if (tid == 0 && R) atomicAdd((unsigned long long*)&rs->total, (unsigned long long)R);
+    // row -> chunk table, then batched copies: every thread issues kPlaceBatch
+    // independent (read-only path) loads before its stores
+    for (int c = 0; c < nch; ++c)
+        for (int row = s_row0[c] + tid; row < s_row0[c + 1]; row += kPlaceThreads) s_rc[row] = (uint8_t)c;
+    __syncthreads();
+    auto src_row = [&](int row) { const int c = s_rc[row]; return (c0 + c) * (int64_t)cmax + (row - s_row0[c]); };
+    auto dst_row = [&](int row) { const int c = s_rc[row]; return s_dst[c] + (row - s_row0[c]); };
+    copy_rows<kPlaceBatch>(R, m, [&](int row, int k) { return __ldg(out.nodes.heads + src_row(row) * m + k); },
+                           [&](int row, int k, int32_t v) { s_store[s_rc[row]].heads[dst_row(row) * m + k] = v; });
+    copy_rows<kPlaceBatch>(R, W, [&](int row, int k) { return __ldg(out.nodes.masks + src_row(row) * W + k); },
+                           [&](int row, int k, uint64_t v) { s_store[s_rc[row]].masks[dst_row(row) * W + k] = v; });
+    // whole prefix rows (bytes past depth + 1 are don't-care in both places)
+    copy_rows<kPlaceBatch>(R, n, [&](int row, int k) { return __ldg(out.nodes.prefix + src_row(row) * n + k); },
+                           [&](int row, int k, uint8_t v) { s_store[s_rc[row]].prefix[dst_row(row) * n + k] = v; });
+    if (s_dlb[0] || (nch > 1 && s_dlb[nch - 1]))
+        copy_rows<kPlaceBatch>(R, 1, [&](int row, int) { return __ldg(out.lb + src_row(row)); },
+                               [&](int row, int, int32_t v) { s_dlb[s_rc[row]][dst_row(row)] = v; });
 }
 
 }  // namespace
@@ -540,13 +565,10 @@ namespace fbb {
 
 cudaError_t launch_place(const DevTables& t, const K2Config& cfg, const Pool* d_pool,
                          const Pool& h_pool, RoundState* rs, ChunkOut out, cudaStream_t stream) {
-    chunk_scan_kernel<<<1, 1024, 0, stream>>>(d_pool, rs, out);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess || h_pool.nchunks == 0) return e;
-    int64_t warps = h_pool.nchunks;
-    int blocks = (int)((warps * 32 + 255) / 256);
-    if (blocks > 1184) blocks = 1184;
-    place_kernel<<<blocks, 256, 0, stream>>>(t, d_pool, cfg.cmax, out);
+    if (h_pool.nchunks == 0) return cudaSuccess;
+    const int64_t blocks = (h_pool.nchunks + kPlaceChunks - 1) / kPlaceChunks;
+    place_kernel<<<(unsigned)blocks, kPlaceThreads, (size_t)cfg.cmax * kPlaceChunks, stream>>>(
+        t, d_pool, cfg.cmax, rs, out);
     return cudaGetLastError();
 }
 

@@ -94,7 +94,7 @@ struct Segment {
     int64_t child_base;  // batch position of the segment's first child
     int64_t chunk_base;  // first chunk index of the segment
     NodeStore dst;       // where survivors go (depth+1 bucket, or the output batch)
-    int64_t dst_base;    // < 0: contiguous output at offsets[chunk]
+    int64_t dst_base;    // < 0: one contiguous output for the whole pool
     int32_t* dst_lb;     // optional survivor bounds
 };
 
@@ -116,13 +116,12 @@ struct K2Config {
 };
 K2Config k2_config(const DevTables& t, int device);
 
-// Per-chunk staging of survivors (compacted, batch order inside the chunk), placed
-// by place_kernel after chunk_scan_kernel computed the exclusive offsets.
+// Per-chunk staging of survivors (compacted, batch order inside the chunk), moved
+// to their final place by place_kernel.
 struct ChunkOut {
     NodeStore nodes;  // capacity nchunks * cmax, chunk c at [c * cmax, c * cmax + count[c])
     int32_t* lb;      // survivor bounds (same indexing)
     int32_t* count;   // survivors per chunk
-    int64_t* offset;  // exclusive prefix of count
 };
 
 // Per-round device state; the head (everything before `schedule`) is zeroed by
@@ -151,8 +150,8 @@ cudaError_t launch_k2_leaves(const DevTables& t, const Pool* d_pool, const Pool&
 cudaError_t launch_k2_internal(const DevTables& t, const K2Config& cfg, const Pool* d_pool,
                                const Pool& h_pool, int first_seg, int32_t ub, int frozen,
                                RoundState* rs, ChunkOut out, cudaStream_t stream);
-// Exclusive offsets of the chunk counts, per-segment totals and the pool total
-// into `rs`; then every chunk's survivors moved to its segment's dst.
+// Every chunk's survivors moved to its segment's dst in batch order; per-segment
+// totals and the pool total added to `rs` (zeroed before the round).
 cudaError_t launch_place(const DevTables& t, const K2Config& cfg, const Pool* d_pool,
                          const Pool& h_pool, RoundState* rs, ChunkOut out, cudaStream_t stream);
 // Schedule of the best leaf when it beats ub (before the parents are recycled).

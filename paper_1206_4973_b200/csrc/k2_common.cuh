@@ -4,11 +4,11 @@
 // Output ordering.  A pool's children are processed in chunks (runs of parents
 // of one segment, claimed in increasing order from an atomic ticket for load
 // balance).  Each chunk compacts its survivors (stable, batch order) into its
-// own staging slot and records the count; chunk_scan_kernel turns the counts
-// into exclusive offsets (and per-segment totals) and place_kernel moves every
-// chunk's survivors to their final, batch-ordered positions (the reference's
-// push order, search.hpp:100-102).  No chunk ever waits on another: an in-kernel
-// decoupled look-back was tried and cost ~30 % of K2 in barrier stalls.
+// own staging slot and records the count; place_kernel derives the exclusive
+// offsets from the counts and moves every chunk's survivors to their final,
+// batch-ordered positions (the reference's push order, search.hpp:100-102).  No
+// chunk ever waits on another: an in-kernel decoupled look-back was tried and
+// cost ~30 % of K2 in barrier stalls.
 #pragma once
 
 #include "fbb_internal.h"

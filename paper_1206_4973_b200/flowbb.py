@@ -265,7 +265,12 @@ class Context:
         return (surv, ol[:k].copy(), best, lpos.value,
                 [int(x) for x in sched] if best is not None else None, rec.as_tuple())
 
-    # device-resident explorer -------------------------------------------------------------
+    # explorer (pending tree in HBM, or in pinned host memory) ------------------------------
+    def explorer_set_residency(self, on_host: bool):
+        """Pending tree in device memory (False) or pinned host memory (True: every round
+        uploads its parents and receives only the survivors).  Clears the tree."""
+        self._check(self.L.fbb_explorer_set_residency(self.h, 1 if on_host else 0))
+
     def explorer_reset(self, nodes: NodeBatch, ub: int, frozen: bool = True):
         cnt = len(nodes)
         pre = np.ascontiguousarray(nodes.prefix.ravel()) if cnt else np.zeros(1, np.uint8)
@@ -522,13 +527,15 @@ def _drive(ctx: Context, targets, autotune, window, probes, budget, max_rounds):
 
 def resolve_workload(inst: Instance, nodes, incumbent_value: int, batch: Optional[int] = None,
                      autotune: bool = False, window: int = 5, probes: int = 2, budget: int = 0,
-                     targets=None, device: int = 0, max_rounds: int = 1 << 40
-                     ) -> ResolutionResult:
+                     targets=None, device: int = 0, max_rounds: int = 1 << 40,
+                     pending_on_host: bool = False) -> ResolutionResult:
     """bench.hpp:63-114 with the incumbent frozen at `incumbent_value`, on the device
     explorer.  `nodes`: NodeBatch or list of prefixes (the snapshot list L, pushed in order).
     `targets` (per-round pool targets) replays a recorded schedule; `budget` stops after the
-    first round whose cumulative bounded count reaches it."""
+    first round whose cumulative bounded count reaches it.  `pending_on_host` keeps the
+    pending tree in pinned host memory (parents uploaded, survivors returned per round)."""
     ctx = context_for(inst, device)
+    ctx.explorer_set_residency(pending_on_host)
     if not isinstance(nodes, NodeBatch):
         nodes = nodes_from_prefixes(inst, nodes)
     if targets is None:
@@ -549,10 +556,12 @@ def resolve_workload(inst: Instance, nodes, incumbent_value: int, batch: Optiona
 
 def solve(inst: Instance, initial_ub: Optional[int] = None, fixed_batch: Optional[int] = None,
           autotune: bool = False, window: int = 5, probes: int = 2, budget: int = 0,
-          targets=None, device: int = 0, max_rounds: int = 1 << 40) -> Solution:
+          targets=None, device: int = 0, max_rounds: int = 1 << 40,
+          pending_on_host: bool = False) -> Solution:
     """search.hpp:124-174 on the device explorer (strict-improvement incumbent, mid-batch
     updates, deepest-first LIFO selection)."""
     ctx = context_for(inst, device)
+    ctx.explorer_set_residency(pending_on_host)
     t0 = time.perf_counter()
     r0 = ctx.explorer_start_solve(initial_ub)
     if targets is None:

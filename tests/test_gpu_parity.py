@@ -198,32 +198,36 @@ def test_k2_random_parents_vs_oracle(oracle):
 
 # ---- device-resident explorer ---------------------------------------------------------------
 
-def test_explorer_resolve_traces_match_reference(instances, traces):
+@pytest.mark.parametrize("on_host", [False, True], ids=["pending_hbm", "pending_host"])
+def test_explorer_resolve_traces_match_reference(instances, traces, on_host):
     for tr in traces["resolve"]:
         inst = inst_of(instance_p(instances, tr["instance"]))
         res = fbb.resolve_workload(inst, tr["roots"], tr["ub"], targets=tr["targets"],
-                                   budget=tr["budget"])
+                                   budget=tr["budget"], pending_on_host=on_host)
         gold = [tuple(r) for r in tr["rounds"]]
         assert res.rounds == gold, (tr["instance"], tr["targets"][:2])
         assert res.nodes_bounded == tr["result"]["bounded"]
         assert (res.best if res.best is not None else -1) == tr["result"]["optimum"]
 
 
-def test_explorer_solve_traces_match_reference(instances, traces):
+@pytest.mark.parametrize("on_host", [False, True], ids=["pending_hbm", "pending_host"])
+def test_explorer_solve_traces_match_reference(instances, traces, on_host):
     for tr in traces["solve"]:
         inst = inst_of(instance_p(instances, tr["instance"]))
         ub = None if tr["initial_ub"] < 0 else tr["initial_ub"]
-        sol = fbb.solve(inst, ub, targets=tr["targets"], budget=tr["budget"])
+        sol = fbb.solve(inst, ub, targets=tr["targets"], budget=tr["budget"],
+                        pending_on_host=on_host)
         gold = [tuple(r) for r in tr["rounds"]]
         assert sol.rounds == gold, tr["instance"]
         assert sol.optimum == tr["result"]["optimum"]
         assert sol.schedule == tr["schedule"]
 
 
-def test_explorer_full_solves_match_reference(traces):
+@pytest.mark.parametrize("on_host", [False, True], ids=["pending_hbm", "pending_host"])
+def test_explorer_full_solves_match_reference(traces, on_host):
     for case in traces["solve_full"]:
         p = np.asarray(case["p"], np.int32).reshape(case["n"], case["m"])
-        sol = fbb.solve(inst_of(p), None, fixed_batch=case["batch"])
+        sol = fbb.solve(inst_of(p), None, fixed_batch=case["batch"], pending_on_host=on_host)
         assert sol.optimum == case["optimum"]
         assert sol.schedule == case["schedule"]
         assert [sol.stats.branched, sol.stats.bounded, sol.stats.pruned] == case["stats"]
