@@ -39,13 +39,15 @@ INT32_LANES_PER_SM = 128  # ALU pipe 64 + FMA pipe 64 integer lanes / clk / SM (
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--target", type=int, default=262144)
     ap.add_argument("--instance", default="ta021")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-seconds", type=float, default=60.0,
+                    help="time cap of the reference arm's timed rounds")
     ap.add_argument("--cpu-sample", type=int, default=1_000_000,
                     help="bounded-node budget of the CPU baseline sample")
     return ap.parse_args()
@@ -56,9 +58,27 @@ def dist_env():
             int(os.environ.get("LOCAL_RANK", 0)))
 
 
+def _clock_poll(device, stop, q, period):
+    """Child process: NVML SM clock + throttle reasons every `period` s until `stop`."""
+    import pynvml
+
+    pynvml.nvmlInit()
+    h = pynvml.nvmlDeviceGetHandleByIndex(device)
+    out = [pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)]
+    while not stop.is_set():
+        try:
+            out.append((time.time(), pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM),
+                        pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)))
+        except Exception:  # noqa: BLE001
+            pass
+        time.sleep(period)
+    q.put(out)
+
+
 class ClockSampler:
-    """SM clock and throttle reasons DURING the timed region, polled through NVML from a
-    background thread every ~1 ms (nvidia-smi's 100 ms period would miss a few-ms region);
+    """SM clock and throttle reasons DURING the timed region, polled through NVML by a
+    separate process (no GIL contention with the timed thread) every 10 ms -- each NVML
+    query holds a driver lock for up to ~1 ms, so faster polling inflates the host side;
     the raw samples go to gpurun_out/clocks_<pid>.csv."""
 
     REASONS = {"hw_slowdown": "nvmlClocksEventReasonHwSlowdown",
@@ -67,53 +87,47 @@ class ClockSampler:
                "sw_power_cap": "nvmlClocksEventReasonSwPowerCap",
                "hw_power_brake": "nvmlClocksEventReasonHwPowerBrakeSlowdown"}
 
-    def __init__(self, device):
-        import threading
+    def __init__(self, device, period=0.01):
+        import multiprocessing as mp
 
-        self.samples, self.stop = [], threading.Event()
         try:
-            import pynvml
-
-            pynvml.nvmlInit()
-            self.nv = pynvml
-            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
-            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
-        except Exception:
-            self.nv = None
+            import pynvml  # noqa: F401
+        except Exception:  # noqa: BLE001
+            self.proc = None
             return
-        self.t = threading.Thread(target=self._run, daemon=True)
-        self.t.start()
-
-    def _run(self):
-        nv = self.nv
-        while not self.stop.is_set():
-            try:
-                mhz = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
-                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
-                self.samples.append((time.perf_counter(), mhz, rs))
-            except Exception:
-                pass
-            time.sleep(0.001)
+        ctx = mp.get_context("spawn")
+        self.stop, self.q = ctx.Event(), ctx.Queue()
+        self.proc = ctx.Process(target=_clock_poll, args=(device, self.stop, self.q, period),
+                                daemon=True)
+        self.proc.start()
+        time.sleep(0.5)  # NVML init in the child before the timed region starts
 
     def result(self):
-        if self.nv is None:
+        if self.proc is None:
             return None
         self.stop.set()
-        self.t.join()
-        if not self.samples:
+        try:
+            out = self.q.get(timeout=30)
+        except Exception:  # noqa: BLE001
             return None
+        self.proc.join(timeout=10)
+        max_mhz, samples = out[0], out[1:]
+        if not samples:
+            return None
+        import pynvml
+
         os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
         with open(os.path.join(ROOT, "gpurun_out", f"clocks_{os.getpid()}.csv"), "w") as f:
-            for t, mhz, rs in self.samples:
+            for t, mhz, rs in samples:
                 f.write(f"{t:.6f},{mhz},{rs:#x}\n")
         reasons = set()
-        for _, _, rs in self.samples:
+        for _, _, rs in samples:
             for name, attr in self.REASONS.items():
-                if rs & getattr(self.nv, attr, 0):
+                if rs & getattr(pynvml, attr, 0):
                     reasons.add(name)
-        return {"sm_mhz": statistics.median(m for _, m, _ in self.samples),
-                "sm_max_mhz": self.max_mhz, "reasons": sorted(reasons),
-                "samples": len(self.samples), "source": "NVML, ~1 ms polling"}
+        return {"sm_mhz": statistics.median(m for _, m, _ in samples),
+                "sm_max_mhz": max_mhz, "reasons": sorted(reasons),
+                "samples": len(samples), "source": "NVML from a child process, ~10 ms polling"}
 
 
 def measured_peaks():
@@ -139,7 +153,10 @@ def reference_arm(args, inst_name):
         ref = Ref()
         cores = ref.detect_units()
         p = ref.generate_instance(n, m, seed)
-        pre, rounds, secs = ref.bench_rounds(p, ub, args.target, args.warmup, args.steps, cores)
+        # each step is one full reference round (~1 s at 262K children on 16 cores): the
+        # timed steps stop after ~60 s so the arm ends within a few minutes at any K
+        pre, rounds, secs = ref.bench_rounds(p, ub, args.target, min(args.warmup, 3), args.steps,
+                                             cores, max_seconds=args.ref_seconds)
         kind = "reference"
     else:  # the C restatement, single thread (reference not compiled on this host)
         orc = Oracle()

@@ -132,9 +132,11 @@ int fbb_expand_bound_prune(fbb_ctx* ctx, const uint64_t* masks, const int32_t* h
  * incumbent) or solve (search.hpp:124-174). */
 
 /* Where the pending tree lives: device memory (0, default) or pinned host
- * memory (1: the paper's Type-1 split -- the host owns the tree, each round
- * uploads its parents and the surviving children come back into the host
- * buckets).  Clears the pending tree.  Same explorer semantics either way. */
+ * memory (1: the paper's Type-1 split -- the host owns the tree; each round K2
+ * reads its parents from the device-mapped host buckets over the host link and
+ * the surviving children are written back into them).  Clears the pending
+ * tree.  Same explorer semantics either way; the per-round h2d/d2h byte counts
+ * are reported in fbb_round_t. */
 int fbb_explorer_set_residency(fbb_ctx* ctx, int pending_on_host);
 
 /* Reset the pending tree to the given nodes (pushed in order, like

@@ -295,21 +295,26 @@ class Ref:
         L.ref_bench_rounds.argtypes = [C.c_int, C.c_int, _i32p, C.c_int32, C.c_int64, C.c_int,
                                        C.c_int, C.c_int, C.POINTER(C.c_int64), C.c_void_p,
                                        np.ctypeslib.ndpointer(dtype=np.float64,
-                                                              flags="C_CONTIGUOUS")]
+                                                              flags="C_CONTIGUOUS"),
+                                       C.c_double, C.POINTER(C.c_int)]
 
-    def bench_rounds(self, p, ub, target, warm, steps, backends):
-        """Prefill-until-full, `warm` untimed rounds, `steps` timed rounds of the reference
-        resolve loop; returns (prefill_rounds, [round tuples], [seconds])."""
+    def bench_rounds(self, p, ub, target, warm, steps, backends, max_seconds=0.0):
+        """Prefill-until-full, `warm` untimed rounds, up to `steps` timed rounds of the
+        reference resolve loop (stopping once `max_seconds` > 0 of them have elapsed);
+        returns (prefill_rounds, [round tuples], [seconds])."""
         n, m = p.shape
         pre = C.c_int64(0)
+        done = C.c_int(0)
         trace = (Round * max(steps, 1))()
         secs = np.zeros(max(steps, 1), np.float64)
         rc = self.lib.ref_bench_rounds(n, m, np.ascontiguousarray(p, np.int32).ravel(), ub, target,
                                        warm, steps, backends, C.byref(pre),
-                                       C.cast(trace, C.c_void_p), secs)
+                                       C.cast(trace, C.c_void_p), secs, float(max_seconds),
+                                       C.byref(done))
         if rc != 0:
             raise RuntimeError("ref_bench_rounds failed")
-        return pre.value, [trace[i].as_tuple() for i in range(steps)], list(secs[:steps])
+        k = done.value
+        return pre.value, [trace[i].as_tuple() for i in range(k)], list(secs[:k])
 
     def detect_units(self):
         return int(self.lib.ref_detect_units())

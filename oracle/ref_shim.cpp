@@ -305,7 +305,7 @@ int ref_detect_units() { return detect_units(); }
 // Per timed round the counts go to trace[0..steps) and the seconds to secs[].
 int ref_bench_rounds(int n, int m, const int32_t* p, int32_t ub, int64_t target, int warm,
                      int steps, int backends, int64_t* prefill_rounds, orc_round* trace,
-                     double* secs) {
+                     double* secs, double max_seconds, int* steps_done) {
     try {
         Instance inst = make_instance(n, m, p);
         BackendSet set(backends, wide_descriptor());
@@ -348,13 +348,18 @@ int ref_bench_rounds(int n, int m, const int32_t* p, int32_t ub, int64_t target,
         }
         *prefill_rounds = pre;
         for (int i = 0; i < warm; ++i) round(nullptr);
-        for (int i = 0; i < steps; ++i) {
+        double spent = 0.0;
+        *steps_done = 0;
+        for (int i = 0; i < steps && (i == 0 || max_seconds <= 0 || spent < max_seconds); ++i) {
             auto t0 = std::chrono::steady_clock::now();
             orc_round r{};
             bool ok = round(&r);
             secs[i] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
             trace[i] = r;
             if (!ok) secs[i] = 0.0;
+            spent += secs[i];
+            *steps_done = i + 1;
+            if (!ok) break;
         }
         return 0;
     } catch (const std::exception&) {

@@ -16,6 +16,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -30,17 +31,79 @@ namespace {
 // threshold raised at context creation), so growing a pending bucket between
 // rounds is an async alloc + D2D copy + async free on the context stream, with
 // no host synchronisation and no cudaMalloc latency.
+// Pinned, device-mapped host memory for the host-resident pending tree.  Page
+// locking is slow (milliseconds per tens of MB), so buckets are carved out of a
+// few large pinned blocks by a first-fit free list instead of being allocated
+// one by one; a bucket's growth is then an arena allocation + a copy.  Every
+// user of the arena is ordered on the context stream, so a freed range can be
+// reused at once.
+class PinnedArena {
+   public:
+    ~PinnedArena() {
+        for (Block& b : blocks_) cudaFreeHost(b.base);
+    }
+    cudaError_t alloc(size_t bytes, void** out) {
+        bytes = (bytes + 255) & ~size_t(255);
+        for (Block& b : blocks_)
+            for (auto it = b.free.begin(); it != b.free.end(); ++it)
+                if (it->second >= bytes) {
+                    const size_t off = it->first, len = it->second;
+                    b.free.erase(it);
+                    if (len > bytes) b.free[off + bytes] = len - bytes;
+                    *out = b.base + off;
+                    return cudaSuccess;
+                }
+        size_t sz = std::max<size_t>(bytes, blocks_.empty() ? (size_t)256 << 20 : 2 * blocks_.back().size);
+        Block nb;
+        cudaError_t e = cudaHostAlloc((void**)&nb.base, sz, cudaHostAllocMapped | cudaHostAllocPortable);
+        if (e != cudaSuccess) return e;
+        nb.size = sz;
+        if (sz > bytes) nb.free[bytes] = sz - bytes;
+        blocks_.push_back(std::move(nb));
+        *out = blocks_.back().base;
+        return cudaSuccess;
+    }
+    void release(void* p, size_t bytes) {
+        bytes = (bytes + 255) & ~size_t(255);
+        for (Block& b : blocks_) {
+            if ((char*)p < b.base || (char*)p >= b.base + b.size) continue;
+            size_t off = (size_t)((char*)p - b.base);
+            auto nx = b.free.lower_bound(off);
+            if (nx != b.free.end() && off + bytes == nx->first) {  // merge with the next range
+                bytes += nx->second;
+                nx = b.free.erase(nx);
+            }
+            if (nx != b.free.begin()) {
+                auto pv = std::prev(nx);
+                if (pv->first + pv->second == off) {  // and with the previous one
+                    pv->second += bytes;
+                    return;
+                }
+            }
+            b.free[off] = bytes;
+            return;
+        }
+    }
+
+   private:
+    struct Block {
+        char* base = nullptr;
+        size_t size = 0;
+        std::map<size_t, size_t> free;  // offset -> length
+    };
+    std::vector<Block> blocks_;
+};
+
 struct DBuf {
     void* p = nullptr;
     size_t bytes = 0;
     cudaStream_t st = nullptr;
-    bool host = false;  // pinned, device-mapped host memory (host-resident pending tree)
+    PinnedArena* arena = nullptr;  // set: pinned host memory (host-resident pending tree)
     cudaError_t ensure(size_t want) {
         if (want <= bytes) return cudaSuccess;
         size_t nb = std::max(want, bytes * 2);
         void* q = nullptr;
-        cudaError_t e = host ? cudaHostAlloc(&q, nb, cudaHostAllocMapped | cudaHostAllocPortable)
-                             : cudaMallocAsync(&q, nb, st);
+        cudaError_t e = arena ? arena->alloc(nb, &q) : cudaMallocAsync(&q, nb, st);
         if (e != cudaSuccess) return e;
         release();
         p = q;
@@ -49,12 +112,8 @@ struct DBuf {
     }
     void release() {
         if (p) {
-            if (host) {
-                cudaStreamSynchronize(st);  // no device access may still be in flight
-                cudaFreeHost(p);
-            } else {
-                cudaFreeAsync(p, st);
-            }
+            if (arena) arena->release(p, bytes);
+            else cudaFreeAsync(p, st);
         }
         p = nullptr;
         bytes = 0;
@@ -90,10 +149,10 @@ struct HBuf {  // pinned host
 struct Store {
     DBuf masks, heads, prefix;
     int64_t cap = 0;
-    void set(cudaStream_t st, bool host) {
+    void set(cudaStream_t st, PinnedArena* arena) {
         for (DBuf* b : {&masks, &heads, &prefix}) {
             b->st = st;
-            b->host = host;
+            b->arena = arena;
         }
     }
     NodeStore view() const { return NodeStore{masks.as<uint64_t>(), heads.as<int32_t>(), prefix.as<uint8_t>()}; }
@@ -122,7 +181,7 @@ struct fbb_ctx {
     // shared per-round device state
     Store staging;          // per-chunk compacted survivors (chunk c at c * cmax)
     Store parents;          // host-resident explorer: this round's parents, uploaded
-    DBuf st_lb, st_count;
+    DBuf st_lb, st_count, st_seg, st_dst;
     DBuf d_pool, d_round;   // Pool, RoundState
     HBuf h_pool, h_round;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -140,6 +199,11 @@ struct fbb_ctx {
     int64_t tot_branched = 0, tot_bounded = 0, tot_pruned = 0, tot_leaves = 0;
     bool explorer_ready = false;
     bool host_pending = false;  // pending tree in pinned host memory (fbb_explorer_set_residency)
+    PinnedArena arena;          // its storage
+    bool mapped_in = true;      // K2 reads the parents in place from the mapped host buckets
+                                // over the host link; FBB_HOST_IN=copy: upload them first
+    bool mapped_out = true;     // place_kernel writes survivors straight into the (device-
+                                // mapped) host buckets; FBB_HOST_OUT=staged: device output + D2H
     int64_t last_h2d = 0, last_d2h = 0;
     bool check = false;  // FBB_CHECK=1: validate the pending tree after every round
 
@@ -167,9 +231,11 @@ size_t node_bytes(const fbb_ctx* ctx) {
 
 cudaError_t store_ensure(fbb_ctx* ctx, Store& s, int64_t want, int64_t keep) {
     if (want <= s.cap) return cudaSuccess;
-    int64_t nc = std::max<int64_t>(want, std::max<int64_t>(s.cap * 2, 1024));
+    // pinned host growth is slow (page locking): start host stores at ~4 MB
+    const int64_t floor_rows = s.masks.arena ? std::max<int64_t>(1024, (1 << 20) / (int64_t)node_bytes(ctx)) : 1024;
+    int64_t nc = std::max<int64_t>(want, std::max<int64_t>(s.cap * 2, floor_rows));
     const int n = ctx->dt.n, m = ctx->dt.m, W = ctx->dt.W;
-    const bool host = s.masks.host;
+    PinnedArena* host = s.masks.arena;
     Store t;
     t.set(ctx->stream, host);
     s.set(ctx->stream, host);
@@ -224,6 +290,8 @@ int run_pool(fbb_ctx* ctx, Pool& pool, int first_internal, int32_t ub, int froze
     CK(store_ensure(ctx, ctx->staging, slots, 0), "staging");
     CK(ctx->st_lb.ensure((size_t)slots * 4), "staging");
     CK(ctx->st_count.ensure((size_t)std::max<int64_t>(pool.nchunks, 1) * 4), "staging");
+    CK(ctx->st_seg.ensure((size_t)std::max<int64_t>(pool.nchunks, 1) * 4), "staging");
+    CK(ctx->st_dst.ensure((size_t)std::max<int64_t>(pool.nchunks, 1) * 8), "staging");
     CK(ctx->d_pool.ensure(sizeof(Pool)), "pool");
     CK(ctx->h_pool.ensure(sizeof(Pool)), "pool");
     CK(ctx->d_round.ensure(sizeof(RoundState)), "round state");
@@ -247,7 +315,8 @@ int run_pool(fbb_ctx* ctx, Pool& pool, int first_internal, int32_t ub, int froze
     }
     CK(cudaEventRecord(ctx->ev[1], st), "event");
     bool has_internal = first_internal < pool.nseg && pool.nchunks > 0;
-    ChunkOut out{ctx->staging.view(), ctx->st_lb.as<int32_t>(), ctx->st_count.as<int32_t>()};
+    ChunkOut out{ctx->staging.view(), ctx->st_lb.as<int32_t>(), ctx->st_count.as<int32_t>(),
+                 ctx->st_seg.as<int32_t>(), ctx->st_dst.as<int64_t>()};
     CK(launch_k2_internal(ctx->dt, ctx->k2, dp, pool, first_internal, ub, frozen, rs, out, st),
        "K2 internal");
     CK(cudaEventRecord(ctx->ev[2], st), "event");
@@ -379,14 +448,16 @@ int check_pending(fbb_ctx* ctx) {
 void explorer_clear(fbb_ctx* ctx) {
     const int n = ctx->dt.n;
     if ((int)ctx->bucket.size() != n + 1) ctx->bucket.resize(n + 1);
+    PinnedArena* want = ctx->host_pending ? &ctx->arena : nullptr;
     for (Store& b : ctx->bucket) {
-        if (b.masks.host != ctx->host_pending) {  // residency changed: drop the old storage
+        if (b.masks.arena != want) {  // residency changed: drop the old storage
+            cudaStreamSynchronize(ctx->stream);
             b.masks.release();
             b.heads.release();
             b.prefix.release();
             b.cap = 0;
         }
-        b.set(ctx->stream, ctx->host_pending);
+        b.set(ctx->stream, want);
     }
     ctx->cnt.assign(n + 1, 0);
     ctx->schedule.assign(n, 0);
@@ -423,7 +494,10 @@ int explorer_round(fbb_ctx* ctx, int64_t target, fbb_round_t* rec) {
     if (local.nseg == 0) return FBB_OK;
     int first_internal = layout_pool(ctx, local);
     // destinations (bucket depth+1) sized for the worst case before launching
-    for (int s = first_internal; s < local.nseg; ++s) {
+    // device buckets: sized for the worst case (all children survive) before K2 writes
+    // into them; host buckets grow after the round, to the actual survivor count
+    const bool staged_out = ctx->host_pending && !ctx->mapped_out;  // device output, then D2H
+    for (int s = first_internal; s < local.nseg && !staged_out; ++s) {
         Segment& sg = local.seg[s];
         int d1 = sg.depth + 1;
         int64_t worst = after[d1] + sg.count * (n - sg.depth);
@@ -431,7 +505,12 @@ int explorer_round(fbb_ctx* ctx, int64_t target, fbb_round_t* rec) {
         CK(store_ensure(ctx, ctx->bucket[d1], worst, ctx->cnt[d1]), "bucket grow");
     }
     int64_t h2d = 0, npar = 0;
-    if (ctx->host_pending) {
+    const bool upload = ctx->host_pending && !ctx->mapped_in;
+    if (ctx->host_pending && ctx->mapped_in) {  // parents read in place over the host link
+        for (int s = 0; s < local.nseg; ++s) npar += local.seg[s].count;
+        h2d = npar * (int64_t)node_bytes(ctx);
+    }
+    if (upload) {
         // host-resident pending tree: this round's parents (the top rows of each
         // selected bucket, contiguous) go host -> device; survivors are written by
         // place_kernel straight into the (device-mapped, pinned) host buckets
@@ -452,10 +531,14 @@ int explorer_round(fbb_ctx* ctx, int64_t target, fbb_round_t* rec) {
         }
         h2d = npar * (int64_t)node_bytes(ctx);
     }
+    if (staged_out) CK(store_ensure(ctx, ctx->batch_out, std::max<int64_t>(local.nchildren, 1), 0), "alloc");
     for (int s = 0; s < local.nseg; ++s) {  // views may have moved after growth
         Segment& sg = local.seg[s];
-        sg.src = ctx->host_pending ? ctx->parents.view() : ctx->bucket[sg.depth].view();
-        if (sg.depth < n - 2) {
+        sg.src = upload ? ctx->parents.view() : ctx->bucket[sg.depth].view();
+        if (sg.depth < n - 2 && staged_out) {  // contiguous device output, then D2H
+            sg.dst = ctx->batch_out.view();
+            sg.dst_base = -1;
+        } else if (sg.depth < n - 2) {
             sg.dst = ctx->bucket[sg.depth + 1].view();
             sg.dst_base = after[sg.depth + 1];
         } else {
@@ -467,7 +550,7 @@ int explorer_round(fbb_ctx* ctx, int64_t target, fbb_round_t* rec) {
     int rc = run_pool(ctx, local, first_internal, ctx->incumbent, ctx->frozen);
     if (rc != FBB_OK) return rc;
     const RoundState* sm = ctx->h_round.as<RoundState>();
-    int64_t internal = 0, leaves = 0;
+    int64_t internal = 0, leaves = 0, out_row = 0;
     for (int s = 0; s < local.nseg; ++s) {
         const Segment& sg = local.seg[s];
         int64_t kids = sg.count * (n - sg.depth);
@@ -476,9 +559,21 @@ int explorer_round(fbb_ctx* ctx, int64_t target, fbb_round_t* rec) {
             leaves += kids;
         } else {
             internal += kids;
-            after[sg.depth + 1] += sm->seg_surv[s];
+            const int64_t k = sm->seg_surv[s];
+            if (staged_out && k > 0) {  // survivors -> the host bucket, in batch order
+                const int m = ctx->dt.m, W = ctx->dt.W;
+                const int64_t at = after[sg.depth + 1];
+                CK(store_ensure(ctx, ctx->bucket[sg.depth + 1], at + k, at), "bucket grow");
+                const NodeStore b = ctx->bucket[sg.depth + 1].view(), o = ctx->batch_out.view();
+                CK(cudaMemcpyAsync(b.masks + at * W, o.masks + out_row * W, (size_t)k * W * 8, cudaMemcpyDefault, ctx->stream), "survivors D2H");
+                CK(cudaMemcpyAsync(b.heads + at * m, o.heads + out_row * m, (size_t)k * m * 4, cudaMemcpyDefault, ctx->stream), "survivors D2H");
+                CK(cudaMemcpyAsync(b.prefix + at * n, o.prefix + out_row * n, (size_t)k * n, cudaMemcpyDefault, ctx->stream), "survivors D2H");
+            }
+            out_row += k;
+            after[sg.depth + 1] += k;
         }
     }
+    if (staged_out && out_row > 0) CK(cudaStreamSynchronize(ctx->stream), "survivors D2H");
     ctx->cnt = after;
     rec->bounded = internal + leaves;
     rec->leaves = leaves;
@@ -583,10 +678,10 @@ fbb_ctx* fbb_create(int device, const int32_t* p, int n, int m) {
             }
         }
         for (DBuf* b : {&ctx->k1_masks, &ctx->k1_heads, &ctx->k1_depth, &ctx->k1_lb, &ctx->out_lb,
-                        &ctx->st_lb, &ctx->st_count, &ctx->d_pool, &ctx->d_round})
+                        &ctx->st_lb, &ctx->st_count, &ctx->st_seg, &ctx->st_dst, &ctx->d_pool, &ctx->d_round})
             b->st = ctx->stream;
         for (Store* st : {&ctx->batch_in, &ctx->batch_out, &ctx->staging, &ctx->parents})
-            st->set(ctx->stream, false);
+            st->set(ctx->stream, nullptr);
     }
     rc = upload_tables(ctx->ht, &ctx->dt, &why);
     if (rc != FBB_OK) {
@@ -623,7 +718,7 @@ void fbb_destroy(fbb_ctx* ctx) {
     cudaSetDevice(ctx->device);
     free_tables(&ctx->dt);
     for (DBuf* b : {&ctx->k1_masks, &ctx->k1_heads, &ctx->k1_depth, &ctx->k1_lb, &ctx->out_lb,
-                    &ctx->st_lb, &ctx->st_count, &ctx->d_pool, &ctx->d_round})
+                    &ctx->st_lb, &ctx->st_count, &ctx->st_seg, &ctx->st_dst, &ctx->d_pool, &ctx->d_round})
         b->release();
     for (Store* s : {&ctx->batch_in, &ctx->batch_out, &ctx->staging, &ctx->parents}) {
         s->masks.release();
@@ -830,6 +925,17 @@ int fbb_explorer_set_residency(fbb_ctx* ctx, int pending_on_host) {
     if (!ctx) return FBB_E_ARG;
     cudaSetDevice(ctx->device);
     ctx->host_pending = pending_on_host != 0;
+    if (ctx->host_pending) {
+        // reserve the pinned arena now (page locking costs ~0.1 s per GB), not mid-run
+        const char* mb = getenv("FBB_PINNED_MB");
+        size_t want = (size_t)(mb ? std::max(64L, atol(mb)) : 1024L) << 20;
+        void* p = nullptr;
+        if (ctx->arena.alloc(want, &p) == cudaSuccess) ctx->arena.release(p, want);
+        const char* o = getenv("FBB_HOST_OUT");
+        ctx->mapped_out = !(o && std::string(o) == "staged");
+        const char* i = getenv("FBB_HOST_IN");
+        ctx->mapped_in = !(i && std::string(i) == "copy");
+    }
     explorer_clear(ctx);
     return FBB_OK;
 }

@@ -69,7 +69,7 @@ __host__ __device__ inline K2Layout k2_layout(int n, int m, int P, int cmax, int
     L.cL = o;   o = a16(o + (size_t)cmax * L.mst * 4);
     L.pre = o;  o = a16(o + (size_t)L.ppc_max * n);
     L.wsum = o; o = a16(o + (size_t)(threads / 32 + 2) * 8);
-    L.total = o;
+    L.total = o > L.Mq + kFinishScratch ? o : L.Mq + kFinishScratch;  // k2_finish reuses Mq..
     return L;
 }
 
@@ -272,7 +272,10 @@ __global__ void __launch_bounds__(128) k2_internal_kernel(DevTables t, const Poo
             base_off += tot;
             __syncthreads();
         }
-        if (tid == 0) out.count[chunk] = base_off;
+        if (tid == 0) {
+            out.count[chunk] = base_off;
+            out.seg[chunk] = s;
+        }
         const int64_t out0 = chunk * (int64_t)cmax;
         const NodeStore dst = out.nodes;
         int run = 0;
@@ -316,6 +319,7 @@ __global__ void __launch_bounds__(128) k2_internal_kernel(DevTables t, const Poo
             __syncthreads();
         }
     }
+    k2_finish(pool, rs, out, (unsigned char*)s_Mq);
 }
 
 // Children of parents at depth >= n-2 are complete schedules: bound = makespan
@@ -391,14 +395,10 @@ __global__ void leaf_schedule_kernel(DevTables t, const Pool* __restrict__ pool,
     *found = 1;
 }
 
-// Places every chunk's survivors at their final, batch-ordered position: the
-// segment's dst at dst_base + (survivors of the segment's earlier chunks), or the
-// contiguous output at (survivors of all earlier chunks) when dst_base < 0; adds
-// the per-segment and pool totals to `rs`.  One CTA per kPlaceChunks consecutive
-// chunks computes its own exclusive offsets (a block reduction over the counts of
-// all earlier chunks -- a few thousand L2-resident ints), so there is no separate
-// scan launch; rows are then copied flat (one thread per 4-byte head, mask word or
-// prefix byte), which keeps many independent loads in flight per thread.
+// Moves every chunk's survivors from its staging slot to its destination row
+// (k2_finish) in its segment's dst.  One CTA per kPlaceChunks consecutive
+// chunks; rows are copied flat (one thread per 4-byte head, mask word or prefix
+// byte), each thread issuing kPlaceBatch independent loads before its stores.
 constexpr int kPlaceChunks = 8;
 constexpr int kPlaceThreads = 256;
 constexpr int kPlaceBatch = 8;
@@ -422,23 +422,11 @@ __device__ __forceinline__ void copy_rows(int rows, int width, Load load, Store 
     }
 }
 
-__device__ __forceinline__ int64_t block_sum(int64_t v, int64_t* s_red) {
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    __syncthreads();
-    if (lane == 0) s_red[warp] = v;
-    __syncthreads();
-    int64_t tot = 0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += s_red[w];
-    return tot;
-}
-
 __global__ void __launch_bounds__(kPlaceThreads) place_kernel(DevTables t, const Pool* __restrict__ pool,
-                                                              int cmax, RoundState* rs, ChunkOut out) {
+                                                              int cmax, ChunkOut out) {
     const int n = t.n, m = t.m, W = t.W;
-    __shared__ int64_t s_red[kPlaceThreads / 32];
     __shared__ int s_row0[kPlaceChunks + 1];  // CTA-local exclusive survivor offsets
-    __shared__ int64_t s_dst[kPlaceChunks];   // destination row of each chunk's first survivor
+    __shared__ int64_t s_dst[kPlaceChunks];
     __shared__ NodeStore s_store[kPlaceChunks];
     __shared__ int32_t* s_dlb[kPlaceChunks];
     extern __shared__ uint8_t s_rc[];          // chunk of each row (cmax * kPlaceChunks)
@@ -446,15 +434,6 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(DevTables t, const
     const int64_t nchunks = pool->nchunks;
     const int64_t c0 = (int64_t)blockIdx.x * kPlaceChunks;
     const int nch = (int)(nchunks - c0 < kPlaceChunks ? nchunks - c0 : kPlaceChunks);
-    const int s0 = find_segment_lb(pool, 0, c0);
-    const int64_t cb0 = pool->seg[s0].chunk_base;
-    int64_t a = 0, b = 0;  // survivors of chunks [0, cb0) and [cb0, c0)
-    for (int64_t i = tid; i < c0; i += blockDim.x) {
-        const int v = out.count[i];
-        if (i < cb0) a += v; else b += v;
-    }
-    const int64_t A = block_sum(a, s_red);
-    const int64_t B = block_sum(b, s_red);
     if (tid < 32) {
         const int v = tid < nch ? out.count[c0 + tid] : 0;
         int incl = v;
@@ -462,26 +441,17 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(DevTables t, const
             const int u = __shfl_up_sync(0xFFFFFFFFu, incl, o);
             if (tid >= o) incl += u;
         }
-        if (tid < nch) s_row0[tid] = incl - v;
+        if (tid < nch) {
+            s_row0[tid] = incl - v;
+            const Segment& sg = pool->seg[out.seg[c0 + tid]];
+            s_dst[tid] = out.dst_row[c0 + tid];
+            s_store[tid] = sg.dst;
+            s_dlb[tid] = sg.dst_lb;
+        }
         if (tid == nch - 1) s_row0[nch] = incl;
     }
     __syncthreads();
-    if (tid < nch) {
-        const int s = find_segment_lb(pool, s0, c0 + tid);
-        const Segment& sg = pool->seg[s];
-        const int64_t glob = A + B + s_row0[tid];
-        const int64_t seg0 = s == s0 ? A : A + B + s_row0[sg.chunk_base - c0];
-        s_dst[tid] = sg.dst_base < 0 ? glob : sg.dst_base + (glob - seg0);
-        s_store[tid] = sg.dst;
-        s_dlb[tid] = sg.dst_lb;
-        const int cnt = s_row0[tid + 1] - s_row0[tid];
-        if (cnt) atomicAdd((unsigned long long*)&rs->seg_surv[s], (unsigned long long)cnt);
-    }
-    __syncthreads();
     const int R = s_row0[nch];
-    if (tid == 0 && R) atomicAdd((unsigned long long*)&rs->total, (unsigned long long)R);
-    // row -> chunk table, then batched copies: every thread issues kPlaceBatch
-    // independent (read-only path) loads before its stores
     for (int c = 0; c < nch; ++c)
         for (int row = s_row0[c] + tid; row < s_row0[c + 1]; row += kPlaceThreads) s_rc[row] = (uint8_t)c;
     __syncthreads();
@@ -494,7 +464,7 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(DevTables t, const
     // whole prefix rows (bytes past depth + 1 are don't-care in both places)
     copy_rows<kPlaceBatch>(R, n, [&](int row, int k) { return __ldg(out.nodes.prefix + src_row(row) * n + k); },
                            [&](int row, int k, uint8_t v) { s_store[s_rc[row]].prefix[dst_row(row) * n + k] = v; });
-    if (s_dlb[0] || (nch > 1 && s_dlb[nch - 1]))
+    if (s_dlb[0])  // all segments of a pool share dst_lb (set or not)
         copy_rows<kPlaceBatch>(R, 1, [&](int row, int) { return __ldg(out.lb + src_row(row)); },
                                [&](int row, int, int32_t v) { s_dlb[s_rc[row]][dst_row(row)] = v; });
 }
@@ -568,7 +538,7 @@ cudaError_t launch_place(const DevTables& t, const K2Config& cfg, const Pool* d_
     if (h_pool.nchunks == 0) return cudaSuccess;
     const int64_t blocks = (h_pool.nchunks + kPlaceChunks - 1) / kPlaceChunks;
     place_kernel<<<(unsigned)blocks, kPlaceThreads, (size_t)cfg.cmax * kPlaceChunks, stream>>>(
-        t, d_pool, cfg.cmax, rs, out);
+        t, d_pool, cfg.cmax, out);
     return cudaGetLastError();
 }
 
