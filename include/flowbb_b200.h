@@ -167,6 +167,25 @@ int fbb_explorer_state(fbb_ctx* ctx, int32_t* incumbent, int32_t* found, int32_t
 int fbb_explorer_pending(fbb_ctx* ctx, uint8_t* prefix, int32_t* depth, int64_t cap,
                          int64_t* count);
 
+/* ---- multi-device exploration (one context per GPU) ---------------------
+ * Lower the pruning incumbent to `ub` when it improves it: the value of a leaf
+ * found on another device, delivered by the caller's min-allreduce (solve mode
+ * only; FBB_E_STATE when frozen). */
+int fbb_explorer_set_incumbent(fbb_ctx* ctx, int32_t ub);
+
+/* This context's own best leaf: returns 1 and its value (and, in solve mode,
+ * its schedule, n int32) when one was found, else 0 with *value = INT32_MAX. */
+int fbb_explorer_best(fbb_ctx* ctx, int32_t* value, int32_t* schedule);
+
+/* Pool rebalancing: remove up to k pending nodes from the tops of the
+ * shallowest non-empty buckets (the roots of the largest unexplored subtrees)
+ * and return them (prefix rows of n bytes, depths); *taken = how many. */
+int fbb_explorer_take(fbb_ctx* ctx, int64_t k, uint8_t* prefix, int32_t* depth, int64_t* taken);
+
+/* Push nodes (given as prefixes) onto the pending tree, in order, without
+ * resetting it (the receiving side of fbb_explorer_take). */
+int fbb_explorer_push(fbb_ctx* ctx, const uint8_t* prefix, const int32_t* depth, int64_t count);
+
 /* ---- adaptive pool-size tuner (autotune.hpp:35-156), re-derived descriptor ----------- */
 typedef struct fbb_tuner fbb_tuner;
 fbb_tuner* fbb_tuner_create(int32_t grain, int32_t base_units, int64_t max_batch, int window,

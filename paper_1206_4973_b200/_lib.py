@@ -20,7 +20,8 @@ EXPORTED = (
     "fbb_create", "fbb_destroy", "fbb_last_error", "fbb_descriptor", "fbb_bound",
     "fbb_bound_device", "fbb_expand_bound_prune", "fbb_explorer_reset",
     "fbb_explorer_start_solve", "fbb_explorer_run", "fbb_explorer_state",
-    "fbb_explorer_pending", "fbb_explorer_set_residency", "fbb_tuner_create", "fbb_tuner_destroy", "fbb_tuner_target",
+    "fbb_explorer_pending", "fbb_explorer_set_residency", "fbb_explorer_set_incumbent",
+    "fbb_explorer_best", "fbb_explorer_take", "fbb_explorer_push", "fbb_tuner_create", "fbb_tuner_destroy", "fbb_tuner_target",
     "fbb_tuner_observe", "fbb_tuner_phase", "fbb_tuner_best_batch",
     "fbb_tuner_best_throughput", "fbb_version",
 )
@@ -103,6 +104,10 @@ def load_library(path: str = LIB_PATH):
         C.POINTER(RoundRec)]
     L.fbb_explorer_reset.argtypes = [_vp, _u8p, _i32p, C.c_int64, C.c_int32, C.c_int]
     L.fbb_explorer_set_residency.argtypes = [_vp, C.c_int]
+    L.fbb_explorer_set_incumbent.argtypes = [_vp, C.c_int32]
+    L.fbb_explorer_best.argtypes = [_vp, C.POINTER(C.c_int32), _i32p]
+    L.fbb_explorer_take.argtypes = [_vp, C.c_int64, _u8p, _i32p, C.POINTER(C.c_int64)]
+    L.fbb_explorer_push.argtypes = [_vp, _u8p, _i32p, C.c_int64]
     L.fbb_explorer_start_solve.argtypes = [_vp, C.c_int32, C.POINTER(RoundRec)]
     L.fbb_explorer_run.argtypes = [_vp, _i64p, C.c_int, C.c_int64, C.c_int64, _vp,
                                    C.POINTER(C.c_int64)]

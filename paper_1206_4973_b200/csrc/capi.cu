@@ -181,7 +181,7 @@ struct fbb_ctx {
     // shared per-round device state
     Store staging;          // per-chunk compacted survivors (chunk c at c * cmax)
     Store parents;          // host-resident explorer: this round's parents, uploaded
-    DBuf st_lb, st_count, st_seg, st_dst;
+    DBuf st_lb, st_count, st_seg;
     DBuf d_pool, d_round;   // Pool, RoundState
     HBuf h_pool, h_round;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
@@ -291,7 +291,6 @@ int run_pool(fbb_ctx* ctx, Pool& pool, int first_internal, int32_t ub, int froze
     CK(ctx->st_lb.ensure((size_t)slots * 4), "staging");
     CK(ctx->st_count.ensure((size_t)std::max<int64_t>(pool.nchunks, 1) * 4), "staging");
     CK(ctx->st_seg.ensure((size_t)std::max<int64_t>(pool.nchunks, 1) * 4), "staging");
-    CK(ctx->st_dst.ensure((size_t)std::max<int64_t>(pool.nchunks, 1) * 8), "staging");
     CK(ctx->d_pool.ensure(sizeof(Pool)), "pool");
     CK(ctx->h_pool.ensure(sizeof(Pool)), "pool");
     CK(ctx->d_round.ensure(sizeof(RoundState)), "round state");
@@ -316,7 +315,7 @@ int run_pool(fbb_ctx* ctx, Pool& pool, int first_internal, int32_t ub, int froze
     CK(cudaEventRecord(ctx->ev[1], st), "event");
     bool has_internal = first_internal < pool.nseg && pool.nchunks > 0;
     ChunkOut out{ctx->staging.view(), ctx->st_lb.as<int32_t>(), ctx->st_count.as<int32_t>(),
-                 ctx->st_seg.as<int32_t>(), ctx->st_dst.as<int64_t>()};
+                 ctx->st_seg.as<int32_t>()};
     CK(launch_k2_internal(ctx->dt, ctx->k2, dp, pool, first_internal, ub, frozen, rs, out, st),
        "K2 internal");
     CK(cudaEventRecord(ctx->ev[2], st), "event");
@@ -678,7 +677,7 @@ fbb_ctx* fbb_create(int device, const int32_t* p, int n, int m) {
             }
         }
         for (DBuf* b : {&ctx->k1_masks, &ctx->k1_heads, &ctx->k1_depth, &ctx->k1_lb, &ctx->out_lb,
-                        &ctx->st_lb, &ctx->st_count, &ctx->st_seg, &ctx->st_dst, &ctx->d_pool, &ctx->d_round})
+                        &ctx->st_lb, &ctx->st_count, &ctx->st_seg, &ctx->d_pool, &ctx->d_round})
             b->st = ctx->stream;
         for (Store* st : {&ctx->batch_in, &ctx->batch_out, &ctx->staging, &ctx->parents})
             st->set(ctx->stream, nullptr);
@@ -718,7 +717,7 @@ void fbb_destroy(fbb_ctx* ctx) {
     cudaSetDevice(ctx->device);
     free_tables(&ctx->dt);
     for (DBuf* b : {&ctx->k1_masks, &ctx->k1_heads, &ctx->k1_depth, &ctx->k1_lb, &ctx->out_lb,
-                    &ctx->st_lb, &ctx->st_count, &ctx->st_seg, &ctx->st_dst, &ctx->d_pool, &ctx->d_round})
+                    &ctx->st_lb, &ctx->st_count, &ctx->st_seg, &ctx->d_pool, &ctx->d_round})
         b->release();
     for (Store* s : {&ctx->batch_in, &ctx->batch_out, &ctx->staging, &ctx->parents}) {
         s->masks.release();
@@ -934,7 +933,9 @@ int fbb_explorer_set_residency(fbb_ctx* ctx, int pending_on_host) {
         const char* o = getenv("FBB_HOST_OUT");
         ctx->mapped_out = !(o && std::string(o) == "staged");
         const char* i = getenv("FBB_HOST_IN");
-        ctx->mapped_in = !(i && std::string(i) == "copy");
+        // in-place reads need occupancy to hide the host-link latency: only the
+        // register-row K2 (3 CTAs/SM) reads mapped parents by default
+        ctx->mapped_in = i ? std::string(i) != "copy" : ctx->k2.variant != 0;
     }
     explorer_clear(ctx);
     return FBB_OK;
@@ -1036,6 +1037,53 @@ int fbb_explorer_state(fbb_ctx* ctx, int32_t* incumbent, int32_t* found, int32_t
         totals4[3] = ctx->tot_leaves;
     }
     return FBB_OK;
+}
+
+int fbb_explorer_set_incumbent(fbb_ctx* ctx, int32_t ub) {
+    if (!ctx) return FBB_E_ARG;
+    if (ctx->frozen) return ctx->fail(FBB_E_STATE, "the incumbent of a frozen exploration is fixed");
+    if (ub < ctx->incumbent) ctx->incumbent = ub;  // a better incumbent found elsewhere
+    return FBB_OK;
+}
+
+int fbb_explorer_best(fbb_ctx* ctx, int32_t* value, int32_t* schedule) {
+    if (!ctx) return FBB_E_ARG;
+    if (!ctx->found) {
+        if (value) *value = INT32_MAX;
+        return 0;
+    }
+    if (value) *value = ctx->best;
+    if (schedule && !ctx->frozen) std::memcpy(schedule, ctx->schedule.data(), ctx->schedule.size() * 4);
+    return 1;
+}
+
+int fbb_explorer_take(fbb_ctx* ctx, int64_t k, uint8_t* prefix, int32_t* depth, int64_t* taken) {
+    if (!ctx || !taken || k < 0 || (k > 0 && (!prefix || !depth))) return FBB_E_ARG;
+    cudaSetDevice(ctx->device);
+    const int n = ctx->dt.n;
+    int64_t t = 0;
+    for (int d = 0; d <= n && t < k; ++d) {
+        const int64_t j = std::min<int64_t>(ctx->cnt[d], k - t);
+        if (j == 0) continue;
+        const int64_t lo = ctx->cnt[d] - j;  // the bucket's top rows
+        CK(cudaMemcpyAsync(prefix + t * n, ctx->bucket[d].prefix.as<uint8_t>() + lo * n, (size_t)j * n,
+                           cudaMemcpyDefault, ctx->stream),
+           "take D2H");
+        for (int64_t i = 0; i < j; ++i) depth[t + i] = d;
+        ctx->cnt[d] = lo;
+        t += j;
+    }
+    CK(cudaStreamSynchronize(ctx->stream), "take");
+    *taken = t;
+    return FBB_OK;
+}
+
+int fbb_explorer_push(fbb_ctx* ctx, const uint8_t* prefix, const int32_t* depth, int64_t count) {
+    if (!ctx) return FBB_E_ARG;
+    if (count < 0 || (count > 0 && (!prefix || !depth))) return ctx->fail(FBB_E_ARG, "invalid nodes");
+    if (!ctx->explorer_ready) return ctx->fail(FBB_E_STATE, "explorer not reset");
+    cudaSetDevice(ctx->device);
+    return push_host_nodes(ctx, prefix, depth, count);
 }
 
 int fbb_explorer_pending(fbb_ctx* ctx, uint8_t* prefix, int32_t* depth, int64_t cap, int64_t* count) {

@@ -69,7 +69,7 @@ __host__ __device__ inline K2Layout k2_layout(int n, int m, int P, int cmax, int
     L.cL = o;   o = a16(o + (size_t)cmax * L.mst * 4);
     L.pre = o;  o = a16(o + (size_t)L.ppc_max * n);
     L.wsum = o; o = a16(o + (size_t)(threads / 32 + 2) * 8);
-    L.total = o > L.Mq + kFinishScratch ? o : L.Mq + kFinishScratch;  // k2_finish reuses Mq..
+    L.total = o;
     return L;
 }
 
@@ -319,7 +319,6 @@ __global__ void __launch_bounds__(128) k2_internal_kernel(DevTables t, const Poo
             __syncthreads();
         }
     }
-    k2_finish(pool, rs, out, (unsigned char*)s_Mq);
 }
 
 // Children of parents at depth >= n-2 are complete schedules: bound = makespan
@@ -395,10 +394,14 @@ __global__ void leaf_schedule_kernel(DevTables t, const Pool* __restrict__ pool,
     *found = 1;
 }
 
-// Moves every chunk's survivors from its staging slot to its destination row
-// (k2_finish) in its segment's dst.  One CTA per kPlaceChunks consecutive
-// chunks; rows are copied flat (one thread per 4-byte head, mask word or prefix
-// byte), each thread issuing kPlaceBatch independent loads before its stores.
+// Moves every chunk's survivors from its staging slot to its final, batch-ordered
+// row: the segment's dst at dst_base + (survivors of the segment's earlier
+// chunks), or the contiguous output at (survivors of all earlier chunks) when
+// dst_base < 0; adds the per-segment and pool totals to `rs`.  One CTA per
+// kPlaceChunks consecutive chunks derives its own offsets by summing the counts
+// of all earlier chunks (a few thousand L2-resident ints, kPlaceBatch
+// independent loads per thread), so no scan pass or grid-wide fence is needed.
+// Rows are copied flat (one thread per 4-byte head, mask word or prefix byte).
 constexpr int kPlaceChunks = 8;
 constexpr int kPlaceThreads = 256;
 constexpr int kPlaceBatch = 8;
@@ -423,17 +426,21 @@ __device__ __forceinline__ void copy_rows(int rows, int width, Load load, Store 
 }
 
 __global__ void __launch_bounds__(kPlaceThreads) place_kernel(DevTables t, const Pool* __restrict__ pool,
-                                                              int cmax, ChunkOut out) {
+                                                              int cmax, RoundState* rs, ChunkOut out) {
     const int n = t.n, m = t.m, W = t.W;
     __shared__ int s_row0[kPlaceChunks + 1];  // CTA-local exclusive survivor offsets
+    __shared__ int s_seg[kPlaceChunks];
     __shared__ int64_t s_dst[kPlaceChunks];
     __shared__ NodeStore s_store[kPlaceChunks];
     __shared__ int32_t* s_dlb[kPlaceChunks];
+    __shared__ int64_t s_red[2][kPlaceThreads / 32];
     extern __shared__ uint8_t s_rc[];          // chunk of each row (cmax * kPlaceChunks)
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t nchunks = pool->nchunks;
     const int64_t c0 = (int64_t)blockIdx.x * kPlaceChunks;
     const int nch = (int)(nchunks - c0 < kPlaceChunks ? nchunks - c0 : kPlaceChunks);
+    const int s0 = out.seg[c0];
+    const int64_t cb0 = pool->seg[s0].chunk_base;
     if (tid < 32) {
         const int v = tid < nch ? out.count[c0 + tid] : 0;
         int incl = v;
@@ -443,15 +450,53 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(DevTables t, const
         }
         if (tid < nch) {
             s_row0[tid] = incl - v;
-            const Segment& sg = pool->seg[out.seg[c0 + tid]];
-            s_dst[tid] = out.dst_row[c0 + tid];
-            s_store[tid] = sg.dst;
-            s_dlb[tid] = sg.dst_lb;
+            s_seg[tid] = out.seg[c0 + tid];
         }
         if (tid == nch - 1) s_row0[nch] = incl;
     }
+    // a = survivors of chunks [0, cb0), b = of [cb0, c0)
+    int64_t a = 0, b = 0;
+    for (int64_t base = tid; base < c0; base += (int64_t)kPlaceBatch * kPlaceThreads) {
+        int v[kPlaceBatch];
+#pragma unroll
+        for (int u = 0; u < kPlaceBatch; ++u) {
+            const int64_t i = base + (int64_t)u * kPlaceThreads;
+            v[u] = i < c0 ? out.count[i] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < kPlaceBatch; ++u) {
+            const int64_t i = base + (int64_t)u * kPlaceThreads;
+            if (i < cb0) a += v[u]; else b += v[u];
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        a += __shfl_xor_sync(0xFFFFFFFFu, a, o);
+        b += __shfl_xor_sync(0xFFFFFFFFu, b, o);
+    }
+    if (lane == 0) {
+        s_red[0][warp] = a;
+        s_red[1][warp] = b;
+    }
     __syncthreads();
+    if (tid < nch) {
+        int64_t A = 0, B = 0;
+        for (int w = 0; w < kPlaceThreads / 32; ++w) {
+            A += s_red[0][w];
+            B += s_red[1][w];
+        }
+        const int s = s_seg[tid];
+        const Segment& sg = pool->seg[s];
+        const int64_t glob = A + B + s_row0[tid];
+        const int64_t seg0 = s == s0 ? A : A + B + s_row0[sg.chunk_base - c0];
+        s_dst[tid] = sg.dst_base < 0 ? glob : sg.dst_base + (glob - seg0);
+        s_store[tid] = sg.dst;
+        s_dlb[tid] = sg.dst_lb;
+        const int cnt = s_row0[tid + 1] - s_row0[tid];
+        if (cnt) atomicAdd((unsigned long long*)&rs->seg_surv[s], (unsigned long long)cnt);
+    }
     const int R = s_row0[nch];
+    if (tid == 0 && R) atomicAdd((unsigned long long*)&rs->total, (unsigned long long)R);
     for (int c = 0; c < nch; ++c)
         for (int row = s_row0[c] + tid; row < s_row0[c + 1]; row += kPlaceThreads) s_rc[row] = (uint8_t)c;
     __syncthreads();
@@ -538,7 +583,7 @@ cudaError_t launch_place(const DevTables& t, const K2Config& cfg, const Pool* d_
     if (h_pool.nchunks == 0) return cudaSuccess;
     const int64_t blocks = (h_pool.nchunks + kPlaceChunks - 1) / kPlaceChunks;
     place_kernel<<<(unsigned)blocks, kPlaceThreads, (size_t)cfg.cmax * kPlaceChunks, stream>>>(
-        t, d_pool, cfg.cmax, out);
+        t, d_pool, cfg.cmax, rs, out);
     return cudaGetLastError();
 }
 

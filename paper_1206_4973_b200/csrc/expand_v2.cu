@@ -55,7 +55,7 @@ __host__ __device__ inline V2Layout v2_layout(int n, int m, int P, int cmax, int
     L.p = o;    o = b16(o + (size_t)n * m * 4);
     L.pre = o;  o = b16(o + (size_t)L.ppc_max * v2_rw(N));
     L.wsum = o; o = b16(o + (size_t)(threads / 32 + 2) * 8);
-    L.total = o > L.Mq + kFinishScratch ? o : L.Mq + kFinishScratch;  // k2_finish reuses Mq..
+    L.total = o;
     return L;
 }
 
@@ -385,7 +385,6 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
             out.lb[o] = mylb;
         }
     }
-    k2_finish(pool, rs, out, s_Mq);
 }
 
 template <int N, int M, int OCC>

@@ -123,7 +123,6 @@ struct ChunkOut {
     int32_t* lb;      // survivor bounds (same indexing)
     int32_t* count;   // survivors per chunk
     int32_t* seg;     // segment of each chunk
-    int64_t* dst_row; // destination row of each chunk's first survivor (k2_finish)
 };
 
 // Per-round device state; the head (everything before `schedule`) is zeroed by
@@ -132,8 +131,6 @@ struct RoundState {
     unsigned long long leaf_inv;  // ~((best leaf value << 32) | batch position); 0 = no leaf
     int32_t found;                // leaf schedule written (value < ub)
     uint32_t ticket;              // next chunk to claim
-    uint32_t done;                // K2 CTAs finished (the last one scans the counts)
-    uint32_t pad_;
     int64_t total;                // survivors of the pool
     int64_t seg_surv[kMaxSegments];
     int32_t schedule[kMaxJobs];
@@ -154,8 +151,8 @@ cudaError_t launch_k2_leaves(const DevTables& t, const Pool* d_pool, const Pool&
 cudaError_t launch_k2_internal(const DevTables& t, const K2Config& cfg, const Pool* d_pool,
                                const Pool& h_pool, int first_seg, int32_t ub, int frozen,
                                RoundState* rs, ChunkOut out, cudaStream_t stream);
-// Every chunk's survivors moved to its destination row (computed by K2's
-// k2_finish) in its segment's dst.
+// Every chunk's survivors moved, in batch order, to its segment's dst; per-segment
+// and pool survivor totals added to `rs` (zeroed before the round).
 cudaError_t launch_place(const DevTables& t, const K2Config& cfg, const Pool* d_pool,
                          const Pool& h_pool, RoundState* rs, ChunkOut out, cudaStream_t stream);
 // Schedule of the best leaf when it beats ub (before the parents are recycled).

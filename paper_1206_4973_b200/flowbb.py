@@ -296,6 +296,37 @@ class Context:
             return rounds, [recs[i].timing() for i in range(done.value)]
         return rounds
 
+    def explorer_set_incumbent(self, ub: int):
+        self._check(self.L.fbb_explorer_set_incumbent(self.h, int(ub)))
+
+    def explorer_best(self):
+        """(value, schedule) of this context's own best leaf, or (None, None)."""
+        v = C.c_int32(0)
+        sched = np.zeros(max(self.n, 1), np.int32)
+        found = self.L.fbb_explorer_best(self.h, C.byref(v), sched)
+        if found < 0:
+            self._check(found)
+        if not found:
+            return None, None
+        return v.value, [int(x) for x in sched[: self.n]]
+
+    def explorer_take(self, k: int):
+        """Removes up to k pending nodes (shallowest buckets first); returns their prefixes."""
+        k = max(0, int(k))
+        pre = np.zeros(max(k, 1) * self.n, np.uint8)
+        dep = np.zeros(max(k, 1), np.int32)
+        got = C.c_int64(0)
+        self._check(self.L.fbb_explorer_take(self.h, k, pre, dep, C.byref(got)))
+        pre = pre.reshape(-1, self.n)
+        return [list(map(int, pre[i, : dep[i]])) for i in range(got.value)]
+
+    def explorer_push(self, prefixes):
+        if not prefixes:
+            return
+        batch = nodes_from_prefixes(self.inst, prefixes)
+        self._check(self.L.fbb_explorer_push(self.h, np.ascontiguousarray(batch.prefix.ravel()),
+                                             np.ascontiguousarray(batch.depth), len(batch)))
+
     def explorer_state(self):
         inc = C.c_int32(0)
         found = C.c_int32(0)

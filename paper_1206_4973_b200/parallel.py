@@ -1,0 +1,229 @@
+"""Multi-GPU exploration: one process per GPU over torch.distributed.
+
+The paper splits each pool across the GPUs of one host and merges the results
+(PAPER.md:290-308); the reference models that as `split_slices` -> k concurrent
+backends -> `merge_slices` (backend.hpp:73-158).  On an NVSwitch box the cheaper
+equivalent is to split the *pending tree*: every rank owns a device-resident
+explorer over its own subtrees (frozen exploration is partition-invariant,
+bench.hpp:60-62: the explored node set does not depend on who explores which
+subtree), and per round the ranks exchange only
+
+  * the incumbent: min-allreduce of one int per rank (solve mode; a leaf found on
+    one GPU prunes on all of them from the next round on), and
+  * the pending sizes, from which every rank computes the same rebalancing plan:
+    a starving rank receives the shallowest pending nodes (the roots of the
+    largest unexplored subtrees) of the richest rank, as (depth, prefix) rows.
+
+Both ride on ONE all_gather of a [incumbent, pending, bounded] triple per rank per
+round (NCCL over NVLink on GPUs, gloo in the CPU tests); rebalancing adds a
+send/recv pair per transfer every `balance_every` rounds.  The explorer behind a
+rank is any object with the `ExplorerPort` methods -- the device explorer in
+production (`DevicePort`), a CPU model in the tests.
+"""
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+from typing import List, Optional, Protocol, Sequence
+
+import numpy as np
+
+INT32_MAX = 2**31 - 1
+
+
+class ExplorerPort(Protocol):
+    def round(self, target: int):  # -> round tuple (target, branched, bounded, ...) or None
+        ...
+
+    def pending(self) -> int:
+        ...
+
+    def take(self, k: int) -> List[List[int]]:
+        ...
+
+    def push(self, prefixes: Sequence[Sequence[int]]) -> None:
+        ...
+
+    def incumbent(self) -> int:  # current pruning bound
+        ...
+
+    def set_incumbent(self, v: int) -> None:
+        ...
+
+    def best(self):  # (value, schedule) of this rank's own best leaf, or (None, None)
+        ...
+
+
+class DevicePort:
+    """ExplorerPort over a device context (fbb_explorer_*)."""
+
+    def __init__(self, ctx, frozen: bool):
+        self.ctx, self.frozen = ctx, frozen
+        self.last_timing = None
+
+    def round(self, target: int):
+        r, t = self.ctx.explorer_run([target], 1, timing=True)
+        self.last_timing = t[0] if t else None
+        return r[0] if r else None
+
+    def pending(self) -> int:
+        return self.ctx.explorer_state()["pending"]
+
+    def take(self, k: int):
+        return self.ctx.explorer_take(k)
+
+    def push(self, prefixes):
+        self.ctx.explorer_push(prefixes)
+
+    def incumbent(self) -> int:
+        st = self.ctx.explorer_state()
+        return st["incumbent"] if not self.frozen else INT32_MAX
+
+    def set_incumbent(self, v: int) -> None:
+        if not self.frozen:
+            self.ctx.explorer_set_incumbent(v)
+
+    def best(self):
+        return self.ctx.explorer_best()
+
+
+def plan_transfers(pending: Sequence[int], low: int, cap: int):
+    """Deterministic rebalancing plan from the gathered pending sizes: every rank whose
+    pending is below `low` (ascending) receives from the richest rank that still has
+    more than 2*low and has not donated this step, half the difference (<= cap).
+    Returns [(donor, receiver, count)]; identical on every rank."""
+    est = list(pending)
+    donated = set()
+    plan = []
+    for rcv in sorted(range(len(est)), key=lambda r: (est[r], r)):
+        if est[rcv] >= low:
+            break
+        donors = [d for d in range(len(est)) if d not in donated and d != rcv and est[d] > 2 * low]
+        if not donors:
+            break
+        d = max(donors, key=lambda r: (est[r], -r))
+        k = min(cap, (est[d] - est[rcv]) // 2)
+        if k <= 0:
+            continue
+        plan.append((d, rcv, k))
+        est[d] -= k
+        est[rcv] += k
+        donated.add(d)
+    return plan
+
+
+@dataclass
+class ParallelResult:
+    rounds: list = field(default_factory=list)   # this rank's round tuples
+    bounded: int = 0                              # all ranks
+    transfers: int = 0                            # nodes moved between ranks
+    exchange_seconds: float = 0.0                 # this rank's time in collectives
+    best: Optional[int] = None                    # global best leaf (min over ranks)
+    best_rank: int = -1
+    schedule: Optional[list] = None
+    exhausted: bool = False
+
+
+class ParallelExplorer:
+    """Runs synchronous rounds on every rank with the per-round exchange above."""
+
+    def __init__(self, port: ExplorerPort, n_jobs: int, group=None, device=None,
+                 balance_every: int = 4, low_water: Optional[int] = None, max_transfer: int = 1 << 16):
+        import torch
+        import torch.distributed as dist
+
+        self.port, self.n, self.group = port, n_jobs, group
+        self.torch, self.dist = torch, dist
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.device = device if device is not None else "cpu"
+        self.balance_every = max(1, balance_every)
+        self.low_water = low_water
+        self.max_transfer = max_transfer
+        self.res = ParallelResult()
+        self._bounded_local = 0
+        self._round = 0
+
+    # -- collectives ---------------------------------------------------------------------------
+    def _gather(self, inc: int, pend: int, bounded: int):
+        t = self.torch
+        mine = t.tensor([inc, pend, bounded], dtype=t.int64, device=self.device)
+        out = [t.zeros(3, dtype=t.int64, device=self.device) for _ in range(self.world)]
+        self.dist.all_gather(out, mine, group=self.group)
+        rows = t.stack(out).cpu().numpy()
+        return rows[:, 0], rows[:, 1], rows[:, 2]
+
+    def _rebalance(self, pending, target):
+        low = self.low_water if self.low_water is not None else max(1, target // max(1, self.n))
+        plan = plan_transfers([int(x) for x in pending], low, self.max_transfer)
+        t = self.torch
+        for donor, rcv, k in plan:
+            if self.rank == donor:
+                nodes = self.port.take(k)
+                buf = np.full((k, self.n + 1), -1, np.int16)
+                for i, pr in enumerate(nodes):
+                    buf[i, 0] = len(pr)
+                    buf[i, 1:1 + len(pr)] = pr
+                self.dist.send(t.from_numpy(buf).to(self.device), rcv, group=self.group)
+            elif self.rank == rcv:
+                buf = t.zeros((k, self.n + 1), dtype=t.int16, device=self.device)
+                self.dist.recv(buf, donor, group=self.group)
+                rows = buf.cpu().numpy()
+                self.port.push([list(map(int, r[1:1 + r[0]])) for r in rows if r[0] >= 0])
+            self.res.transfers += k
+
+    # -- driver --------------------------------------------------------------------------------
+    def step(self, target: int) -> bool:
+        """One synchronous round on every rank; False once every rank's pending is empty."""
+        rec = self.port.round(target) if self.port.pending() > 0 else None
+        if rec is not None:
+            self.res.rounds.append(tuple(rec))
+            self._bounded_local += int(rec[2])
+        t0 = time.perf_counter()
+        inc, pend, bnd = self._gather(self.port.incumbent(), self.port.pending(), self._bounded_local)
+        g = int(inc.min())
+        if g < self.port.incumbent():
+            self.port.set_incumbent(g)
+        self.res.bounded = int(bnd.sum())
+        self._round += 1
+        if int(pend.sum()) == 0:
+            self.res.exchange_seconds += time.perf_counter() - t0
+            self.res.exhausted = True
+            return False
+        if self.world > 1 and self._round % self.balance_every == 0:
+            self._rebalance(pend, target)
+        self.res.exchange_seconds += time.perf_counter() - t0
+        return True
+
+    def run(self, targets, max_rounds: int = 1 << 40, budget: int = 0) -> ParallelResult:
+        targets = list(np.atleast_1d(targets))
+        r = 0
+        while r < max_rounds:
+            tgt = int(targets[min(r, len(targets) - 1)])
+            if not self.step(tgt):
+                break
+            r += 1
+            if budget and self.res.bounded >= budget:
+                break
+        return self.finish()
+
+    def finish(self) -> ParallelResult:
+        """Global best leaf: min over ranks of (value, rank); its schedule is broadcast."""
+        t = self.torch
+        v, sched = self.port.best()
+        mine = t.tensor([v if v is not None else INT32_MAX, self.rank], dtype=t.int64,
+                        device=self.device)
+        out = [t.zeros(2, dtype=t.int64, device=self.device) for _ in range(self.world)]
+        self.dist.all_gather(out, mine, group=self.group)
+        rows = sorted(tuple(int(x) for x in o.cpu().tolist()) for o in out)
+        best, who = rows[0]
+        self.res.best = None if best == INT32_MAX else best
+        self.res.best_rank = who if best != INT32_MAX else -1
+        if self.res.best is not None:
+            buf = t.full((self.n,), -1, dtype=t.int32, device=self.device)
+            if self.rank == who and sched is not None:
+                buf = t.tensor(sched, dtype=t.int32, device=self.device)
+            self.dist.broadcast(buf, who, group=self.group)
+            s = [int(x) for x in buf.cpu().tolist()]
+            self.res.schedule = s if s and s[0] >= 0 else None
+        return self.res

@@ -65,3 +65,84 @@ def test_frontier_partition_is_count_invariant(world, oracle):
     # and the frontier resolution + the root round equals the full resolve from the root
     assert single["bounded"] + len(kids) == full["bounded"]
     assert fbb.split_slices(len(frontier), world)[0][0] == 0
+
+
+# ---- the multi-GPU driver (paper_1206_4973_b200.parallel) over gloo ---------------------------
+
+def _parallel_worker(rank, world, port, p, ub, frozen, roots_by_rank, target, q):
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from model_port import OraclePort
+    from oracle import Oracle
+    from paper_1206_4973_b200.parallel import ParallelExplorer
+
+    ex = ParallelExplorer(OraclePort(Oracle(), p, ub, frozen, roots_by_rank[rank]), p.shape[0],
+                          balance_every=1)
+    res = ex.run([target])
+    q.put((rank, res.bounded, res.best, res.schedule, res.transfers, res.exhausted,
+           sum(r[2] for r in res.rounds)))
+    dist.destroy_process_group()
+
+
+def _run_parallel(world, p, ub, frozen, roots_by_rank, target=16):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29600 + (os.getpid() % 1000)
+    procs = [ctx.Process(target=_parallel_worker,
+                         args=(r, world, port, p, ub, frozen, roots_by_rank, target, q))
+             for r in range(world)]
+    for pr in procs:
+        pr.start()
+    out = sorted(q.get(timeout=300) for _ in range(world))
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    return out
+
+
+def test_plan_transfers_is_deterministic_and_conserving():
+    from paper_1206_4973_b200.parallel import plan_transfers
+
+    assert plan_transfers([100, 0], 10, 1000) == [(0, 1, 50)]
+    assert plan_transfers([5, 5, 5], 10, 1000) == []            # nobody rich enough
+    plan = plan_transfers([0, 400, 3, 90], 10, 64)
+    assert plan == [(1, 0, 64), (3, 2, 43)]                      # one donation per donor
+    assert plan_transfers([0, 400], 10, 64) == [(1, 0, 64)]     # capped
+
+
+@pytest.mark.parametrize("world", [2])
+def test_parallel_frozen_exploration_is_partition_invariant(world, oracle):
+    """Frozen UB, all work on rank 0 at the start: rebalancing feeds rank 1, and the total
+    bounded count over ranks equals the single-explorer resolve (bench.hpp:60-62)."""
+    rng = np.random.default_rng(11)
+    p = rng.integers(1, 30, size=(8, 4)).astype(np.int32)
+    opt, _, _ = oracle.solve(p, -1, targets=[64])
+    ub = opt["optimum"] + 8
+    single, _ = oracle.resolve(p, ub, [[]], targets=[16])
+    out = _run_parallel(world, p, ub, True, [[[]], []])
+    assert all(o[1] == single["bounded"] for o in out)          # gathered total, every rank
+    assert sum(o[6] for o in out) == single["bounded"]          # per-rank work adds up
+    assert all(o[5] for o in out)                               # exhausted everywhere
+    assert out[1][6] > 0 and out[0][4] > 0                      # rank 1 got work
+    best = single["optimum"] if single["found"] else None
+    assert all(o[2] == best for o in out)
+
+
+@pytest.mark.parametrize("world", [2])
+def test_parallel_solve_reaches_the_optimum_with_ub_exchange(world, oracle):
+    """Solve mode: each rank prunes with the min-allreduced incumbent; the global best
+    is the brute-force optimum and its schedule (from the finding rank) achieves it."""
+    rng = np.random.default_rng(5)
+    p = rng.integers(1, 30, size=(7, 3)).astype(np.int32)
+    opt, sched, _ = oracle.solve(p, -1, targets=[64])
+    ident = oracle.makespan(p, list(range(7)))
+    # the root's children split across the ranks
+    kids, _ = oracle.branch(p, [])
+    kids = [list(map(int, k)) for k in kids]
+    out = _run_parallel(world, p, ident + 1, False, [kids[0::2], kids[1::2]])
+    vals = {o[2] for o in out}
+    assert vals == {opt["optimum"]}
+    s = out[0][3]
+    assert s is not None and oracle.makespan(p, s) == opt["optimum"]
