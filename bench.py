@@ -12,8 +12,10 @@ expand + bound + prune + compact every child on the GPU (K2), push the survivors
 
 Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--target T] [--impl ours|reference]
 Multi-GPU (torchrun): each rank explores its own contiguous slice of the frontier
-(split_slices, backend.hpp:73-84); frozen UB means no data-path collective
-(scaling "weak"); the max over ranks of the device time is reported.
+(split_slices, backend.hpp:73-84) and every round ends with the rank exchange of
+paper_1206_4973_b200.parallel (incumbent + pending sizes all_gather, rebalancing
+transfers every 4 rounds); per-GPU pool fixed (scaling "weak"); the value is all
+ranks' bounded nodes over the max over ranks of (round device time + exchange).
 """
 from __future__ import annotations
 
@@ -219,12 +221,19 @@ def main():
     rank, world, local = dist_env()
     import torch
 
-    dev = local if world > 1 else 0
+    # FBB_SAME_GPU=1 + FBB_DIST_BACKEND=gloo: every rank on cuda:0, collectives over gloo
+    # (exercises the N > 1 path on a one-GPU box; never used for reported numbers)
+    dev = local if world > 1 and not os.environ.get("FBB_SAME_GPU") else 0
     torch.cuda.set_device(dev)
+    backend = os.environ.get("FBB_DIST_BACKEND", "nccl")
+    coll_dev = f"cuda:{dev}" if backend == "nccl" else "cpu"
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
     import paper_1206_4973_b200 as fbb
 
     n, m, seed, ub = INSTANCES[inst_name]
@@ -244,21 +253,47 @@ def main():
         if r[0][2] >= T:
             break
     frontier = ctx.explorer_pending()
-    if world > 1:  # each rank keeps its contiguous slice (split_slices, backend.hpp:73-84)
+    px = None
+    if world > 1:
+        # each rank keeps its contiguous slice (split_slices, backend.hpp:73-84); from here on
+        # every round ends with the rank exchange of parallel.ParallelExplorer (one all_gather
+        # of [incumbent, pending, bounded] + rebalancing transfers every 4 rounds, NCCL)
+        from paper_1206_4973_b200.parallel import DevicePort, ParallelExplorer
+
         off, ln = fbb.split_slices(len(frontier), world)[rank]
-        mine = frontier[off:off + ln]
-        ctx.explorer_reset(fbb.nodes_from_prefixes(inst, mine), ub, frozen=True)
-        frontier = mine
-        while True:  # regrow to full pools on this rank's subtree
-            r = ctx.explorer_run([T], 1)
-            if not r or r[0][2] >= T:
-                break
-        frontier = ctx.explorer_pending()
+        frontier = frontier[off:off + ln]
+        ctx.explorer_reset(fbb.nodes_from_prefixes(inst, frontier), ub, frozen=True)
     snapshot = fbb.nodes_from_prefixes(inst, frontier)
+
+    def make_px():
+        if world == 1:
+            return None
+        return ParallelExplorer(DevicePort(ctx, frozen=True), n, device=coll_dev,
+                                balance_every=4)
+
+    px = make_px()
+
+    def one_round(timed, px):
+        """One explorer round (+ the rank exchange when N > 1): (rounds, timings)."""
+        if px is None:
+            return ctx.explorer_run([T], 1, timing=timed) if timed else (ctx.explorer_run([T], 1), None)
+        before = len(px.res.rounds)
+        x0 = px.res.exchange_seconds
+        px.step(T)
+        r = px.res.rounds[before:]
+        t = [px.port.last_timing] if r else []
+        if t:
+            t[0] = dict(t[0])
+            t[0]["exchange_ms"] = 1e3 * (px.res.exchange_seconds - x0)
+        else:
+            t = [{"round_ms": 0.0, "k2_ms": 0.0, "launches": 0, "host_ms": 0.0, "sync_ms": 0.0,
+                  "h2d_bytes": 0, "d2h_bytes": 0,
+                  "exchange_ms": 1e3 * (px.res.exchange_seconds - x0)}]
+        return r, t
 
     # ---- device-resident explorer: W warm-up rounds, K timed rounds -------------------------
     for _ in range(args.warmup):
-        ctx.explorer_run([T], 1)
+        one_round(False, px)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{dev}")
     if world > 1:
         torch.distributed.barrier()
@@ -271,15 +306,19 @@ def main():
         torch.cuda.synchronize()
         w0 = time.perf_counter()  # wall clock of the round itself (the flush excluded)
         flush_s += w0 - f0
-        r, t = ctx.explorer_run([T], 1, timing=True)
+        r, t = one_round(True, px)
         wall += time.perf_counter() - w0
-        if not r:
+        if px is None and not r:
+            break
+        if px is not None and px.res.exhausted:
+            timing += t
             break
         rounds += r
         timing += t
     torch.cuda.synchronize()
     clocks = sampler.result() if sampler else None
-    dev_ms = sum(t["round_ms"] for t in timing)
+    # device time per rank: the rounds' CUDA-event time plus the rank exchange (N > 1)
+    dev_ms = sum(t["round_ms"] + t.get("exchange_ms", 0.0) for t in timing)
     k2_ms = sum(t["k2_ms"] for t in timing)
     bounded = sum(r[2] for r in rounds)
     branched = sum(r[1] for r in rounds)
@@ -287,7 +326,7 @@ def main():
     survivors = sum(r[3] for r in rounds)
     launches = sum(t["launches"] for t in timing)
     stats = torch.tensor([dev_ms, k2_ms, wall, bounded, branched, leaves, survivors, launches,
-                          len(rounds)], dtype=torch.float64, device=f"cuda:{dev}")
+                          len(rounds)], dtype=torch.float64, device=coll_dev)
     if world > 1:
         import torch.distributed as dist
 
@@ -306,23 +345,24 @@ def main():
     if not args.no_e2e:
         ctx.explorer_set_residency(True)
         ctx.explorer_reset(snapshot, ub, frozen=True)
+        pxe = make_px()
         for _ in range(args.warmup):
-            ctx.explorer_run([T], 1)
+            one_round(False, pxe)
         if world > 1:
             torch.distributed.barrier()
         e_rounds, e_tim, e_secs = [], [], 0.0
         for _ in range(args.steps):
             w0 = time.perf_counter()
-            r, t = ctx.explorer_run([T], 1, timing=True)
+            r, t = one_round(True, pxe)
             e_secs += time.perf_counter() - w0
-            if not r:
+            if (pxe is None and not r) or (pxe is not None and pxe.res.exhausted):
                 break
             e_rounds += r
             e_tim += t
         ctx.explorer_set_residency(False)
         stepsd = max(1, len(e_rounds))
         e_stats = torch.tensor([e_secs, sum(r[2] for r in e_rounds)], dtype=torch.float64,
-                               device=f"cuda:{dev}")
+                               device=coll_dev)
         if world > 1:
             mx = e_stats.clone()
             torch.distributed.all_reduce(mx, op=torch.distributed.ReduceOp.MAX)
@@ -384,7 +424,9 @@ def main():
                                f"full pool, then rounds at pool target {T}; step = one explorer "
                                f"round (select + K2 expand/bound/prune/compact + push)",
                    "instance": inst_name, "pool_target": T, "ub": ub,
-                   "parallelism": f"dp{world} (frontier slices)",
+                   "parallelism": (f"dp{world}: pending-tree slices per GPU, per-round "
+                                   "incumbent/pending all_gather + rebalancing (NCCL)")
+                                  if world > 1 else "dp1",
                    "l2": "flushed between timed rounds (256 MiB write)"},
         "wall_value": bounded_all / wall_max if wall_max > 0 else 0.0,
         "wall_breakdown_ms_per_step": {

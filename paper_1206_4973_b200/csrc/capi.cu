@@ -58,6 +58,7 @@ class PinnedArena {
         cudaError_t e = cudaHostAlloc((void**)&nb.base, sz, cudaHostAllocMapped | cudaHostAllocPortable);
         if (e != cudaSuccess) return e;
         nb.size = sz;
+        if (getenv("FBB_VERBOSE")) std::fprintf(stderr, "[fbb] pinned arena +%zu MiB\n", sz >> 20);
         if (sz > bytes) nb.free[bytes] = sz - bytes;
         blocks_.push_back(std::move(nb));
         *out = blocks_.back().base;
@@ -925,9 +926,14 @@ int fbb_explorer_set_residency(fbb_ctx* ctx, int pending_on_host) {
     cudaSetDevice(ctx->device);
     ctx->host_pending = pending_on_host != 0;
     if (ctx->host_pending) {
-        // reserve the pinned arena now (page locking costs ~0.1 s per GB), not mid-run
+        // reserve the pinned arena now (page locking costs ~0.25 s per GB), not mid-run:
+        // 1 GiB, or twice what the HBM-resident tree of this context has grown to
+        size_t dev_bytes = 0;
+        for (const Store& b : ctx->bucket)
+            if (!b.masks.arena) dev_bytes += (size_t)b.cap * node_bytes(ctx);
         const char* mb = getenv("FBB_PINNED_MB");
-        size_t want = (size_t)(mb ? std::max(64L, atol(mb)) : 1024L) << 20;
+        size_t want = mb ? (size_t)std::max(64L, atol(mb)) << 20
+                         : std::max<size_t>((size_t)1 << 30, 2 * dev_bytes);
         void* p = nullptr;
         if (ctx->arena.alloc(want, &p) == cudaSuccess) ctx->arena.release(p, want);
         const char* o = getenv("FBB_HOST_OUT");

@@ -502,13 +502,28 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(DevTables t, const
     __syncthreads();
     auto src_row = [&](int row) { const int c = s_rc[row]; return (c0 + c) * (int64_t)cmax + (row - s_row0[c]); };
     auto dst_row = [&](int row) { const int c = s_rc[row]; return s_dst[c] + (row - s_row0[c]); };
-    copy_rows<kPlaceBatch>(R, m, [&](int row, int k) { return __ldg(out.nodes.heads + src_row(row) * m + k); },
-                           [&](int row, int k, int32_t v) { s_store[s_rc[row]].heads[dst_row(row) * m + k] = v; });
-    copy_rows<kPlaceBatch>(R, W, [&](int row, int k) { return __ldg(out.nodes.masks + src_row(row) * W + k); },
-                           [&](int row, int k, uint64_t v) { s_store[s_rc[row]].masks[dst_row(row) * W + k] = v; });
+    // Each array moves row by row in the widest unit that divides its row size (rows of
+    // one array start at multiples of the row size in both places): 16-byte units for
+    // 20-machine heads, 4-byte units for 20/100/200-job prefixes.  Wide units matter
+    // most when the destination is pinned host memory written over the host link.
+    auto copy_array = [&](const void* src_base, int row_bytes, auto dst_of) {
+        auto go = [&](auto unit) {
+            using T = decltype(unit);
+            const int w = row_bytes / (int)sizeof(T);
+            const T* src = (const T*)src_base;
+            copy_rows<kPlaceBatch>(R, w, [&](int row, int k) { return __ldg(src + src_row(row) * w + k); },
+                                   [&](int row, int k, T v) { ((T*)dst_of(row))[dst_row(row) * w + k] = v; });
+        };
+        if (row_bytes % 16 == 0) go(uint4{});
+        else if (row_bytes % 8 == 0) go(uint2{});
+        else if (row_bytes % 4 == 0) go(0u);
+        else if (row_bytes % 2 == 0) go((unsigned short)0);
+        else go((unsigned char)0);
+    };
+    copy_array(out.nodes.heads, m * 4, [&](int row) { return (void*)s_store[s_rc[row]].heads; });
+    copy_array(out.nodes.masks, W * 8, [&](int row) { return (void*)s_store[s_rc[row]].masks; });
     // whole prefix rows (bytes past depth + 1 are don't-care in both places)
-    copy_rows<kPlaceBatch>(R, n, [&](int row, int k) { return __ldg(out.nodes.prefix + src_row(row) * n + k); },
-                           [&](int row, int k, uint8_t v) { s_store[s_rc[row]].prefix[dst_row(row) * n + k] = v; });
+    copy_array(out.nodes.prefix, n, [&](int row) { return (void*)s_store[s_rc[row]].prefix; });
     if (s_dlb[0])  // all segments of a pool share dst_lb (set or not)
         copy_rows<kPlaceBatch>(R, 1, [&](int row, int) { return __ldg(out.lb + src_row(row)); },
                                [&](int row, int, int32_t v) { s_dlb[s_rc[row]][dst_row(row)] = v; });
