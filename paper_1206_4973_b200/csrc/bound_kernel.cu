@@ -22,11 +22,11 @@ struct K1Layout {
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
-__host__ __device__ inline K1Layout k1_layout(int n, int m, int P, int tile) {
+__host__ __device__ inline K1Layout k1_layout(int n, int m, int P, int tile, bool jm_in_smem) {
     int W32 = (n + 31) / 32;
     K1Layout L;
     size_t o = 0;
-    L.jm = o;  o = align16(o + (size_t)n * P * 4);
+    L.jm = o;  o = align16(o + (jm_in_smem ? (size_t)n * P * 4 : 0));
     L.pk = o;  o = align16(o + (size_t)P * 4);
     L.p = o;   o = align16(o + (size_t)n * m * 4);
     L.tl = o;  o = align16(o + (size_t)n * m * 4);
@@ -39,7 +39,9 @@ __host__ __device__ inline K1Layout k1_layout(int n, int m, int P, int tile) {
     return L;
 }
 
-template <bool kOneWord>
+// kJmSmem: the Johnson table is staged in shared memory; when it does not fit next
+// to the tile (n*P*4 > ~half the opt-in maximum, e.g. 256x20) it is read through L1.
+template <bool kOneWord, bool kJmSmem>
 __global__ void __launch_bounds__(256) k1_bound_kernel(DevTables t, int tile,
                                                       const uint64_t* __restrict__ masks,
                                                       const int32_t* __restrict__ heads,
@@ -48,8 +50,8 @@ __global__ void __launch_bounds__(256) k1_bound_kernel(DevTables t, int tile,
     extern __shared__ __align__(16) unsigned char smem[];
     const int n = t.n, m = t.m, P = t.P, W = t.W;
     const int W32 = (n + 31) / 32;
-    const K1Layout L = k1_layout(n, m, P, tile);
-    uint32_t* s_jm = (uint32_t*)(smem + L.jm);
+    const K1Layout L = k1_layout(n, m, P, tile, kJmSmem);
+    const uint32_t* s_jm = kJmSmem ? (const uint32_t*)(smem + L.jm) : t.jm;
     int32_t* s_pk = (int32_t*)(smem + L.pk);
     int32_t* s_p = (int32_t*)(smem + L.p);
     int32_t* s_tl = (int32_t*)(smem + L.tl);
@@ -61,7 +63,8 @@ __global__ void __launch_bounds__(256) k1_bound_kernel(DevTables t, int tile,
     const int tid = threadIdx.x, bd = blockDim.x;
 
     // stage the instance constants once per CTA
-    for (int x = tid; x < n * P; x += bd) s_jm[x] = t.jm[x];
+    if (kJmSmem)
+        for (int x = tid; x < n * P; x += bd) ((uint32_t*)(smem + L.jm))[x] = t.jm[x];
     for (int x = tid; x < P; x += bd) s_pk[x] = (int32_t)t.pair_k[x] | ((int32_t)t.pair_l[x] << 16);
     for (int x = tid; x < n * m; x += bd) {
         s_p[x] = t.p[x];
@@ -151,13 +154,16 @@ K1Config k1_config(const DevTables& t, int device) {
     int P = t.P;
     c.tile = P > 0 ? (c.threads * 16 + P - 1) / P : 1024;
     c.tile = c.tile < 32 ? 32 : (c.tile > 1024 ? 1024 : c.tile);
-    c.smem = k1_layout(t.n, t.m, t.P, c.tile).total;
-    int sms = 148, per_sm = 1;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    auto kern = (t.n <= 32) ? k1_bound_kernel<true> : k1_bound_kernel<false>;
-    // the attribute is per kernel, not per context: allow the device maximum once
     int optin = 0;
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    c.smem = k1_layout(t.n, t.m, t.P, c.tile, true).total;
+    c.jm_in_smem = c.smem <= (size_t)optin;
+    if (!c.jm_in_smem) c.smem = k1_layout(t.n, t.m, t.P, c.tile, false).total;
+    int sms = 148, per_sm = 1;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    auto kern = t.n <= 32 ? (c.jm_in_smem ? k1_bound_kernel<true, true> : k1_bound_kernel<true, false>)
+                          : (c.jm_in_smem ? k1_bound_kernel<false, true> : k1_bound_kernel<false, false>);
+    // the attribute is per kernel, not per context: allow the device maximum once
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, c.threads, c.smem);
     if (per_sm < 1) per_sm = 1;
@@ -171,12 +177,15 @@ cudaError_t launch_k1(const DevTables& t, const K1Config& cfg, const uint64_t* m
     if (count <= 0) return cudaSuccess;
     int64_t ntiles = (count + cfg.tile - 1) / cfg.tile;
     int blocks = (int)(ntiles < cfg.blocks ? ntiles : cfg.blocks);
-    if (t.n <= 32)
-        k1_bound_kernel<true><<<blocks, cfg.threads, cfg.smem, stream>>>(t, cfg.tile, masks, heads,
-                                                                         depth, count, lb);
-    else
-        k1_bound_kernel<false><<<blocks, cfg.threads, cfg.smem, stream>>>(t, cfg.tile, masks, heads,
-                                                                          depth, count, lb);
+#define K1_LAUNCH(ONE, SM)                                                                      \
+    k1_bound_kernel<ONE, SM><<<blocks, cfg.threads, cfg.smem, stream>>>(t, cfg.tile, masks, heads, \
+                                                                       depth, count, lb)
+    if (t.n <= 32) {
+        if (cfg.jm_in_smem) K1_LAUNCH(true, true); else K1_LAUNCH(true, false);
+    } else {
+        if (cfg.jm_in_smem) K1_LAUNCH(false, true); else K1_LAUNCH(false, false);
+    }
+#undef K1_LAUNCH
     return cudaGetLastError();
 }
 

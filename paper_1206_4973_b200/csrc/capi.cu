@@ -273,7 +273,7 @@ int layout_pool(const fbb_ctx* ctx, Pool& pool) {
         sg.chunk_base = chunk;
         if (sg.depth >= n - 2) continue;  // leaves: no chunks
         if (first_internal == pool.nseg) first_internal = s;
-        int ppc = cmax / r;
+        int ppc = parents_per_chunk(n, sg.depth, cmax, ctx->k2.ppc_cap);
         chunk += (sg.count + ppc - 1) / ppc;
     }
     pool.nchunks = chunk;
@@ -698,7 +698,11 @@ fbb_ctx* fbb_create(int device, const int32_t* p, int n, int m) {
         K2Config kc;
         const char* sel = getenv("FBB_K2");
         bool generic = sel && std::string(sel) == "generic";
-        if (max_tail < 0x7FFF && !generic && k2_v2_config(ctx->dt, device, &kc)) ctx->k2 = kc;
+        // (both register-row kernels pack d as int8 and tails as 16 bits)
+        if (max_tail < 0x7FFF && ctx->ht.max_abs_d <= 127 && !generic) {
+            if (k2_v2_config(ctx->dt, device, &kc)) ctx->k2 = kc;
+            else if (k2_v3_config(ctx->dt, device, &kc)) ctx->k2 = kc;
+        }
     }
     int max_smem = 0;
     cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);

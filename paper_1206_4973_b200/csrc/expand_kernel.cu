@@ -572,6 +572,8 @@ cudaError_t launch_k2_internal(const DevTables& t, const K2Config& cfg, const Po
     int64_t nch = h_pool.nchunks - h_pool.seg[first_seg].chunk_base;
     if (nch <= 0) return cudaSuccess;
     int blocks = (int)(nch < cfg.blocks ? nch : cfg.blocks);
+    if (cfg.variant >= 100000)
+        return launch_k2_v3(t, cfg, d_pool, first_seg, blocks, ub, frozen, rs, out, stream);
     if (cfg.variant != 0)
         return launch_k2_v2(t, cfg, d_pool, first_seg, blocks, ub, frozen, rs, out, stream);
     if (cfg.jm_in_smem)

@@ -1,0 +1,399 @@
+// expand_v3.cu -- K2 for 64 < n <= 256 jobs and m in {5, 10, 20} (Taillard 100xm and
+// 200xm: configs 4-5).  Same contract and output as k2_internal_kernel
+// (expand_kernel.cu) and k2_v2_kernel (expand_v2.cu); a mapping that does not keep
+// per-position state in registers, so it scales to n = 256:
+//
+//  * the repacked Johnson rows (DevTables::rowpk, [i][q]) are read from global memory
+//    through L1 -- 76 KB at 100x20, 152 KB at 200x20, too large for shared memory next
+//    to the per-child output rows -- lanes of a warp reading consecutive pairs of one
+//    position (coalesced 128-byte rows);
+//  * thread (g, q) owns machine pair q of parent lane g.  Per (parent, pair) the forward
+//    pass writes every member's exclusive prefix max to its child's Mq slot, the
+//    backward pass folds in the suffix max, max(slot, sufmax - d), by a read-modify-write
+//    of the slot (SURVEY finding 3; bound.hpp:27-44 in max-plus form);
+//  * per (parent, machine) the load and the two smallest tails (lb_one_machine,
+//    bound.hpp:61-74) by warp reductions over the unscheduled jobs;
+//  * Phase B (one child per thread: child_heads, the one-machine term, max over the
+//    pairs with 128-bit Mq row loads) and the stable per-chunk compaction as in v2.
+#include <climits>
+#include <cstdlib>
+
+#include "k2_common.cuh"
+
+namespace fbb {
+
+namespace {
+
+constexpr int32_t kNeg3 = -(1 << 20);
+constexpr int kV3Ppc = 16;  // parents per chunk at most (per-parent tables are N bytes)
+
+__host__ __device__ inline size_t c16(size_t x) { return (x + 15) & ~size_t(15); }
+
+__host__ __device__ inline int v3_row_bytes(int P) {
+    int b = (P * 2 + 15) / 16;  // 16-byte units
+    if ((b & 1) == 0) b += 1;   // odd -> consecutive rows hit distinct bank groups
+    return b * 16;
+}
+
+struct V3Layout {
+    size_t u, rank, ujob, R, load, mins, amin, Mq, pre, wsum, total;
+    int rowb;
+};
+
+__host__ __device__ inline V3Layout v3_layout(int m, int P, int cmax, int threads, int NW) {
+    V3Layout L;
+    const int N = 32 * NW;
+    L.rowb = v3_row_bytes(P);
+    size_t o = 0;
+    L.u = o;    o = c16(o + (size_t)kV3Ppc * NW * 4);
+    L.rank = o; o = c16(o + (size_t)kV3Ppc * N);
+    L.ujob = o; o = c16(o + (size_t)kV3Ppc * N);
+    L.R = o;    o = c16(o + (size_t)kV3Ppc * m * 4);
+    L.load = o; o = c16(o + (size_t)kV3Ppc * m * 4);
+    L.mins = o; o = c16(o + (size_t)kV3Ppc * m * 4);  // min1 | min2 << 16
+    L.amin = o; o = c16(o + (size_t)kV3Ppc * m);
+    L.Mq = o;   o = c16(o + (size_t)cmax * L.rowb);
+    L.pre = o;  o = c16(o + (size_t)kV3Ppc * N);
+    L.wsum = o; o = c16(o + (size_t)(threads / 32 + 2) * 8);
+    L.total = o;
+    return L;
+}
+
+__device__ __forceinline__ uint32_t v3_lds_u32(uint32_t addr) {
+    uint32_t v;
+    asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ uint32_t v3_lds_u8(uint32_t addr) {
+    uint32_t v;
+    asm("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ int32_t v3_lds_s16(uint32_t addr) {
+    int16_t v;
+    asm volatile("ld.shared.s16 %0, [%1];" : "=h"(v) : "r"(addr));
+    return (int32_t)v;
+}
+__device__ __forceinline__ void v3_sts_u16(uint32_t addr, int32_t v) {
+    asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"((unsigned short)v));
+}
+
+template <int M>
+struct PairTab3 {  // (k, l) of pair index q in bound.hpp:97-98 order
+    int k[M * (M - 1) / 2], l[M * (M - 1) / 2];
+    constexpr PairTab3() : k(), l() {
+        int q = 0;
+        for (int a = 0; a < M; ++a)
+            for (int b = a + 1; b < M; ++b) {
+                k[q] = a;
+                l[q] = b;
+                ++q;
+            }
+    }
+};
+
+// (min1, argmin, min2) of a set of tails, merged across lanes; ties keep the
+// smallest job index as the argmin, as the ascending scan of v2 does.
+struct Mins {
+    int32_t m1, a1, m2;
+};
+__device__ __forceinline__ Mins mins_merge(Mins x, Mins y) {
+    const bool xf = x.m1 < y.m1 || (x.m1 == y.m1 && x.a1 < y.a1);
+    Mins r;
+    r.m1 = xf ? x.m1 : y.m1;
+    r.a1 = xf ? x.a1 : y.a1;
+    r.m2 = xf ? min(x.m2, y.m1) : min(y.m2, x.m1);
+    return r;
+}
+
+template <int NW, int M>
+__global__ void __launch_bounds__(NW <= 4 ? 192 : 256, NW <= 4 ? 3 : 2)
+    k2_v3_kernel(DevTables t, const Pool* __restrict__ pool, int first_seg, int cmax, int32_t ub,
+                 int frozen, RoundState* rs, ChunkOut out) {
+    constexpr int P = M * (M - 1) / 2;
+    constexpr int N = 32 * NW;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int n = t.n, W = t.W;
+    const V3Layout L = v3_layout(M, P, cmax, blockDim.x, NW);
+    uint32_t* s_u = (uint32_t*)(smem + L.u);  // unscheduled jobs, NW words per parent
+    uint8_t* s_rank = (uint8_t*)(smem + L.rank);
+    uint8_t* s_ujob = (uint8_t*)(smem + L.ujob);
+    int32_t* s_R = (int32_t*)(smem + L.R);
+    int32_t* s_load = (int32_t*)(smem + L.load);
+    uint32_t* s_mins = (uint32_t*)(smem + L.mins);
+    uint8_t* s_amin = (uint8_t*)(smem + L.amin);
+    unsigned char* s_Mq = smem + L.Mq;
+    uint8_t* s_pre = (uint8_t*)(smem + L.pre);
+    int64_t* s_slot = (int64_t*)(smem + L.wsum);
+    int32_t* s_wsum = (int32_t*)(smem + L.wsum + 16);
+    const int tid = threadIdx.x, bd = blockDim.x, lane = tid & 31, warp = tid >> 5;
+    const int nwarps = bd >> 5;
+    const int G = bd / P;
+    const int q = tid % P, g = tid / P;
+    const uint32_t* __restrict__ rows = t.rowpk;
+
+    int32_t ub_eff = ub;
+    if (!frozen) {
+        unsigned long long inv = rs->leaf_inv;
+        int32_t v = (int32_t)((~inv) >> 32);
+        if (inv != 0ull && v < ub_eff) ub_eff = v;
+    }
+
+    const int64_t c_begin = pool->seg[first_seg].chunk_base;
+    const int64_t c_end = pool->nchunks;
+    for (int64_t chunk = claim_chunk(rs, c_begin, s_slot); chunk < c_end;
+         chunk = claim_chunk(rs, c_begin, s_slot)) {
+        const int s = find_segment_lb(pool, first_seg, chunk);
+        const Segment& sg = pool->seg[s];
+        const int depth = sg.depth;
+        const int r = n - depth;
+        const int ppc = min(cmax / r, kV3Ppc);
+        const int64_t p0 = (chunk - sg.chunk_base) * ppc;
+        const int np = (int)(sg.count - p0 < ppc ? sg.count - p0 : ppc);
+        const int nc = np * r;
+        const NodeStore src = sg.src;
+        const int64_t first = sg.first, step = sg.step;
+        // ---- stage the parents
+        for (int x = tid; x < np * depth; x += bd) {
+            const int pp = x / depth, i = x - pp * depth;
+            s_pre[pp * N + i] = src.prefix[(first + step * (p0 + pp)) * n + i];
+        }
+        for (int x = tid; x < np * NW; x += bd) {
+            const int pp = x / NW, w = x - pp * NW;
+            const int64_t node = first + step * (p0 + pp);
+            const int w64 = w >> 1;
+            const uint64_t word = w64 < W ? src.masks[node * W + w64] : ~0ull;
+            const uint32_t half = (w & 1) ? (uint32_t)(word >> 32) : (uint32_t)word;
+            const int valid = min(32, max(0, n - 32 * w));
+            const uint32_t vmask = valid >= 32 ? 0xFFFFFFFFu : ((1u << valid) - 1u);
+            s_u[x] = ~half & vmask;
+        }
+        for (int x = tid; x < np * M; x += bd) {
+            const int pp = x / M, k = x - pp * M;
+            s_R[x] = src.heads[(first + step * (p0 + pp)) * M + k];
+        }
+        __syncthreads();
+        // rank of each unscheduled job at its entry code (j & ~31) | (31 - (j & 31)), and
+        // the ascending list of unscheduled jobs
+        for (int x = tid; x < np * N; x += bd) {
+            const int pp = x / N, code = x - pp * N;
+            const int j = (code & ~31) | (31 - (code & 31));
+            const uint32_t* u = s_u + pp * NW;
+            if (j < n && ((u[j >> 5] >> (j & 31)) & 1u)) {
+                int rk = __popc(u[j >> 5] & ((1u << (j & 31)) - 1u));
+                for (int w = 0; w < (j >> 5); ++w) rk += __popc(u[w]);
+                s_rank[x] = (uint8_t)rk;
+                s_ujob[pp * N + rk] = (uint8_t)j;
+            }
+        }
+        // per (parent, machine): load and the two smallest tails, a warp per item
+        for (int x = warp; x < np * M; x += nwarps) {
+            const int pp = x / M, k = x - pp * M;
+            const uint32_t* u = s_u + pp * NW;
+            int32_t load = 0;
+            Mins mn{0x7FFF, 0, 0x7FFF};
+#pragma unroll
+            for (int w = 0; w < NW; ++w) {
+                const int j = 32 * w + lane;
+                if ((u[w] >> lane) & 1u) {
+                    load += __ldg(t.p + j * M + k);
+                    const int32_t tv = __ldg(t.tails + j * M + k);
+                    mn = mins_merge(mn, Mins{tv, j, 0x7FFF});
+                }
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                load += __shfl_xor_sync(0xFFFFFFFFu, load, o);
+                Mins other{__shfl_xor_sync(0xFFFFFFFFu, mn.m1, o), __shfl_xor_sync(0xFFFFFFFFu, mn.a1, o),
+                           __shfl_xor_sync(0xFFFFFFFFu, mn.m2, o)};
+                mn = mins_merge(mn, other);
+            }
+            if (lane == 0) {
+                s_load[x] = load;
+                s_mins[x] = (uint32_t)mn.m1 | ((uint32_t)mn.m2 << 16);
+                s_amin[x] = (uint8_t)mn.a1;
+            }
+        }
+        __syncthreads();
+        // ---- Phase A: per (parent, pair) forward / backward max-plus scans into Mq
+        if (g < G) {
+            const uint32_t* rowq = rows + q;
+            for (int pp = g; pp < np; pp += G) {
+                const uint32_t u_sa = (uint32_t)__cvta_generic_to_shared(s_u + pp * NW);
+                const uint32_t rank_sa = (uint32_t)__cvta_generic_to_shared(s_rank + pp * N);
+                const uint32_t out_sa =
+                    (uint32_t)__cvta_generic_to_shared(s_Mq + (size_t)(pp * r) * L.rowb + 2 * q);
+                const uint32_t rowb = (uint32_t)L.rowb;
+                int32_t D = 0, PM = kNeg3;
+#pragma unroll 8
+                for (int i = 0; i < n; ++i) {
+                    const uint32_t e = __ldg(rowq + i * P);
+                    const uint32_t w = NW == 1 ? v3_lds_u32(u_sa) : v3_lds_u32(u_sa + ((e >> 3) & 0x1Cu));
+                    if ((int32_t)(w << (e & 31u)) < 0) {  // job of position i unscheduled
+                        const uint32_t rk = v3_lds_u8(rank_sa + (e & 0xFFu));
+                        v3_sts_u16(out_sa + rk * rowb, max(PM, -32768));  // exclusive prefix max
+                        PM = max(PM, D + (int32_t)((e >> 8) & 0xFFFFu));
+                        D += (int32_t)e >> 24;
+                    }
+                }
+                int32_t SM = kNeg3;
+#pragma unroll 8
+                for (int i = n - 1; i >= 0; --i) {
+                    const uint32_t e = __ldg(rowq + i * P);
+                    const uint32_t w = NW == 1 ? v3_lds_u32(u_sa) : v3_lds_u32(u_sa + ((e >> 3) & 0x1Cu));
+                    if ((int32_t)(w << (e & 31u)) < 0) {
+                        const uint32_t rk = v3_lds_u8(rank_sa + (e & 0xFFu));
+                        const int32_t d = (int32_t)e >> 24;
+                        const int32_t Db = D - d;  // D before position i
+                        const uint32_t slot = out_sa + rk * rowb;
+                        v3_sts_u16(slot, max(v3_lds_s16(slot), SM - d));
+                        SM = max(SM, Db + (int32_t)((e >> 8) & 0xFFFFu));
+                        D = Db;
+                    }
+                }
+            }
+        }
+        __syncthreads();
+        // ---- Phase B: per child bound with register-resident heads
+        int32_t myR[M];
+        int32_t mylb = 0;
+        int myx = 0, mypp = 0;
+        const bool b_lane = tid < nc;  // cmax <= blockDim
+        if (b_lane) {
+            const int pp = tid / r, rk = tid - pp * r;
+            const int x = s_ujob[pp * N + rk];
+            myx = x;
+            mypp = pp;
+            int32_t Lc[M];
+            int32_t prev = 0, lb = 0;
+#pragma unroll
+            for (int k = 0; k < M; ++k) {
+                const int pk = pp * M + k;
+                const int32_t px = __ldg(t.p + x * M + k);
+                prev = max(prev, s_R[pk]) + px;  // child_heads, instance.hpp:81-89
+                myR[k] = prev;
+                const uint32_t mins = s_mins[pk];
+                const int32_t mt = (x == (int)s_amin[pk]) ? (int32_t)(mins >> 16) : (int32_t)(mins & 0xFFFFu);
+                Lc[k] = s_load[pk] - px + mt;
+                lb = max(lb, prev + Lc[k]);  // one-machine term (bound.hpp:61-74)
+            }
+            const uint4* mrow = (const uint4*)(s_Mq + (size_t)tid * L.rowb);
+            constexpr PairTab3<M> tab{};
+#pragma unroll
+            for (int q8 = 0; q8 < (P + 7) / 8; ++q8) {
+                const uint4 cur = mrow[q8];
+                const uint32_t wv[4] = {cur.x, cur.y, cur.z, cur.w};
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int qq = q8 * 8 + u;
+                    if (qq < P) {
+                        const uint32_t w = wv[u >> 1];
+                        const int32_t mq = (u & 1) ? ((int32_t)w >> 16) : (int32_t)(int16_t)(w & 0xFFFFu);
+                        lb = max(lb, Lc[tab.l[qq]] + max(myR[tab.l[qq]], myR[tab.k[qq]] + mq));
+                    }
+                }
+            }
+            mylb = lb;
+        }
+        // ---- prune + stable compaction into the chunk's staging slot
+        const bool keep = b_lane && mylb < ub_eff;
+        const unsigned ballot = __ballot_sync(0xFFFFFFFFu, keep);
+        if (lane == 0) s_wsum[warp] = __popc(ballot);
+        __syncthreads();
+        int woff = 0, tot = 0;
+        for (int w = 0; w < nwarps; ++w) {
+            const int v = s_wsum[w];
+            if (w < warp) woff += v;
+            tot += v;
+        }
+        if (tid == 0) {
+            out.count[chunk] = tot;
+            out.seg[chunk] = s;
+        }
+        if (keep) {
+            const int64_t o = chunk * (int64_t)cmax + woff + __popc(ballot & ((1u << lane) - 1u));
+            const NodeStore dst = out.nodes;
+#pragma unroll
+            for (int k = 0; k < M; ++k) dst.heads[o * M + k] = myR[k];
+            const uint32_t* u = s_u + mypp * NW;
+            for (int w = 0; w < W; ++w) {
+                const uint32_t lo = 2 * w < NW ? u[2 * w] : 0u;
+                const uint32_t hi = 2 * w + 1 < NW ? u[2 * w + 1] : 0u;
+                const int vlo = min(32, max(0, n - 64 * w));
+                const int vhi = min(32, max(0, n - 64 * w - 32));
+                const uint32_t mlo = vlo >= 32 ? 0xFFFFFFFFu : ((1u << vlo) - 1u);
+                const uint32_t mhi = vhi >= 32 ? 0xFFFFFFFFu : ((1u << vhi) - 1u);
+                uint64_t sched = ((uint64_t)(~hi & mhi) << 32) | (uint64_t)(~lo & mlo);
+                if ((myx >> 6) == w) sched |= 1ull << (myx & 63);
+                dst.masks[o * W + w] = sched;
+            }
+            uint8_t* dp = dst.prefix + o * n;
+            for (int i = 0; i < depth; ++i) dp[i] = s_pre[mypp * N + i];
+            dp[depth] = (uint8_t)myx;
+            out.lb[o] = mylb;
+        }
+    }
+}
+
+template <int NW, int M>
+cudaError_t v3_setup(K2Config& c, int device) {
+    int optin = 0, sms = 148, per_sm = 1;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    cudaError_t e = cudaFuncSetAttribute(k2_v3_kernel<NW, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+    if (e != cudaSuccess) return e;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_v3_kernel<NW, M>, c.threads, c.smem);
+    c.blocks = sms * (per_sm < 1 ? 1 : per_sm);
+    return cudaSuccess;
+}
+
+}  // namespace
+
+bool k2_v3_config(const DevTables& t, int device, K2Config* out) {
+    const int m = t.m, n = t.n;
+    if (n <= 64 || n > 256 || !(m == 5 || m == 10 || m == 20) || !t.rowpk) return false;
+    K2Config c;
+    const int NW = n <= 128 ? 4 : 8;
+    c.cmax = ((n + 31) / 32) * 32;          // one parent's children always fit a chunk
+    c.threads = NW <= 4 ? 192 : 256;        // >= cmax (Phase B: a child per thread), >= P
+    c.ppc_cap = kV3Ppc;
+    c.variant = 100000 + NW * 100 + m;
+    c.jm_in_smem = false;
+    c.smem = v3_layout(m, t.P, c.cmax, c.threads, NW).total;
+    cudaError_t e;
+    switch (c.variant) {
+        case 100405: e = v3_setup<4, 5>(c, device); break;
+        case 100410: e = v3_setup<4, 10>(c, device); break;
+        case 100420: e = v3_setup<4, 20>(c, device); break;
+        case 100805: e = v3_setup<8, 5>(c, device); break;
+        case 100810: e = v3_setup<8, 10>(c, device); break;
+        case 100820: e = v3_setup<8, 20>(c, device); break;
+        default: return false;
+    }
+    if (e != cudaSuccess) return false;
+    *out = c;
+    return true;
+}
+
+cudaError_t launch_k2_v3(const DevTables& t, const K2Config& cfg, const Pool* d_pool, int first_seg,
+                         int blocks, int32_t ub, int frozen, RoundState* rs, ChunkOut out,
+                         cudaStream_t stream) {
+#define V3_CASE(NW, MM)                                                                      \
+    case 100000 + NW * 100 + MM:                                                             \
+        k2_v3_kernel<NW, MM><<<blocks, cfg.threads, cfg.smem, stream>>>(t, d_pool, first_seg, \
+                                                                       cfg.cmax, ub, frozen, rs, out); \
+        break;
+    switch (cfg.variant) {
+        V3_CASE(4, 5)
+        V3_CASE(4, 10)
+        V3_CASE(4, 20)
+        V3_CASE(8, 5)
+        V3_CASE(8, 10)
+        V3_CASE(8, 20)
+        default: return cudaErrorInvalidValue;
+    }
+#undef V3_CASE
+    return cudaGetLastError();
+}
+
+}  // namespace fbb

@@ -41,11 +41,19 @@ struct DevTables {
     uint32_t* jm;     // n*P, position-major: jm[i*P + q]
     int16_t* pair_k;  // P
     int16_t* pair_l;  // P
+    // The same Johnson rows repacked for the register-row kernels (n*P, [i][q]):
+    //   bits 0..4  31 - (j & 31)   (a left funnel shift by it moves j's U bit to bit 31)
+    //   bits 5..7  j >> 5          (which 32-bit word of U)
+    //   bits 8..23 c,  bits 24..31 d as int8
+    // so bits 0..7 are also the index of j in the per-parent rank tables.  Null when
+    // some |d| > 127 (then only the generic kernel runs).
+    uint32_t* rowpk;
 };
 
 // Host copy of the same tables (for tests of the table builder).
 struct HostTables {
     int n = 0, m = 0, P = 0, W = 0;
+    int max_abs_d = 0;  // max |p[j][k] - p[j][l]| over pairs
     std::vector<int32_t> p, tails;
     std::vector<uint32_t> jm;
     std::vector<int16_t> pair_k, pair_l;
@@ -64,6 +72,7 @@ void free_tables(DevTables* d);
 struct K1Config {
     int threads = 256;
     int tile = 32;       // nodes per tile
+    bool jm_in_smem = true;
     int blocks = 0;      // persistent grid
     size_t smem = 0;
 };
@@ -110,7 +119,9 @@ struct K2Config {
     int threads = 128;
     int cmax = 128;      // children per chunk (>= n)
     bool jm_in_smem = true;
-    int variant = 0;     // 0: generic kernel; N*100+M: k2_v2_kernel<N,M> (expand_v2.cu)
+    int variant = 0;     // 0: generic kernel; OCC*10000+N*100+M: k2_v2_kernel (expand_v2.cu);
+                         // 100000+NW*100+M: k2_v3_kernel (expand_v3.cu)
+    int ppc_cap = 0;     // > 0: at most this many parents per chunk
     int blocks = 0;
     size_t smem = 0;
 };
@@ -143,6 +154,12 @@ cudaError_t launch_k2_v2(const DevTables& t, const K2Config& cfg, const Pool* d_
                          int blocks, int32_t ub, int frozen, RoundState* rs, ChunkOut out,
                          cudaStream_t stream);
 
+// 64 < n <= 256, m in {5,10,20}: rows through L1, RMW scans; false when not applicable.
+bool k2_v3_config(const DevTables& t, int device, K2Config* out);
+cudaError_t launch_k2_v3(const DevTables& t, const K2Config& cfg, const Pool* d_pool, int first_seg,
+                         int blocks, int32_t ub, int frozen, RoundState* rs, ChunkOut out,
+                         cudaStream_t stream);
+
 // Leaves (parents at depth >= n-2): batch minimum (value, first position).
 cudaError_t launch_k2_leaves(const DevTables& t, const Pool* d_pool, const Pool& h_pool,
                              int seg_index, RoundState* rs, cudaStream_t stream);
@@ -159,10 +176,11 @@ cudaError_t launch_place(const DevTables& t, const K2Config& cfg, const Pool* d_
 cudaError_t launch_leaf_schedule(const DevTables& t, const Pool* d_pool, RoundState* rs,
                                  int32_t ub, cudaStream_t stream);
 
-// Chunk geometry of a segment: parents per chunk and chunk count.
-inline int parents_per_chunk(int n, int depth, int cmax) {
+// Chunk geometry of a segment: parents per chunk.
+inline int parents_per_chunk(int n, int depth, int cmax, int ppc_cap) {
     int r = n - depth;
-    return r > 0 ? cmax / r : 1;
+    int ppc = r > 0 ? cmax / r : 1;
+    return ppc_cap > 0 && ppc > ppc_cap ? ppc_cap : ppc;
 }
 
 }  // namespace fbb

@@ -81,6 +81,7 @@ int build_host_tables(const int32_t* p, int n, int m, HostTables* out, std::stri
                 return FBB_E_RANGE;
             }
             h.jm[(size_t)i * P + q] = pack_entry(j, d, c);
+            h.max_abs_d = std::max(h.max_abs_d, d < 0 ? -d : d);
         }
     }
     // every head / bound fits int32 comfortably; check the worst makespan
@@ -115,6 +116,19 @@ int upload_tables(const HostTables& h, DevTables* d, std::string* why) {
         *why = std::string("table upload: ") + cudaGetErrorString(e);
         return FBB_E_CUDA;
     }
+    if (h.max_abs_d <= 127) {
+        std::vector<uint32_t> rp(h.jm.size());
+        for (size_t x = 0; x < h.jm.size(); ++x) {
+            const uint32_t e = h.jm[x];
+            const uint32_t j = (uint32_t)entry_job(e);
+            rp[x] = (31u - (j & 31u)) | ((j >> 5) << 5) | ((uint32_t)entry_c(e) << 8) |
+                    ((uint32_t)(entry_d(e) & 0xFF) << 24);
+        }
+        if ((e = upload(&d->rowpk, rp)) != cudaSuccess) {
+            *why = std::string("table upload: ") + cudaGetErrorString(e);
+            return FBB_E_CUDA;
+        }
+    }
     return FBB_OK;
 }
 
@@ -124,6 +138,7 @@ void free_tables(DevTables* d) {
     cudaFree(d->jm);
     cudaFree(d->pair_k);
     cudaFree(d->pair_l);
+    cudaFree(d->rowpk);
     *d = DevTables{};
 }
 

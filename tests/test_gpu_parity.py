@@ -177,8 +177,11 @@ def test_k2_rejects_non_pop_order():
 
 def test_k2_random_parents_vs_oracle(oracle):
     rng = np.random.default_rng(99)
+    # covers the generic kernel (m not in {5,10,20}), v2 (n <= 64) and v3 (64 < n <= 256)
     for (n, m, cnt) in [(20, 20, 300), (20, 5, 800), (50, 20, 40), (40, 6, 200), (100, 5, 30),
-                        (5, 3, 50), (3, 2, 4), (2, 3, 3), (1, 2, 1), (128, 3, 10), (129, 2, 10)]:
+                        (5, 3, 50), (3, 2, 4), (2, 3, 3), (1, 2, 1), (128, 3, 10), (129, 2, 10),
+                        (65, 10, 30), (100, 20, 24), (128, 20, 8), (129, 10, 10), (200, 20, 8),
+                        (200, 10, 10), (256, 5, 6), (256, 20, 3)]:
         p = rng.integers(1, 100, size=(n, m)).astype(np.int32)
         inst = inst_of(p)
         parents = sorted([list(rng.permutation(n)[: rng.integers(0, n)]) for _ in range(cnt)],
