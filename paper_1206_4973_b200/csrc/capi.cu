@@ -669,7 +669,9 @@ fbb_ctx* fbb_create(int device, const int32_t* p, int n, int m) {
                 reserved[device] = true;
                 size_t free_b = 0, total_b = 0;
                 cudaMemGetInfo(&free_b, &total_b);
-                size_t want = std::min<size_t>((size_t)4 << 30, free_b / 16);
+                // deep trees at large n keep one worst-case bucket per depth (200x20:
+                // ~80 MB each), so map a generous working set: min(24 GiB, free / 4)
+                size_t want = std::min<size_t>((size_t)24 << 30, free_b / 4);
                 void* tmp = nullptr;
                 if (cudaMallocAsync(&tmp, want, ctx->stream) == cudaSuccess) {
                     cudaFreeAsync(tmp, ctx->stream);

@@ -40,7 +40,7 @@ struct fbb_tuner {
         }
     }
 
-    int64_t scale(int64_t base, int step) const {  // autotune.hpp:563-569
+    int64_t scale(int64_t base, int step) const {  // autotune.hpp:134-140
         double factor = std::pow(2.0, (double)step / (2.0 * probes_per_side));
         int64_t raw = (int64_t)std::floor((double)base * factor);
         raw = std::clamp<int64_t>(raw, grain, max_batch);
@@ -48,7 +48,7 @@ struct fbb_tuner {
         return std::max<int64_t>(raw, grain);
     }
 
-    void build_probes() {  // autotune.hpp:552-561
+    void build_probes() {  // autotune.hpp:123-132
         std::vector<int64_t> cand;
         for (int i = probes_per_side; i >= 1; --i) cand.push_back(scale(best_batch, -i));
         for (int i = 1; i <= probes_per_side; ++i) cand.push_back(scale(best_batch, i));
@@ -57,7 +57,7 @@ struct fbb_tuner {
                 probes.push_back(c);
     }
 
-    void advance() {  // autotune.hpp:518-547
+    void advance() {  // autotune.hpp:89-121
         if (phase == 0) {
             if (grain * units * 2 <= max_batch) {
                 units *= 2;
@@ -72,7 +72,7 @@ struct fbb_tuner {
         }
     }
 
-    void observe(int64_t nodes, double seconds) {  // autotune.hpp:498-515
+    void observe(int64_t nodes, double seconds) {  // autotune.hpp:69-86
         if (phase == 2) return;
         window_nodes += nodes;
         window_time += seconds;
@@ -94,7 +94,7 @@ extern "C" {
 
 fbb_tuner* fbb_tuner_create(int32_t grain, int32_t base_units, int64_t max_batch, int window,
                             int probes_per_side) {
-    // autotune.hpp:470-478 argument checks
+    // autotune.hpp:41-49 argument checks
     if (window < 1 || probes_per_side < 0 || grain < 1 || base_units < 1 ||
         max_batch < (int64_t)grain * base_units)
         return nullptr;

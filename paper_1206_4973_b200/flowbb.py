@@ -465,7 +465,7 @@ class TunerPhase(enum.IntEnum):
 
 
 class Tuner:
-    """autotune.hpp:458-585 through fbb_tuner_* (host C++ state machine)."""
+    """autotune.hpp:35-156 through fbb_tuner_* (host C++ state machine)."""
 
     def __init__(self, descriptor: BackendDescriptor, window: int, probes_per_side: int = 2):
         self.L = load_library()

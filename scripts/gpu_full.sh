@@ -7,10 +7,15 @@ timeout 1200 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.txt 2>&1; 
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.txt 2>&1; tail -1 gpurun_out/smoke.txt
 timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -2 gpurun_out/bench.err
 timeout 900 python bench.py --impl reference > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; tail -2 gpurun_out/bench_ref.err
-for I in ${INSTANCES:-ta001 ta051 ta081}; do timeout 600 python bench.py --instance $I --no-cpu-baseline > gpurun_out/bench_$I.json 2> gpurun_out/bench_$I.err; tail -1 gpurun_out/bench_$I.err; done
+for I in ${INSTANCES:-ta001 ta051 ta081 ta101}; do timeout 600 python bench.py --instance $I --no-cpu-baseline > gpurun_out/bench_$I.json 2> gpurun_out/bench_$I.err; tail -1 gpurun_out/bench_$I.err; done
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
    --log-file gpurun_out/launches.csv python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k2_|place" -s 12 -c 2 \
    -o gpurun_out/prof_k2_final -f python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_final.log 2>&1
 tail -1 gpurun_out/ncu_final.log
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k2_v3" -s 8 -c 1 \
+   -o gpurun_out/prof_k2v3_ta081 -f python bench.py --instance ta081 --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_v3.log 2>&1
+tail -1 gpurun_out/ncu_v3.log
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+   --log-file gpurun_out/launches_ta081.csv python bench.py --instance ta081 --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 python scripts/show.py gpurun_out/bench*.json
