@@ -47,6 +47,11 @@ def parse():
     ap.add_argument("--instance", default="ta021")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--mode", default="explore", choices=["explore", "bound"],
+                    help="explore: explorer rounds (configs 1-4); bound: K1 bound-only passes "
+                         "over a synthetic pool in HBM (config 5, bounding stress)")
+    ap.add_argument("--pool", type=int, default=8_000_000,
+                    help="--mode bound: nodes in the synthetic pool")
     ap.add_argument("--tuner", action="store_true",
                     help="adaptive pool size (autotune.hpp) instead of a fixed --target")
     ap.add_argument("--tuner-window", type=int, default=4)
@@ -150,6 +155,27 @@ def reference_arm(args, inst_name):
     from oracle import REF_SO, Oracle, Ref
 
     n, m, seed, ub = INSTANCES[inst_name]
+    if args.mode == "bound":  # the reference evaluate_batch over random_node pools
+        ref = Ref()
+        cores = ref.detect_units()
+        p = ref.generate_instance(n, m, seed)
+        k, secs, _ = ref_evaluate_timed(ref, p, lambda k: ref.random_nodes(p, 0x5EED, k), cores,
+                                        target_s=min(60.0, args.ref_seconds))
+        value = k / secs
+        print(json.dumps({
+            "metric": METRIC, "value": value, "unit": "bounded subproblems/s", "n_gpus": world,
+            "steps": 1, "warmup": 1, "ms_per_step": 1e3 * secs, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic (Taillard generator; reference random_node pool)",
+            "config": {"workload": f"{inst_name} {n}x{m} bounding stress: reference "
+                                   f"BackendSet::evaluate over a random_node pool",
+                       "instance": inst_name, "parallelism": "host threads"},
+            "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": "bounded subproblems/s", "cores": cores,
+                             "kind": "reference", "sample": f"{k} random_node nodes, {secs:.1f} s"},
+            "e2e": {"value": value, "unit": "bounded subproblems/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}), flush=True)
+        return
     cfg = {"workload": f"{inst_name} {n}x{m} frozen UB {ub}, root pushed, pool target "
                        f"{args.target}, step = one explorer round",
            "instance": inst_name, "pool_target": args.target, "ub": ub,
@@ -215,9 +241,169 @@ def cpu_baseline(inst_name, target, sample_nodes):
                                     f"{secs:.1f} s)"}
 
 
+def ref_evaluate_timed(ref, p, prefixes_of, cores, target_s=10.0):
+    """Times the reference BackendSet::evaluate (all host cores) on a sample sized to take
+    about target_s: a 64-node calibration call first.  prefixes_of(k) -> k prefixes."""
+    t0 = time.perf_counter()
+    ref.evaluate(p, prefixes_of(64), backends=cores)
+    per = (time.perf_counter() - t0) / 64
+    k = int(min(2_000_000, max(256, target_s / max(per, 1e-9))))
+    pre = prefixes_of(k)
+    t0 = time.perf_counter()
+    lb, _ = ref.evaluate(p, pre, backends=cores)
+    return k, time.perf_counter() - t0, lb
+
+
+def bound_stress(args, inst_name):
+    """BASELINE configs[4]: bound-only (K1 = CpuBackend::evaluate's drop-in) passes over a
+    synthetic pool resident in HBM; a step = one pass over the whole pool.  The pool is
+    random_node (tests/helpers.hpp:47-55) generated on the device (fbb_synth_pool);
+    N GPUs each hold and bound their own pool (weak scaling, no collective)."""
+    rank, world, local = dist_env()
+    import torch
+
+    dev = local if world > 1 and not os.environ.get("FBB_SAME_GPU") else 0
+    torch.cuda.set_device(dev)
+    backend = os.environ.get("FBB_DIST_BACKEND", "nccl")
+    coll_dev = f"cuda:{dev}" if backend == "nccl" else "cpu"
+    if world > 1:
+        import torch.distributed as dist
+
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
+    import paper_1206_4973_b200 as fbb
+
+    n, m, seed, ub = INSTANCES[inst_name]
+    inst = fbb.generate_instance(n, m, seed)
+    ctx = fbb.Context(inst, dev)
+    cnt, W, P = args.pool, (n + 63) // 64, m * (m - 1) // 2
+    cuda = f"cuda:{dev}"
+    masks = torch.empty(cnt * W, dtype=torch.int64, device=cuda)
+    heads = torch.empty(cnt * m, dtype=torch.int32, device=cuda)
+    depth = torch.empty(cnt, dtype=torch.int32, device=cuda)
+    lbs = torch.empty(cnt, dtype=torch.int32, device=cuda)
+    ts = torch.cuda.Stream(device=cuda)  # K1 and the timing events on one (non-null) stream
+    stream = ts.cuda_stream
+    ctx.synth_pool(0x5EED + rank, cnt, 0, n - 1, masks.data_ptr(), heads.data_ptr(),
+                   depth.data_ptr(), 0, stream)
+    torch.cuda.synchronize()
+    n_u = float((n - depth.double()).mean())
+
+    def one_pass():
+        ctx.bound_device(masks.data_ptr(), heads.data_ptr(), depth.data_ptr(), cnt, lbs.data_ptr(),
+                         stream)
+
+    for _ in range(args.warmup):
+        one_pass()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(dev) if rank == 0 and not os.environ.get("FBB_NO_CLOCKS") else None
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(ts)
+    for _ in range(args.steps):
+        one_pass()  # pool (cnt x ~100-300 B) > L2: every pass streams it from HBM
+    ev1.record(ts)
+    torch.cuda.synchronize()
+    clocks = sampler.result() if sampler else None
+    ms = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms], dtype=torch.float64, device=coll_dev)
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    ms_max = float(t[0])
+    total_nodes = cnt * args.steps * world
+
+    e2e = None
+    if not args.no_e2e:  # through fbb_bound: pinned host pool in, bounds out, every step
+        sub = min(cnt, 1 << 22)
+        hm = torch.empty(sub * W, dtype=torch.int64, pin_memory=True)
+        hh = torch.empty(sub * m, dtype=torch.int32, pin_memory=True)
+        hd = torch.empty(sub, dtype=torch.int32, pin_memory=True)
+        hm.copy_(masks[: sub * W])
+        hh.copy_(heads[: sub * m])
+        hd.copy_(depth[:sub])
+        hmn, hhn, hdn = hm.numpy().view(np.uint64), hh.numpy(), hd.numpy()
+        out = torch.empty(sub, dtype=torch.int32, pin_memory=True).numpy()
+        L = ctx.L
+        for _ in range(2):
+            ctx._check(L.fbb_bound(ctx.h, hmn, hhn, hdn, sub, out))
+        steps_e = max(1, min(args.steps, 20))
+        w0 = time.perf_counter()
+        for _ in range(steps_e):
+            ctx._check(L.fbb_bound(ctx.h, hmn, hhn, hdn, sub, out))
+        es = time.perf_counter() - w0
+        e2e = {"value": sub * steps_e * world / es, "unit": "bounded subproblems/s",
+               "h2d_bytes_per_step": sub * (W * 8 + m * 4 + 4), "d2h_bytes_per_step": sub * 4,
+               "timing": f"wall clock of fbb_bound over {sub} pinned host nodes per step "
+                         f"(H2D + K1 + D2H), {steps_e} steps",
+               "matches_device_pass": bool(np.array_equal(out, lbs[:sub].cpu().numpy()))}
+    if rank != 0:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        from oracle import REF_SO, Ref
+
+        if os.path.exists(REF_SO):
+            ref = Ref()
+            cores = ref.detect_units()
+            def prefixes_of(k):  # the first k nodes of this pool, regenerated with prefixes
+                pre = torch.empty(k * n, dtype=torch.uint8, device=cuda)
+                dd = torch.empty(k, dtype=torch.int32, device=cuda)
+                mm = torch.empty(k * W, dtype=torch.int64, device=cuda)
+                hh2 = torch.empty(k * m, dtype=torch.int32, device=cuda)
+                ctx.synth_pool(0x5EED, k, 0, n - 1, mm.data_ptr(), hh2.data_ptr(), dd.data_ptr(),
+                               pre.data_ptr(), stream)
+                torch.cuda.synchronize()
+                dnp, pnp = dd.cpu().numpy(), pre.cpu().numpy().reshape(k, n)
+                return [list(map(int, pnp[i, : dnp[i]])) for i in range(k)]
+
+            ns, secs, ref_lb = ref_evaluate_timed(ref, inst.p, prefixes_of, cores)
+            same = bool(np.array_equal(np.asarray(ref_lb, np.int32), lbs[:ns].cpu().numpy()))
+            cpu = {"value": ns / secs, "unit": "bounded subproblems/s", "cores": cores,
+                   "kind": "reference", "sample": f"first {ns} nodes of the pool through the "
+                   f"reference BackendSet::evaluate ({secs:.1f} s, node construction included); "
+                   f"bounds identical to K1: {same}"}
+    ops_per_node = 4 * P * n_u + 2 * m * n_u  # SURVEY 8(a) W_K1
+    peaks = measured_peaks()
+    clock_mhz = (clocks or {}).get("sm_max_mhz") or peaks.get("sm_max_mhz", 1965.0)
+    int_peak = 148 * INT32_LANES_PER_SM * clock_mhz * 1e6 / 1e9
+    achieved = cnt * args.steps * ops_per_node / (ms / 1e3) / 1e9
+    node_b = W * 8 + m * 4 + 4 + 4
+    line = {
+        "metric": METRIC, "value": total_nodes / (ms_max / 1e3), "unit": "bounded subproblems/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic (Taillard generator, published seed; random_node pool generated on device)",
+        "config": {"workload": f"{inst_name} {n}x{m} bounding stress: K1 (bound-only) passes over "
+                               f"a synthetic pool of {cnt} nodes per GPU resident in HBM; step = "
+                               f"one pass", "instance": inst_name, "pool_nodes": cnt,
+                   "mean_unscheduled": n_u, "parallelism": f"dp{world} (own pool per GPU)",
+                   "l2": f"pool {cnt * node_b / 2**30:.2f} GiB > L2 (126 MB), no flush needed"},
+        "e2e": e2e,
+        "roofline": {"bound": "int32-alu", "kernel": "k1_bound_kernel (bound-only)",
+                     "achieved": achieved, "peak": int_peak, "unit": "Gop/s",
+                     "frac": achieved / int_peak, "traffic": None,
+                     "ops_per_node": ops_per_node,
+                     "hbm": {"achieved": cnt * args.steps * node_b / (ms / 1e3) / 1e9,
+                             "peak": peaks.get("hbm_gbs", 6553.9), "unit": "GB/s"}},
+        "cpu_baseline": cpu, "clocks": clocks, "gpu_launches": args.steps * world,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
 def main():
     args = parse()
     inst_name = args.instance
+    if args.mode == "bound" and args.impl == "ours":
+        bound_stress(args, inst_name)
+        return
     if args.impl == "reference":
         reference_arm(args, inst_name)
         return

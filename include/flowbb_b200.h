@@ -104,6 +104,16 @@ int fbb_bound(fbb_ctx* ctx, const uint64_t* masks, const int32_t* heads, const i
 int fbb_bound_device(fbb_ctx* ctx, const uint64_t* d_masks, const int32_t* d_heads,
                      const int32_t* d_depth, int64_t count, int32_t* d_lb_out, void* stream);
 
+/* Synthetic node pool on the device (bounding-stress workload): node i is the
+ * reference test helper's random_node (tests/helpers.hpp:47-55) with a
+ * counter-based generator -- depth uniform in [min_depth, max_depth], the first
+ * `depth` picks of a Fisher-Yates shuffle (splitmix64 of seed ^ i*0xD1B54A32D192ED03),
+ * heads folded with child_heads.  Device pointers (d_prefix may be NULL);
+ * asynchronous on `stream` (NULL = the context's stream). */
+int fbb_synth_pool(fbb_ctx* ctx, uint64_t seed, int64_t count, int32_t min_depth, int32_t max_depth,
+                   uint64_t* d_masks, int32_t* d_heads, int32_t* d_depth, uint8_t* d_prefix,
+                   void* stream);
+
 /* ---- K2: fused expand + bound + prune + compact of one pool.
  * Replaces, for the given parents (in pop order), branch (search.hpp:40-59)
  * + evaluate + integrate (search.hpp:84-107) / the frozen prune

@@ -18,7 +18,7 @@ FBB_E_STATE = -5
 
 EXPORTED = (
     "fbb_create", "fbb_destroy", "fbb_last_error", "fbb_descriptor", "fbb_bound",
-    "fbb_bound_device", "fbb_expand_bound_prune", "fbb_explorer_reset",
+    "fbb_bound_device", "fbb_synth_pool", "fbb_expand_bound_prune", "fbb_explorer_reset",
     "fbb_explorer_start_solve", "fbb_explorer_run", "fbb_explorer_state",
     "fbb_explorer_pending", "fbb_explorer_set_residency", "fbb_explorer_set_incumbent",
     "fbb_explorer_best", "fbb_explorer_take", "fbb_explorer_push", "fbb_tuner_create", "fbb_tuner_destroy", "fbb_tuner_target",
@@ -98,6 +98,8 @@ def load_library(path: str = LIB_PATH):
     L.fbb_descriptor.argtypes = [_vp, C.POINTER(Descriptor)]
     L.fbb_bound.argtypes = [_vp, _u64p, _i32p, _i32p, C.c_int64, _i32p]
     L.fbb_bound_device.argtypes = [_vp, _vp, _vp, _vp, C.c_int64, _vp, _vp]
+    L.fbb_synth_pool.argtypes = [_vp, C.c_uint64, C.c_int64, C.c_int32, C.c_int32, _vp, _vp, _vp,
+                                 _vp, _vp]
     L.fbb_expand_bound_prune.argtypes = [
         _vp, _u64p, _i32p, _i32p, _u8p, C.c_int64, C.c_int32, C.c_int, _u64p, _i32p, _i32p, _u8p,
         _i32p, C.POINTER(C.c_int64), C.POINTER(C.c_int32), C.POINTER(C.c_int64), _i32p,

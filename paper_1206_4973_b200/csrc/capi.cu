@@ -779,6 +779,9 @@ int fbb_descriptor(fbb_ctx* ctx, fbb_descriptor_t* out) {
     // children per round bounded by what the staging + buckets can hold in a quarter of HBM
     int64_t per_child = (int64_t)node_bytes(ctx) * 3 + 16;
     int64_t cap = (int64_t)(total_b / 4) / per_child;
+    // and by 128 waves of resident tiles: past a few million children per round the
+    // per-round fixed costs are amortised and bigger pools only grow the pending tree
+    cap = std::min<int64_t>(cap, (int64_t)out->grain * out->base_units * 128);
     out->max_batch = std::max<int64_t>(cap - cap % out->grain, (int64_t)out->grain * out->base_units);
     (void)sms;
     return FBB_OK;
@@ -792,6 +795,20 @@ int fbb_bound_device(fbb_ctx* ctx, const uint64_t* d_masks, const int32_t* d_hea
     cudaSetDevice(ctx->device);
     cudaStream_t st = stream ? (cudaStream_t)stream : ctx->stream;
     CK(launch_k1(ctx->dt, ctx->k1, d_masks, d_heads, d_depth, count, d_lb_out, st), "K1 launch");
+    return FBB_OK;
+}
+
+int fbb_synth_pool(fbb_ctx* ctx, uint64_t seed, int64_t count, int32_t min_depth, int32_t max_depth,
+                   uint64_t* d_masks, int32_t* d_heads, int32_t* d_depth, uint8_t* d_prefix, void* stream) {
+    if (!ctx) return FBB_E_ARG;
+    const int n = ctx->dt.n;
+    if (count < 0 || min_depth < 0 || max_depth < min_depth || max_depth > n ||
+        (count > 0 && (!d_masks || !d_heads || !d_depth)))
+        return ctx->fail(FBB_E_ARG, "invalid synthetic pool request");
+    cudaSetDevice(ctx->device);
+    cudaStream_t st = stream ? (cudaStream_t)stream : ctx->stream;
+    CK(launch_synth(ctx->dt, seed, count, min_depth, max_depth, d_masks, d_heads, d_depth, d_prefix, st),
+       "synth launch");
     return FBB_OK;
 }
 

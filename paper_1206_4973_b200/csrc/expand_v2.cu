@@ -21,6 +21,9 @@ namespace fbb {
 namespace {
 
 constexpr int32_t kNeg2 = -(1 << 20);
+// Offset that takes a non-member's c out of every max (not a power of two, so the
+// compiler keeps c + sched * kOff as one IMAD).  Values: |D| <= 98 * 64, c < 2^14.
+constexpr int32_t kOff = 0x100003;
 
 __host__ __device__ inline size_t b16(size_t x) { return (x + 15) & ~size_t(15); }
 
@@ -31,28 +34,33 @@ __host__ __device__ inline int v2_row_bytes(int P) {
 }
 
 struct V2Layout {
-    size_t row, um, rank, R, load, mins, amin, Mq, p, pre, wsum, total;
+    size_t row, um, rank, R, load, mins, amin, Mq, p, tl, pre, wsum, total;
     int ppc_max, rowb;
 };
 
-// Per-parent job-indexed arrays (ranks, staged prefixes) hold RW = 32 entries for
+// Per-parent job-indexed arrays (Mq offsets, staged prefixes) hold RW = 32 entries for
 // n <= 32 and 64 for the wide variant (32 < n <= 64).
 __host__ __device__ inline int v2_rw(int N) { return N <= 32 ? 32 : 64; }
+// Parents per chunk: the wide variant caps them at 16 so that its per-parent arrays
+// leave room for 2 CTAs per SM (its 64-position rows take 48 KB).
+__host__ __device__ inline int v2_ppc_cap(int N) { return N <= 32 ? (1 << 20) : 16; }
 
 __host__ __device__ inline V2Layout v2_layout(int n, int m, int P, int cmax, int threads, int N) {
     V2Layout L;
     L.ppc_max = cmax / 3 > 0 ? cmax / 3 : 1;
+    if (L.ppc_max > v2_ppc_cap(N)) L.ppc_max = v2_ppc_cap(N);
     L.rowb = v2_row_bytes(P);
     size_t o = 0;
     L.row = o;  o = b16(o + (size_t)N * P * 4);  // rows padded to N positions
     L.um = o;   o = b16(o + (size_t)L.ppc_max * 8);
-    L.rank = o; o = b16(o + (size_t)L.ppc_max * v2_rw(N));
+    L.rank = o; o = b16(o + (size_t)L.ppc_max * v2_rw(N) * 2);  // u16 Mq offsets
     L.R = o;    o = b16(o + (size_t)L.ppc_max * m * 4);
     L.load = o; o = b16(o + (size_t)L.ppc_max * m * 4);
     L.mins = o; o = b16(o + (size_t)L.ppc_max * m * 4);  // min1 | min2 << 16
     L.amin = o; o = b16(o + (size_t)L.ppc_max * m);
     L.Mq = o;   o = b16(o + (size_t)(cmax + 1) * L.rowb);  // + a dummy row for non-members
     L.p = o;    o = b16(o + (size_t)n * m * 4);
+    L.tl = o;   o = b16(o + (size_t)n * m * 2);  // tails as int16
     L.pre = o;  o = b16(o + (size_t)L.ppc_max * v2_rw(N));
     L.wsum = o; o = b16(o + (size_t)(threads / 32 + 2) * 8);
     L.total = o;
@@ -80,6 +88,11 @@ __device__ __forceinline__ uint32_t lds_u32_v(uint32_t addr) {
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
     return v;
 }
+__device__ __forceinline__ uint32_t lds_u16(uint32_t addr) {
+    uint32_t v;
+    asm("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
 __device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
     uint32_t v;
     asm("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
@@ -92,49 +105,52 @@ __device__ __forceinline__ void sts_u16(uint32_t addr, int32_t v) {
 // Is the job of row entry e unscheduled?  Its U bit is moved to the sign bit by a
 // wrapped left funnel shift (shift = e & 31 = 31 - (job & 31)); bit 5 of e picks
 // the 32-bit word of U (always the low word for n <= 32).
-__device__ __forceinline__ bool member(uint32_t e, uint32_t lo, uint32_t hi) {
-    return (int32_t)__funnelshift_l(0u, (e & 32u) ? hi : lo, e) < 0;
+__device__ __forceinline__ bool member(uint32_t e, uint32_t slo, uint32_t shi) {
+    return (int32_t)__funnelshift_l(0u, (e & 32u) ? shi : slo, e) >= 0;  // not scheduled
 }
 
 // Forward + backward scan of NB consecutive row positions of one pair for one
 // parent, entering with D0 and prefix max PM0 (the block's start state) and the
 // suffix max SM0 of the positions after the block; emits M' = max(prefix max,
-// suffix max - d) of every member to its child's Mq slot (non-members to the
-// dummy row) and returns the suffix max including this block.  FULL: the scan
-// covers the whole row (n <= 32), so the U bit is always in the low word.
+// suffix max - d) of every member to its child's Mq slot and returns the suffix
+// max including this block.  Per position the per-parent offset table gives the
+// child's Mq row (or the dummy row for a non-member), so the only per-position
+// selects are two LOP3 masks (c -> -inf, -d -> 0 for non-members).  The table
+// rows hold nd = -d (b - a), which saves the negation.
 template <int NB, int P, bool WIDE>
-__device__ __forceinline__ int32_t scan_block(uint32_t row_sa, uint32_t lo, uint32_t hi,
-                                              uint32_t rank_sa, uint32_t out_sa, uint32_t dummy_sa,
-                                              uint32_t rowb, int32_t D0, int32_t PM0, int32_t SM0) {
-    // the rows (loads issued back to back), then the ranks of their jobs
+__device__ __forceinline__ int32_t scan_block(uint32_t row_sa, uint32_t slo, uint32_t shi,
+                                              uint32_t off_sa, uint32_t base_sa, int32_t D0,
+                                              int32_t PM0, int32_t SM0) {
     uint32_t e[NB];
 #pragma unroll
     for (int i = 0; i < NB; ++i) e[i] = lds_u32(row_sa + (uint32_t)(i * P * 4));
     uint32_t at[NB];
 #pragma unroll
-    for (int i = 0; i < NB; ++i) at[i] = lds_u8(rank_sa + (e[i] & (WIDE ? 63u : 31u)));
-    // forward: prefix maxima; per position the effective c (-inf for non-members),
-    // -d (0 for non-members) and the store address
+    for (int i = 0; i < NB; ++i) at[i] = base_sa + lds_u16(off_sa + (e[i] & (WIDE ? 63u : 31u)) * 2u);
     int32_t D = D0, PM = PM0;
-    int32_t pm[NB], ce[NB], nd[NB];
+    int32_t pm[NB], ce[NB], ndm[NB];
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
-        const bool in = WIDE ? member(e[i], lo, hi) : (int32_t)__funnelshift_l(0u, lo, e[i]) < 0;
+        // slo/shi hold the SCHEDULED jobs: the funnel shift moves the job's bit to the
+        // sign, and its sign extension (IMAD.HI, FMA pipe) is -1 for a scheduled job
+        const uint32_t f = WIDE ? __funnelshift_l(0u, (e[i] & 32u) ? shi : slo, e[i])
+                                : __funnelshift_l(0u, slo, e[i]);
+        const int32_t sched = __mulhi((int32_t)f, 1);
         const int32_t c = (int32_t)__byte_perm(e[i], 0u, 0x4421);  // bytes 1..2
-        const int32_t d = (int32_t)e[i] >> 24;
-        ce[i] = in ? c : kNeg2;
-        nd[i] = in ? -d : 0;
-        at[i] = in ? out_sa + at[i] * rowb : dummy_sa;
+        const int32_t nd = __mulhi((int32_t)e[i], 256);             // -d (top byte, signed)
+        // non-members: c - kOff (IMAD, FMA pipe) can never win a max; -d -> 0 (LOP3, ALU
+        // pipe) -- one select per pipe keeps the two pipes balanced
+        ce[i] = c + sched * kOff;
+        ndm[i] = nd & ~sched;
         pm[i] = PM;
         PM = max(PM, D + ce[i]);
-        D -= nd[i];
+        D -= ndm[i];
     }
-    // backward: suffix maxima and M' = max(prefix, suffix - d), unconditional
     int32_t SM = SM0;
 #pragma unroll
     for (int i = NB - 1; i >= 0; --i) {
-        const int32_t Db = D + nd[i];  // D before position i
-        sts_u16(at[i], max(pm[i], SM + nd[i]));
+        const int32_t Db = D + ndm[i];  // D before position i
+        sts_u16(at[i], max(pm[i], SM + ndm[i]));
         SM = max(SM, Db + ce[i]);
         D = Db;
     }
@@ -167,7 +183,7 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
     const V2Layout L = v2_layout(n, M, P, cmax, blockDim.x, N);
     uint64_t* s_um = (uint64_t*)(smem + L.um);  // unscheduled jobs of each parent
     constexpr int RW = N <= 32 ? 32 : 64;
-    uint8_t* s_rank = (uint8_t*)(smem + L.rank);
+    uint16_t* s_off = (uint16_t*)(smem + L.rank);  // per parent: Mq byte offset of each job code
     int32_t* s_R = (int32_t*)(smem + L.R);
     int32_t* s_load = (int32_t*)(smem + L.load);
     uint32_t* s_mins = (uint32_t*)(smem + L.mins);
@@ -183,12 +199,16 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
     const int q = tid % P, g = tid / P;
     const bool a_lane = g < G;
 
-    for (int x = tid; x < n * M; x += bd) s_p[x] = t.p[x];
+    int16_t* s_tl = (int16_t*)(smem + L.tl);
+    for (int x = tid; x < n * M; x += bd) {
+        s_p[x] = t.p[x];
+        s_tl[x] = (int16_t)t.tails[x];  // < 0x7FFF (checked at configuration)
+    }
 
     // Johnson rows repacked for the scans, one word per (position, pair), [i][q]:
     //   bits 0..4 = 31 - (job & 31) (a left funnel shift by it moves the job's U bit
     //   to the sign bit), bit 5 = job >> 5 (which 32-bit word of U, wide variant),
-    //   bits 8..23 c, bits 24..31 d (int8).  Padding positions i >= n read the top bit
+    //   bits 8..23 c, bits 24..31 -d (int8).  Padding positions i >= n read the top bit
     //   of U (bit 31, or 63 in the wide variant), which is 0 when padding exists.
     uint32_t* s_row = (uint32_t*)(smem + L.row);
     for (int x = tid; x < N * P; x += bd) {
@@ -197,7 +217,7 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
             uint32_t e = t.jm[x];
             const uint32_t j = (uint32_t)entry_job(e);
             v = (31u - (j & 31u)) | (j & 32u) | ((uint32_t)entry_c(e) << 8) |
-                ((uint32_t)entry_d(e) << 24);
+                ((uint32_t)(-entry_d(e)) << 24);
         }
         s_row[x] = v;
     }
@@ -219,7 +239,7 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
         const Segment& sg = pool->seg[s];
         const int depth = sg.depth;
         const int r = n - depth;
-        const int ppc = cmax / r;
+        const int ppc = min(cmax / r, v2_ppc_cap(N));
         const int64_t p0 = (chunk - sg.chunk_base) * ppc;
         const int np = (int)(sg.count - p0 < ppc ? sg.count - p0 : ppc);
         const int nc = np * r;
@@ -240,10 +260,16 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
             s_R[x] = src.heads[(first + step * (p0 + pp)) * M + k];
         }
         __syncthreads();
-        for (int x = tid; x < np * RW; x += bd) {  // rank of job j among U, at its entry code
+        // per parent and job code: byte offset of the job's child row in Mq relative to
+        // the parent's first child row (rank of the job among U), or of the dummy row
+        // for a scheduled / absent job
+        for (int x = tid; x < np * RW; x += bd) {
             const int pp = x / RW, idx = x - pp * RW;
             const int j = (idx & 32) | (31 - (idx & 31));
-            s_rank[x] = (uint8_t)__popcll(s_um[pp] & ((1ull << j) - 1ull));
+            const uint64_t um = s_um[pp];
+            const bool in = j < n && ((um >> j) & 1ull);
+            const int row = in ? __popcll(um & ((1ull << j) - 1ull)) : cmax - pp * r;
+            s_off[x] = (uint16_t)(row * L.rowb);
         }
         // per (parent, machine): load, two smallest tails (+ argmin)
         for (int x = tid; x < np * M; x += bd) {
@@ -254,7 +280,7 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
                 int j = __ffsll((long long)um) - 1;
                 um &= um - 1;
                 load += s_p[j * M + k];
-                int32_t tv = t.tails[j * M + k];
+                int32_t tv = s_tl[j * M + k];
                 if (tv < m1) {
                     m2 = m1;
                     m1 = tv;
@@ -272,19 +298,15 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
         if (a_lane) {
             for (int pp = g; pp < np; pp += G) {
                 const uint64_t um64 = s_um[pp];
-                const uint32_t rank_sa = (uint32_t)__cvta_generic_to_shared(s_rank + pp * RW);
-                const uint32_t out_sa =
+                const uint32_t off_sa = (uint32_t)__cvta_generic_to_shared(s_off + pp * RW);
+                const uint32_t base_sa =
                     (uint32_t)__cvta_generic_to_shared(s_Mq + (size_t)(pp * r) * L.rowb + 2 * q);
-                const uint32_t dummy_sa =
-                    (uint32_t)__cvta_generic_to_shared(s_Mq + (size_t)cmax * L.rowb + 2 * q);
-                const uint32_t rowb = (uint32_t)L.rowb;
                 if constexpr (N <= 32) {
-                    scan_block<N, P, false>(row_sa, (uint32_t)um64, 0u, rank_sa, out_sa, dummy_sa,
-                                            rowb, 0, kNeg2, 0);
+                    scan_block<N, P, false>(row_sa, ~(uint32_t)um64, ~0u, off_sa, base_sa, 0, kNeg2, 0);
                 } else {
                     // wide: forward pass keeps (D, prefix max) checkpoints every 16
                     // positions; each block is then recomputed and scanned backward
-                    const uint32_t lo = (uint32_t)um64, hi = (uint32_t)(um64 >> 32);
+                    const uint32_t lo = ~(uint32_t)um64, hi = ~(uint32_t)(um64 >> 32);  // scheduled
                     int32_t ckD[N / 16], ckP[N / 16];
                     int32_t D = 0, PM = kNeg2;
 #pragma unroll
@@ -297,17 +319,16 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
                             const uint32_t e = lds_u32_v(row_sa + (uint32_t)((b * 16 + i) * P * 4));
                             const bool in = member(e, lo, hi);
                             const int32_t c = (int32_t)__byte_perm(e, 0u, 0x4421);
-                            const int32_t d = (int32_t)e >> 24;
+                            const int32_t nd = (int32_t)e >> 24;  // -d
                             PM = in ? max(PM, D + c) : PM;
-                            D = in ? D + d : D;
+                            D = in ? D - nd : D;
                         }
                     }
                     int32_t SM = kNeg2;
 #pragma unroll
                     for (int b = N / 16 - 1; b >= 0; --b)
                         SM = scan_block<16, P, true>(row_sa + (uint32_t)(b * 16 * P * 4), lo, hi,
-                                                     rank_sa, out_sa, dummy_sa, rowb, ckD[b],
-                                                     ckP[b], SM);
+                                                     off_sa, base_sa, ckD[b], ckP[b], SM);
                 }
             }
         }
@@ -412,6 +433,7 @@ bool k2_v2_config(const DevTables& t, int device, K2Config* out) {
     c.cmax = occ == 3 ? 112 : 128;
     const int NN = n <= 20 ? 20 : (n <= 32 ? 32 : 64);
     c.variant = occ * 10000 + NN * 100 + m;
+    c.ppc_cap = NN <= 32 ? 0 : v2_ppc_cap(NN);
     c.jm_in_smem = false;
     c.smem = v2_layout(n, m, t.P, c.cmax, c.threads, NN).total;
     cudaError_t e;

@@ -81,6 +81,11 @@ cudaError_t launch_k1(const DevTables& t, const K1Config& cfg, const uint64_t* m
                       const int32_t* heads, const int32_t* depth, int64_t count, int32_t* lb,
                       cudaStream_t stream);
 
+// Synthetic pool (synth.cu): node i = random_node(seed, i) in SoA, device pointers.
+cudaError_t launch_synth(const DevTables& t, uint64_t seed, int64_t count, int min_depth, int max_depth,
+                         uint64_t* masks, int32_t* heads, int32_t* depth, uint8_t* prefix,
+                         cudaStream_t stream);
+
 // ---- K2 ----------------------------------------------------------------------------------
 // A pool is a list of parent segments, each a run of parents of one depth read
 // from a node store either forward (a host-supplied batch) or backward (the

@@ -233,6 +233,19 @@ class Context:
                                          np.ascontiguousarray(batch.depth), cnt, out))
         return out
 
+    def bound_device(self, d_masks: int, d_heads: int, d_depth: int, count: int, d_lb: int,
+                     stream: int = 0):
+        """K1 on device pointers (fbb_bound_device), asynchronous on `stream`."""
+        self._check(self.L.fbb_bound_device(self.h, d_masks, d_heads, d_depth, int(count), d_lb,
+                                            stream or None))
+
+    def synth_pool(self, seed: int, count: int, min_depth: int, max_depth: int, d_masks: int,
+                   d_heads: int, d_depth: int, d_prefix: int = 0, stream: int = 0):
+        """Synthetic random nodes generated on the device (fbb_synth_pool)."""
+        self._check(self.L.fbb_synth_pool(self.h, int(seed) & (2**64 - 1), int(count),
+                                          int(min_depth), int(max_depth), d_masks, d_heads,
+                                          d_depth, d_prefix or None, stream or None))
+
     # K2 ----------------------------------------------------------------------------------
     def expand_bound_prune(self, parents: NodeBatch, ub: int, frozen: bool):
         """Returns (survivors NodeBatch, survivor lbs, leaf_best or None, leaf_pos,

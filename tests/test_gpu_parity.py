@@ -261,3 +261,35 @@ def test_solve_small_kats():
     assert not sol.found() and sol.optimum == 9
     sol = fbb.solve(inst_of(SMALL_3x2), initial_ub=11, fixed_batch=8)
     assert sol.optimum == 10 and sol.schedule == [1, 0, 2]
+
+
+# ---- synthetic pools + K1 on device pointers (bounding-stress workload) -------------------------
+
+@pytest.mark.parametrize("nm", [(20, 20), (200, 20), (100, 5)])
+def test_synth_pool_and_k1_device_vs_oracle(oracle, nm):
+    import torch
+
+    from synth_ref import synth_prefix
+
+    n, m = nm
+    inst = fbb.generate_instance(n, m, 2013025619 if n == 200 else 479340445)
+    ctx = fbb.Context(inst)
+    cnt, seed, W = 700, 12345, (n + 63) // 64
+    dm = torch.zeros(cnt * W, dtype=torch.int64, device="cuda")
+    dh = torch.zeros(cnt * m, dtype=torch.int32, device="cuda")
+    dd = torch.zeros(cnt, dtype=torch.int32, device="cuda")
+    dp = torch.zeros(cnt * n, dtype=torch.uint8, device="cuda")
+    dl = torch.zeros(cnt, dtype=torch.int32, device="cuda")
+    ctx.synth_pool(seed, cnt, 0, n, dm.data_ptr(), dh.data_ptr(), dd.data_ptr(), dp.data_ptr())
+    ctx.bound_device(dm.data_ptr(), dh.data_ptr(), dd.data_ptr(), cnt, dl.data_ptr())
+    torch.cuda.synchronize()
+    dep = dd.cpu().numpy()
+    pre = dp.cpu().numpy().reshape(cnt, n)
+    got = [list(map(int, pre[i, : dep[i]])) for i in range(cnt)]
+    exp = [synth_prefix(n, seed, i, 0, n) for i in range(cnt)]
+    assert got == exp
+    ref = fbb.nodes_from_prefixes(inst, exp)
+    assert np.array_equal(dh.cpu().numpy().reshape(cnt, m), ref.heads)
+    assert np.array_equal(dm.cpu().numpy().view(np.uint64).reshape(cnt, W), ref.masks)
+    lb = oracle.evaluate_batch(inst.p, ref.masks, ref.heads, ref.depth)
+    assert np.array_equal(dl.cpu().numpy(), lb)
