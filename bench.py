@@ -47,9 +47,15 @@ def parse():
     ap.add_argument("--instance", default="ta021")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--mode", default="explore", choices=["explore", "bound"],
+    ap.add_argument("--mode", default="explore", choices=["explore", "bound", "exhaust"],
                     help="explore: explorer rounds (configs 1-4); bound: K1 bound-only passes "
-                         "over a synthetic pool in HBM (config 5, bounding stress)")
+                         "over a synthetic pool in HBM (config 5, bounding stress); exhaust: "
+                         "explore the whole tree (time-to-explore / proof of optimality)")
+    ap.add_argument("--ub", type=int, default=None,
+                    help="--mode exhaust: frozen UB (default: the instance's UB + 1, so the "
+                         "optimum is found and proven)")
+    ap.add_argument("--max-seconds", type=float, default=1800.0,
+                    help="--mode exhaust: wall-clock cap")
     ap.add_argument("--pool", type=int, default=8_000_000,
                     help="--mode bound: nodes in the synthetic pool")
     ap.add_argument("--tuner", action="store_true",
@@ -398,8 +404,59 @@ def bound_stress(args, inst_name):
         torch.distributed.destroy_process_group()
 
 
+def exhaust(args, inst_name):
+    """Time-to-explore: the frozen-UB exploration from the root run to exhaustion on one GPU
+    (resolve_workload, bench.hpp:63-114, with the pending tree in HBM).  With UB = opt + 1
+    the run finds an optimal schedule's makespan and proves that nothing better exists
+    (BASELINE configs[0]'s 'full B&B to optimality' for an instance whose tree fits)."""
+    import torch
+
+    import paper_1206_4973_b200 as fbb
+
+    torch.cuda.set_device(0)
+    n, m, seed, ub0 = INSTANCES[inst_name]
+    ub = args.ub if args.ub is not None else ub0 + 1
+    inst = fbb.generate_instance(n, m, seed)
+    ctx = fbb.Context(inst, 0)
+    ctx.explorer_reset(fbb.NodeBatch.root(inst), ub, frozen=True)
+    sampler = ClockSampler(0) if not os.environ.get("FBB_NO_CLOCKS") else None
+    t0 = time.perf_counter()
+    dev_ms, rounds, chunk = 0.0, 0, 2000
+    while True:
+        r, t = ctx.explorer_run([args.target], chunk, timing=True)
+        dev_ms += sum(x["round_ms"] for x in t)
+        rounds += len(r)
+        st = ctx.explorer_state()
+        if st["pending"] == 0 or time.perf_counter() - t0 > args.max_seconds:
+            break
+    wall = time.perf_counter() - t0
+    clocks = sampler.result() if sampler else None
+    st = ctx.explorer_state()
+    done = st["pending"] == 0
+    line = {
+        "metric": METRIC, "value": st["bounded"] / wall, "unit": "bounded subproblems/s",
+        "n_gpus": 1, "steps": rounds, "warmup": 0, "ms_per_step": 1e3 * wall / max(1, rounds),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic (Taillard generator, published seed; no dataset)",
+        "config": {"workload": f"{inst_name} {n}x{m} exhaustive frozen-UB exploration from the "
+                               f"root at UB {ub}, pool target {args.target}",
+                   "instance": inst_name, "ub": ub, "pool_target": args.target},
+        "explore_seconds": wall, "device_seconds": dev_ms / 1e3, "exhausted": done,
+        "bounded": st["bounded"], "branched": st["branched"], "pruned": st["pruned"],
+        "leaves": st["leaves"], "best_leaf": st["incumbent"] if st["found"] else None,
+        "proof": (f"optimum {st['incumbent']}: no complete schedule below it exists"
+                  if done and st["found"] else
+                  f"no schedule below {ub}" if done else "time cap reached"),
+        "clocks": clocks, "gpu_launches": rounds * 2,
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
+    if args.mode == "exhaust":
+        exhaust(args, args.instance)
+        return
     inst_name = args.instance
     if args.mode == "bound" and args.impl == "ours":
         bound_stress(args, inst_name)
