@@ -146,6 +146,19 @@ class ClockSampler:
                 "samples": len(samples), "source": "NVML from a child process, ~10 ms polling"}
 
 
+def k2_traffic(inst_name):
+    """DRAM bytes (read + write) of one K2 launch from the committed ncu --set full capture
+    (profiles/r01_k2_dram.json), when one exists for this instance; else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_k2_dram.json")) as f:
+            d = json.load(f)[inst_name]
+        return {"bytes_per_launch": d["dram_read_bytes"] + d["dram_write_bytes"],
+                "children_per_launch": d["children_per_launch"], "kernel": d["kernel"],
+                "source": "ncu --set full, profiles/r01_k2_dram.json"}
+    except Exception:  # noqa: BLE001
+        return None
+
+
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -656,7 +669,8 @@ def main():
     roofline = {
         "bound": "int32-alu", "kernel": "k2_internal_kernel (fused expand+bound+prune)",
         "achieved": ops / k2_s / 1e9 if k2_s > 0 else 0.0, "peak": int_peak, "unit": "Gop/s",
-        "frac": (ops / k2_s / 1e9) / int_peak if k2_s > 0 else 0.0, "traffic": None,
+        "frac": (ops / k2_s / 1e9) / int_peak if k2_s > 0 else 0.0,
+        "traffic": k2_traffic(inst_name),
         "ops_per_child": ops / max(1, bounded),
         "peak_note": "148 SMs x 128 int32 lanes/clk (alu+fma pipes) x max SM clock; derived, "
                      "not measured (MEASURED_PEAKS has no integer figure)",

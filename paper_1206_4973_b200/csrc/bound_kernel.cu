@@ -9,6 +9,8 @@
 // pairs (conflict-free jm[i*P + q] reads).  Per item the Johnson simulation is
 // the 3-op max-plus step  if (j in U) { M = max(M, D + c); D += d; }.
 #include <climits>
+#include <cstdlib>
+#include <string>
 
 #include "fbb_internal.h"
 
@@ -150,6 +152,11 @@ __global__ void __launch_bounds__(256) k1_bound_kernel(DevTables t, int tile,
 
 K1Config k1_config(const DevTables& t, int device) {
     K1Config c;
+    {
+        const char* sel = getenv("FBB_K1");  // FBB_K1=v1 forces this kernel (A/B runs)
+        if (!(sel && std::string(sel) == "v1") && k1v2_config(t, device, &c)) return c;
+        c = K1Config{};
+    }
     c.threads = 256;
     int P = t.P;
     c.tile = P > 0 ? (c.threads * 16 + P - 1) / P : 1024;
@@ -175,6 +182,7 @@ cudaError_t launch_k1(const DevTables& t, const K1Config& cfg, const uint64_t* m
                       const int32_t* heads, const int32_t* depth, int64_t count, int32_t* lb,
                       cudaStream_t stream) {
     if (count <= 0) return cudaSuccess;
+    if (cfg.variant != 0) return launch_k1v2(t, cfg, masks, heads, depth, count, lb, stream);
     int64_t ntiles = (count + cfg.tile - 1) / cfg.tile;
     int blocks = (int)(ntiles < cfg.blocks ? ntiles : cfg.blocks);
 #define K1_LAUNCH(ONE, SM)                                                                      \

@@ -73,6 +73,7 @@ struct K1Config {
     int threads = 256;
     int tile = 32;       // nodes per tile
     bool jm_in_smem = true;
+    int variant = 0;     // 0: k1_bound_kernel; 1/2/8: k1v2_kernel<NW> (bound_v2.cu)
     int blocks = 0;      // persistent grid
     size_t smem = 0;
 };
@@ -80,6 +81,13 @@ K1Config k1_config(const DevTables& t, int device);
 cudaError_t launch_k1(const DevTables& t, const K1Config& cfg, const uint64_t* masks,
                       const int32_t* heads, const int32_t* depth, int64_t count, int32_t* lb,
                       cudaStream_t stream);
+
+// K1 v2 (bound_v2.cu): packed rows through L1, NPT nodes per row sweep; false when
+// the instance does not qualify (|d| > 127, m > 20, n > 256).
+bool k1v2_config(const DevTables& t, int device, K1Config* out);
+cudaError_t launch_k1v2(const DevTables& t, const K1Config& cfg, const uint64_t* masks,
+                        const int32_t* heads, const int32_t* depth, int64_t count, int32_t* lb,
+                        cudaStream_t stream);
 
 // Synthetic pool (synth.cu): node i = random_node(seed, i) in SoA, device pointers.
 cudaError_t launch_synth(const DevTables& t, uint64_t seed, int64_t count, int min_depth, int max_depth,

@@ -293,3 +293,42 @@ def test_synth_pool_and_k1_device_vs_oracle(oracle, nm):
     assert np.array_equal(dm.cpu().numpy().view(np.uint64).reshape(cnt, W), ref.masks)
     lb = oracle.evaluate_batch(inst.p, ref.masks, ref.heads, ref.depth)
     assert np.array_equal(dl.cpu().numpy(), lb)
+
+
+@pytest.mark.parametrize("nm", [(20, 20), (50, 10), (200, 20), (20, 7)])
+def test_k1_v1_and_v2_agree(oracle, nm, monkeypatch):
+    """Both K1 kernels (the smem-table v1 and the packed-row v2) give the oracle's bounds."""
+    n, m = nm
+    rng = np.random.default_rng(n * 100 + m)
+    inst = inst_of(rng.integers(1, 100, size=(n, m)).astype(np.int32))
+    prefixes = [list(rng.permutation(n)[: rng.integers(0, n + 1)]) for _ in range(300)]
+    nodes = fbb.nodes_from_prefixes(inst, prefixes)
+    ref = oracle.evaluate_batch(inst.p, nodes.masks, nodes.heads, nodes.depth)
+    got = {}
+    for sel in ("v1", "v2"):
+        monkeypatch.setenv("FBB_K1", sel)
+        ctx = fbb.Context(inst)
+        got[sel] = ctx.bound(nodes)
+        ctx.close()
+    assert np.array_equal(got["v1"], ref) and np.array_equal(got["v2"], ref)
+
+
+def test_k2_generic_and_specialised_agree(monkeypatch):
+    """The generic K2 and the register-row kernels (v2 n<=64, v3 n<=256) give identical
+    survivors, bounds and counts on the same parents."""
+    rng = np.random.default_rng(5)
+    for n, m in [(20, 20), (50, 20), (100, 10)]:
+        inst = inst_of(rng.integers(1, 100, size=(n, m)).astype(np.int32))
+        parents = sorted([list(rng.permutation(n)[: rng.integers(0, n - 2)]) for _ in range(60)],
+                         key=len, reverse=True)
+        pb = fbb.nodes_from_prefixes(inst, parents)
+        outs = []
+        for sel in ("generic", "auto"):
+            monkeypatch.setenv("FBB_K2", sel)
+            ctx = fbb.Context(inst)
+            surv, slb, best, pos, sched, counts = ctx.expand_bound_prune(pb, 10**6, frozen=True)
+            k = int(np.median(slb)) if len(slb) else 0
+            s2, l2, *_ = ctx.expand_bound_prune(pb, k, frozen=True)
+            outs.append((surv.prefixes(), list(slb), counts, s2.prefixes(), list(l2)))
+            ctx.close()
+        assert outs[0] == outs[1], (n, m)
