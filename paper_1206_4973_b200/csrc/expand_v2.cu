@@ -271,22 +271,38 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
             const int row = in ? __popcll(um & ((1ull << j) - 1ull)) : cmax - pp * r;
             s_off[x] = (uint16_t)(row * L.rowb);
         }
-        // per (parent, machine): load, two smallest tails (+ argmin)
+        // per (parent, machine): load, two smallest tails (+ argmin, smallest job on ties)
         for (int x = tid; x < np * M; x += bd) {
             int pp = x / M, k = x - pp * M;
             uint64_t um = s_um[pp];
             int32_t load = 0, m1 = 0x7FFF, m2 = 0x7FFF, am = 0;
-            while (um) {
-                int j = __ffsll((long long)um) - 1;
-                um &= um - 1;
-                load += s_p[j * M + k];
-                int32_t tv = s_tl[j * M + k];
-                if (tv < m1) {
-                    m2 = m1;
-                    m1 = tv;
-                    am = j;
-                } else if (tv < m2) {
-                    m2 = tv;
+            if constexpr (N <= 32) {
+                // branch-free over all positions: independent (predicated) loads instead of
+                // a dependent ffs / load / compare chain per unscheduled job
+                const uint32_t u32 = (uint32_t)um;
+#pragma unroll
+                for (int j = 0; j < N; ++j) {
+                    const bool in = (u32 >> j) & 1u;
+                    load += in ? s_p[j * M + k] : 0;
+                    const int32_t tv = in ? (int32_t)s_tl[j * M + k] : 0x7FFF;
+                    const bool lt = tv < m1;
+                    m2 = lt ? m1 : min(m2, tv);
+                    am = lt ? j : am;
+                    m1 = lt ? tv : m1;
+                }
+            } else {
+                while (um) {
+                    int j = __ffsll((long long)um) - 1;
+                    um &= um - 1;
+                    load += s_p[j * M + k];
+                    int32_t tv = s_tl[j * M + k];
+                    if (tv < m1) {
+                        m2 = m1;
+                        m1 = tv;
+                        am = j;
+                    } else if (tv < m2) {
+                        m2 = tv;
+                    }
                 }
             }
             s_load[x] = load;
