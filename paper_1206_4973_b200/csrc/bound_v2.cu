@@ -7,8 +7,7 @@
 // warp) and its (c, -d) extraction serve NPT independent max-plus chains:
 //   per node:  sched = sign of (scheduled-job word << code)   (funnel shift + IMAD.HI)
 //              ce  = c + sched * kOff      (IMAD: a scheduled job's c never wins)
-//              ndm = -d & ~sched           (LOP3)
-//              M   = max(M, D + ce);  D -= ndm
+//              M   = max(M, D + ce);  D += d & ~sched
 // then  lb_pair = Lc_l + max(R_l, R_k + M)  (bound.hpp:79-90 in max-plus form; M starts
 // at 0 instead of -inf, harmless because heads are non-decreasing in the machine
 // index, R_k <= R_l).  The pair maxima of a node are reduced in the warp and folded
@@ -22,8 +21,13 @@ namespace fbb {
 
 namespace {
 
-constexpr int kK1Tile = 32;      // nodes per tile
 constexpr int kK1Threads = 192;
+// nodes per tile: 32 per pair group (8 sweeps of NPT = 4 nodes), i.e. 32 at m = 20
+// (one group of 190 pairs) and up to 608 at m = 5 (19 groups of 10 pairs)
+__host__ __device__ inline int k1v2_tile(int P) {
+    const int t = (kK1Threads / P) * 32;
+    return t < 1024 ? t : 1024;
+}
 constexpr int32_t kK1Off = 0x100003;
 
 template <int NW, int NPT>
@@ -32,11 +36,13 @@ __global__ void __launch_bounds__(kK1Threads) k1v2_kernel(DevTables t, const uin
                                                           const int32_t* __restrict__ depth, int64_t count,
                                                           int32_t* __restrict__ lb_out) {
     const int n = t.n, m = t.m, P = t.P, W = t.W;
-    __shared__ uint32_t s_sched[kK1Tile * NW];  // scheduled jobs (and bits >= n) per node
-    __shared__ int32_t s_R[kK1Tile * kMaxMachines];
-    __shared__ int32_t s_Lc[kK1Tile * kMaxMachines];
-    __shared__ int32_t s_lb[kK1Tile];
-    __shared__ int32_t s_dep[kK1Tile];
+    const int kK1Tile = k1v2_tile(P);
+    extern __shared__ __align__(16) uint32_t k1smem[];
+    uint32_t* s_sched = k1smem;                            // tile * NW: scheduled jobs (+ bits >= n)
+    int32_t* s_R = (int32_t*)(s_sched + kK1Tile * NW);     // tile * m
+    int32_t* s_Lc = s_R + kK1Tile * m;                     // tile * m
+    int32_t* s_lb = s_Lc + kK1Tile * m;                    // tile
+    int32_t* s_dep = s_lb + kK1Tile;                       // tile
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = kK1Threads / 32;
     const int G = kK1Threads / P;  // P <= 190 for m <= 20
     const int q = tid % P, g = tid / P;
@@ -105,7 +111,7 @@ __global__ void __launch_bounds__(kK1Threads) k1v2_kernel(DevTables t, const uin
                 for (int i = 0; i < n; ++i) {
                     const uint32_t e = __ldg(rowq + i * P);
                     const int32_t c = (int32_t)__byte_perm(e, 0u, 0x4421);
-                    const int32_t nd = __mulhi((int32_t)e, 256);
+                    const int32_t d = __mulhi((int32_t)e, 256);  // rowpk holds +d (a - b)
 #pragma unroll
                     for (int u = 0; u < NPT; ++u) {
                         uint32_t w;
@@ -120,9 +126,8 @@ __global__ void __launch_bounds__(kK1Threads) k1v2_kernel(DevTables t, const uin
                         }
                         const int32_t sched = __mulhi((int32_t)__funnelshift_l(0u, w, e), 1);
                         const int32_t ce = c + sched * kK1Off;
-                        const int32_t ndm = nd & ~sched;
                         Mx[u] = max(Mx[u], D[u] + ce);
-                        D[u] -= ndm;
+                        D[u] += d & ~sched;
                     }
                 }
 #pragma unroll
@@ -148,26 +153,35 @@ __global__ void __launch_bounds__(kK1Threads) k1v2_kernel(DevTables t, const uin
     }
 }
 
+size_t k1v2_smem(const DevTables& t, int NW) {
+    const size_t tile = (size_t)k1v2_tile(t.P);
+    return tile * NW * 4 + tile * t.m * 8 + tile * 8;
+}
+
 template <int NW, int NPT>
-int k1v2_blocks(int device) {
+int k1v2_blocks(const DevTables& t, int device) {
     int sms = 148, per_sm = 1;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1v2_kernel<NW, NPT>, kK1Threads, 0);
+    cudaFuncSetAttribute(k1v2_kernel<NW, NPT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k1v2_kernel<NW, NPT>, kK1Threads,
+                                                  k1v2_smem(t, NW));
     return sms * (per_sm < 1 ? 1 : per_sm);
 }
 
 }  // namespace
 
 bool k1v2_config(const DevTables& t, int device, K1Config* out) {
-    if (!t.rowpk || t.m > 20 || t.m < 2 || t.n > 256) return false;
+    // Measured (profiles/r01_reading.md): the row-sweep kernel wins for n > 64 (200x20:
+    // 43-47 vs 31 M nodes/s); for n <= 64 the smem-table kernel is faster.
+    if (!t.rowpk || t.m > 20 || t.m < 2 || t.n > 256 || t.n <= 64) return false;
     K1Config c;
     c.threads = kK1Threads;
-    c.tile = kK1Tile;
-    c.smem = 0;
+    c.tile = k1v2_tile(t.P);
     c.jm_in_smem = false;
     c.variant = t.n <= 32 ? 1 : (t.n <= 64 ? 2 : 8);
-    c.blocks = c.variant == 1 ? k1v2_blocks<1, 4>(device)
-                              : (c.variant == 2 ? k1v2_blocks<2, 4>(device) : k1v2_blocks<8, 4>(device));
+    c.smem = k1v2_smem(t, c.variant);
+    c.blocks = c.variant == 1 ? k1v2_blocks<1, 4>(t, device)
+                              : (c.variant == 2 ? k1v2_blocks<2, 4>(t, device) : k1v2_blocks<8, 4>(t, device));
     *out = c;
     return true;
 }
@@ -175,12 +189,12 @@ bool k1v2_config(const DevTables& t, int device, K1Config* out) {
 cudaError_t launch_k1v2(const DevTables& t, const K1Config& cfg, const uint64_t* masks,
                         const int32_t* heads, const int32_t* depth, int64_t count, int32_t* lb,
                         cudaStream_t stream) {
-    const int64_t ntiles = (count + kK1Tile - 1) / kK1Tile;
+    const int64_t ntiles = (count + cfg.tile - 1) / cfg.tile;
     const int blocks = (int)(ntiles < cfg.blocks ? ntiles : cfg.blocks);
     switch (cfg.variant) {
-        case 1: k1v2_kernel<1, 4><<<blocks, kK1Threads, 0, stream>>>(t, masks, heads, depth, count, lb); break;
-        case 2: k1v2_kernel<2, 4><<<blocks, kK1Threads, 0, stream>>>(t, masks, heads, depth, count, lb); break;
-        default: k1v2_kernel<8, 4><<<blocks, kK1Threads, 0, stream>>>(t, masks, heads, depth, count, lb); break;
+        case 1: k1v2_kernel<1, 4><<<blocks, kK1Threads, cfg.smem, stream>>>(t, masks, heads, depth, count, lb); break;
+        case 2: k1v2_kernel<2, 4><<<blocks, kK1Threads, cfg.smem, stream>>>(t, masks, heads, depth, count, lb); break;
+        default: k1v2_kernel<8, 4><<<blocks, kK1Threads, cfg.smem, stream>>>(t, masks, heads, depth, count, lb); break;
     }
     return cudaGetLastError();
 }

@@ -295,7 +295,7 @@ def test_synth_pool_and_k1_device_vs_oracle(oracle, nm):
     assert np.array_equal(dl.cpu().numpy(), lb)
 
 
-@pytest.mark.parametrize("nm", [(20, 20), (50, 10), (200, 20), (20, 7)])
+@pytest.mark.parametrize("nm", [(20, 20), (50, 10), (200, 20), (20, 7), (100, 5), (65, 2), (130, 3)])
 def test_k1_v1_and_v2_agree(oracle, nm, monkeypatch):
     """Both K1 kernels (the smem-table v1 and the packed-row v2) give the oracle's bounds."""
     n, m = nm
