@@ -19,8 +19,11 @@
 #ifndef FLOWBB_B200_GPU_BACKEND_HPP
 #define FLOWBB_B200_GPU_BACKEND_HPP
 
+#include <algorithm>
+#include <chrono>
 #include <cstdint>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <mutex>
 #include <optional>
@@ -28,9 +31,12 @@
 #include <string>
 #include <vector>
 
+#include "flowbb/autotune.hpp"
 #include "flowbb/backend.hpp"
+#include "flowbb/bench.hpp"
 #include "flowbb/pending.hpp"
 #include "flowbb/search.hpp"
+#include "flowbb/workload.hpp"
 #include "flowbb_b200.h"
 
 namespace flowbb_b200 {
@@ -225,6 +231,117 @@ inline RoundCounts gpu_round(const GpuBackend& backend, const flowbb::Instance& 
     return rc;
 }
 
+// ---- workload snapshots and the speedup protocol ----------------------------
+
+// generate_workload (workload.hpp:62-98) with the children's bounds from the GPU: the
+// same frozen-UB sequential capture, the same mt19937 deterministic shuffle of each
+// expansion's children, the same pushes -- so save_workload of the result is
+// byte-identical to the reference's.
+inline flowbb::WorkloadSnapshot generate_workload(const GpuBackend& gpu, const flowbb::Instance& inst,
+                                                  int initial_ub, flowbb::CaptureCutoff cutoff,
+                                                  std::uint32_t seed,
+                                                  std::function<double()> clock = {}) {
+    using flowbb::CaptureCutoff;
+    if (cutoff.kind == CaptureCutoff::Kind::wall_time && !clock) {
+        auto start = std::chrono::steady_clock::now();
+        clock = [start] {
+            return std::chrono::duration<double>(std::chrono::steady_clock::now() - start).count();
+        };
+    }
+    std::mt19937 rng(seed);
+    flowbb::PendingTree pending(inst.jobs());
+    auto expand = [&](const flowbb::Node& node) {
+        std::vector<flowbb::Node> children = flowbb::branch(inst, node);
+        flowbb::detail::deterministic_shuffle(children, rng);
+        std::vector<int> lbs = gpu.evaluate(inst, children);  // K1, one call per expansion
+        for (std::size_t i = 0; i < children.size(); ++i) {
+            flowbb::Node& child = children[i];
+            if (child.depth() == inst.jobs()) continue;  // incumbent frozen, leaves dropped
+            child.lb = lbs[i];
+            if (child.lb < initial_ub) pending.push(std::move(child));
+        }
+    };
+    expand(flowbb::Node::root(inst));
+    std::int64_t branched = 0;
+    while (!pending.empty()) {
+        if (cutoff.kind == CaptureCutoff::Kind::node_count) {
+            if (branched >= cutoff.nodes) break;
+        } else if (clock() >= cutoff.seconds) {
+            break;
+        }
+        expand(pending.pop());
+        ++branched;
+    }
+    return flowbb::WorkloadSnapshot{inst, pending.drain(), initial_ub, seed, cutoff};
+}
+
+// resolve_workload (bench.hpp:63-114) on the GPU: fused rounds (gpu_round, frozen) over
+// the reference's own PendingTree; batch from config.batch, or the adaptive tuner
+// observing each round's time (config.autotune).  Same best and nodes_bounded as the
+// reference for every batch (frozen-UB exploration is partition-invariant).
+inline flowbb::ResolutionResult resolve_workload(const GpuBackend& gpu,
+                                                 const flowbb::WorkloadSnapshot& snapshot,
+                                                 const flowbb::BenchConfig& config) {
+    using clock = std::chrono::steady_clock;
+    const flowbb::Instance& inst = snapshot.instance;
+    std::optional<flowbb::Tuner> tuner;
+    if (config.autotune) tuner.emplace(config.descriptor, config.window, config.probes);
+    const std::size_t fixed = config.batch ? static_cast<std::size_t>(*config.batch)
+                                           : static_cast<std::size_t>(config.descriptor.grain) *
+                                                 config.descriptor.base_units;
+    auto t0 = clock::now();
+    flowbb::PendingTree pending(inst.jobs());
+    for (const flowbb::Node& node : snapshot.nodes) pending.push(node);
+    flowbb::Incumbent inc{snapshot.incumbent_value, std::nullopt};
+    flowbb::ResolutionResult result;
+    std::size_t last = fixed;
+    while (!pending.empty()) {
+        const std::size_t target = tuner ? static_cast<std::size_t>(tuner->target()) : fixed;
+        last = target;
+        auto e0 = clock::now();
+        RoundCounts rc = gpu_round(gpu, inst, pending, inc, target, true, &result.best);
+        result.nodes_bounded += rc.bounded;
+        if (tuner)
+            tuner->observe(rc.bounded, std::max(std::chrono::duration<double>(clock::now() - e0).count(), 1e-9));
+    }
+    result.elapsed_seconds = std::chrono::duration<double>(clock::now() - t0).count();
+    result.batch_used = tuner ? tuner->best_batch() : static_cast<int>(last);
+    if (tuner && result.batch_used == 0) result.batch_used = tuner->target();
+    return result;
+}
+
+// run_experiment (bench.hpp:119-145) with the parallel side on the GPU: the reference's
+// strictly sequential CPU resolution (one backend, batch 1 -- the paper's Tcpu) against
+// each GPU configuration; any disagreement in the best leaf or the bounded-node count
+// throws flowbb::ResolutionMismatch.
+inline flowbb::Report run_experiment(const GpuBackend& gpu, const flowbb::WorkloadSnapshot& snapshot,
+                                     const std::vector<flowbb::BenchConfig>& configs) {
+    flowbb::BenchConfig sequential;
+    sequential.backends = 1;
+    sequential.batch = 1;
+    flowbb::ResolutionResult seq = flowbb::resolve_workload(snapshot, sequential);
+    flowbb::Report report;
+    for (const flowbb::BenchConfig& config : configs) {
+        flowbb::ResolutionResult par = resolve_workload(gpu, snapshot, config);
+        if (par.best != seq.best)
+            throw flowbb::ResolutionMismatch("optimum mismatch between sequential and GPU resolution");
+        if (par.nodes_bounded != seq.nodes_bounded)
+            throw flowbb::ResolutionMismatch("bounded-node count mismatch between resolutions");
+        flowbb::ReportRow row;
+        row.jobs = snapshot.instance.jobs();
+        row.machines = snapshot.instance.machines();
+        row.batch = par.batch_used;
+        row.backends = 1;
+        row.t_seq = seq.elapsed_seconds;
+        row.t_par = par.elapsed_seconds;
+        row.speedup = seq.elapsed_seconds / std::max(par.elapsed_seconds, 1e-12);
+        row.nodes_bounded = par.nodes_bounded;
+        report.rows.push_back(row);
+    }
+    return report;
+}
+
 }  // namespace flowbb_b200
+
 
 #endif  // FLOWBB_B200_GPU_BACKEND_HPP

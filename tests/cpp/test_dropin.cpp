@@ -132,6 +132,46 @@ int main() {
         CHECK(same, "pending trees identical after 12 rounds");
         std::printf("ok gpu_round frozen resolve Ta021 == reference (12 rounds, pending identical)\n");
     }
+    // 5. generate_workload on the GPU == the reference's capture, byte for byte (workload.hpp)
+    {
+        flowbb_b200::GpuBackend gpu;
+        Instance ta021 = generate_instance(20, 20, 479340445);
+        for (std::int64_t budget : {0, 7, 500, 4000}) {
+            auto cut = CaptureCutoff::by_nodes(budget);
+            std::string ref = save_workload(generate_workload(ta021, 2297, cut, 42));
+            std::string got = save_workload(flowbb_b200::generate_workload(gpu, ta021, 2297, cut, 42));
+            CHECK(ref == got, "generate_workload Ta021");
+        }
+        std::mt19937 rng(5);
+        for (int trial = 0; trial < 6; ++trial) {
+            Instance inst = testutil::random_instance(rng, 8 + trial, 3 + trial % 4);
+            int ub = solve(inst, [] { SolveConfig c; c.fixed_batch = 64; c.descriptor = BackendDescriptor{1, 1, 1 << 20}; return c; }()).optimum + 3;
+            auto cut = CaptureCutoff::by_nodes(40 + 30 * trial);
+            std::string ref = save_workload(generate_workload(inst, ub, cut, 1000u + trial));
+            std::string got = save_workload(flowbb_b200::generate_workload(gpu, inst, ub, cut, 1000u + trial));
+            CHECK(ref == got, "generate_workload random");
+            // 6. run_experiment: sequential CPU vs GPU resolutions agree (bench.hpp:119-145)
+            WorkloadSnapshot snap = load_workload(got);
+            std::vector<BenchConfig> cfgs(3);
+            cfgs[0].batch = 1;
+            cfgs[1].batch = 64;
+            cfgs[2].autotune = true;
+            cfgs[2].descriptor = BackendDescriptor{8, 2, 4096};
+            cfgs[2].window = 2;
+            try {
+                Report rep = flowbb_b200::run_experiment(gpu, snap, cfgs);
+                CHECK(rep.rows.size() == 3, "run_experiment rows");
+                BenchConfig c64;
+                c64.batch = 64;
+                c64.backends = 4;
+                ResolutionResult cpu = resolve_workload(snap, c64);
+                CHECK(rep.rows[1].nodes_bounded == cpu.nodes_bounded, "resolve nodes_bounded");
+            } catch (const ResolutionMismatch&) {
+                CHECK(false, "run_experiment ResolutionMismatch");
+            }
+        }
+        std::printf("ok generate_workload byte-identical; run_experiment GPU == sequential CPU\n");
+    }
     std::printf(failures ? "FAILED %d\n" : "ALL PASS\n", failures);
     return failures ? 1 : 0;
 }
