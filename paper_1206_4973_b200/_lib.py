@@ -8,6 +8,8 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libflowbb_b200.so")
+# FBB_LIB: an alternative build of the same library (A/B measurements only)
+LIB_PATH = os.environ.get("FBB_LIB", LIB_PATH)
 
 FBB_OK = 0
 FBB_E_ARG = -1

@@ -19,3 +19,11 @@ tail -1 gpurun_out/ncu_v3.log
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
    --log-file gpurun_out/launches_ta081.csv python bench.py --instance ta081 --steps 5 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 python scripts/show.py gpurun_out/bench*.json
+for I in ta101 ta021; do timeout 600 python bench.py --mode bound --instance $I --steps 10 > gpurun_out/bench_bound_$I.json 2> gpurun_out/bench_bound_$I.err; done
+timeout 600 python bench.py --mode bound --instance ta101 --impl reference > gpurun_out/bench_bound_ref.json 2>/dev/null
+bash scripts/gpu_sweep.sh > gpurun_out/sweep_table.md
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k2_v2" -s 5 -c 1 \
+   -o gpurun_out/prof_k2v2_pool -f python scripts/k2_pool_bench.py 2 > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none -k regex:"k1v2" -s 1 -c 1 \
+   -o gpurun_out/prof_k1v2_ta101 -f python bench.py --mode bound --instance ta101 --steps 2 --warmup 1 --pool 1000000 --no-e2e --no-cpu-baseline > /dev/null 2>&1
+timeout 600 oracle/_ref/dropin_test > gpurun_out/dropin.txt 2>&1; tail -1 gpurun_out/dropin.txt

@@ -111,6 +111,29 @@ def main(tag):
                   f"{e2e:.4g} | {rf.get('k2_share_of_round', 0):.3f} | {rf.get('frac', 0):.3f} | "
                   f"{cpu if cpu is None else f'{cpu:.4g}'} |")
         shutil.copy(os.path.join(OUT, f), os.path.join(PROF, f"{tag}_{f}"))
+    header = False
+    for f in ["bench_bound_ta101.json", "bench_bound_ta021.json", "bench_bound_ref.json"]:
+        d = bench_line(os.path.join(OUT, f))
+        if d:
+            if not header:
+                header = True
+                md += ["", "## bound-only stress (`bench.py --mode bound`, K1 over a synthetic pool in HBM)", "",
+                       "| run | value (bounded/s) | ms/pass | e2e (bounded/s) | roofline frac | cpu baseline |",
+                       "|---|---|---|---|---|---|"]
+            rf = d.get("roofline") or {}
+            e2e = (d.get("e2e") or {}).get("value")
+            cpu = (d.get("cpu_baseline") or {}).get("value")
+            md.append(f"| {f} | {d['value']:.4g} | {d['ms_per_step']:.3f} | {e2e:.4g} | "
+                      f"{rf.get('frac', 0):.3f} | {cpu if cpu is None else f'{cpu:.4g}'} |")
+            shutil.copy(os.path.join(OUT, f), os.path.join(PROF, f"{tag}_{f}"))
+    sw = os.path.join(OUT, "sweep_table.md")
+    if os.path.exists(sw):
+        md += ["", "## Ta021 pool-size sweep (BASELINE configs[1]; `scripts/gpu_sweep.sh`)", "",
+               open(sw).read().strip()]
+    dr = os.path.join(OUT, "dropin.txt")
+    if os.path.exists(dr):
+        md += ["", "## reference API driven by the GPU drop-in (`oracle/_ref/dropin_test`)", "", "```",
+               open(dr).read().strip(), "```"]
     for lf, title in [("launches.csv", "Ta021 (bench.py --steps 5 --warmup 3)"),
                       ("launches_ta081.csv", "Ta081 (bench.py --instance ta081 --steps 5 --warmup 3)")]:
         p = os.path.join(OUT, lf)
@@ -120,7 +143,9 @@ def main(tag):
                        "serialised: compare shares, not absolute times)", "", launches(p)]
             shutil.copy(p, os.path.join(PROF, f"{tag}_{lf}"))
     for rep, title in [("prof_k2_final.ncu-rep", "K2 (v2, Ta021) and place"),
-                       ("prof_k2v3_ta081.ncu-rep", "K2 (v3, Ta081)")]:
+                       ("prof_k2v2_pool.ncu-rep", "K2 (v2) on a fixed 262K-child Ta021 pool (k2_pool_bench)"),
+                       ("prof_k2v3_ta081.ncu-rep", "K2 (v3, Ta081)"),
+                       ("prof_k1v2_ta101.ncu-rep", "K1 (v2, 200x20 bound-only pool)")]:
         p = os.path.join(OUT, rep)
         if os.path.exists(p):
             md += ["", f"## ncu --set full: {title}", ncu_metrics(p)]
