@@ -27,9 +27,35 @@ constexpr int32_t kOff = 0x100003;
 
 __host__ __device__ inline size_t b16(size_t x) { return (x + 15) & ~size_t(15); }
 
-__host__ __device__ inline int v2_row_bytes(int P) {
-    int b = (P * 2 + 15) / 16;  // 16-byte units
-    if ((b & 1) == 0) b += 1;   // odd -> 8 consecutive rows hit 8 distinct bank groups
+// Mq row layout: the slots of one k cover l = lo_k .. hi_k - 1 with lo_k = (k+1) & ~1 and
+// hi_k = m rounded up to even, so Phase B reads them as 16x2 words whose halves are
+// (l, l+1) with l even.  The pad slots (l = k when k is even, l = m when m is odd) are
+// zeroed once per CTA and never written; the terms they produce, Lc_k + R_k and
+// -16384 + R_k, never exceed the one-machine term.
+__host__ __device__ constexpr int v2_lo(int k) { return (k + 1) & ~1; }
+__host__ __device__ constexpr int v2_hi(int m) { return (m + 1) & ~1; }
+__host__ __device__ constexpr int v2_group_base(int m, int k) {
+    int b = 0;
+    for (int kk = 0; kk < k; ++kk) b += v2_hi(m) - v2_lo(kk);
+    return b;
+}
+__host__ __device__ constexpr int v2_slots(int m) { return v2_group_base(m, m - 1); }
+// Slot of each pair index q (bound.hpp:97-98 order) in that layout.
+template <int M>
+struct SlotTab {
+    unsigned char s[M * (M - 1) / 2 > 0 ? M * (M - 1) / 2 : 1];
+    constexpr SlotTab() : s() {
+        int q = 0;
+        for (int k = 0; k < M; ++k)
+            for (int l = k + 1; l < M; ++l) s[q++] = (unsigned char)(v2_group_base(M, k) + l - v2_lo(k));
+    }
+};
+template <int M>
+__constant__ SlotTab<M> kSlotOf = SlotTab<M>();
+
+__host__ __device__ inline int v2_row_bytes(int m) {
+    int b = (2 * v2_slots(m) + 15) / 16;  // 16-byte units
+    if ((b & 1) == 0) b += 1;             // odd -> 8 consecutive rows hit 8 distinct bank groups
     return b * 16;
 }
 
@@ -49,7 +75,7 @@ __host__ __device__ inline V2Layout v2_layout(int n, int m, int P, int cmax, int
     V2Layout L;
     L.ppc_max = cmax / 3 > 0 ? cmax / 3 : 1;
     if (L.ppc_max > v2_ppc_cap(N)) L.ppc_max = v2_ppc_cap(N);
-    L.rowb = v2_row_bytes(P);
+    L.rowb = v2_row_bytes(m);
     size_t o = 0;
     L.row = o;  o = b16(o + (size_t)N * P * 4);  // rows padded to N positions
     L.um = o;   o = b16(o + (size_t)L.ppc_max * 8);
@@ -157,20 +183,6 @@ __device__ __forceinline__ int32_t scan_block(uint32_t row_sa, uint32_t slo, uin
     return SM;
 }
 
-template <int M>
-struct PairTab {  // (k, l) of pair index q in bound.hpp:97-98 order
-    int k[M * (M - 1) / 2 > 0 ? M * (M - 1) / 2 : 1];
-    int l[M * (M - 1) / 2 > 0 ? M * (M - 1) / 2 : 1];
-    constexpr PairTab() : k(), l() {
-        int q = 0;
-        for (int a = 0; a < M; ++a)
-            for (int b = a + 1; b < M; ++b) {
-                k[q] = a;
-                l[q] = b;
-                ++q;
-            }
-    }
-};
 
 // OCC = target CTAs per SM: 2 -> up to 168 registers, 3 -> 112 (smaller chunks too)
 template <int N, int M, int OCC>
@@ -178,6 +190,9 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
                                                    int first_seg, int cmax, int32_t ub, int frozen,
                                                    RoundState* rs, ChunkOut out) {
     constexpr int P = M * (M - 1) / 2;
+    // Phase B: the 16x2 grouped form at 2 CTAs/SM (168 registers); at 3 CTAs/SM (96
+    // registers) the per-pair form over q-ordered Mq rows, which spills least there
+    constexpr bool kGroupedB = OCC == 2;
     extern __shared__ __align__(16) unsigned char smem[];
     const int n = t.n, W = t.W;
     const V2Layout L = v2_layout(n, M, P, cmax, blockDim.x, N);
@@ -223,6 +238,8 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
     }
     // 32-bit shared addresses: each scan step is one LDS [reg + immediate]
     const uint32_t row_sa = (uint32_t)__cvta_generic_to_shared(s_row + q);
+    for (int x = tid; x < (int)((cmax + 1) * L.rowb / 16); x += bd)  // padding slots stay 0
+        ((uint4*)s_Mq)[x] = make_uint4(0u, 0u, 0u, 0u);
 
     int32_t ub_eff = ub;
     if (!frozen) {
@@ -315,8 +332,11 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
             for (int pp = g; pp < np; pp += G) {
                 const uint64_t um64 = s_um[pp];
                 const uint32_t off_sa = (uint32_t)__cvta_generic_to_shared(s_off + pp * RW);
+                // Mq slot of pair q in the grouped row layout, from a __constant__ table (a
+                // kernel-long register for it pushed Phase A into spilling at 96 regs)
+                const int slot_q = kGroupedB ? (int)kSlotOf<M>.s[q] : q;
                 const uint32_t base_sa =
-                    (uint32_t)__cvta_generic_to_shared(s_Mq + (size_t)(pp * r) * L.rowb + 2 * q);
+                    (uint32_t)__cvta_generic_to_shared(s_Mq + (size_t)(pp * r) * L.rowb + 2 * slot_q);
                 if constexpr (N <= 32) {
                     scan_block<N, P, false>(row_sa, ~(uint32_t)um64, ~0u, off_sa, base_sa, 0, kNeg2, 0);
                 } else {
@@ -363,36 +383,71 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
                                    : 32 + (int)__fns((uint32_t)(um >> 32), 0, rk - nlo + 1);
             myx = x;
             mypp = pp;
-            int32_t Lc[M];
-            int32_t prev = 0, lb = 0;
+            if constexpr (kGroupedB) {
+                uint32_t LcE[(M + 1) / 2];  // (Lc_l, Lc_l+1) for even l, int16 halves
+                int32_t prev = 0, lb = 0, lc_even = 0;
+    #pragma unroll
+                for (int k = 0; k < M; ++k) {
+                    const int pk = pp * M + k;
+                    prev = max(prev, s_R[pk]) + s_p[x * M + k];  // child_heads, instance.hpp:81-89
+                    myR[k] = prev;
+                    uint32_t mins = s_mins[pk];
+                    int32_t mt = (x == (int)s_amin[pk]) ? (int32_t)(mins >> 16) : (int32_t)(mins & 0xFFFFu);
+                    const int32_t lc = s_load[pk] - s_p[x * M + k] + mt;
+                    lb = max(lb, prev + lc);  // one-machine term (bound.hpp:61-74)
+                    if (k & 1) LcE[k >> 1] = ((uint32_t)lc_even & 0xFFFFu) | ((uint32_t)lc << 16);
+                    else lc_even = lc;
+                }
+                if (M & 1) LcE[M >> 1] = ((uint32_t)lc_even & 0xFFFFu) | 0xC0000000u;  // l = M: pad
+                // Pairs: Lc_l + max(R_l, R_k + M'_kl).  Lc_l + R_l never exceeds the one-
+                // machine term already in lb, so per k only max_l (Lc_l + M'_kl) + R_k is
+                // needed: a running max over the k-group's slots, two pairs per 16x2
+                // VIADDMNMX (Lc_l + M' < 2^14 for n <= 64).
+                const uint4* mrow = (const uint4*)(s_Mq + (size_t)tid * L.rowb);
+    #pragma unroll
+                for (int k = 0; k < M - 1; ++k) {
+                    const int g0 = v2_group_base(M, k) / 2;  // first 32-bit word of the group
+                    uint32_t acc = 0xC000C000u;             // (-16384, -16384)
+    #pragma unroll
+                    for (int w = 0; w < (v2_hi(M) - v2_lo(k)) / 2; ++w) {
+                        const int gw = g0 + w;
+                        const uint4 v4 = mrow[gw >> 2];
+                        const uint32_t word = (gw & 3) == 0 ? v4.x : (gw & 3) == 1 ? v4.y : (gw & 3) == 2 ? v4.z : v4.w;
+                        acc = __viaddmax_s16x2(LcE[v2_lo(k) / 2 + w], word, acc);
+                    }
+                    const int32_t best = max((int32_t)(int16_t)(acc & 0xFFFFu), (int32_t)acc >> 16);
+                    lb = max(lb, best + myR[k]);
+                }
+                mylb = lb;
+            } else {
+                // 3 CTAs/SM (96 registers): the per-pair form, which keeps fewer values live
+                int32_t Lc[M];
+                int32_t prev = 0, lb = 0;
 #pragma unroll
-            for (int k = 0; k < M; ++k) {
-                const int pk = pp * M + k;
-                prev = max(prev, s_R[pk]) + s_p[x * M + k];  // child_heads, instance.hpp:81-89
-                myR[k] = prev;
-                uint32_t mins = s_mins[pk];
-                int32_t mt = (x == (int)s_amin[pk]) ? (int32_t)(mins >> 16) : (int32_t)(mins & 0xFFFFu);
-                Lc[k] = s_load[pk] - s_p[x * M + k] + mt;
-                lb = max(lb, prev + Lc[k]);  // one-machine term (bound.hpp:61-74)
-            }
-            const uint4* mrow = (const uint4*)(s_Mq + (size_t)tid * L.rowb);
-            constexpr PairTab<M> tab{};
+                for (int k = 0; k < M; ++k) {
+                    const int pk = pp * M + k;
+                    prev = max(prev, s_R[pk]) + s_p[x * M + k];  // child_heads, instance.hpp:81-89
+                    myR[k] = prev;
+                    uint32_t mins = s_mins[pk];
+                    int32_t mt = (x == (int)s_amin[pk]) ? (int32_t)(mins >> 16) : (int32_t)(mins & 0xFFFFu);
+                    Lc[k] = s_load[pk] - s_p[x * M + k] + mt;
+                    lb = max(lb, prev + Lc[k]);  // one-machine term (bound.hpp:61-74)
+                }
+                const uint4* mrow = (const uint4*)(s_Mq + (size_t)tid * L.rowb);
 #pragma unroll
-            for (int q8 = 0; q8 < (P + 7) / 8; ++q8) {
-                const uint4 cur = mrow[q8];
-                const uint32_t wv[4] = {cur.x, cur.y, cur.z, cur.w};
+                for (int k = 0; k < M - 1; ++k) {
 #pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const int qq = q8 * 8 + u;
-                    if (qq < P) {
-                        const uint32_t w = wv[u >> 1];
-                        const int32_t mq = (u & 1) ? ((int32_t)w >> 16) : (int32_t)(int16_t)(w & 0xFFFFu);
-                        const int k = tab.k[qq], l = tab.l[qq];
+                    for (int l = k + 1; l < M; ++l) {
+                        const int slot = k * (2 * M - k - 1) / 2 + (l - k - 1);  // q
+                        const uint4 v4 = mrow[slot >> 3];
+                        const int wi = (slot >> 1) & 3;
+                        const uint32_t w = wi == 0 ? v4.x : wi == 1 ? v4.y : wi == 2 ? v4.z : v4.w;
+                        const int32_t mq = (slot & 1) ? ((int32_t)w >> 16) : (int32_t)(int16_t)(w & 0xFFFFu);
                         lb = max(lb, Lc[l] + max(myR[l], myR[k] + mq));
                     }
                 }
+                mylb = lb;
             }
-            mylb = lb;
         }
         // ---- prune + stable compaction straight into the destination (one child per thread)
         const bool keep = b_lane && mylb < ub_eff;
@@ -444,8 +499,10 @@ bool k2_v2_config(const DevTables& t, int device, K2Config* out) {
     if (n > 64 || !(m == 5 || m == 10 || m == 20)) return false;
     K2Config c;
     c.threads = 192;
+    // measured (profiles/r01_reading.md): m = 20 runs fastest at 2 CTAs/SM with the
+    // 16x2 grouped Phase B, m in {5, 10} at 3 CTAs/SM; FBB_K2_OCC=2|3 overrides
     const char* occ_env = getenv("FBB_K2_OCC");
-    const int occ = occ_env && occ_env[0] == '2' ? 2 : 3;
+    const int occ = occ_env ? (occ_env[0] == '2' ? 2 : 3) : (m == 20 ? 2 : 3);
     c.cmax = occ == 3 ? 112 : 128;
     const int NN = n <= 20 ? 20 : (n <= 32 ? 32 : 64);
     c.variant = occ * 10000 + NN * 100 + m;
