@@ -183,6 +183,49 @@ __device__ __forceinline__ int32_t scan_block(uint32_t row_sa, uint32_t slo, uin
     return SM;
 }
 
+// Two parents per thread in 16x2 SIMD (n <= 20 at 2 CTAs/SM, where the 168-register
+// budget holds six 20-entry arrays): one row entry feeds both parents' max-plus chains,
+// each as one VIADDMNMX.S16x2 / VIADD.16x2.  Values fit int16 for n <= 20 (|D| <= 1960,
+// c < 2^12); a scheduled job gets c = -16384 and d = 0 in its half.  The backward pass
+// uses the suffix form  T = max(d_i + T, c_i),  M'_x = max(prefmax_<x, D_<x + T_x),
+// which needs no subtraction (rows hold +d for this path).  Parent 1 may be a copy of
+// parent 0 with every job scheduled (odd tail): its half is stored first, so parent
+// 0's store to the same slot wins.
+template <int NB, int P>
+__device__ __forceinline__ void scan_pair16(uint32_t row_sa, uint32_t s0, uint32_t s1, uint32_t off0,
+                                            uint32_t off1, uint32_t base0, uint32_t base1) {
+    constexpr uint32_t kNeg16x2 = 0xC000C000u;  // (-16384, -16384)
+    uint32_t at0[NB], at1[NB], ce2[NB], dm2[NB], pm2[NB], dp2[NB];
+    uint32_t D2 = 0u, PM2 = kNeg16x2;
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+        const uint32_t e = lds_u32(row_sa + (uint32_t)(i * P * 4));
+        const uint32_t code2 = (e & 31u) * 2u;
+        at0[i] = base0 + lds_u16(off0 + code2);
+        at1[i] = base1 + lds_u16(off1 + code2);
+        const uint32_t f0 = __funnelshift_l(0u, s0, e), f1 = __funnelshift_l(0u, s1, e);
+        uint32_t m2, c2, d2;
+        asm("prmt.b32 %0, %1, %2, 0xFFBB;" : "=r"(m2) : "r"(f0), "r"(f1));  // 0xFFFF where scheduled
+        asm("prmt.b32 %0, %1, 0, 0x2121;" : "=r"(c2) : "r"(e));             // (c, c)
+        asm("prmt.b32 %0, %1, 0, 0xB3B3;" : "=r"(d2) : "r"(e));             // (d, d) sign-extended
+        ce2[i] = (c2 & ~m2) | (kNeg16x2 & m2);
+        dm2[i] = d2 & ~m2;
+        pm2[i] = PM2;
+        dp2[i] = D2;
+        PM2 = __viaddmax_s16x2(D2, ce2[i], PM2);
+        D2 = __vadd2(D2, dm2[i]);
+    }
+    uint32_t T2 = kNeg16x2;
+#pragma unroll
+    for (int i = NB - 1; i >= 0; --i) {
+        const uint32_t r2 = __viaddmax_s16x2(dp2[i], T2, pm2[i]);
+        sts_u16(at1[i], (int32_t)(r2 >> 16));
+        sts_u16(at0[i], (int32_t)r2);
+        T2 = __viaddmax_s16x2(dm2[i], T2, ce2[i]);
+    }
+}
+
+
 
 // OCC = target CTAs per SM: 2 -> up to 168 registers, 3 -> 112 (smaller chunks too)
 template <int N, int M, int OCC>
@@ -193,6 +236,7 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
     // Phase B: the 16x2 grouped form at 2 CTAs/SM (168 registers); at 3 CTAs/SM (96
     // registers) the per-pair form over q-ordered Mq rows, which spills least there
     constexpr bool kGroupedB = OCC == 2;
+    constexpr bool kDual16 = OCC == 2 && N == 20;  // Phase A: two parents per thread, 16x2
     extern __shared__ __align__(16) unsigned char smem[];
     const int n = t.n, W = t.W;
     const V2Layout L = v2_layout(n, M, P, cmax, blockDim.x, N);
@@ -232,7 +276,7 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
             uint32_t e = t.jm[x];
             const uint32_t j = (uint32_t)entry_job(e);
             v = (31u - (j & 31u)) | (j & 32u) | ((uint32_t)entry_c(e) << 8) |
-                ((uint32_t)(-entry_d(e)) << 24);
+                ((uint32_t)(kDual16 ? entry_d(e) : -entry_d(e)) << 24);
         }
         s_row[x] = v;
     }
@@ -328,7 +372,19 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
         }
         __syncthreads();  // rank table and per-machine terms visible to every lane
         // ---- Phase A: forward / backward max-plus scans of pair q over parent pp
-        if (a_lane) {
+        if (a_lane && kDual16) {
+            const int slot_q = kSlotOf<M>.s[q];
+            for (int pp = 2 * g; pp < np; pp += 2 * G) {
+                const int pb = pp + 1 < np ? pp + 1 : pp;  // odd tail: a copy with no members
+                const uint32_t s0 = ~(uint32_t)s_um[pp];
+                const uint32_t s1 = pp + 1 < np ? ~(uint32_t)s_um[pb] : 0xFFFFFFFFu;
+                scan_pair16<N, P>(row_sa, s0, s1,
+                                  (uint32_t)__cvta_generic_to_shared(s_off + pp * RW),
+                                  (uint32_t)__cvta_generic_to_shared(s_off + pb * RW),
+                                  (uint32_t)__cvta_generic_to_shared(s_Mq + (size_t)(pp * r) * L.rowb + 2 * slot_q),
+                                  (uint32_t)__cvta_generic_to_shared(s_Mq + (size_t)(pb * r) * L.rowb + 2 * slot_q));
+            }
+        } else if (a_lane) {
             for (int pp = g; pp < np; pp += G) {
                 const uint64_t um64 = s_um[pp];
                 const uint32_t off_sa = (uint32_t)__cvta_generic_to_shared(s_off + pp * RW);
