@@ -3,14 +3,16 @@
 // (expand_kernel.cu) and k2_v2_kernel (expand_v2.cu); a mapping that does not keep
 // per-position state in registers, so it scales to n = 256:
 //
-//  * the repacked Johnson rows (DevTables::rowpk, [i][q]) are read from global memory
+//  * the repacked Johnson rows (DevTables::rowv3, [i][q]) are read from global memory
 //    through L1 -- 76 KB at 100x20, 152 KB at 200x20, too large for shared memory next
 //    to the per-child output rows -- lanes of a warp reading consecutive pairs of one
 //    position (coalesced 128-byte rows);
 //  * thread (g, q) owns machine pair q of parent lane g.  Per (parent, pair) the forward
 //    pass writes every member's exclusive prefix max to its child's Mq slot, the
 //    backward pass folds in the suffix max, max(slot, sufmax - d), by a read-modify-write
-//    of the slot (SURVEY finding 3; bound.hpp:27-44 in max-plus form);
+//    of the slot (SURVEY finding 3; bound.hpp:27-44 in max-plus form).  A per-parent
+//    u16 table indexed by the job gives both the child's Mq row (or a dummy row) and
+//    the membership mask, so the scans are branch-free;
 //  * per (parent, machine) the load and the two smallest tails (lb_one_machine,
 //    bound.hpp:61-74) by warp reductions over the unscheduled jobs;
 //  * Phase B (one child per thread: child_heads, the one-machine term, max over the
@@ -25,6 +27,8 @@ namespace fbb {
 namespace {
 
 constexpr int32_t kNeg3 = -(1 << 20);
+// takes a scheduled job's c out of every max (not a power of two: stays one IMAD)
+constexpr int32_t kV3Off = 0x100003;
 constexpr int kV3Ppc = 16;  // parents per chunk at most (per-parent tables are N bytes)
 
 __host__ __device__ inline size_t c16(size_t x) { return (x + 15) & ~size_t(15); }
@@ -46,13 +50,13 @@ __host__ __device__ inline V3Layout v3_layout(int m, int P, int cmax, int thread
     L.rowb = v3_row_bytes(P);
     size_t o = 0;
     L.u = o;    o = c16(o + (size_t)kV3Ppc * NW * 4);
-    L.rank = o; o = c16(o + (size_t)kV3Ppc * N);
+    L.rank = o; o = c16(o + (size_t)kV3Ppc * N * 2);  // u16 slot table per parent
     L.ujob = o; o = c16(o + (size_t)kV3Ppc * N);
     L.R = o;    o = c16(o + (size_t)kV3Ppc * m * 4);
     L.load = o; o = c16(o + (size_t)kV3Ppc * m * 4);
     L.mins = o; o = c16(o + (size_t)kV3Ppc * m * 4);  // min1 | min2 << 16
     L.amin = o; o = c16(o + (size_t)kV3Ppc * m);
-    L.Mq = o;   o = c16(o + (size_t)cmax * L.rowb);
+    L.Mq = o;   o = c16(o + (size_t)(cmax + 1) * L.rowb);  // + a dummy row for scheduled jobs
     L.pre = o;  o = c16(o + (size_t)kV3Ppc * N);
     L.wsum = o; o = c16(o + (size_t)(threads / 32 + 2) * 8);
     L.total = o;
@@ -62,6 +66,11 @@ __host__ __device__ inline V3Layout v3_layout(int m, int P, int cmax, int thread
 __device__ __forceinline__ uint32_t v3_lds_u32(uint32_t addr) {
     uint32_t v;
     asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ uint32_t v3_lds_u16(uint32_t addr) {
+    uint32_t v;
+    asm("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(addr));
     return v;
 }
 __device__ __forceinline__ uint32_t v3_lds_u8(uint32_t addr) {
@@ -116,7 +125,9 @@ __global__ void __launch_bounds__(NW <= 4 ? 192 : 256, NW <= 4 ? 3 : 2)
     const int n = t.n, W = t.W;
     const V3Layout L = v3_layout(M, P, cmax, blockDim.x, NW);
     uint32_t* s_u = (uint32_t*)(smem + L.u);  // unscheduled jobs, NW words per parent
-    uint8_t* s_rank = (uint8_t*)(smem + L.rank);
+    // per parent and job: (child row offset in Mq / 16) | 0x8000 if the job is scheduled
+    // (then the offset is the dummy row's)
+    uint16_t* s_slot16 = (uint16_t*)(smem + L.rank);
     uint8_t* s_ujob = (uint8_t*)(smem + L.ujob);
     int32_t* s_R = (int32_t*)(smem + L.R);
     int32_t* s_load = (int32_t*)(smem + L.load);
@@ -130,7 +141,6 @@ __global__ void __launch_bounds__(NW <= 4 ? 192 : 256, NW <= 4 ? 3 : 2)
     const int nwarps = bd >> 5;
     const int G = bd / P;
     const int q = tid % P, g = tid / P;
-    const uint32_t* __restrict__ rows = t.rowpk;
 
     int32_t ub_eff = ub;
     if (!frozen) {
@@ -173,17 +183,17 @@ __global__ void __launch_bounds__(NW <= 4 ? 192 : 256, NW <= 4 ? 3 : 2)
             s_R[x] = src.heads[(first + step * (p0 + pp)) * M + k];
         }
         __syncthreads();
-        // rank of each unscheduled job at its entry code (j & ~31) | (31 - (j & 31)), and
-        // the ascending list of unscheduled jobs
+        // per parent and job: the slot table and the ascending list of unscheduled jobs
         for (int x = tid; x < np * N; x += bd) {
-            const int pp = x / N, code = x - pp * N;
-            const int j = (code & ~31) | (31 - (code & 31));
+            const int pp = x / N, j = x - pp * N;
             const uint32_t* u = s_u + pp * NW;
             if (j < n && ((u[j >> 5] >> (j & 31)) & 1u)) {
                 int rk = __popc(u[j >> 5] & ((1u << (j & 31)) - 1u));
                 for (int w = 0; w < (j >> 5); ++w) rk += __popc(u[w]);
-                s_rank[x] = (uint8_t)rk;
+                s_slot16[x] = (uint16_t)(rk * L.rowb / 16);
                 s_ujob[pp * N + rk] = (uint8_t)j;
+            } else {
+                s_slot16[x] = (uint16_t)(0x8000u | ((cmax - pp * r) * L.rowb / 16));
             }
         }
         // per (parent, machine): load and the two smallest tails, a warp per item
@@ -215,41 +225,46 @@ __global__ void __launch_bounds__(NW <= 4 ? 192 : 256, NW <= 4 ? 3 : 2)
             }
         }
         __syncthreads();
-        // ---- Phase A: per (parent, pair) forward / backward max-plus scans into Mq
+        // ---- Phase A: per (parent, pair) forward / backward max-plus scans into Mq.
+        // Per position: the job's slot entry gives the child row (dummy row for a
+        // scheduled job) and the membership mask (PRMT sign replication of bit 15);
+        // a scheduled job's c drops out of every max (IMAD) and its d becomes 0 (LOP3).
         if (g < G) {
-            const uint32_t* rowq = rows + q;
+            const uint32_t* rowq = t.rowv3 + q;
             for (int pp = g; pp < np; pp += G) {
-                const uint32_t u_sa = (uint32_t)__cvta_generic_to_shared(s_u + pp * NW);
-                const uint32_t rank_sa = (uint32_t)__cvta_generic_to_shared(s_rank + pp * N);
-                const uint32_t out_sa =
+                const uint32_t tab_sa = (uint32_t)__cvta_generic_to_shared(s_slot16 + pp * N);
+                const uint32_t base_sa =
                     (uint32_t)__cvta_generic_to_shared(s_Mq + (size_t)(pp * r) * L.rowb + 2 * q);
-                const uint32_t rowb = (uint32_t)L.rowb;
-                int32_t D = 0, PM = kNeg3;
+                int32_t D = 0, PM = -32768;  // PM stays within int16 (stored as is)
 #pragma unroll 8
                 for (int i = 0; i < n; ++i) {
                     const uint32_t e = __ldg(rowq + i * P);
-                    const uint32_t w = NW == 1 ? v3_lds_u32(u_sa) : v3_lds_u32(u_sa + ((e >> 3) & 0x1Cu));
-                    if ((int32_t)(w << (e & 31u)) < 0) {  // job of position i unscheduled
-                        const uint32_t rk = v3_lds_u8(rank_sa + (e & 0xFFu));
-                        v3_sts_u16(out_sa + rk * rowb, max(PM, -32768));  // exclusive prefix max
-                        PM = max(PM, D + (int32_t)((e >> 8) & 0xFFFFu));
-                        D += (int32_t)e >> 24;
-                    }
+                    const uint32_t ent = v3_lds_u16(tab_sa + (e & 0xFFu) * 2u);
+                    uint32_t sched, d;
+                    asm("prmt.b32 %0, %1, 0, 0x9999;" : "=r"(sched) : "r"(ent));  // bit 15 -> mask
+                    asm("prmt.b32 %0, %1, 0, 0x9991;" : "=r"(d) : "r"(e));        // int8 d
+                    const uint32_t at = base_sa + (ent & 0x7FFFu) * 16u;
+                    const int32_t ce = (int32_t)(e >> 16) + (int32_t)sched * kV3Off;
+                    const int32_t dm = (int32_t)(d & ~sched);
+                    v3_sts_u16(at, PM);  // exclusive prefix max
+                    PM = max(PM, D + ce);
+                    D += dm;
                 }
-                int32_t SM = kNeg3;
+                int32_t SM = -32768;
 #pragma unroll 8
                 for (int i = n - 1; i >= 0; --i) {
                     const uint32_t e = __ldg(rowq + i * P);
-                    const uint32_t w = NW == 1 ? v3_lds_u32(u_sa) : v3_lds_u32(u_sa + ((e >> 3) & 0x1Cu));
-                    if ((int32_t)(w << (e & 31u)) < 0) {
-                        const uint32_t rk = v3_lds_u8(rank_sa + (e & 0xFFu));
-                        const int32_t d = (int32_t)e >> 24;
-                        const int32_t Db = D - d;  // D before position i
-                        const uint32_t slot = out_sa + rk * rowb;
-                        v3_sts_u16(slot, max(v3_lds_s16(slot), SM - d));
-                        SM = max(SM, Db + (int32_t)((e >> 8) & 0xFFFFu));
-                        D = Db;
-                    }
+                    const uint32_t ent = v3_lds_u16(tab_sa + (e & 0xFFu) * 2u);
+                    uint32_t sched, d;
+                    asm("prmt.b32 %0, %1, 0, 0x9999;" : "=r"(sched) : "r"(ent));
+                    asm("prmt.b32 %0, %1, 0, 0x9991;" : "=r"(d) : "r"(e));
+                    const uint32_t at = base_sa + (ent & 0x7FFFu) * 16u;
+                    const int32_t ce = (int32_t)(e >> 16) + (int32_t)sched * kV3Off;
+                    const int32_t dm = (int32_t)(d & ~sched);
+                    const int32_t Db = D - dm;  // D before position i
+                    v3_sts_u16(at, max(v3_lds_s16(at), SM - dm));
+                    SM = max(SM, Db + ce);
+                    D = Db;
                 }
             }
         }
@@ -351,7 +366,7 @@ cudaError_t v3_setup(K2Config& c, int device) {
 
 bool k2_v3_config(const DevTables& t, int device, K2Config* out) {
     const int m = t.m, n = t.n;
-    if (n <= 64 || n > 256 || !(m == 5 || m == 10 || m == 20) || !t.rowpk) return false;
+    if (n <= 64 || n > 256 || !(m == 5 || m == 10 || m == 20) || !t.rowv3) return false;
     K2Config c;
     const int NW = n <= 128 ? 4 : 8;
     c.cmax = ((n + 31) / 32) * 32;          // one parent's children always fit a chunk

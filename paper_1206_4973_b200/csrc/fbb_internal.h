@@ -48,6 +48,10 @@ struct DevTables {
     // so bits 0..7 are also the index of j in the per-parent rank tables.  Null when
     // some |d| > 127 (then only the generic kernel runs).
     uint32_t* rowpk;
+    // The rows again for k2_v3 (n*P, [i][q]): bits 0..7 j, bits 8..15 d as int8,
+    // bits 16..31 c -- membership and the child slot come from a per-parent table
+    // indexed by j, so no code/shift field is needed.  Null when rowpk is.
+    uint32_t* rowv3;
 };
 
 // Host copy of the same tables (for tests of the table builder).

@@ -128,6 +128,15 @@ int upload_tables(const HostTables& h, DevTables* d, std::string* why) {
             *why = std::string("table upload: ") + cudaGetErrorString(e);
             return FBB_E_CUDA;
         }
+        for (size_t x = 0; x < h.jm.size(); ++x) {
+            const uint32_t en = h.jm[x];
+            rp[x] = (uint32_t)entry_job(en) | ((uint32_t)(entry_d(en) & 0xFF) << 8) |
+                    ((uint32_t)entry_c(en) << 16);
+        }
+        if ((e = upload(&d->rowv3, rp)) != cudaSuccess) {
+            *why = std::string("table upload: ") + cudaGetErrorString(e);
+            return FBB_E_CUDA;
+        }
     }
     return FBB_OK;
 }
@@ -139,6 +148,7 @@ void free_tables(DevTables* d) {
     cudaFree(d->pair_k);
     cudaFree(d->pair_l);
     cudaFree(d->rowpk);
+    cudaFree(d->rowv3);
     *d = DevTables{};
 }
 
