@@ -294,33 +294,93 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
 
     const int64_t c_begin = pool->seg[first_seg].chunk_base;
     const int64_t c_end = pool->nchunks;
-    for (int64_t chunk = claim_chunk(rs, c_begin, s_slot); chunk < c_end;
-         chunk = claim_chunk(rs, c_begin, s_slot)) {
-        const int s = v2_find_segment(pool, first_seg, chunk);
+    // Chunk staging.  At 2 CTAs/SM the parents of the NEXT chunk are loaded into
+    // registers while this chunk runs Phase A / B (software pipelining: the global --
+    // or, host-resident, host-link -- latency of the staging loads hides behind
+    // compute), and the next ticket is claimed during setup, so a chunk costs one
+    // barrier less.  At 3 CTAs/SM (96 registers) the staging loads stay direct.
+    constexpr bool kPipe = OCC == 2 && N != 32;  // (N = 32: the prefetch registers spill)
+    constexpr int kPpcCt = N <= 32 ? 43 : 16;                  // >= parents per chunk
+    constexpr int kPfPre = (kPpcCt * N + 191) / 192;           // prefix bytes per thread
+    constexpr int kPfHead = (kPpcCt * M + 191) / 192;          // heads per thread
+    uint32_t pf_pre[kPipe ? kPfPre : 1];
+    int32_t pf_head[kPipe ? kPfHead : 1];
+    uint64_t pf_mask = 0;
+    auto chunk_geo = [&](int64_t c, int& s_, int& depth_, int& np_, int64_t& p0_) {
+        s_ = v2_find_segment(pool, first_seg, c);
+        const Segment& g_ = pool->seg[s_];
+        depth_ = g_.depth;
+        const int ppc_ = min(cmax / (n - depth_), v2_ppc_cap(N));
+        p0_ = (c - g_.chunk_base) * ppc_;
+        np_ = (int)(g_.count - p0_ < ppc_ ? g_.count - p0_ : ppc_);
+    };
+    auto prefetch = [&](int64_t c) {  // global loads of chunk c's parents into registers
+        if (c >= c_end) return;
+        int s_, depth_, np_;
+        int64_t p0_;
+        chunk_geo(c, s_, depth_, np_, p0_);
+        const Segment& g_ = pool->seg[s_];
+#pragma unroll
+        for (int u = 0; u < kPfPre; ++u) {
+            const int x = tid + u * 192;
+            if (x < np_ * depth_) {
+                const int pp = x / depth_, i = x - pp * depth_;
+                pf_pre[u] = g_.src.prefix[(g_.first + g_.step * (p0_ + pp)) * n + i];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kPfHead; ++u) {
+            const int x = tid + u * 192;
+            if (x < np_ * M) {
+                const int pp = x / M, k = x - pp * M;
+                pf_head[u] = g_.src.heads[(g_.first + g_.step * (p0_ + pp)) * M + k];
+            }
+        }
+        if (tid < np_) pf_mask = g_.src.masks[(g_.first + g_.step * (p0_ + tid)) * W];
+    };
+    int64_t chunk = claim_chunk(rs, c_begin, s_slot);
+    if constexpr (kPipe) prefetch(chunk);
+    while (chunk < c_end) {
+        int s, depth, np;
+        int64_t p0;
+        chunk_geo(chunk, s, depth, np, p0);
         const Segment& sg = pool->seg[s];
-        const int depth = sg.depth;
         const int r = n - depth;
-        const int ppc = min(cmax / r, v2_ppc_cap(N));
-        const int64_t p0 = (chunk - sg.chunk_base) * ppc;
-        const int np = (int)(sg.count - p0 < ppc ? sg.count - p0 : ppc);
         const int nc = np * r;
-        const NodeStore src = sg.src;
-        const int64_t first = sg.first, step = sg.step;
-        // every global read of the parents happens before this chunk publishes
-        for (int x = tid; x < np * depth; x += bd) {
-            int pp = x / depth, i = x - pp * depth;
-            s_pre[pp * RW + i] = src.prefix[(first + step * (p0 + pp)) * n + i];
-        }
         const uint64_t valid = n >= 64 ? ~0ull : ((1ull << n) - 1ull);
-        for (int pp = tid; pp < np; pp += bd) {
-            int64_t node = first + step * (p0 + pp);
-            s_um[pp] = ~src.masks[node * W] & valid;
-        }
-        for (int x = tid; x < np * M; x += bd) {
-            int pp = x / M, k = x - pp * M;
-            s_R[x] = src.heads[(first + step * (p0 + pp)) * M + k];
+        if constexpr (kPipe) {
+#pragma unroll
+            for (int u = 0; u < kPfPre; ++u) {
+                const int x = tid + u * 192;
+                if (x < np * depth) {
+                    const int pp = x / depth, i = x - pp * depth;
+                    s_pre[pp * RW + i] = (uint8_t)pf_pre[u];
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < kPfHead; ++u) {
+                const int x = tid + u * 192;
+                if (x < np * M) s_R[x] = pf_head[u];
+            }
+            if (tid < np) s_um[tid] = ~pf_mask & valid;
+        } else {
+            const NodeStore src = sg.src;
+            const int64_t first = sg.first, step = sg.step;
+            for (int x = tid; x < np * depth; x += bd) {
+                int pp = x / depth, i = x - pp * depth;
+                s_pre[pp * RW + i] = src.prefix[(first + step * (p0 + pp)) * n + i];
+            }
+            for (int pp = tid; pp < np; pp += bd) {
+                int64_t node = first + step * (p0 + pp);
+                s_um[pp] = ~src.masks[node * W] & valid;
+            }
+            for (int x = tid; x < np * M; x += bd) {
+                int pp = x / M, k = x - pp * M;
+                s_R[x] = src.heads[(first + step * (p0 + pp)) * M + k];
+            }
         }
         __syncthreads();
+        if (kPipe && tid == 0) *s_slot = c_begin + (int64_t)atomicAdd(&rs->ticket, 1u);  // next chunk
         // per parent and job code: byte offset of the job's child row in Mq relative to
         // the parent's first child row (rank of the job among U), or of the dummy row
         // for a scheduled / absent job
@@ -371,6 +431,11 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
             s_amin[x] = (uint8_t)am;
         }
         __syncthreads();  // rank table and per-machine terms visible to every lane
+        int64_t next_chunk = 0;
+        if constexpr (kPipe) {
+            next_chunk = *s_slot;
+            prefetch(next_chunk);
+        }
         // ---- Phase A: forward / backward max-plus scans of pair q over parent pp
         if (a_lane && kDual16) {
             const int slot_q = kSlotOf<M>.s[q];
@@ -531,6 +596,12 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
             for (int i = 0; i < depth; ++i) dp[i] = s_pre[mypp * RW + i];
             dp[depth] = (uint8_t)myx;
             out.lb[o] = mylb;
+        }
+        if constexpr (kPipe) {
+            __syncthreads();  // this chunk's staging arrays fully consumed
+            chunk = next_chunk;
+        } else {
+            chunk = claim_chunk(rs, c_begin, s_slot);
         }
     }
 }
