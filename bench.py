@@ -418,51 +418,101 @@ def bound_stress(args, inst_name):
 
 
 def exhaust(args, inst_name):
-    """Time-to-explore: the frozen-UB exploration from the root run to exhaustion on one GPU
+    """Time-to-explore: the frozen-UB exploration from the root run to exhaustion
     (resolve_workload, bench.hpp:63-114, with the pending tree in HBM).  With UB = opt + 1
     the run finds an optimal schedule's makespan and proves that nothing better exists
-    (BASELINE configs[0]'s 'full B&B to optimality' for an instance whose tree fits)."""
+    (BASELINE configs[0]'s 'full B&B to optimality' for an instance whose tree fits).
+    N > 1 (torchrun): each rank starts from its split_slices share of the first round's
+    frontier and the ranks rebalance their pending trees (parallel.ParallelExplorer)
+    until every rank is empty; the explore time is the max over ranks."""
     import torch
 
+    rank, world, local = dist_env()
+    dev = local if world > 1 and not os.environ.get("FBB_SAME_GPU") else 0
+    torch.cuda.set_device(dev)
+    backend = os.environ.get("FBB_DIST_BACKEND", "nccl")
+    coll_dev = f"cuda:{dev}" if backend == "nccl" else "cpu"
+    if world > 1:
+        import torch.distributed as dist
+
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
     import paper_1206_4973_b200 as fbb
 
-    torch.cuda.set_device(0)
     n, m, seed, ub0 = INSTANCES[inst_name]
     ub = args.ub if args.ub is not None else ub0 + 1
     inst = fbb.generate_instance(n, m, seed)
-    ctx = fbb.Context(inst, 0)
+    ctx = fbb.Context(inst, dev)
     ctx.explorer_reset(fbb.NodeBatch.root(inst), ub, frozen=True)
-    sampler = ClockSampler(0) if not os.environ.get("FBB_NO_CLOCKS") else None
+    root_round = []
+    if world > 1:  # the root round on every rank (deterministic), then split its frontier
+        root_round = ctx.explorer_run([args.target], 1)
+        frontier = ctx.explorer_pending()
+        off, ln = fbb.split_slices(len(frontier), world)[rank]
+        ctx.explorer_reset(fbb.nodes_from_prefixes(inst, frontier[off:off + ln]), ub, frozen=True)
+    sampler = ClockSampler(dev) if rank == 0 and not os.environ.get("FBB_NO_CLOCKS") else None
+    if world > 1:
+        torch.distributed.barrier()
     t0 = time.perf_counter()
-    dev_ms, rounds, chunk = 0.0, 0, 2000
-    while True:
-        r, t = ctx.explorer_run([args.target], chunk, timing=True)
-        dev_ms += sum(x["round_ms"] for x in t)
-        rounds += len(r)
-        st = ctx.explorer_state()
-        if st["pending"] == 0 or time.perf_counter() - t0 > args.max_seconds:
-            break
+    dev_ms, rounds, transfers = 0.0, 0, 0
+    if world == 1:
+        while True:
+            r, t = ctx.explorer_run([args.target], 2000, timing=True)
+            dev_ms += sum(x["round_ms"] for x in t)
+            rounds += len(r)
+            if ctx.explorer_state()["pending"] == 0 or time.perf_counter() - t0 > args.max_seconds:
+                break
+    else:
+        from paper_1206_4973_b200.parallel import DevicePort, ParallelExplorer
+
+        px = ParallelExplorer(DevicePort(ctx, frozen=True), n, device=coll_dev, balance_every=4)
+        while px.step(args.target):
+            if px.port.last_timing:
+                dev_ms += px.port.last_timing["round_ms"]
+            if time.perf_counter() - t0 > args.max_seconds:
+                break
+        rounds, transfers = len(px.res.rounds), px.res.transfers
     wall = time.perf_counter() - t0
     clocks = sampler.result() if sampler else None
     st = ctx.explorer_state()
-    done = st["pending"] == 0
-    line = {
-        "metric": METRIC, "value": st["bounded"] / wall, "unit": "bounded subproblems/s",
-        "n_gpus": 1, "steps": rounds, "warmup": 0, "ms_per_step": 1e3 * wall / max(1, rounds),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
-        "data": "synthetic (Taillard generator, published seed; no dataset)",
-        "config": {"workload": f"{inst_name} {n}x{m} exhaustive frozen-UB exploration from the "
-                               f"root at UB {ub}, pool target {args.target}",
-                   "instance": inst_name, "ub": ub, "pool_target": args.target},
-        "explore_seconds": wall, "device_seconds": dev_ms / 1e3, "exhausted": done,
-        "bounded": st["bounded"], "branched": st["branched"], "pruned": st["pruned"],
-        "leaves": st["leaves"], "best_leaf": st["incumbent"] if st["found"] else None,
-        "proof": (f"optimum {st['incumbent']}: no complete schedule below it exists"
-                  if done and st["found"] else
-                  f"no schedule below {ub}" if done else "time cap reached"),
-        "clocks": clocks, "gpu_launches": rounds * 2,
-    }
-    print(json.dumps(line), flush=True)
+    best_mine = st["incumbent"] if st["found"] else 2**31 - 1
+    tot = torch.tensor([st["bounded"], st["branched"], st["pruned"], st["leaves"], st["pending"]],
+                       dtype=torch.int64, device=coll_dev)
+    mx = torch.tensor([wall, dev_ms / 1e3], dtype=torch.float64, device=coll_dev)
+    best = torch.tensor([best_mine], dtype=torch.int64, device=coll_dev)
+    if world > 1:
+        torch.distributed.all_reduce(tot, op=torch.distributed.ReduceOp.SUM)
+        torch.distributed.all_reduce(mx, op=torch.distributed.ReduceOp.MAX)
+        torch.distributed.all_reduce(best, op=torch.distributed.ReduceOp.MIN)
+    bounded, branched, pruned, leaves, pending = (int(x) for x in tot.cpu().tolist())
+    bounded += sum(r[2] for r in root_round)
+    wall_max, dev_max = (float(x) for x in mx.cpu().tolist())
+    found = int(best.item()) < 2**31 - 1
+    done = pending == 0
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": bounded / wall_max, "unit": "bounded subproblems/s",
+            "n_gpus": world, "steps": rounds, "warmup": 0,
+            "ms_per_step": 1e3 * wall_max / max(1, rounds), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic (Taillard generator, published seed; no dataset)",
+            "config": {"workload": f"{inst_name} {n}x{m} exhaustive frozen-UB exploration from "
+                                   f"the root at UB {ub}, pool target {args.target} per GPU",
+                       "instance": inst_name, "ub": ub, "pool_target": args.target,
+                       "parallelism": f"dp{world}" + (" (pending-tree rebalancing)" if world > 1 else "")},
+            "explore_seconds": wall_max, "device_seconds": dev_max, "exhausted": done,
+            "bounded": bounded, "branched": branched, "pruned": pruned, "leaves": leaves,
+            "nodes_moved_between_gpus": transfers, "best_leaf": int(best.item()) if found else None,
+            "proof": (f"optimum {int(best.item())}: no complete schedule below it exists"
+                      if done and found else
+                      f"no schedule below {ub}" if done else "time cap reached"),
+            "clocks": clocks, "gpu_launches": rounds * 2,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
 
 
 def main():
