@@ -186,6 +186,11 @@ struct fbb_ctx {
     DBuf d_pool, d_round;   // Pool, RoundState
     HBuf h_pool, h_round;
     cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    // batched device-planned explorer loop (explorer_loop.cu)
+    DBuf d_loop;
+    HBuf h_loop;
+    std::vector<cudaEvent_t> loop_ev;  // 4 per round of a batch
+    bool device_loop = false;          // FBB_DEVICE_LOOP=1: batched device-planned rounds
     float last_k2_ms = 0.f, last_round_ms = 0.f, last_sync_ms = 0.f;
     int last_launches = 0;
 
@@ -297,6 +302,9 @@ int run_pool(fbb_ctx* ctx, Pool& pool, int first_internal, int32_t ub, int froze
     CK(ctx->d_round.ensure(sizeof(RoundState)), "round state");
     CK(ctx->h_round.ensure(sizeof(RoundState)), "round state");
 
+    pool.ub = ub;  // the round's bound, semantics and first internal segment travel with the pool
+    pool.frozen = frozen;
+    pool.first_internal = first_internal;
     size_t pool_bytes = offsetof(Pool, seg) + (size_t)pool.nseg * sizeof(Segment);
     std::memcpy(ctx->h_pool.p, &pool, pool_bytes);
     int launches = 0;
@@ -616,6 +624,139 @@ int explorer_round(fbb_ctx* ctx, int64_t target, fbb_round_t* rec) {
     return FBB_OK;
 }
 
+// Rounds planned and closed on the device (explorer_loop.cu), up to kLoopMax per batch
+// with no host synchronisation inside a batch; same semantics and per-round records as
+// explorer_round.  Used when the parents can be read in place (HBM buckets, or host
+// buckets read and written through the mapping).
+bool device_loop_ok(const fbb_ctx* ctx) {
+    return ctx->device_loop && (!ctx->host_pending || (ctx->mapped_in && ctx->mapped_out));
+}
+
+int explorer_run_batched(fbb_ctx* ctx, const int64_t* targets, int ntargets, int64_t max_rounds,
+                         int64_t budget, fbb_round_t* rounds, int64_t* done) {
+    const int n = ctx->dt.n;
+    cudaStream_t st = ctx->stream;
+    int64_t r = 0;
+    if (done) *done = 0;
+    if ((int)ctx->loop_ev.size() < 4 * kLoopMax) {
+        ctx->loop_ev.resize(4 * kLoopMax, nullptr);
+        for (cudaEvent_t& e : ctx->loop_ev)
+            if (!e) CK(cudaEventCreate(&e), "event");
+    }
+    CK(ctx->d_loop.ensure(sizeof(LoopState)), "loop state");
+    CK(ctx->h_loop.ensure(sizeof(LoopState)), "loop state");
+    CK(ctx->d_pool.ensure(sizeof(Pool)), "pool");
+    CK(ctx->d_round.ensure(sizeof(RoundState)), "round state");
+    LoopState* hl = ctx->h_loop.as<LoopState>();
+    while (r < max_rounds) {
+        if (pending_total(ctx) == 0) break;
+        if (budget > 0 && ctx->tot_bounded >= budget) break;
+        const int R = (int)std::min<int64_t>(kLoopMax, max_rounds - r);
+        int64_t tmax = 1;
+        for (int i = 0; i < R; ++i) {
+            const int64_t ri = r + i;
+            tmax = std::max<int64_t>(tmax, targets[ri < ntargets ? ri : ntargets - 1]);
+        }
+        // staging for the largest pool of the batch: a chunk holds >= cmax/2 children
+        const int cmax = ctx->k2.cmax;
+        const int64_t chunks = 2 * tmax / cmax + n + 2;
+        CK(store_ensure(ctx, ctx->staging, chunks * cmax, 0), "staging");
+        CK(ctx->st_lb.ensure((size_t)chunks * cmax * 4), "staging");
+        CK(ctx->st_count.ensure((size_t)chunks * 4), "staging");
+        CK(ctx->st_seg.ensure((size_t)chunks * 4), "staging");
+        std::memset(hl, 0, offsetof(LoopState, rec));
+        for (int d = 0; d <= n; ++d) {
+            hl->cnt[d] = ctx->cnt[d];
+            hl->cap[d] = ctx->bucket[d].cap;
+            hl->bucket[d] = ctx->bucket[d].view();
+        }
+        for (int i = 0; i < R; ++i) {
+            const int64_t ri = r + i;
+            hl->targets[i] = targets[ri < ntargets ? ri : ntargets - 1];
+        }
+        hl->tot_bounded = ctx->tot_bounded;
+        hl->budget = budget;
+        hl->incumbent = ctx->incumbent;
+        hl->best = ctx->best;
+        hl->found = ctx->found;
+        hl->frozen = ctx->frozen;
+        hl->cmax = cmax;
+        hl->ppc_cap = ctx->k2.ppc_cap;
+        hl->nrounds = R;
+        for (int i = 0; i < n; ++i) hl->schedule[i] = ctx->schedule[i];
+        LoopState* dl = ctx->d_loop.as<LoopState>();
+        Pool* dp = ctx->d_pool.as<Pool>();
+        RoundState* rs = ctx->d_round.as<RoundState>();
+        ChunkOut out{ctx->staging.view(), ctx->st_lb.as<int32_t>(), ctx->st_count.as<int32_t>(),
+                     ctx->st_seg.as<int32_t>()};
+        const auto w0 = std::chrono::steady_clock::now();
+        CK(cudaMemcpyAsync(dl, hl, offsetof(LoopState, rec), cudaMemcpyHostToDevice, st), "loop H2D");
+        for (int i = 0; i < R; ++i) {
+            cudaEvent_t* ev = &ctx->loop_ev[4 * i];
+            CK(cudaEventRecord(ev[0], st), "event");
+            CK(launch_loop_plan(ctx->dt, dl, dp, rs, i, st), "plan");
+            CK(launch_round_device(ctx->dt, ctx->k2, dp, rs, out, st, ev[1], ev[2]), "round");
+            CK(launch_loop_close(ctx->dt, dl, dp, rs, i, st), "close");
+            CK(cudaEventRecord(ev[3], st), "event");
+        }
+        CK(cudaMemcpyAsync(hl, dl, sizeof(LoopState), cudaMemcpyDeviceToHost, st), "loop D2H");
+        const auto t_sync = std::chrono::steady_clock::now();
+        CK(cudaStreamSynchronize(st), "batch");
+        const auto w1 = std::chrono::steady_clock::now();
+        const float sync_ms = std::chrono::duration<float, std::milli>(w1 - t_sync).count();
+        const float wall_ms = std::chrono::duration<float, std::milli>(w1 - w0).count();
+        if (hl->stop == 4) return ctx->fail(FBB_E_STATE, "corrupt pending node (unscheduled-job count mismatch)");
+        int valid = 0;
+        while (valid < R && hl->rec[valid].valid) ++valid;
+        const int64_t nb = (int64_t)node_bytes(ctx);
+        for (int i = 0; i < valid; ++i) {
+            const LoopRecord& lr = hl->rec[i];
+            fbb_round_t rec;
+            std::memset(&rec, 0, sizeof(rec));
+            rec.target = lr.target;
+            rec.branched = lr.branched;
+            rec.bounded = lr.bounded;
+            rec.inserted = lr.inserted;
+            rec.pruned = lr.pruned;
+            rec.leaves = lr.leaves;
+            rec.incumbent = lr.incumbent;
+            rec.pending = lr.pending;
+            cudaEvent_t* ev = &ctx->loop_ev[4 * i];
+            cudaEventElapsedTime(&rec.k2_ms, ev[1], ev[2]);
+            cudaEventElapsedTime(&rec.round_ms, ev[0], ev[3]);
+            rec.launches = 6;
+            rec.host_ms = wall_ms / valid;
+            rec.sync_ms = sync_ms / valid;
+            rec.h2d_bytes = ctx->host_pending ? lr.branched * nb : 0;
+            rec.d2h_bytes = ctx->host_pending ? lr.inserted * nb : 0;
+            ctx->tot_branched += lr.branched;
+            ctx->tot_bounded += lr.bounded;
+            ctx->tot_pruned += lr.pruned;
+            ctx->tot_leaves += lr.leaves;
+            if (rounds) rounds[r] = rec;
+            ++r;
+        }
+        if (done) *done = r;
+        for (int d = 0; d <= n; ++d) ctx->cnt[d] = hl->cnt[d];
+        ctx->incumbent = hl->incumbent;
+        ctx->best = hl->best;
+        ctx->found = hl->found;
+        if (!ctx->frozen && hl->found)
+            for (int i = 0; i < n; ++i) ctx->schedule[i] = hl->schedule[i];
+        if (ctx->check) {
+            int rc2 = check_pending(ctx);
+            if (rc2 != FBB_OK) return rc2;
+        }
+        if (hl->stop == 3) {  // a destination bucket must grow before the next round
+            const int d = hl->need_depth;
+            CK(store_ensure(ctx, ctx->bucket[d], hl->need_rows, ctx->cnt[d]), "bucket grow");
+            continue;
+        }
+        if (hl->stop == 1 || hl->stop == 2) break;
+    }
+    return FBB_OK;
+}
+
 }  // namespace
 
 // =========================================================================================
@@ -680,7 +821,7 @@ fbb_ctx* fbb_create(int device, const int32_t* p, int n, int m) {
             }
         }
         for (DBuf* b : {&ctx->k1_masks, &ctx->k1_heads, &ctx->k1_depth, &ctx->k1_lb, &ctx->out_lb,
-                        &ctx->st_lb, &ctx->st_count, &ctx->st_seg, &ctx->d_pool, &ctx->d_round})
+                        &ctx->st_lb, &ctx->st_count, &ctx->st_seg, &ctx->d_pool, &ctx->d_round, &ctx->d_loop})
             b->st = ctx->stream;
         for (Store* st : {&ctx->batch_in, &ctx->batch_out, &ctx->staging, &ctx->parents})
             st->set(ctx->stream, nullptr);
@@ -714,6 +855,11 @@ fbb_ctx* fbb_create(int device, const int32_t* p, int n, int m) {
     }
     explorer_clear(ctx);
     ctx->incumbent = INT_MAX;
+    // Measured (r01): the device-planned loop costs more device time per round (plan /
+    // close kernels and fixed-grid launches) than the host planner saves; it stays
+    // opt-in (FBB_DEVICE_LOOP=1) and covered by the parity tests.
+    const char* dlp = getenv("FBB_DEVICE_LOOP");
+    ctx->device_loop = dlp && dlp[0] == '1';
     const char* chk = getenv("FBB_CHECK");
     ctx->check = chk && chk[0] == '1';
     return ctx;
@@ -739,6 +885,10 @@ void fbb_destroy(fbb_ctx* ctx) {
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     ctx->h_pool.release();
     ctx->h_round.release();
+    ctx->h_loop.release();
+    ctx->d_loop.release();
+    for (cudaEvent_t ev : ctx->loop_ev)
+        if (ev) cudaEventDestroy(ev);
     for (cudaEvent_t ev : ctx->ev)
         if (ev) cudaEventDestroy(ev);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -1035,6 +1185,7 @@ int fbb_explorer_run(fbb_ctx* ctx, const int64_t* targets, int ntargets, int64_t
     if (!ctx) return FBB_E_ARG;
     if (!targets || ntargets < 1) return ctx->fail(FBB_E_ARG, "need at least one target");
     cudaSetDevice(ctx->device);
+    if (device_loop_ok(ctx)) return explorer_run_batched(ctx, targets, ntargets, max_rounds, budget, rounds, done);
     int64_t r = 0;
     if (done) *done = 0;
     while (r < max_rounds) {

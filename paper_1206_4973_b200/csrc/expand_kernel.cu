@@ -124,6 +124,12 @@ __global__ void __launch_bounds__(128) k2_internal_kernel(DevTables t, const Poo
         s_tl[x] = t.tails[x];
     }
     // incumbent for internal children: min(UB, batch leaf minimum) unless frozen
+    // the round's bound, semantics and first internal segment come from the pool
+    // (written by the host, or by the device-side planner of the batched explorer loop)
+    ub = pool->ub;
+    frozen = pool->frozen;
+    first_seg = pool->first_internal;
+    if (first_seg >= pool->nseg) return;
     int32_t ub_eff = ub;
     if (!frozen) {
         unsigned long long inv = rs->leaf_inv;
@@ -326,6 +332,7 @@ __global__ void __launch_bounds__(128) k2_internal_kernel(DevTables t, const Poo
 __global__ void k2_leaf_kernel(DevTables t, const Pool* __restrict__ pool, int seg_index,
                                RoundState* rs) {
     const int n = t.n, m = t.m, W = t.W;
+    if (pool->nseg <= seg_index || pool->seg[seg_index].depth < n - 2) return;  // no leaves
     const Segment& sg = pool->seg[seg_index];
     const int depth = sg.depth;
     const int r = n - depth;
@@ -367,6 +374,11 @@ __global__ void k2_leaf_kernel(DevTables t, const Pool* __restrict__ pool, int s
 __global__ void leaf_schedule_kernel(DevTables t, const Pool* __restrict__ pool, RoundState* rs,
                                      int32_t ub) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    ub = pool->ub;
+    if (pool->nseg == 0 || pool->seg[0].depth < t.n - 2) {  // no leaves this round
+        rs->found = 0;
+        return;
+    }
     unsigned long long inv = rs->leaf_inv;
     unsigned long long key = ~inv;
     int32_t* schedule = rs->schedule;
@@ -425,6 +437,10 @@ __device__ __forceinline__ void copy_rows(int rows, int width, Load load, Store 
     }
 }
 
+// kGridStride: a fixed grid strides over the chunk groups (the device-planned loop, whose
+// pool size the host does not know); otherwise one group per CTA -- the plain form,
+// measurably faster (19 vs 26 us per 262K-child round) when the host sizes the grid.
+template <bool kGridStride>
 __global__ void __launch_bounds__(kPlaceThreads) place_kernel(DevTables t, const Pool* __restrict__ pool,
                                                               int cmax, RoundState* rs, ChunkOut out) {
     const int n = t.n, m = t.m, W = t.W;
@@ -437,7 +453,9 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(DevTables t, const
     extern __shared__ uint8_t s_rc[];          // chunk of each row (cmax * kPlaceChunks)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t nchunks = pool->nchunks;
-    const int64_t c0 = (int64_t)blockIdx.x * kPlaceChunks;
+    for (int64_t c0 = (int64_t)blockIdx.x * kPlaceChunks; c0 < nchunks;
+         c0 += kGridStride ? (int64_t)gridDim.x * kPlaceChunks : nchunks) {
+    if (kGridStride) __syncthreads();  // previous group's shared tables consumed
     const int nch = (int)(nchunks - c0 < kPlaceChunks ? nchunks - c0 : kPlaceChunks);
     const int s0 = out.seg[c0];
     const int64_t cb0 = pool->seg[s0].chunk_base;
@@ -527,6 +545,7 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(DevTables t, const
     if (s_dlb[0])  // all segments of a pool share dst_lb (set or not)
         copy_rows<kPlaceBatch>(R, 1, [&](int row, int) { return __ldg(out.lb + src_row(row)); },
                                [&](int row, int, int32_t v) { s_dlb[s_rc[row]][dst_row(row)] = v; });
+    }
 }
 
 }  // namespace
@@ -599,9 +618,41 @@ cudaError_t launch_place(const DevTables& t, const K2Config& cfg, const Pool* d_
                          const Pool& h_pool, RoundState* rs, ChunkOut out, cudaStream_t stream) {
     if (h_pool.nchunks == 0) return cudaSuccess;
     const int64_t blocks = (h_pool.nchunks + kPlaceChunks - 1) / kPlaceChunks;
-    place_kernel<<<(unsigned)blocks, kPlaceThreads, (size_t)cfg.cmax * kPlaceChunks, stream>>>(
+    place_kernel<false><<<(unsigned)blocks, kPlaceThreads, (size_t)cfg.cmax * kPlaceChunks, stream>>>(
         t, d_pool, cfg.cmax, rs, out);
     return cudaGetLastError();
 }
 
 }  // namespace fbb
+
+namespace fbb {
+
+// One round of the batched (device-planned) explorer loop: every kernel reads the
+// round's plan from the device Pool / RoundState and exits when it has nothing to do,
+// so the grids are fixed and nothing here needs the host.
+cudaError_t launch_round_device(const DevTables& t, const K2Config& cfg, const Pool* d_pool,
+                                RoundState* rs, ChunkOut out, cudaStream_t stream, cudaEvent_t k2_begin,
+                                cudaEvent_t k2_end) {
+    k2_leaf_kernel<<<148 * 4, 256, 0, stream>>>(t, d_pool, 0, rs);
+    leaf_schedule_kernel<<<1, 32, 0, stream>>>(t, d_pool, rs, 0);
+    if (k2_begin) cudaEventRecord(k2_begin, stream);
+    cudaError_t e;
+    if (cfg.variant >= 100000)
+        e = launch_k2_v3(t, cfg, d_pool, 0, cfg.blocks, 0, 0, rs, out, stream);
+    else if (cfg.variant != 0)
+        e = launch_k2_v2(t, cfg, d_pool, 0, cfg.blocks, 0, 0, rs, out, stream);
+    else if (cfg.jm_in_smem)
+        k2_internal_kernel<true><<<cfg.blocks, cfg.threads, cfg.smem, stream>>>(t, d_pool, 0, cfg.cmax, 0, 0,
+                                                                                rs, out);
+    else
+        k2_internal_kernel<false><<<cfg.blocks, cfg.threads, cfg.smem, stream>>>(t, d_pool, 0, cfg.cmax, 0, 0,
+                                                                                 rs, out);
+    if (k2_end) cudaEventRecord(k2_end, stream);
+    place_kernel<true><<<148 * 2, kPlaceThreads, (size_t)cfg.cmax * kPlaceChunks, stream>>>(t, d_pool, cfg.cmax, rs,
+                                                                                      out);
+    e = cudaGetLastError();
+    return e;
+}
+
+}  // namespace fbb
+

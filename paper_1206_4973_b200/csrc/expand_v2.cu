@@ -285,6 +285,12 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
     for (int x = tid; x < (int)((cmax + 1) * L.rowb / 16); x += bd)  // padding slots stay 0
         ((uint4*)s_Mq)[x] = make_uint4(0u, 0u, 0u, 0u);
 
+    // the round's bound, semantics and first internal segment come from the pool
+    // (written by the host, or by the device-side planner of the batched explorer loop)
+    ub = pool->ub;
+    frozen = pool->frozen;
+    first_seg = pool->first_internal;
+    if (first_seg >= pool->nseg) return;
     int32_t ub_eff = ub;
     if (!frozen) {
         unsigned long long inv = rs->leaf_inv;

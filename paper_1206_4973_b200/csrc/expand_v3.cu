@@ -142,6 +142,12 @@ __global__ void __launch_bounds__(NW <= 4 ? 192 : 256, NW <= 4 ? 3 : 2)
     const int G = bd / P;
     const int q = tid % P, g = tid / P;
 
+    // the round's bound, semantics and first internal segment come from the pool
+    // (written by the host, or by the device-side planner of the batched explorer loop)
+    ub = pool->ub;
+    frozen = pool->frozen;
+    first_seg = pool->first_internal;
+    if (first_seg >= pool->nseg) return;
     int32_t ub_eff = ub;
     if (!frozen) {
         unsigned long long inv = rs->leaf_inv;

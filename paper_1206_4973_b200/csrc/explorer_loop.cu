@@ -1,0 +1,173 @@
+// explorer_loop.cu -- the explorer round planned and closed on the device, so that a
+// batch of rounds runs back to back without the host (fbb_explorer_run).
+//
+//   plan  (1 thread)   fill_buffer (search.hpp:64-73) on the bucket sizes: pop the
+//                      deepest bucket tops, LIFO, until the children reach the target;
+//                      lay out segments and chunks exactly as the host planner does
+//                      (capi.cu layout_pool); point each segment at its source and
+//                      destination buckets; reset the round state.
+//   round              leaves, leaf schedule, K2, place (expand_kernel.cu)
+//   close (1 thread)   integrate / frozen prune bookkeeping (search.hpp:84-107,
+//                      bench.hpp:96-106): bucket sizes, incumbent and schedule, the
+//                      round's counters, stop conditions (empty tree, node budget).
+// A round whose destination bucket is too small is not started: the batch stops with
+// stop = 3 and the host grows that bucket and resumes, so device buckets never
+// reallocate inside a batch.
+#include "fbb_internal.h"
+
+namespace fbb {
+
+namespace {
+
+__global__ void loop_plan_kernel(DevTables t, LoopState* ls, Pool* pool, RoundState* rs, int round) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const int n = t.n;
+    pool->nseg = 0;
+    pool->nchunks = 0;
+    pool->nchildren = 0;
+    rs->leaf_inv = 0ull;
+    rs->found = 0;
+    rs->ticket = 0u;
+    rs->total = 0;
+    pool->ub = ls->incumbent;
+    pool->frozen = ls->frozen;
+    pool->first_internal = 0;
+    if (ls->stop || round >= ls->nrounds) return;
+    const int64_t target = ls->targets[round] < 1 ? 1 : ls->targets[round];
+    // fill_buffer on the sizes (deepest bucket first, LIFO, until >= target)
+    int64_t have = 0;
+    int nseg = 0;
+    for (int d = n; d >= 0 && have < target; --d) {
+        const int64_t c = ls->cnt[d];
+        if (c == 0) continue;
+        const int r = n - d;
+        const int64_t k = min(c, (target - have + r - 1) / r);
+        Segment& sg = pool->seg[nseg++];
+        sg.src = ls->bucket[d];
+        sg.first = c - 1;
+        sg.step = -1;
+        sg.count = k;
+        sg.depth = d;
+        sg.pad = 0;
+        sg.dst_lb = nullptr;
+        have += k * r;
+    }
+    if (nseg == 0) {
+        ls->stop = 1;
+        return;
+    }
+    // destinations: bucket d+1 after this round's pops; all sizes checked first
+    for (int s = 0; s < nseg; ++s) {
+        Segment& sg = pool->seg[s];
+        const int d = sg.depth;
+        if (d >= n - 2) {
+            sg.dst = NodeStore{nullptr, nullptr, nullptr};
+            sg.dst_base = 0;
+            continue;
+        }
+        int64_t after = ls->cnt[d + 1];
+        for (int s2 = 0; s2 < s; ++s2)
+            if (pool->seg[s2].depth == d + 1) after -= pool->seg[s2].count;
+        const int64_t worst = after + sg.count * (n - d);
+        if (worst > ls->cap[d + 1]) {
+            ls->stop = 3;
+            ls->need_depth = d + 1;
+            ls->need_rows = worst;
+            return;  // nseg stays 0: nothing of this round runs
+        }
+        sg.dst = ls->bucket[d + 1];
+        sg.dst_base = after;
+    }
+    // chunk layout (capi.cu layout_pool)
+    const int cmax = ls->cmax;
+    int64_t child = 0, chunk = 0;
+    int first_internal = nseg;
+    for (int s = 0; s < nseg; ++s) {
+        Segment& sg = pool->seg[s];
+        const int r = n - sg.depth;
+        sg.child_base = child;
+        child += sg.count * r;
+        sg.chunk_base = chunk;
+        if (sg.depth >= n - 2) continue;
+        if (first_internal == nseg) first_internal = s;
+        const int ppc = parents_per_chunk(n, sg.depth, cmax, ls->ppc_cap);
+        chunk += (sg.count + ppc - 1) / ppc;
+    }
+    for (int s = 0; s < nseg; ++s) rs->seg_surv[s] = 0;
+    pool->first_internal = first_internal;
+    pool->nchunks = chunk;
+    pool->nchildren = child;
+    pool->pad = 0;
+    pool->nseg = nseg;
+}
+
+__global__ void loop_close_kernel(DevTables t, LoopState* ls, const Pool* pool, const RoundState* rs,
+                                  int round) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const int n = t.n;
+    LoopRecord& rec = ls->rec[round];
+    rec.valid = 0;
+    if (pool->nseg == 0) return;  // stopped before this round
+    if (rs->found < 0) {          // corrupt pending node (leaf kernel's check)
+        ls->stop = 4;
+        return;
+    }
+    int64_t branched = 0, internal = 0, leaves = 0;
+    for (int s = 0; s < pool->nseg; ++s) {
+        const Segment& sg = pool->seg[s];
+        const int64_t kids = sg.count * (n - sg.depth);
+        branched += sg.count;
+        ls->cnt[sg.depth] -= sg.count;  // pops (the bucket tops)
+        if (sg.depth >= n - 2) leaves += kids;
+        else internal += kids;
+    }
+    for (int s = 0; s < pool->nseg; ++s) {  // pushes, batch order
+        const Segment& sg = pool->seg[s];
+        if (sg.depth < n - 2) ls->cnt[sg.depth + 1] += rs->seg_surv[s];
+    }
+    if (leaves > 0 && rs->leaf_inv != 0ull) {
+        const int32_t v = (int32_t)((~rs->leaf_inv) >> 32);
+        if (ls->frozen) {
+            if (v < ls->incumbent && (!ls->found || v < ls->best)) {  // bench.hpp:99-102
+                ls->best = v;
+                ls->found = 1;
+            }
+        } else if (v < ls->incumbent) {  // search.hpp:93-99
+            ls->incumbent = v;
+            ls->best = v;
+            ls->found = 1;
+            if (rs->found > 0)
+                for (int i = 0; i < n; ++i) ls->schedule[i] = rs->schedule[i];
+        }
+    }
+    int64_t pending = 0;
+    for (int d = 0; d <= n; ++d) pending += ls->cnt[d];
+    rec.target = ls->targets[round];
+    rec.branched = branched;
+    rec.bounded = internal + leaves;
+    rec.inserted = rs->total;
+    rec.pruned = internal - rs->total;
+    rec.leaves = leaves;
+    rec.pending = pending;
+    rec.incumbent = ls->frozen ? (ls->found ? ls->best : ls->incumbent) : ls->incumbent;
+    rec.valid = 1;
+    ls->tot_bounded += internal + leaves;
+    if (pending == 0) ls->stop = 1;
+    else if (ls->budget > 0 && ls->tot_bounded >= ls->budget) ls->stop = 2;
+}
+
+}  // namespace
+
+cudaError_t launch_loop_plan(const DevTables& t, LoopState* ls, Pool* pool, RoundState* rs, int round,
+                             cudaStream_t stream) {
+    loop_plan_kernel<<<1, 32, 0, stream>>>(t, ls, pool, rs, round);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_loop_close(const DevTables& t, LoopState* ls, const Pool* pool, const RoundState* rs,
+                              int round, cudaStream_t stream) {
+    loop_close_kernel<<<1, 32, 0, stream>>>(t, ls, pool, rs, round);
+    return cudaGetLastError();
+}
+
+}  // namespace fbb

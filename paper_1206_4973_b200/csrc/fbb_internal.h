@@ -129,6 +129,10 @@ struct Pool {
     int pad;             // always 0 (an opaque zero for the kernels)
     int64_t nchunks;
     int64_t nchildren;
+    int32_t ub;          // pruning bound of the round (the incumbent, or the frozen UB)
+    int32_t frozen;      // resolve (1) or solve (0) semantics
+    int32_t first_internal;  // first segment with internal children (nseg: none)
+    int32_t pad2;
     Segment seg[kMaxSegments];
 };
 
@@ -193,8 +197,41 @@ cudaError_t launch_place(const DevTables& t, const K2Config& cfg, const Pool* d_
 cudaError_t launch_leaf_schedule(const DevTables& t, const Pool* d_pool, RoundState* rs,
                                  int32_t ub, cudaStream_t stream);
 
+// ---- batched explorer loop (explorer_loop.cu): rounds planned and closed on the device --
+constexpr int kLoopMax = 64;  // rounds per batch
+
+struct LoopRecord {  // one round's counters (search.hpp:21-26, 75-79)
+    int64_t target, branched, bounded, inserted, pruned, leaves, pending;
+    int32_t incumbent, valid;
+};
+
+// Device-resident explorer state for a batch of rounds.  The host writes the head
+// (everything before `rec`) before a batch and reads the whole struct back after it.
+struct LoopState {
+    int64_t cnt[kMaxJobs + 1];        // pending bucket sizes
+    int64_t cap[kMaxJobs + 1];        // their capacities (rows)
+    NodeStore bucket[kMaxJobs + 1];   // their storage (HBM, or device-mapped host memory)
+    int64_t targets[kLoopMax];        // pool target of each round of the batch
+    int64_t tot_bounded, budget;      // cumulative bounded count; stop when >= budget (> 0)
+    int32_t incumbent, best, found, frozen;
+    int32_t stop;                     // 0 running, 1 pending empty, 2 budget, 3 bucket too small
+    int32_t need_depth;               // stop == 3: the bucket that must grow ...
+    int64_t need_rows;                // ... to at least this many rows
+    int32_t cmax, ppc_cap, nrounds, pad;
+    int32_t schedule[kMaxJobs];       // incumbent schedule (solve mode)
+    LoopRecord rec[kLoopMax];
+};
+
+cudaError_t launch_loop_plan(const DevTables& t, LoopState* ls, Pool* pool, RoundState* rs, int round,
+                             cudaStream_t stream);
+cudaError_t launch_loop_close(const DevTables& t, LoopState* ls, const Pool* pool, const RoundState* rs,
+                              int round, cudaStream_t stream);
+cudaError_t launch_round_device(const DevTables& t, const K2Config& cfg, const Pool* d_pool,
+                                RoundState* rs, ChunkOut out, cudaStream_t stream, cudaEvent_t k2_begin,
+                                cudaEvent_t k2_end);
+
 // Chunk geometry of a segment: parents per chunk.
-inline int parents_per_chunk(int n, int depth, int cmax, int ppc_cap) {
+__host__ __device__ inline int parents_per_chunk(int n, int depth, int cmax, int ppc_cap) {
     int r = n - depth;
     int ppc = r > 0 ? cmax / r : 1;
     return ppc_cap > 0 && ppc > ppc_cap ? ppc_cap : ppc;

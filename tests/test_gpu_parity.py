@@ -332,3 +332,28 @@ def test_k2_generic_and_specialised_agree(monkeypatch):
             outs.append((surv.prefixes(), list(slb), counts, s2.prefixes(), list(l2)))
             ctx.close()
         assert outs[0] == outs[1], (n, m)
+
+
+@pytest.mark.parametrize("on_host", [False, True], ids=["pending_hbm", "pending_host"])
+def test_device_planned_loop_matches_reference(instances, traces, on_host, monkeypatch):
+    """The batched, device-planned explorer loop (FBB_DEVICE_LOOP=1) reproduces the
+    reference's per-round traces like the host-planned one."""
+    monkeypatch.setenv("FBB_DEVICE_LOOP", "1")
+    for tr in traces["resolve"][:4]:
+        inst = inst_of(instance_p(instances, tr["instance"]))
+        ctx = fbb.Context(inst)  # a fresh context picks up the environment
+        ctx.explorer_set_residency(on_host)
+        ctx.explorer_reset(fbb.nodes_from_prefixes(inst, tr["roots"]), tr["ub"], frozen=True)
+        rounds = ctx.explorer_run(tr["targets"], 1 << 20, tr["budget"])
+        assert rounds == [tuple(r) for r in tr["rounds"]], tr["instance"]
+        ctx.close()
+    for case in traces["solve_full"][:5]:
+        p = np.asarray(case["p"], np.int32).reshape(case["n"], case["m"])
+        ctx = fbb.Context(inst_of(p))
+        ctx.explorer_set_residency(on_host)
+        r0 = ctx.explorer_start_solve(None)
+        rounds = ctx.explorer_run([case["batch"]], 1 << 20)
+        st = ctx.explorer_state()
+        assert [r0] + rounds == [tuple(r) for r in case["rounds"]]
+        assert st["incumbent"] == case["optimum"] and st["schedule"] == case["schedule"]
+        ctx.close()
