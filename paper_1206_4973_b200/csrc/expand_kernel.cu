@@ -414,7 +414,10 @@ __global__ void leaf_schedule_kernel(DevTables t, const Pool* __restrict__ pool,
 // of all earlier chunks (a few thousand L2-resident ints, kPlaceBatch
 // independent loads per thread), so no scan pass or grid-wide fence is needed.
 // Rows are copied flat (one thread per 4-byte head, mask word or prefix byte).
-constexpr int kPlaceChunks = 8;
+#ifndef FBB_PLACE_CHUNKS
+#define FBB_PLACE_CHUNKS 8
+#endif
+constexpr int kPlaceChunks = FBB_PLACE_CHUNKS;
 constexpr int kPlaceThreads = 256;
 constexpr int kPlaceBatch = 8;
 

@@ -1,0 +1,31 @@
+"""Small workloads for compute-sanitizer (memcheck / racecheck / synccheck): every kernel
+path -- K1 v1/v2, K2 v2 (both occupancies), v3, generic, leaves, place, the explorer
+with its tree in HBM and in host memory, and the device-planned loop -- on inputs
+small enough for the sanitizer, each checked against the oracle."""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+
+import paper_1206_4973_b200 as fbb
+from oracle import Oracle
+
+orc = Oracle()
+rng = np.random.default_rng(1)
+for n, m in [(20, 20), (20, 5), (50, 20), (100, 20), (12, 7)]:
+    p = rng.integers(1, 100, size=(n, m)).astype(np.int32)
+    inst = fbb.Instance(n, m, p)
+    ctx = fbb.Context(inst)
+    pre = [list(rng.permutation(n)[: rng.integers(0, n + 1)]) for _ in range(64)]
+    nodes = fbb.nodes_from_prefixes(inst, pre)
+    assert np.array_equal(ctx.bound(nodes), orc.evaluate_batch(p, nodes.masks, nodes.heads, nodes.depth))
+    par = sorted([list(rng.permutation(n)[: rng.integers(0, n - 2)]) for _ in range(24)], key=len,
+                 reverse=True)
+    surv, slb, *_ = ctx.expand_bound_prune(fbb.nodes_from_prefixes(inst, par), 10**6, frozen=True)
+    for on_host in (False, True):
+        ctx.explorer_set_residency(on_host)
+        ctx.explorer_reset(fbb.NodeBatch.root(inst), 10**6, frozen=True)
+        ctx.explorer_run([2048], 3)
+    ctx.close()
+    print("ok", n, m, flush=True)
