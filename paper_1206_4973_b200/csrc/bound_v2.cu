@@ -14,6 +14,8 @@
 // into the node's bound with one shared atomicMax per warp.  The one-machine terms
 // (bound.hpp:61-74) come from warp reductions over the unscheduled jobs.
 #include <climits>
+#include <cstdlib>
+#include <string>
 
 #include "fbb_internal.h"
 
@@ -73,7 +75,26 @@ __global__ void __launch_bounds__(kK1Threads) k1v2_kernel(DevTables t, const uin
             s_lb[x] = 0;
         }
         __syncthreads();
-        // ---- one-machine terms: a warp per (node, machine), lanes over the jobs
+        // ---- one-machine terms: for n <= 64 a thread per (node, machine) walking the
+        // unscheduled jobs; beyond, a warp per item with lanes over the jobs
+        if (NW <= 2) {
+            for (int x = tid; x < tn * m; x += kK1Threads) {
+                const int tt = x / m, kk = x - tt * m;
+                int32_t load = 0, mt = INT_MAX;
+                for (int w = 0; w < NW; ++w) {
+                    uint32_t u = ~s_sched[tt * NW + w];
+                    while (u) {
+                        const int j = 32 * w + __ffs(u) - 1;
+                        u &= u - 1;
+                        load += __ldg(t.p + j * m + kk);
+                        mt = min(mt, __ldg(t.tails + j * m + kk));
+                    }
+                }
+                const int32_t lc = mt == INT_MAX ? 0 : load + mt;
+                s_Lc[x] = lc;
+                if (s_dep[tt] < n) atomicMax(&s_lb[tt], s_R[x] + lc);
+            }
+        } else
         for (int x = warp; x < tn * m; x += nwarps) {
             const int tt = x / m, kk = x - tt * m;
             int32_t load = 0, mt = INT_MAX;
@@ -171,9 +192,9 @@ int k1v2_blocks(const DevTables& t, int device) {
 }  // namespace
 
 bool k1v2_config(const DevTables& t, int device, K1Config* out) {
-    // Measured (profiles/r01_reading.md): the row-sweep kernel wins for n > 64 (200x20:
-    // 43-47 vs 31 M nodes/s); for n <= 64 the smem-table kernel is faster.
-    if (!t.rowpk || t.m > 20 || t.m < 2 || t.n > 256 || t.n <= 64) return false;
+    // Measured (r01, bound-only pools): v2 beats the smem-table v1 on every class --
+    // 20x20 497 vs 354, 20x5 5626 vs 4837, 50x20 191 vs 128, 100x20 80 vs 65 M nodes/s.
+    if (!t.rowpk || t.m > 20 || t.m < 2 || t.n > 256) return false;
     K1Config c;
     c.threads = kK1Threads;
     c.tile = k1v2_tile(t.P);

@@ -59,6 +59,8 @@ __host__ __device__ inline int v2_row_bytes(int m) {
     return b * 16;
 }
 
+__host__ __device__ inline int v2_dummy_rows(int P) { return 2 * (192 / P > 0 ? 192 / P : 1); }
+
 struct V2Layout {
     size_t row, um, rank, R, load, mins, amin, Mq, p, tl, pre, wsum, total;
     int ppc_max, rowb;
@@ -84,7 +86,9 @@ __host__ __device__ inline V2Layout v2_layout(int n, int m, int P, int cmax, int
     L.load = o; o = b16(o + (size_t)L.ppc_max * m * 4);
     L.mins = o; o = b16(o + (size_t)L.ppc_max * m * 4);  // min1 | min2 << 16
     L.amin = o; o = b16(o + (size_t)L.ppc_max * m);
-    L.Mq = o;   o = b16(o + (size_t)(cmax + 1) * L.rowb);  // + a dummy row for non-members
+    // + dummy rows for non-members: one per parent processed at the same time (two per
+    // parent lane, 192 / P lanes), so concurrent garbage stores never share an address
+    L.Mq = o;   o = b16(o + (size_t)(cmax + v2_dummy_rows(P)) * L.rowb);
     L.p = o;    o = b16(o + (size_t)n * m * 4);
     L.tl = o;   o = b16(o + (size_t)n * m * 2);  // tails as int16
     L.pre = o;  o = b16(o + (size_t)L.ppc_max * v2_rw(N));
@@ -282,7 +286,7 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
     }
     // 32-bit shared addresses: each scan step is one LDS [reg + immediate]
     const uint32_t row_sa = (uint32_t)__cvta_generic_to_shared(s_row + q);
-    for (int x = tid; x < (int)((cmax + 1) * L.rowb / 16); x += bd)  // padding slots stay 0
+    for (int x = tid; x < (int)((cmax + v2_dummy_rows(P)) * L.rowb / 16); x += bd)  // padding slots stay 0
         ((uint4*)s_Mq)[x] = make_uint4(0u, 0u, 0u, 0u);
 
     // the round's bound, semantics and first internal segment come from the pool
@@ -395,7 +399,7 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
             const int j = (idx & 32) | (31 - (idx & 31));
             const uint64_t um = s_um[pp];
             const bool in = j < n && ((um >> j) & 1ull);
-            const int row = in ? __popcll(um & ((1ull << j) - 1ull)) : cmax - pp * r;
+            const int row = in ? __popcll(um & ((1ull << j) - 1ull)) : cmax + pp % v2_dummy_rows(P) - pp * r;
             s_off[x] = (uint16_t)(row * L.rowb);
         }
         // per (parent, machine): load, two smallest tails (+ argmin, smallest job on ties)

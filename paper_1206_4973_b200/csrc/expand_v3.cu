@@ -56,7 +56,9 @@ __host__ __device__ inline V3Layout v3_layout(int m, int P, int cmax, int thread
     L.load = o; o = c16(o + (size_t)kV3Ppc * m * 4);
     L.mins = o; o = c16(o + (size_t)kV3Ppc * m * 4);  // min1 | min2 << 16
     L.amin = o; o = c16(o + (size_t)kV3Ppc * m);
-    L.Mq = o;   o = c16(o + (size_t)(cmax + 1) * L.rowb);  // + a dummy row for scheduled jobs
+    // + dummy rows for scheduled jobs, one per parent lane (threads / P), so concurrent
+    // read-modify-writes of garbage never share an address
+    L.Mq = o;   o = c16(o + (size_t)(cmax + threads / P) * L.rowb);
     L.pre = o;  o = c16(o + (size_t)kV3Ppc * N);
     L.wsum = o; o = c16(o + (size_t)(threads / 32 + 2) * 8);
     L.total = o;
@@ -199,7 +201,7 @@ __global__ void __launch_bounds__(NW <= 4 ? 192 : 256, NW <= 4 ? 3 : 2)
                 s_slot16[x] = (uint16_t)(rk * L.rowb / 16);
                 s_ujob[pp * N + rk] = (uint8_t)j;
             } else {
-                s_slot16[x] = (uint16_t)(0x8000u | ((cmax - pp * r) * L.rowb / 16));
+                s_slot16[x] = (uint16_t)(0x8000u | ((cmax + pp % G - pp * r) * L.rowb / 16));
             }
         }
         // per (parent, machine): load and the two smallest tails, a warp per item
