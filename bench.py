@@ -728,7 +728,8 @@ def main():
         "bound": "int32-alu", "kernel": "k2_internal_kernel (fused expand+bound+prune)",
         "achieved": ops / k2_s / 1e9 if k2_s > 0 else 0.0, "peak": int_peak, "unit": "Gop/s",
         "frac": (ops / k2_s / 1e9) / int_peak if k2_s > 0 else 0.0,
-        "traffic": k2_traffic(inst_name),
+        "traffic": (k2_traffic(inst_name) or {}).get("bytes_per_launch"),
+        "traffic_source": k2_traffic(inst_name),
         "ops_per_child": ops / max(1, bounded),
         "peak_note": "148 SMs x 128 int32 lanes/clk (alu+fma pipes) x max SM clock; derived, "
                      "not measured (MEASURED_PEAKS has no integer figure)",

@@ -89,19 +89,6 @@ __device__ __forceinline__ void v3_sts_u16(uint32_t addr, int32_t v) {
     asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"((unsigned short)v));
 }
 
-template <int M>
-struct PairTab3 {  // (k, l) of pair index q in bound.hpp:97-98 order
-    int k[M * (M - 1) / 2], l[M * (M - 1) / 2];
-    constexpr PairTab3() : k(), l() {
-        int q = 0;
-        for (int a = 0; a < M; ++a)
-            for (int b = a + 1; b < M; ++b) {
-                k[q] = a;
-                l[q] = b;
-                ++q;
-            }
-    }
-};
 
 // (min1, argmin, min2) of a set of tails, merged across lanes; ties keep the
 // smallest job index as the argmin, as the ascending scan of v2 does.
@@ -300,21 +287,23 @@ __global__ void __launch_bounds__(NW <= 4 ? 192 : 256, NW <= 4 ? 3 : 2)
                 Lc[k] = s_load[pk] - px + mt;
                 lb = max(lb, prev + Lc[k]);  // one-machine term (bound.hpp:61-74)
             }
+            // Pairs: Lc_l + max(R_l, R_k + M'_kl).  Lc_l + R_l never exceeds the one-machine
+            // term already in lb, so per k only max_l (Lc_l + M'_kl) + R_k is needed: one
+            // VIADDMNMX per pair (the pairs of one k are consecutive in q order).
             const uint4* mrow = (const uint4*)(s_Mq + (size_t)tid * L.rowb);
-            constexpr PairTab3<M> tab{};
 #pragma unroll
-            for (int q8 = 0; q8 < (P + 7) / 8; ++q8) {
-                const uint4 cur = mrow[q8];
-                const uint32_t wv[4] = {cur.x, cur.y, cur.z, cur.w};
+            for (int k = 0; k < M - 1; ++k) {
+                int32_t acc = kNeg3;
 #pragma unroll
-                for (int u = 0; u < 8; ++u) {
-                    const int qq = q8 * 8 + u;
-                    if (qq < P) {
-                        const uint32_t w = wv[u >> 1];
-                        const int32_t mq = (u & 1) ? ((int32_t)w >> 16) : (int32_t)(int16_t)(w & 0xFFFFu);
-                        lb = max(lb, Lc[tab.l[qq]] + max(myR[tab.l[qq]], myR[tab.k[qq]] + mq));
-                    }
+                for (int l = k + 1; l < M; ++l) {
+                    const int qq = k * (2 * M - k - 1) / 2 + (l - k - 1);
+                    const uint4 v4 = mrow[qq >> 3];
+                    const int wi = (qq >> 1) & 3;
+                    const uint32_t w = wi == 0 ? v4.x : wi == 1 ? v4.y : wi == 2 ? v4.z : v4.w;
+                    const int32_t mq = (qq & 1) ? ((int32_t)w >> 16) : (int32_t)(int16_t)(w & 0xFFFFu);
+                    acc = __viaddmax_s32(Lc[l], mq, acc);
                 }
+                lb = max(lb, acc + myR[k]);
             }
             mylb = lb;
         }

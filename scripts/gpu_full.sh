@@ -13,7 +13,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k2_|place" -s 12 -c 2 \
    -o gpurun_out/prof_k2_final -f python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_final.log 2>&1
 tail -1 gpurun_out/ncu_final.log
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k2_v3" -s 8 -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k2_v3" -s 5 -c 1 \
    -o gpurun_out/prof_k2v3_ta081 -f python bench.py --instance ta081 --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_v3.log 2>&1
 tail -1 gpurun_out/ncu_v3.log
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
