@@ -61,12 +61,14 @@ class RoundRec(C.Structure):
         ("sync_ms", C.c_float),
         ("h2d_bytes", C.c_int64),
         ("d2h_bytes", C.c_int64),
+        ("place_ms", C.c_float),
+        ("reserved", C.c_int32),
     ]
 
     def timing(self):
         return {"k2_ms": self.k2_ms, "round_ms": self.round_ms, "launches": self.launches,
                 "host_ms": self.host_ms, "sync_ms": self.sync_ms, "h2d_bytes": self.h2d_bytes,
-                "d2h_bytes": self.d2h_bytes}
+                "d2h_bytes": self.d2h_bytes, "place_ms": self.place_ms}
 
     def as_tuple(self):
         return (self.target, self.branched, self.bounded, self.inserted, self.pruned,

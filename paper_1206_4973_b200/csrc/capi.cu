@@ -55,7 +55,10 @@ class PinnedArena {
                 }
         size_t sz = std::max<size_t>(bytes, blocks_.empty() ? (size_t)256 << 20 : 2 * blocks_.back().size);
         Block nb;
-        cudaError_t e = cudaHostAlloc((void**)&nb.base, sz, cudaHostAllocMapped | cudaHostAllocPortable);
+        const char* wc = getenv("FBB_PINNED_WC");  // write-combined: no CPU caching / snooping
+        const unsigned flags = cudaHostAllocMapped | cudaHostAllocPortable |
+                               (wc && wc[0] == '1' ? cudaHostAllocWriteCombined : 0u);
+        cudaError_t e = cudaHostAlloc((void**)&nb.base, sz, flags);
         if (e != cudaSuccess) return e;
         nb.size = sz;
         if (getenv("FBB_VERBOSE")) std::fprintf(stderr, "[fbb] pinned arena +%zu MiB\n", sz >> 20);
@@ -146,17 +149,24 @@ struct HBuf {  // pinned host
     T* as() const { return static_cast<T*>(p); }
 };
 
-// A growable node store (one pending bucket, or a scratch batch).
+// A growable node store (one pending bucket, or a scratch batch).  Compact stores
+// (the host-resident pending tree) keep the prefixes only: heads and masks are folded
+// from the prefix by the K2 kernels when they stage a parent, which cuts the bytes
+// that cross the host link per pending node from W*8 + 4m + n to n (108 -> 20 at 20x20).
 struct Store {
     DBuf masks, heads, prefix;
     int64_t cap = 0;
+    bool compact = false;
     void set(cudaStream_t st, PinnedArena* arena) {
         for (DBuf* b : {&masks, &heads, &prefix}) {
             b->st = st;
             b->arena = arena;
         }
     }
-    NodeStore view() const { return NodeStore{masks.as<uint64_t>(), heads.as<int32_t>(), prefix.as<uint8_t>()}; }
+    NodeStore view() const {
+        return compact ? NodeStore{nullptr, nullptr, prefix.as<uint8_t>()}
+                       : NodeStore{masks.as<uint64_t>(), heads.as<int32_t>(), prefix.as<uint8_t>()};
+    }
 };
 
 }  // namespace
@@ -183,15 +193,17 @@ struct fbb_ctx {
     Store staging;          // per-chunk compacted survivors (chunk c at c * cmax)
     Store parents;          // host-resident explorer: this round's parents, uploaded
     DBuf st_lb, st_count, st_seg;
-    DBuf d_pool, d_round;   // Pool, RoundState
+    DBuf d_pool, d_round;   // Pool, RoundState (device-planned loop)
     HBuf h_pool, h_round;
-    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    DBuf d_rp;              // host-planned rounds: [RoundState | Pool], uploaded by one copy
+    HBuf h_rp;              // its pinned source; the RoundState part stays zero
+    cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
     // batched device-planned explorer loop (explorer_loop.cu)
     DBuf d_loop;
     HBuf h_loop;
     std::vector<cudaEvent_t> loop_ev;  // 4 per round of a batch
     bool device_loop = false;          // FBB_DEVICE_LOOP=1: batched device-planned rounds
-    float last_k2_ms = 0.f, last_round_ms = 0.f, last_sync_ms = 0.f;
+    float last_k2_ms = 0.f, last_round_ms = 0.f, last_sync_ms = 0.f, last_place_ms = 0.f;
     int last_launches = 0;
 
     // explorer
@@ -208,6 +220,7 @@ struct fbb_ctx {
     PinnedArena arena;          // its storage
     bool mapped_in = true;      // K2 reads the parents in place from the mapped host buckets
                                 // over the host link; FBB_HOST_IN=copy: upload them first
+    bool compact_rows = true;   // host-resident tree as prefixes only (FBB_HOST_ROWS=compact|full)
     bool mapped_out = true;     // place_kernel writes survivors straight into the (device-
                                 // mapped) host buckets; FBB_HOST_OUT=staged: device output + D2H
     int64_t last_h2d = 0, last_d2h = 0;
@@ -234,24 +247,31 @@ namespace {
 size_t node_bytes(const fbb_ctx* ctx) {
     return (size_t)ctx->dt.W * 8 + (size_t)ctx->dt.m * 4 + (size_t)ctx->dt.n;
 }
+size_t row_bytes(const fbb_ctx* ctx, bool compact) { return compact ? (size_t)ctx->dt.n : node_bytes(ctx); }
 
 cudaError_t store_ensure(fbb_ctx* ctx, Store& s, int64_t want, int64_t keep) {
     if (want <= s.cap) return cudaSuccess;
     // pinned host growth is slow (page locking): start host stores at ~4 MB
-    const int64_t floor_rows = s.masks.arena ? std::max<int64_t>(1024, (1 << 20) / (int64_t)node_bytes(ctx)) : 1024;
+    const int64_t floor_rows =
+        s.prefix.arena ? std::max<int64_t>(1024, (1 << 20) / (int64_t)row_bytes(ctx, s.compact)) : 1024;
     int64_t nc = std::max<int64_t>(want, std::max<int64_t>(s.cap * 2, floor_rows));
     const int n = ctx->dt.n, m = ctx->dt.m, W = ctx->dt.W;
-    PinnedArena* host = s.masks.arena;
+    PinnedArena* host = s.prefix.arena;
     Store t;
+    t.compact = s.compact;
     t.set(ctx->stream, host);
     s.set(ctx->stream, host);
     cudaError_t e;
-    if ((e = t.masks.ensure((size_t)nc * W * 8)) != cudaSuccess) return e;
-    if ((e = t.heads.ensure((size_t)nc * m * 4)) != cudaSuccess) return e;
+    if (!t.compact) {
+        if ((e = t.masks.ensure((size_t)nc * W * 8)) != cudaSuccess) return e;
+        if ((e = t.heads.ensure((size_t)nc * m * 4)) != cudaSuccess) return e;
+    }
     if ((e = t.prefix.ensure((size_t)nc * n)) != cudaSuccess) return e;
     if (keep > 0) {  // stream-ordered: the copy precedes the old buffers' release
-        cudaMemcpyAsync(t.masks.p, s.masks.p, (size_t)keep * W * 8, cudaMemcpyDefault, ctx->stream);
-        cudaMemcpyAsync(t.heads.p, s.heads.p, (size_t)keep * m * 4, cudaMemcpyDefault, ctx->stream);
+        if (!t.compact) {
+            cudaMemcpyAsync(t.masks.p, s.masks.p, (size_t)keep * W * 8, cudaMemcpyDefault, ctx->stream);
+            cudaMemcpyAsync(t.heads.p, s.heads.p, (size_t)keep * m * 4, cudaMemcpyDefault, ctx->stream);
+        }
         cudaMemcpyAsync(t.prefix.p, s.prefix.p, (size_t)keep * n, cudaMemcpyDefault, ctx->stream);
     }
     s.masks.release();
@@ -297,22 +317,25 @@ int run_pool(fbb_ctx* ctx, Pool& pool, int first_internal, int32_t ub, int froze
     CK(ctx->st_lb.ensure((size_t)slots * 4), "staging");
     CK(ctx->st_count.ensure((size_t)std::max<int64_t>(pool.nchunks, 1) * 4), "staging");
     CK(ctx->st_seg.ensure((size_t)std::max<int64_t>(pool.nchunks, 1) * 4), "staging");
-    CK(ctx->d_pool.ensure(sizeof(Pool)), "pool");
-    CK(ctx->h_pool.ensure(sizeof(Pool)), "pool");
-    CK(ctx->d_round.ensure(sizeof(RoundState)), "round state");
+    constexpr size_t kPoolOff = (sizeof(RoundState) + 255) & ~size_t(255);
+    if (ctx->h_rp.bytes < kPoolOff + sizeof(Pool)) {
+        CK(ctx->h_rp.ensure(kPoolOff + sizeof(Pool)), "pool");
+        std::memset(ctx->h_rp.p, 0, kPoolOff);
+    }
+    CK(ctx->d_rp.ensure(kPoolOff + sizeof(Pool)), "pool");
     CK(ctx->h_round.ensure(sizeof(RoundState)), "round state");
 
     pool.ub = ub;  // the round's bound, semantics and first internal segment travel with the pool
     pool.frozen = frozen;
     pool.first_internal = first_internal;
     size_t pool_bytes = offsetof(Pool, seg) + (size_t)pool.nseg * sizeof(Segment);
-    std::memcpy(ctx->h_pool.p, &pool, pool_bytes);
+    std::memcpy((char*)ctx->h_rp.p + kPoolOff, &pool, pool_bytes);
     int launches = 0;
     CK(cudaEventRecord(ctx->ev[0], st), "event");
-    CK(cudaMemcpyAsync(ctx->d_pool.p, ctx->h_pool.p, pool_bytes, cudaMemcpyHostToDevice, st), "pool H2D");
-    CK(cudaMemsetAsync(ctx->d_round.p, 0, kRoundStateHead, st), "round state");
-    const Pool* dp = ctx->d_pool.as<Pool>();
-    RoundState* rs = ctx->d_round.as<RoundState>();
+    // one copy uploads the pool and zeroes the round state (counters, ticket, leaf key)
+    CK(cudaMemcpyAsync(ctx->d_rp.p, ctx->h_rp.p, kPoolOff + pool_bytes, cudaMemcpyHostToDevice, st), "pool H2D");
+    const Pool* dp = (const Pool*)((char*)ctx->d_rp.p + kPoolOff);
+    RoundState* rs = ctx->d_rp.as<RoundState>();
     bool has_leaf = pool.nseg > 0 && pool.seg[0].depth >= n - 2;
     if (has_leaf) {
         // leaves, then the best leaf's schedule -- before K2 recycles the leaf
@@ -329,13 +352,12 @@ int run_pool(fbb_ctx* ctx, Pool& pool, int first_internal, int32_t ub, int froze
        "K2 internal");
     CK(cudaEventRecord(ctx->ev[2], st), "event");
     CK(launch_place(ctx->dt, ctx->k2, dp, pool, rs, out, st), "place");
+    CK(cudaEventRecord(ctx->ev[4], st), "event");
     launches += has_internal ? 2 : 0;  // K2 + place
-    size_t head = offsetof(RoundState, seg_surv) + (size_t)pool.nseg * 8;
+    // one download: the counters (and, after a leaf round, the schedule behind them)
+    const size_t head = has_leaf ? offsetof(RoundState, schedule) + (size_t)n * 4
+                                 : offsetof(RoundState, seg_surv) + (size_t)pool.nseg * 8;
     CK(cudaMemcpyAsync(ctx->h_round.p, rs, head, cudaMemcpyDeviceToHost, st), "round D2H");
-    if (has_leaf)
-        CK(cudaMemcpyAsync(ctx->h_round.as<RoundState>()->schedule, rs->schedule, (size_t)n * 4,
-                           cudaMemcpyDeviceToHost, st),
-           "schedule D2H");
     CK(cudaEventRecord(ctx->ev[3], st), "event");
     const auto t_sync = std::chrono::steady_clock::now();
     CK(cudaStreamSynchronize(st), "round");
@@ -344,6 +366,14 @@ int run_pool(fbb_ctx* ctx, Pool& pool, int first_internal, int32_t ub, int froze
         return ctx->fail(FBB_E_STATE, "corrupt pending node (unscheduled-job count mismatch)");
     cudaEventElapsedTime(&ctx->last_k2_ms, ctx->ev[1], ctx->ev[2]);
     cudaEventElapsedTime(&ctx->last_round_ms, ctx->ev[0], ctx->ev[3]);
+    cudaEventElapsedTime(&ctx->last_place_ms, ctx->ev[2], ctx->ev[4]);
+    if (getenv("FBB_TIMING_DEBUG")) {
+        float pre = 0.f, post = 0.f;
+        cudaEventElapsedTime(&pre, ctx->ev[0], ctx->ev[1]);
+        cudaEventElapsedTime(&post, ctx->ev[4], ctx->ev[3]);
+        std::fprintf(stderr, "[fbb] pre %.1f us  k2 %.1f  place %.1f  post %.1f\n", pre * 1e3,
+                     ctx->last_k2_ms * 1e3, ctx->last_place_ms * 1e3, post * 1e3);
+    }
     ctx->last_launches = launches;
     return FBB_OK;
 }
@@ -411,8 +441,10 @@ int push_host_nodes(fbb_ctx* ctx, const uint8_t* prefix, const int32_t* depth, i
         CK(store_ensure(ctx, ctx->bucket[d], c0 + k, c0), "bucket grow");
         Store& b = ctx->bucket[d];
         cudaStream_t st = ctx->stream;
-        CK(cudaMemcpyAsync(b.masks.as<uint64_t>() + c0 * W, hm.data(), hm.size() * 8, cudaMemcpyDefault, st), "push");
-        CK(cudaMemcpyAsync(b.heads.as<int32_t>() + c0 * m, hh.data(), hh.size() * 4, cudaMemcpyDefault, st), "push");
+        if (!b.compact) {
+            CK(cudaMemcpyAsync(b.masks.as<uint64_t>() + c0 * W, hm.data(), hm.size() * 8, cudaMemcpyDefault, st), "push");
+            CK(cudaMemcpyAsync(b.heads.as<int32_t>() + c0 * m, hh.data(), hh.size() * 4, cudaMemcpyDefault, st), "push");
+        }
         CK(cudaMemcpyAsync(b.prefix.as<uint8_t>() + c0 * n, hp.data(), hp.size(), cudaMemcpyDefault, st), "push");
         CK(cudaStreamSynchronize(st), "push");  // host vectors are reused
         ctx->cnt[d] = c0 + k;
@@ -432,16 +464,22 @@ int check_pending(fbb_ctx* ctx) {
         std::vector<int32_t> hd((size_t)k * m);
         std::vector<uint8_t> pr((size_t)k * n);
         cudaStream_t st = ctx->stream;
-        CK(cudaMemcpyAsync(mk.data(), ctx->bucket[d].masks.p, mk.size() * 8, cudaMemcpyDefault, st), "check");
-        CK(cudaMemcpyAsync(hd.data(), ctx->bucket[d].heads.p, hd.size() * 4, cudaMemcpyDefault, st), "check");
+        const bool compact = ctx->bucket[d].compact;
+        if (!compact) {
+            CK(cudaMemcpyAsync(mk.data(), ctx->bucket[d].masks.p, mk.size() * 8, cudaMemcpyDefault, st), "check");
+            CK(cudaMemcpyAsync(hd.data(), ctx->bucket[d].heads.p, hd.size() * 4, cudaMemcpyDefault, st), "check");
+        }
         CK(cudaMemcpyAsync(pr.data(), ctx->bucket[d].prefix.p, pr.size(), cudaMemcpyDefault, st), "check");
         CK(cudaStreamSynchronize(st), "check");
         std::vector<uint64_t> m2(W);
         std::vector<int32_t> h2(m);
         for (int64_t i = 0; i < k; ++i) {
             node_from_prefix(ctx->ht, &pr[i * n], d, m2.data(), h2.data());
-            bool ok = std::memcmp(m2.data(), &mk[i * W], W * 8) == 0 &&
-                      std::memcmp(h2.data(), &hd[i * m], m * 4) == 0;
+            int jobs = 0;  // compact rows: the prefix must name d distinct jobs
+            for (int w = 0; w < W; ++w) jobs += __builtin_popcountll(m2[w]);
+            bool ok = compact ? jobs == d
+                              : std::memcmp(m2.data(), &mk[i * W], W * 8) == 0 &&
+                                    std::memcmp(h2.data(), &hd[i * m], m * 4) == 0;
             if (!ok) {
                 char buf[160];
                 std::snprintf(buf, sizeof buf, "check: bad pending node depth %d index %lld of %lld",
@@ -457,15 +495,25 @@ void explorer_clear(fbb_ctx* ctx) {
     const int n = ctx->dt.n;
     if ((int)ctx->bucket.size() != n + 1) ctx->bucket.resize(n + 1);
     PinnedArena* want = ctx->host_pending ? &ctx->arena : nullptr;
+    const bool compact = ctx->host_pending && ctx->compact_rows;
     for (Store& b : ctx->bucket) {
-        if (b.masks.arena != want) {  // residency changed: drop the old storage
+        if (b.prefix.arena != want || b.compact != compact) {  // residency changed: drop the old storage
             cudaStreamSynchronize(ctx->stream);
             b.masks.release();
             b.heads.release();
             b.prefix.release();
             b.cap = 0;
         }
+        b.compact = compact;
         b.set(ctx->stream, want);
+    }
+    if (ctx->parents.compact != compact) {  // the upload scratch follows the tree's row format
+        cudaStreamSynchronize(ctx->stream);
+        ctx->parents.masks.release();
+        ctx->parents.heads.release();
+        ctx->parents.prefix.release();
+        ctx->parents.cap = 0;
+        ctx->parents.compact = compact;
     }
     ctx->cnt.assign(n + 1, 0);
     ctx->schedule.assign(n, 0);
@@ -516,7 +564,7 @@ int explorer_round(fbb_ctx* ctx, int64_t target, fbb_round_t* rec) {
     const bool upload = ctx->host_pending && !ctx->mapped_in;
     if (ctx->host_pending && ctx->mapped_in) {  // parents read in place over the host link
         for (int s = 0; s < local.nseg; ++s) npar += local.seg[s].count;
-        h2d = npar * (int64_t)node_bytes(ctx);
+        h2d = npar * (int64_t)row_bytes(ctx, ctx->compact_rows);
     }
     if (upload) {
         // host-resident pending tree: this round's parents (the top rows of each
@@ -531,13 +579,15 @@ int explorer_round(fbb_ctx* ctx, int64_t target, fbb_round_t* rec) {
             Segment& sg = local.seg[s];
             const NodeStore b = ctx->bucket[sg.depth].view();
             const int64_t lo = after[sg.depth], k = sg.count;
-            CK(cudaMemcpyAsync(pv.masks + o * W, b.masks + lo * W, (size_t)k * W * 8, cudaMemcpyDefault, ctx->stream), "parents H2D");
-            CK(cudaMemcpyAsync(pv.heads + o * m, b.heads + lo * m, (size_t)k * m * 4, cudaMemcpyDefault, ctx->stream), "parents H2D");
+            if (b.heads) {
+                CK(cudaMemcpyAsync(pv.masks + o * W, b.masks + lo * W, (size_t)k * W * 8, cudaMemcpyDefault, ctx->stream), "parents H2D");
+                CK(cudaMemcpyAsync(pv.heads + o * m, b.heads + lo * m, (size_t)k * m * 4, cudaMemcpyDefault, ctx->stream), "parents H2D");
+            }
             CK(cudaMemcpyAsync(pv.prefix + o * n, b.prefix + lo * n, (size_t)k * n, cudaMemcpyDefault, ctx->stream), "parents H2D");
             sg.first = o + k - 1;  // LIFO: the bucket top is popped first
             o += k;
         }
-        h2d = npar * (int64_t)node_bytes(ctx);
+        h2d = npar * (int64_t)row_bytes(ctx, ctx->compact_rows);
     }
     if (staged_out) CK(store_ensure(ctx, ctx->batch_out, std::max<int64_t>(local.nchildren, 1), 0), "alloc");
     for (int s = 0; s < local.nseg; ++s) {  // views may have moved after growth
@@ -573,8 +623,10 @@ int explorer_round(fbb_ctx* ctx, int64_t target, fbb_round_t* rec) {
                 const int64_t at = after[sg.depth + 1];
                 CK(store_ensure(ctx, ctx->bucket[sg.depth + 1], at + k, at), "bucket grow");
                 const NodeStore b = ctx->bucket[sg.depth + 1].view(), o = ctx->batch_out.view();
-                CK(cudaMemcpyAsync(b.masks + at * W, o.masks + out_row * W, (size_t)k * W * 8, cudaMemcpyDefault, ctx->stream), "survivors D2H");
-                CK(cudaMemcpyAsync(b.heads + at * m, o.heads + out_row * m, (size_t)k * m * 4, cudaMemcpyDefault, ctx->stream), "survivors D2H");
+                if (b.heads) {
+                    CK(cudaMemcpyAsync(b.masks + at * W, o.masks + out_row * W, (size_t)k * W * 8, cudaMemcpyDefault, ctx->stream), "survivors D2H");
+                    CK(cudaMemcpyAsync(b.heads + at * m, o.heads + out_row * m, (size_t)k * m * 4, cudaMemcpyDefault, ctx->stream), "survivors D2H");
+                }
                 CK(cudaMemcpyAsync(b.prefix + at * n, o.prefix + out_row * n, (size_t)k * n, cudaMemcpyDefault, ctx->stream), "survivors D2H");
             }
             out_row += k;
@@ -607,6 +659,7 @@ int explorer_round(fbb_ctx* ctx, int64_t target, fbb_round_t* rec) {
     rec->incumbent = ctx->frozen ? (ctx->found ? ctx->best : ctx->incumbent) : ctx->incumbent;
     rec->k2_ms = ctx->last_k2_ms;
     rec->round_ms = ctx->last_round_ms;
+    rec->place_ms = ctx->last_place_ms;
     rec->launches = ctx->last_launches;
     if (ctx->check) {
         int rc2 = check_pending(ctx);
@@ -619,7 +672,7 @@ int explorer_round(fbb_ctx* ctx, int64_t target, fbb_round_t* rec) {
     rec->pending = pending_total(ctx);
     rec->sync_ms = ctx->last_sync_ms;
     rec->h2d_bytes = h2d;
-    rec->d2h_bytes = ctx->host_pending ? rec->inserted * (int64_t)node_bytes(ctx) : 0;
+    rec->d2h_bytes = ctx->host_pending ? rec->inserted * (int64_t)row_bytes(ctx, ctx->compact_rows) : 0;
     rec->host_ms = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t0).count();
     return FBB_OK;
 }
@@ -629,7 +682,7 @@ int explorer_round(fbb_ctx* ctx, int64_t target, fbb_round_t* rec) {
 // explorer_round.  Used when the parents can be read in place (HBM buckets, or host
 // buckets read and written through the mapping).
 bool device_loop_ok(const fbb_ctx* ctx) {
-    return ctx->device_loop && (!ctx->host_pending || (ctx->mapped_in && ctx->mapped_out));
+    return ctx->device_loop && (!ctx->host_pending || (ctx->mapped_in && ctx->mapped_out && !ctx->compact_rows));
 }
 
 int explorer_run_batched(fbb_ctx* ctx, const int64_t* targets, int ntargets, int64_t max_rounds,
@@ -821,7 +874,8 @@ fbb_ctx* fbb_create(int device, const int32_t* p, int n, int m) {
             }
         }
         for (DBuf* b : {&ctx->k1_masks, &ctx->k1_heads, &ctx->k1_depth, &ctx->k1_lb, &ctx->out_lb,
-                        &ctx->st_lb, &ctx->st_count, &ctx->st_seg, &ctx->d_pool, &ctx->d_round, &ctx->d_loop})
+                        &ctx->st_lb, &ctx->st_count, &ctx->st_seg, &ctx->d_pool, &ctx->d_round, &ctx->d_loop,
+                        &ctx->d_rp})
             b->st = ctx->stream;
         for (Store* st : {&ctx->batch_in, &ctx->batch_out, &ctx->staging, &ctx->parents})
             st->set(ctx->stream, nullptr);
@@ -870,7 +924,7 @@ void fbb_destroy(fbb_ctx* ctx) {
     cudaSetDevice(ctx->device);
     free_tables(&ctx->dt);
     for (DBuf* b : {&ctx->k1_masks, &ctx->k1_heads, &ctx->k1_depth, &ctx->k1_lb, &ctx->out_lb,
-                    &ctx->st_lb, &ctx->st_count, &ctx->st_seg, &ctx->d_pool, &ctx->d_round})
+                    &ctx->st_lb, &ctx->st_count, &ctx->st_seg, &ctx->d_pool, &ctx->d_round, &ctx->d_rp})
         b->release();
     for (Store* s : {&ctx->batch_in, &ctx->batch_out, &ctx->staging, &ctx->parents}) {
         s->masks.release();
@@ -885,6 +939,7 @@ void fbb_destroy(fbb_ctx* ctx) {
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     ctx->h_pool.release();
     ctx->h_round.release();
+    ctx->h_rp.release();
     ctx->h_loop.release();
     ctx->d_loop.release();
     for (cudaEvent_t ev : ctx->loop_ev)
@@ -1103,12 +1158,17 @@ int fbb_explorer_set_residency(fbb_ctx* ctx, int pending_on_host) {
         // 1 GiB, or twice what the HBM-resident tree of this context has grown to
         size_t dev_bytes = 0;
         for (const Store& b : ctx->bucket)
-            if (!b.masks.arena) dev_bytes += (size_t)b.cap * node_bytes(ctx);
+            if (!b.prefix.arena) dev_bytes += (size_t)b.cap * node_bytes(ctx);
         const char* mb = getenv("FBB_PINNED_MB");
         size_t want = mb ? (size_t)std::max(64L, atol(mb)) << 20
                          : std::max<size_t>((size_t)1 << 30, 2 * dev_bytes);
         void* p = nullptr;
         if (ctx->arena.alloc(want, &p) == cudaSuccess) ctx->arena.release(p, want);
+        // compact (prefix-only) rows when the staging fold is short: it costs depth * m
+        // dependent max-plus steps per parent, free at n <= 32 (Ta021: K2 unchanged) but
+        // +20 % of K2 at 100x20, where deep parents fold up to ~100 jobs
+        const char* rows = getenv("FBB_HOST_ROWS");
+        ctx->compact_rows = rows ? std::string(rows) != "full" : ctx->dt.n <= 32;
         const char* o = getenv("FBB_HOST_OUT");
         ctx->mapped_out = !(o && std::string(o) == "staged");
         const char* i = getenv("FBB_HOST_IN");

@@ -156,7 +156,8 @@ __global__ void __launch_bounds__(128) k2_internal_kernel(DevTables t, const Poo
             int pp = x / depth, i = x - pp * depth;
             s_pre[pp * n + i] = src.prefix[(first + step * (p0 + pp)) * n + i];
         }
-        for (int x = tid; x < np * W32; x += bd) {
+        const bool compact = src.heads == nullptr;  // prefix-only rows (host-resident tree)
+        for (int x = tid; x < np * W32 && !compact; x += bd) {
             int pp = x / W32, w = x - pp * W32;
             int64_t node = first + step * (p0 + pp);
             uint64_t word = src.masks[node * W + (w >> 1)];
@@ -165,12 +166,34 @@ __global__ void __launch_bounds__(128) k2_internal_kernel(DevTables t, const Poo
             uint32_t vmask = valid >= 32 ? 0xFFFFFFFFu : ((1u << valid) - 1u);
             s_um[x] = ~half & vmask;
         }
-        for (int x = tid; x < np * m; x += bd) {
+        for (int x = tid; x < np * m && !compact; x += bd) {
             int pp = x / m, k = x - pp * m;
             int64_t node = first + step * (p0 + pp);
             s_R[x] = src.heads[node * m + k];
         }
         __syncthreads();
+        if (compact) {  // heads and unscheduled set folded from the staged prefixes
+            for (int pp = tid; pp < np; pp += bd) {
+                const uint8_t* pre = s_pre + pp * n;
+                int32_t* R = s_R + pp * m;
+                for (int k = 0; k < m; ++k) R[k] = 0;
+                for (int i = 0; i < depth; ++i) {  // child_heads, instance.hpp:81-89
+                    const int j = pre[i];
+                    int32_t prev = 0;
+                    for (int k = 0; k < m; ++k) {
+                        prev = max(prev, R[k]) + s_p[j * m + k];
+                        R[k] = prev;
+                    }
+                }
+                uint32_t* um = s_um + pp * W32;
+                for (int w = 0; w < W32; ++w) {
+                    const int valid = min(32, n - w * 32);
+                    um[w] = valid >= 32 ? 0xFFFFFFFFu : ((1u << valid) - 1u);
+                }
+                for (int i = 0; i < depth; ++i) um[pre[i] >> 5] &= ~(1u << (pre[i] & 31));
+            }
+            __syncthreads();
+        }
         // ---- per parent: rank of each unscheduled job, ascending job list
         for (int pp = tid; pp < np; pp += bd) {
             const uint32_t* um = s_um + pp * W32;
@@ -342,20 +365,38 @@ __global__ void k2_leaf_kernel(DevTables t, const Pool* __restrict__ pool, int s
         int64_t pp = c / r;
         int rk = (int)(c - pp * r);
         int64_t node = sg.first + sg.step * pp;
-        const uint64_t* mk = sg.src.masks + node * W;
         // the unscheduled jobs in ascending order: x = rk-th, y = the other
         int u[2] = {-1, -1}, cnt = 0;
-        for (int j = 0; j < n && cnt < 2; ++j)
-            if (!((mk[j >> 6] >> (j & 63)) & 1ull)) u[cnt++] = j;
+        int32_t prev = 0, h[kMaxMachines];
+        if (sg.src.heads) {
+            const uint64_t* mk = sg.src.masks + node * W;
+            for (int j = 0; j < n && cnt < 2; ++j)
+                if (!((mk[j >> 6] >> (j & 63)) & 1ull)) u[cnt++] = j;
+            for (int k = 0; k < m; ++k) h[k] = sg.src.heads[node * m + k];
+        } else {  // compact rows: heads and unscheduled jobs from the prefix
+            const uint8_t* pre = sg.src.prefix + node * n;
+            uint64_t sm[kMaxWords] = {0, 0, 0, 0};
+            for (int k = 0; k < m; ++k) h[k] = 0;
+            for (int i = 0; i < depth; ++i) {  // child_heads, instance.hpp:81-89
+                const int j = pre[i];
+                sm[j >> 6] |= 1ull << (j & 63);
+                prev = 0;
+                for (int k = 0; k < m; ++k) {
+                    prev = max(prev, h[k]) + t.p[j * m + k];
+                    h[k] = prev;
+                }
+            }
+            for (int j = 0; j < n && cnt < 2; ++j)
+                if (!((sm[j >> 6] >> (j & 63)) & 1ull)) u[cnt++] = j;
+        }
         if (cnt < r) {  // a pending node must have exactly r unscheduled jobs
             atomicExch(&rs->found, -1);
             continue;
         }
         int x = u[rk], y = (r == 2) ? u[1 - rk] : -1;
-        int32_t prev = 0, h[kMaxMachines];
-        const int32_t* R = sg.src.heads + node * m;
+        prev = 0;
         for (int k = 0; k < m; ++k) {
-            prev = max(prev, R[k]) + t.p[x * m + k];
+            prev = max(prev, h[k]) + t.p[x * m + k];
             h[k] = prev;
         }
         if (y >= 0) {
@@ -395,12 +436,15 @@ __global__ void leaf_schedule_kernel(DevTables t, const Pool* __restrict__ pool,
     int64_t pp = c / r;
     int rk = (int)(c - pp * r);
     int64_t node = sg.first + sg.step * pp;
-    const uint64_t* mk = sg.src.masks + node * W;
     const uint8_t* pre = sg.src.prefix + node * n;
-    for (int i = 0; i < sg.depth; ++i) schedule[i] = pre[i];
+    uint64_t sm[kMaxWords] = {0, 0, 0, 0};  // scheduled jobs, from the prefix
+    for (int i = 0; i < sg.depth; ++i) {
+        schedule[i] = pre[i];
+        sm[pre[i] >> 6] |= 1ull << (pre[i] & 63);
+    }
     int u[2] = {-1, -1}, cnt = 0;
     for (int j = 0; j < n && cnt < 2; ++j)
-        if (!((mk[j >> 6] >> (j & 63)) & 1ull)) u[cnt++] = j;
+        if (!((sm[j >> 6] >> (j & 63)) & 1ull)) u[cnt++] = j;
     schedule[sg.depth] = u[rk];
     if (r == 2) schedule[sg.depth + 1] = u[1 - rk];
     *found = 1;
@@ -453,6 +497,7 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(DevTables t, const
     __shared__ NodeStore s_store[kPlaceChunks];
     __shared__ int32_t* s_dlb[kPlaceChunks];
     __shared__ int64_t s_red[2][kPlaceThreads / 32];
+    __shared__ int s_need;                     // prefix bytes that matter: max child depth
     extern __shared__ uint8_t s_rc[];          // chunk of each row (cmax * kPlaceChunks)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t nchunks = pool->nchunks;
@@ -462,6 +507,7 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(DevTables t, const
     const int nch = (int)(nchunks - c0 < kPlaceChunks ? nchunks - c0 : kPlaceChunks);
     const int s0 = out.seg[c0];
     const int64_t cb0 = pool->seg[s0].chunk_base;
+    if (tid == 0) s_need = 0;
     if (tid < 32) {
         const int v = tid < nch ? out.count[c0 + tid] : 0;
         int incl = v;
@@ -515,6 +561,7 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(DevTables t, const
         s_dlb[tid] = sg.dst_lb;
         const int cnt = s_row0[tid + 1] - s_row0[tid];
         if (cnt) atomicAdd((unsigned long long*)&rs->seg_surv[s], (unsigned long long)cnt);
+        atomicMax(&s_need, sg.depth + 1);
     }
     const int R = s_row0[nch];
     if (tid == 0 && R) atomicAdd((unsigned long long*)&rs->total, (unsigned long long)R);
@@ -527,12 +574,14 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(DevTables t, const
     // one array start at multiples of the row size in both places): 16-byte units for
     // 20-machine heads, 4-byte units for 20/100/200-job prefixes.  Wide units matter
     // most when the destination is pinned host memory written over the host link.
-    auto copy_array = [&](const void* src_base, int row_bytes, auto dst_of) {
+    // Only the first `used_bytes` of a row are copied (prefix rows: the child depth).
+    auto copy_array = [&](const void* src_base, int row_bytes, int used_bytes, auto dst_of) {
         auto go = [&](auto unit) {
             using T = decltype(unit);
             const int w = row_bytes / (int)sizeof(T);
+            const int wu = min(w, (used_bytes + (int)sizeof(T) - 1) / (int)sizeof(T));
             const T* src = (const T*)src_base;
-            copy_rows<kPlaceBatch>(R, w, [&](int row, int k) { return __ldg(src + src_row(row) * w + k); },
+            copy_rows<kPlaceBatch>(R, wu, [&](int row, int k) { return __ldg(src + src_row(row) * w + k); },
                                    [&](int row, int k, T v) { ((T*)dst_of(row))[dst_row(row) * w + k] = v; });
         };
         if (row_bytes % 16 == 0) go(uint4{});
@@ -541,10 +590,55 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(DevTables t, const
         else if (row_bytes % 2 == 0) go((unsigned short)0);
         else go((unsigned char)0);
     };
-    copy_array(out.nodes.heads, m * 4, [&](int row) { return (void*)s_store[s_rc[row]].heads; });
-    copy_array(out.nodes.masks, W * 8, [&](int row) { return (void*)s_store[s_rc[row]].masks; });
-    // whole prefix rows (bytes past depth + 1 are don't-care in both places)
-    copy_array(out.nodes.prefix, n, [&](int row) { return (void*)s_store[s_rc[row]].prefix; });
+    // compact destinations (prefix-only rows, the host-resident tree) have no heads /
+    // masks; all segments of a pool share one residency
+    if (s_store[0].heads) {
+        copy_array(out.nodes.heads, m * 4, m * 4, [&](int row) { return (void*)s_store[s_rc[row]].heads; });
+        copy_array(out.nodes.masks, W * 8, W * 8, [&](int row) { return (void*)s_store[s_rc[row]].masks; });
+    }
+    // prefix rows up to the child depth (the bytes past it are don't-care in both places)
+    if (2 * s_need <= n) {
+        copy_array(out.nodes.prefix, n, s_need, [&](int row) { return (void*)s_store[s_rc[row]].prefix; });
+    } else {
+        // mostly-used rows: whole rows, as one contiguous byte range per chunk written in
+        // aligned 16-byte stores (a host-mapped destination takes ~2x more bytes/s from
+        // full 16-byte stores than from 4-byte row-unit stores); the 16-byte blocks of
+        // all the CTA's chunks form one flat index space
+        __shared__ int64_t s_blk[kPlaceChunks + 1];
+        if (tid == 0) {
+            int64_t acc = 0;
+            for (int c = 0; c < nch; ++c) {
+                s_blk[c] = acc;
+                const int64_t len = (int64_t)(s_row0[c + 1] - s_row0[c]) * n;
+                const uintptr_t d0 = (uintptr_t)(s_store[c].prefix + s_dst[c] * n);
+                acc += len ? (int64_t)((d0 + len - (d0 & ~(uintptr_t)15) + 15) >> 4) : 0;
+            }
+            s_blk[nch] = acc;
+        }
+        __syncthreads();
+        for (int64_t b = tid; b < s_blk[nch]; b += kPlaceThreads) {
+            int c = 0;
+            while (b >= s_blk[c + 1]) ++c;
+            const int64_t len = (int64_t)(s_row0[c + 1] - s_row0[c]) * n;
+            const uint8_t* src = out.nodes.prefix + ((c0 + c) * (int64_t)cmax) * n;
+            uint8_t* dst = s_store[c].prefix + s_dst[c] * n;
+            const uintptr_t a0 = (uintptr_t)dst & ~(uintptr_t)15;
+            const int64_t off = (int64_t)(a0 + 16 * (b - s_blk[c]) - (uintptr_t)dst);  // block in dst
+            if (off >= 0 && off + 16 <= len) {
+                uint32_t w[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const uint8_t* sp = src + off + 4 * q;
+                    w[q] = (uint32_t)__ldg(sp) | ((uint32_t)__ldg(sp + 1) << 8) |
+                           ((uint32_t)__ldg(sp + 2) << 16) | ((uint32_t)__ldg(sp + 3) << 24);
+                }
+                *(uint4*)(dst + off) = make_uint4(w[0], w[1], w[2], w[3]);
+            } else {  // a partial block at either end of the range
+                for (int q = 0; q < 16; ++q)
+                    if (off + q >= 0 && off + q < len) dst[off + q] = __ldg(src + off + q);
+            }
+        }
+    }
     if (s_dlb[0])  // all segments of a pool share dst_lb (set or not)
         copy_rows<kPlaceBatch>(R, 1, [&](int row, int) { return __ldg(out.lb + src_row(row)); },
                                [&](int row, int, int32_t v) { s_dlb[s_rc[row]][dst_row(row)] = v; });

@@ -330,6 +330,7 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
         int64_t p0_;
         chunk_geo(c, s_, depth_, np_, p0_);
         const Segment& g_ = pool->seg[s_];
+        const bool cpt_ = g_.src.heads == nullptr;  // compact rows: prefixes only
 #pragma unroll
         for (int u = 0; u < kPfPre; ++u) {
             const int x = tid + u * 192;
@@ -341,12 +342,12 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
 #pragma unroll
         for (int u = 0; u < kPfHead; ++u) {
             const int x = tid + u * 192;
-            if (x < np_ * M) {
+            if (x < np_ * M && !cpt_) {
                 const int pp = x / M, k = x - pp * M;
                 pf_head[u] = g_.src.heads[(g_.first + g_.step * (p0_ + pp)) * M + k];
             }
         }
-        if (tid < np_) pf_mask = g_.src.masks[(g_.first + g_.step * (p0_ + tid)) * W];
+        if (tid < np_ && !cpt_) pf_mask = g_.src.masks[(g_.first + g_.step * (p0_ + tid)) * W];
     };
     int64_t chunk = claim_chunk(rs, c_begin, s_slot);
     if constexpr (kPipe) prefetch(chunk);
@@ -358,6 +359,7 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
         const int r = n - depth;
         const int nc = np * r;
         const uint64_t valid = n >= 64 ? ~0ull : ((1ull << n) - 1ull);
+        const bool compact = sg.src.heads == nullptr;  // prefix-only rows (host-resident tree)
         if constexpr (kPipe) {
 #pragma unroll
             for (int u = 0; u < kPfPre; ++u) {
@@ -370,9 +372,9 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
 #pragma unroll
             for (int u = 0; u < kPfHead; ++u) {
                 const int x = tid + u * 192;
-                if (x < np * M) s_R[x] = pf_head[u];
+                if (x < np * M && !compact) s_R[x] = pf_head[u];
             }
-            if (tid < np) s_um[tid] = ~pf_mask & valid;
+            if (tid < np && !compact) s_um[tid] = ~pf_mask & valid;
         } else {
             const NodeStore src = sg.src;
             const int64_t first = sg.first, step = sg.step;
@@ -380,17 +382,30 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
                 int pp = x / depth, i = x - pp * depth;
                 s_pre[pp * RW + i] = src.prefix[(first + step * (p0 + pp)) * n + i];
             }
-            for (int pp = tid; pp < np; pp += bd) {
+            for (int pp = tid; pp < np && !compact; pp += bd) {
                 int64_t node = first + step * (p0 + pp);
                 s_um[pp] = ~src.masks[node * W] & valid;
             }
-            for (int x = tid; x < np * M; x += bd) {
+            for (int x = tid; x < np * M && !compact; x += bd) {
                 int pp = x / M, k = x - pp * M;
                 s_R[x] = src.heads[(first + step * (p0 + pp)) * M + k];
             }
         }
         __syncthreads();
         if (kPipe && tid == 0) *s_slot = c_begin + (int64_t)atomicAdd(&rs->ticket, 1u);  // next chunk
+        if (compact) {  // heads and scheduled set folded from the staged prefixes
+            if (tid < np) {
+                const uint8_t* pre = s_pre + tid * RW;
+                int32_t h[M];
+                heads_from_prefix<M>(pre, depth, [&](int j, int k) { return s_p[j * M + k]; }, h);
+#pragma unroll
+                for (int k = 0; k < M; ++k) s_R[tid * M + k] = h[k];
+                uint64_t sm = 0;
+                for (int i = 0; i < depth; ++i) sm |= 1ull << pre[i];
+                s_um[tid] = ~sm & valid;
+            }
+            __syncthreads();
+        }
         // per parent and job code: byte offset of the job's child row in Mq relative to
         // the parent's first child row (rank of the job among U), or of the dummy row
         // for a scheduled / absent job

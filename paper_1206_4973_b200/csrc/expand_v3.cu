@@ -163,7 +163,8 @@ __global__ void __launch_bounds__(NW <= 4 ? 192 : 256, NW <= 4 ? 3 : 2)
             const int pp = x / depth, i = x - pp * depth;
             s_pre[pp * N + i] = src.prefix[(first + step * (p0 + pp)) * n + i];
         }
-        for (int x = tid; x < np * NW; x += bd) {
+        const bool compact = src.heads == nullptr;  // prefix-only rows (host-resident tree)
+        for (int x = tid; x < np * NW && !compact; x += bd) {
             const int pp = x / NW, w = x - pp * NW;
             const int64_t node = first + step * (p0 + pp);
             const int w64 = w >> 1;
@@ -173,11 +174,33 @@ __global__ void __launch_bounds__(NW <= 4 ? 192 : 256, NW <= 4 ? 3 : 2)
             const uint32_t vmask = valid >= 32 ? 0xFFFFFFFFu : ((1u << valid) - 1u);
             s_u[x] = ~half & vmask;
         }
-        for (int x = tid; x < np * M; x += bd) {
+        for (int x = tid; x < np * M && !compact; x += bd) {
             const int pp = x / M, k = x - pp * M;
             s_R[x] = src.heads[(first + step * (p0 + pp)) * M + k];
         }
         __syncthreads();
+        if (compact) {  // heads and unscheduled set folded from the staged prefixes
+            for (int pp = tid; pp < np; pp += bd) {
+                const uint8_t* pre = s_pre + pp * N;
+                int32_t h[M];
+                heads_from_prefix<M>(pre, depth, [&](int j, int k) { return __ldg(t.p + j * M + k); }, h);
+#pragma unroll
+                for (int k = 0; k < M; ++k) s_R[pp * M + k] = h[k];
+            }
+            for (int x = tid; x < np * NW; x += bd) {
+                const int pp = x / NW, w = x - pp * NW;
+                const uint8_t* pre = s_pre + pp * N;
+                uint32_t sched = 0;
+                for (int i = 0; i < depth; ++i) {
+                    const int j = pre[i];
+                    if ((j >> 5) == w) sched |= 1u << (j & 31);
+                }
+                const int valid = min(32, max(0, n - 32 * w));
+                const uint32_t vmask = valid >= 32 ? 0xFFFFFFFFu : ((1u << valid) - 1u);
+                s_u[x] = ~sched & vmask;
+            }
+            __syncthreads();
+        }
         // per parent and job: the slot table and the ascending list of unscheduled jobs
         for (int x = tid; x < np * N; x += bd) {
             const int pp = x / N, j = x - pp * N;

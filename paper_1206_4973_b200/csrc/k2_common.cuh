@@ -33,6 +33,24 @@ __device__ inline int64_t claim_chunk(RoundState* rs, int64_t c_begin, int64_t* 
     return *s_slot;
 }
 
+// Compact pending rows (the host-resident tree stores prefixes only, see capi.cu): a
+// parent's heads are child_heads (instance.hpp:81-89) folded over its prefix.  One
+// thread per parent, the M heads in registers; pj(j, k) = p[j][k].
+template <int M, class PJ>
+__device__ __forceinline__ void heads_from_prefix(const uint8_t* pre, int depth, PJ pj, int32_t (&h)[M]) {
+#pragma unroll
+    for (int k = 0; k < M; ++k) h[k] = 0;
+    for (int i = 0; i < depth; ++i) {
+        const int j = pre[i];
+        int32_t prev = 0;
+#pragma unroll
+        for (int k = 0; k < M; ++k) {
+            prev = max(prev, h[k]) + pj(j, k);
+            h[k] = prev;
+        }
+    }
+}
+
 __device__ __forceinline__ void leaf_offer(RoundState* rs, int32_t value, int64_t pos) {
     // min over (value, position) == max over its complement; 0 means "none yet"
     unsigned long long key = ((unsigned long long)(uint32_t)value << 32) | (uint32_t)pos;

@@ -334,11 +334,40 @@ def test_k2_generic_and_specialised_agree(monkeypatch):
         assert outs[0] == outs[1], (n, m)
 
 
+@pytest.mark.parametrize("nm_sel", [((20, 20), "auto"), ((30, 10), "auto"), ((50, 20), "auto"),
+                                    ((100, 20), "auto"), ((70, 5), "auto"), ((20, 7), "auto"),
+                                    ((20, 20), "generic")],
+                         ids=lambda v: f"{v[0][0]}x{v[0][1]}-{v[1]}")
+def test_host_tree_row_formats_match_hbm(nm_sel, monkeypatch):
+    """The host-resident pending tree in its compact form (prefixes only: every K2 kernel
+    folds heads and masks from the prefix when it stages a parent, and place_kernel moves
+    only the prefix bytes up to the child depth) and in the full-row form both reproduce
+    the HBM-resident explorer round for round, pending tree included."""
+    (n, m), sel = nm_sel
+    monkeypatch.setenv("FBB_K2", sel)
+    rng = np.random.default_rng(n * 31 + m)
+    inst = inst_of(rng.integers(1, 100, size=(n, m)).astype(np.int32))
+    ub = fbb.makespan(inst, list(range(n))) - 1
+    out = {}
+    for mode in ("hbm", "host", "host_full"):
+        monkeypatch.setenv("FBB_HOST_ROWS", "full" if mode == "host_full" else "compact")
+        ctx = fbb.Context(inst)
+        ctx.explorer_set_residency(mode != "hbm")
+        ctx.explorer_reset(fbb.NodeBatch.root(inst), ub, frozen=True)
+        rounds = ctx.explorer_run([64, 1024, 4096, 16384], 40, 400_000)
+        out[mode] = (rounds, ctx.explorer_pending(), ctx.explorer_state()["bounded"])
+        ctx.close()
+    assert len(out["hbm"][0]) > 3
+    assert out["host"] == out["hbm"] and out["host_full"] == out["hbm"]
+
+
 @pytest.mark.parametrize("on_host", [False, True], ids=["pending_hbm", "pending_host"])
 def test_device_planned_loop_matches_reference(instances, traces, on_host, monkeypatch):
     """The batched, device-planned explorer loop (FBB_DEVICE_LOOP=1) reproduces the
-    reference's per-round traces like the host-planned one."""
+    reference's per-round traces like the host-planned one (host-resident: full rows,
+    the form the device loop reads)."""
     monkeypatch.setenv("FBB_DEVICE_LOOP", "1")
+    monkeypatch.setenv("FBB_HOST_ROWS", "full")
     for tr in traces["resolve"][:4]:
         inst = inst_of(instance_p(instances, tr["instance"]))
         ctx = fbb.Context(inst)  # a fresh context picks up the environment
