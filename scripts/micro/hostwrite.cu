@@ -1,6 +1,6 @@
 // Micro-benchmark: GPU stores into pinned, device-mapped host memory (the e2e
-// Build: nvcc -O2 -gencode arch=compute_100a,code=sm_100a -o scripts/micro/hostwrite scripts/micro/hostwrite.cu
 // explorer's survivor path).  Prints us per launch for sizes x store widths x grids.
+// Build: nvcc -O2 -gencode arch=compute_100a,code=sm_100a -o scripts/micro/hostwrite scripts/micro/hostwrite.cu
 #include <cstdio>
 #include <cstdint>
 #include <cuda_runtime.h>

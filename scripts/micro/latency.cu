@@ -1,7 +1,7 @@
 // Micro-benchmark: per-round fixed costs on the stream -- small pinned H2D / D2H
-// Build: nvcc -O2 -gencode arch=compute_100a,code=sm_100a -o scripts/micro/latency scripts/micro/latency.cu
 // copies vs a kernel with a large __grid_constant__ parameter vs a kernel storing a
 // few hundred bytes into mapped host memory.
+// Build: nvcc -O2 -gencode arch=compute_100a,code=sm_100a -o scripts/micro/latency scripts/micro/latency.cu
 #include <cstdio>
 #include <cstdint>
 #include <cuda_runtime.h>
