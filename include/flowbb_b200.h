@@ -76,7 +76,7 @@ typedef struct {
     float sync_ms;     /* part of host_ms spent waiting for the device */
     int64_t h2d_bytes; /* host -> device bytes of the round (host-resident explorer) */
     int64_t d2h_bytes; /* device -> host bytes of the round (host-resident explorer) */
-    float place_ms;    /* device time of place_kernel (survivors -> pending buckets) */
+    float place_ms;    /* device time of place_kernel + the round summary download */
     int32_t reserved;
 } fbb_round_t;
 

@@ -197,7 +197,7 @@ struct fbb_ctx {
     HBuf h_pool, h_round;
     DBuf d_rp;              // host-planned rounds: [RoundState | Pool], uploaded by one copy
     HBuf h_rp;              // its pinned source; the RoundState part stays zero
-    cudaEvent_t ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
     // batched device-planned explorer loop (explorer_loop.cu)
     DBuf d_loop;
     HBuf h_loop;
@@ -352,7 +352,6 @@ int run_pool(fbb_ctx* ctx, Pool& pool, int first_internal, int32_t ub, int froze
        "K2 internal");
     CK(cudaEventRecord(ctx->ev[2], st), "event");
     CK(launch_place(ctx->dt, ctx->k2, dp, pool, rs, out, st), "place");
-    CK(cudaEventRecord(ctx->ev[4], st), "event");
     launches += has_internal ? 2 : 0;  // K2 + place
     // one download: the counters (and, after a leaf round, the schedule behind them)
     const size_t head = has_leaf ? offsetof(RoundState, schedule) + (size_t)n * 4
@@ -366,14 +365,7 @@ int run_pool(fbb_ctx* ctx, Pool& pool, int first_internal, int32_t ub, int froze
         return ctx->fail(FBB_E_STATE, "corrupt pending node (unscheduled-job count mismatch)");
     cudaEventElapsedTime(&ctx->last_k2_ms, ctx->ev[1], ctx->ev[2]);
     cudaEventElapsedTime(&ctx->last_round_ms, ctx->ev[0], ctx->ev[3]);
-    cudaEventElapsedTime(&ctx->last_place_ms, ctx->ev[2], ctx->ev[4]);
-    if (getenv("FBB_TIMING_DEBUG")) {
-        float pre = 0.f, post = 0.f;
-        cudaEventElapsedTime(&pre, ctx->ev[0], ctx->ev[1]);
-        cudaEventElapsedTime(&post, ctx->ev[4], ctx->ev[3]);
-        std::fprintf(stderr, "[fbb] pre %.1f us  k2 %.1f  place %.1f  post %.1f\n", pre * 1e3,
-                     ctx->last_k2_ms * 1e3, ctx->last_place_ms * 1e3, post * 1e3);
-    }
+    cudaEventElapsedTime(&ctx->last_place_ms, ctx->ev[2], ctx->ev[3]);  // place + summary download
     ctx->last_launches = launches;
     return FBB_OK;
 }
@@ -549,6 +541,7 @@ int explorer_round(fbb_ctx* ctx, int64_t target, fbb_round_t* rec) {
     }
     if (local.nseg == 0) return FBB_OK;
     int first_internal = layout_pool(ctx, local);
+    local.host_dst = ctx->host_pending && ctx->mapped_out;  // survivors written over the host link
     // destinations (bucket depth+1) sized for the worst case before launching
     // device buckets: sized for the worst case (all children survive) before K2 writes
     // into them; host buckets grow after the round, to the actual survivor count
@@ -1090,6 +1083,7 @@ int fbb_expand_bound_prune(fbb_ctx* ctx, const uint64_t* masks, const int32_t* h
     CK(cudaMemcpyAsync(in.heads.p, heads, (size_t)nparents * m * 4, cudaMemcpyHostToDevice, st), "H2D");
     CK(cudaMemcpyAsync(in.prefix.p, prefix, (size_t)nparents * n, cudaMemcpyHostToDevice, st), "H2D");
     int first_internal = layout_pool(ctx, pool);
+    pool.host_dst = 0;  // survivors go to the device output batch
     CK(store_ensure(ctx, ctx->batch_out, std::max<int64_t>(pool.nchildren, 1), 0), "alloc");
     CK(ctx->out_lb.ensure((size_t)std::max<int64_t>(pool.nchildren, 1) * 4), "alloc");
     for (int s = 0; s < pool.nseg; ++s) {

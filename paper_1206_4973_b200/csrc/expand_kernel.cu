@@ -597,13 +597,13 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(DevTables t, const
         copy_array(out.nodes.masks, W * 8, W * 8, [&](int row) { return (void*)s_store[s_rc[row]].masks; });
     }
     // prefix rows up to the child depth (the bytes past it are don't-care in both places)
-    if (2 * s_need <= n) {
+    if (2 * s_need <= n || !pool->host_dst) {
         copy_array(out.nodes.prefix, n, s_need, [&](int row) { return (void*)s_store[s_rc[row]].prefix; });
     } else {
-        // mostly-used rows: whole rows, as one contiguous byte range per chunk written in
-        // aligned 16-byte stores (a host-mapped destination takes ~2x more bytes/s from
-        // full 16-byte stores than from 4-byte row-unit stores); the 16-byte blocks of
-        // all the CTA's chunks form one flat index space
+        // host buckets, mostly-used rows: whole rows, as one contiguous byte range per
+        // chunk written in aligned 16-byte stores (the host link takes ~2x more bytes/s
+        // from those than from 4-byte row-unit stores; in HBM the row form is faster);
+        // the 16-byte blocks of all the CTA's chunks form one flat index space
         __shared__ int64_t s_blk[kPlaceChunks + 1];
         if (tid == 0) {
             int64_t acc = 0;

@@ -98,6 +98,7 @@ __global__ void loop_plan_kernel(DevTables t, LoopState* ls, Pool* pool, RoundSt
     pool->nchunks = chunk;
     pool->nchildren = child;
     pool->pad = 0;
+    pool->host_dst = 0;
     pool->nseg = nseg;
 }
 

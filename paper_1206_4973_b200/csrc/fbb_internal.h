@@ -132,7 +132,7 @@ struct Pool {
     int32_t ub;          // pruning bound of the round (the incumbent, or the frozen UB)
     int32_t frozen;      // resolve (1) or solve (0) semantics
     int32_t first_internal;  // first segment with internal children (nseg: none)
-    int32_t pad2;
+    int32_t host_dst;    // survivors go to pinned host buckets (place: contiguous 16-byte stores)
     Segment seg[kMaxSegments];
 };
 

@@ -43,6 +43,10 @@ int main() {
         }
         printf("%-40s best %6.2f us  mean %6.2f us\n", what, best * 1e3, sum / 45 * 1e3);
     };
+    time("H2D 448 B pinned", [&] { cudaMemcpyAsync(d, hp, 448, cudaMemcpyHostToDevice, st); });
+    time("H2D 448 B + memset 2 KB", [&] { cudaMemcpyAsync(d, hp, 448, cudaMemcpyHostToDevice, st);
+                                         cudaMemsetAsync((char*)d + 8192, 0, 2048, st); });
+    time("event record x1 extra", [&] { cudaEventRecord(e[2], st); });
     time("H2D 3.5 KB pinned", [&] { cudaMemcpyAsync(d, hp, 3584, cudaMemcpyHostToDevice, st); });
     time("H2D 3.5 KB + memset 2 KB", [&] { cudaMemcpyAsync(d, hp, 3584, cudaMemcpyHostToDevice, st);
                                            cudaMemsetAsync((char*)d + 8192, 0, 2048, st); });
