@@ -613,13 +613,10 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
         if (keep) {
             const int64_t o = chunk * (int64_t)cmax + woff + __popc(ballot & ((1u << lane) - 1u));
             const NodeStore dst = out.nodes;
-#pragma unroll
-            for (int k = 0; k < M; ++k) dst.heads[o * M + k] = myR[k];
+            store_heads<M>(dst.heads + o * M, myR);
             const uint64_t valid = n >= 64 ? ~0ull : ((1ull << n) - 1ull);
             dst.masks[o * W] = (~s_um[mypp] & valid) | (1ull << myx);
-            uint8_t* dp = dst.prefix + o * n;
-            for (int i = 0; i < depth; ++i) dp[i] = s_pre[mypp * RW + i];
-            dp[depth] = (uint8_t)myx;
+            store_prefix(dst.prefix + o * n, s_pre + mypp * RW, depth, myx, n);
             out.lb[o] = mylb;
         }
         if constexpr (kPipe) {

@@ -348,8 +348,7 @@ __global__ void __launch_bounds__(NW <= 4 ? 192 : 256, NW <= 4 ? 3 : 2)
         if (keep) {
             const int64_t o = chunk * (int64_t)cmax + woff + __popc(ballot & ((1u << lane) - 1u));
             const NodeStore dst = out.nodes;
-#pragma unroll
-            for (int k = 0; k < M; ++k) dst.heads[o * M + k] = myR[k];
+            store_heads<M>(dst.heads + o * M, myR);
             const uint32_t* u = s_u + mypp * NW;
             for (int w = 0; w < W; ++w) {
                 const uint32_t lo = 2 * w < NW ? u[2 * w] : 0u;
@@ -362,9 +361,7 @@ __global__ void __launch_bounds__(NW <= 4 ? 192 : 256, NW <= 4 ? 3 : 2)
                 if ((myx >> 6) == w) sched |= 1ull << (myx & 63);
                 dst.masks[o * W + w] = sched;
             }
-            uint8_t* dp = dst.prefix + o * n;
-            for (int i = 0; i < depth; ++i) dp[i] = s_pre[mypp * N + i];
-            dp[depth] = (uint8_t)myx;
+            store_prefix(dst.prefix + o * n, s_pre + mypp * N, depth, myx, n);
             out.lb[o] = mylb;
         }
     }

@@ -51,6 +51,42 @@ __device__ __forceinline__ void heads_from_prefix(const uint8_t* pre, int depth,
     }
 }
 
+// A survivor's staged row written with the widest stores its alignment allows (one
+// thread per survivor, so narrow stores scatter): heads as 16- or 8-byte vectors, the
+// prefix -- the parent's staged prefix (smem, 4-byte aligned rows) with the child's
+// job at `depth` -- as 4-byte words when rows are word aligned (n % 4 == 0).
+template <int M>
+__device__ __forceinline__ void store_heads(int32_t* dst, const int32_t (&R)[M]) {
+    if constexpr (M % 4 == 0) {
+#pragma unroll
+        for (int k = 0; k < M / 4; ++k)
+            reinterpret_cast<uint4*>(dst)[k] = make_uint4(R[4 * k], R[4 * k + 1], R[4 * k + 2], R[4 * k + 3]);
+    } else if constexpr (M % 2 == 0) {
+#pragma unroll
+        for (int k = 0; k < M / 2; ++k) reinterpret_cast<uint2*>(dst)[k] = make_uint2(R[2 * k], R[2 * k + 1]);
+    } else {
+#pragma unroll
+        for (int k = 0; k < M; ++k) dst[k] = R[k];
+    }
+}
+__device__ __forceinline__ void store_prefix(uint8_t* dp, const uint8_t* sp, int depth, int x, int n) {
+    if ((n & 3) == 0) {
+        const uint32_t* s32 = reinterpret_cast<const uint32_t*>(sp);
+        uint32_t* d32 = reinterpret_cast<uint32_t*>(dp);
+        for (int w = 0; w <= (depth >> 2); ++w) {
+            uint32_t v = s32[w];
+            if (w == (depth >> 2)) {
+                const int sh = (depth & 3) * 8;
+                v = (v & ~(0xFFu << sh)) | ((uint32_t)x << sh);
+            }
+            d32[w] = v;
+        }
+    } else {
+        for (int i = 0; i < depth; ++i) dp[i] = sp[i];
+        dp[depth] = (uint8_t)x;
+    }
+}
+
 __device__ __forceinline__ void leaf_offer(RoundState* rs, int32_t value, int64_t pos) {
     // min over (value, position) == max over its complement; 0 means "none yet"
     unsigned long long key = ((unsigned long long)(uint32_t)value << 32) | (uint32_t)pos;
