@@ -23,9 +23,12 @@ for n, m in [(20, 20), (20, 5), (50, 20), (100, 20), (12, 7)]:
     par = sorted([list(rng.permutation(n)[: rng.integers(0, n - 2)]) for _ in range(24)], key=len,
                  reverse=True)
     surv, slb, *_ = ctx.expand_bound_prune(fbb.nodes_from_prefixes(inst, par), 10**6, frozen=True)
-    for on_host in (False, True):
-        ctx.explorer_set_residency(on_host)
+    # tree in HBM, in host memory (compact prefix rows at n <= 32), and host full rows;
+    # deep enough at n <= 20 to reach the leaf kernels
+    for mode in ("hbm", "host", "host_full"):
+        os.environ["FBB_HOST_ROWS"] = "full" if mode == "host_full" else "compact"
+        ctx.explorer_set_residency(mode != "hbm")
         ctx.explorer_reset(fbb.NodeBatch.root(inst), 10**6, frozen=True)
-        ctx.explorer_run([2048], 3)
+        ctx.explorer_run([2048], n + 2 if n <= 20 else 3)
     ctx.close()
     print("ok", n, m, flush=True)

@@ -238,6 +238,21 @@ def test_explorer_full_solves_match_reference(traces, on_host):
         assert sol.exhausted
 
 
+def test_resolution_equivalent_across_batches_and_tuner(traces):
+    """test_bench.cpp:22-43,97-111 on the device explorer: a frozen-UB resolution to
+    exhaustion explores the same node set whatever the pool size or the tuner does --
+    same bounded count and the same best leaf."""
+    for case in traces["solve_full"][:6]:
+        p = np.asarray(case["p"], np.int32).reshape(case["n"], case["m"])
+        inst = inst_of(p)
+        ub = case["optimum"] + 1
+        runs = [fbb.resolve_workload(inst, [[]], ub, batch=b) for b in (1, 8, 64, 512)]
+        runs.append(fbb.resolve_workload(inst, [[]], ub, autotune=True, window=2, probes=2))
+        for r in runs:
+            assert r.exhausted and r.best == case["optimum"]
+            assert r.nodes_bounded == runs[0].nodes_bounded
+
+
 def test_explorer_pending_matches_oracle_drain(oracle):
     # after a budget stop, the device pending tree equals the reference's (drain order)
     inst = fbb.generate_instance(20, 5, 873654221)
