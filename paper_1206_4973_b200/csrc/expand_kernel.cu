@@ -465,22 +465,33 @@ constexpr int kPlaceChunks = FBB_PLACE_CHUNKS;
 constexpr int kPlaceThreads = 256;
 constexpr int kPlaceBatch = 8;
 
-// Copies rows x width elements: element f = (row, k) with row = f / width.
+// Copies rows x width elements: element f = (row, k) with row = f / width.  The thread's
+// (row, k) advance by a fixed (kPlaceThreads / width, kPlaceThreads % width) step with one
+// carry, so no integer division per element (the division emulation was most of the
+// kernel's instructions).
 template <int B, class Load, class Store>
 __device__ __forceinline__ void copy_rows(int rows, int width, Load load, Store store) {
     const int total = rows * width;
+    const int qs = kPlaceThreads / width, rs = kPlaceThreads - qs * width;
+    int row = threadIdx.x / width, k = threadIdx.x - row * width;
     for (int base = threadIdx.x; base < total; base += B * kPlaceThreads) {
         decltype(load(0, 0)) v[B];
+        int rr[B], kk[B];
 #pragma unroll
         for (int u = 0; u < B; ++u) {
-            const int f = base + u * kPlaceThreads;
-            if (f < total) v[u] = load(f / width, f % width);
+            rr[u] = row;
+            kk[u] = k;
+            if (base + u * kPlaceThreads < total) v[u] = load(row, k);
+            row += qs;
+            k += rs;
+            if (k >= width) {
+                k -= width;
+                ++row;
+            }
         }
 #pragma unroll
-        for (int u = 0; u < B; ++u) {
-            const int f = base + u * kPlaceThreads;
-            if (f < total) store(f / width, f % width, v[u]);
-        }
+        for (int u = 0; u < B; ++u)
+            if (base + u * kPlaceThreads < total) store(rr[u], kk[u], v[u]);
     }
 }
 

@@ -1,8 +1,10 @@
-for T in 4096 16384 65536 131072 262144; do
-  for V in old new; do
-    if [ $V = old ]; then export FBB_NO_ROUND_PPC=1; else unset FBB_NO_ROUND_PPC; fi
-    python bench.py --target $T --steps 100 --no-cpu-baseline --no-e2e 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.readline()); print('$V $T', round(d['value']/1e6,1), round(d['ms_per_step']*1e3,1), 'us', round(d['roofline']['k2_share_of_round'],3))"
-  done
+for i in 1 2 3; do
+  (cd _ab_old && python bench.py --no-e2e --no-cpu-baseline 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.readline()); print('old', round(d['value']/1e6,1), d['ms_per_step'])")
+  python bench.py --no-e2e --no-cpu-baseline 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.readline()); print('new', round(d['value']/1e6,1), d['ms_per_step'])"
 done
-unset FBB_NO_ROUND_PPC
+for I in ta081 ta001; do
+  (cd _ab_old && python bench.py --instance $I --no-e2e --no-cpu-baseline 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.readline()); print('old $I', round(d['value']/1e6,1), d['ms_per_step'])")
+  python bench.py --instance $I --no-e2e --no-cpu-baseline 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.readline()); print('new $I', round(d['value']/1e6,1), d['ms_per_step'])"
+done
+python scripts/diag_e2e.py ta021
 timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -1
