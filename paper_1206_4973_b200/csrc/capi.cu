@@ -224,6 +224,7 @@ struct fbb_ctx {
     bool mapped_out = true;     // place_kernel writes survivors straight into the (device-
                                 // mapped) host buckets; FBB_HOST_OUT=staged: device output + D2H
     int64_t last_h2d = 0, last_d2h = 0;
+    bool summary_by_place = true;  // FBB_SUMMARY=copy: download the round summary instead
     bool check = false;  // FBB_CHECK=1: validate the pending tree after every round
 
     int fail(int code, const std::string& m) {
@@ -351,12 +352,18 @@ int run_pool(fbb_ctx* ctx, Pool& pool, int first_internal, int32_t ub, int froze
     CK(launch_k2_internal(ctx->dt, ctx->k2, dp, pool, first_internal, ub, frozen, rs, out, st),
        "K2 internal");
     CK(cudaEventRecord(ctx->ev[2], st), "event");
-    CK(launch_place(ctx->dt, ctx->k2, dp, pool, rs, out, st), "place");
+    // with internal chunks, place_kernel's last CTA writes the round summary straight into
+    // the pinned (UVA-mapped) h_round; otherwise one download of the counters (and, after
+    // a leaf round, the schedule behind them)
+    const bool publish = has_internal && ctx->summary_by_place;
+    CK(launch_place(ctx->dt, ctx->k2, dp, pool, rs, out, st, publish ? ctx->h_round.as<RoundState>() : nullptr),
+       "place");
     launches += has_internal ? 2 : 0;  // K2 + place
-    // one download: the counters (and, after a leaf round, the schedule behind them)
-    const size_t head = has_leaf ? offsetof(RoundState, schedule) + (size_t)n * 4
-                                 : offsetof(RoundState, seg_surv) + (size_t)pool.nseg * 8;
-    CK(cudaMemcpyAsync(ctx->h_round.p, rs, head, cudaMemcpyDeviceToHost, st), "round D2H");
+    if (!publish) {
+        const size_t head = has_leaf ? offsetof(RoundState, schedule) + (size_t)n * 4
+                                     : offsetof(RoundState, seg_surv) + (size_t)pool.nseg * 8;
+        CK(cudaMemcpyAsync(ctx->h_round.p, rs, head, cudaMemcpyDeviceToHost, st), "round D2H");
+    }
     CK(cudaEventRecord(ctx->ev[3], st), "event");
     const auto t_sync = std::chrono::steady_clock::now();
     CK(cudaStreamSynchronize(st), "round");
@@ -907,6 +914,8 @@ fbb_ctx* fbb_create(int device, const int32_t* p, int n, int m) {
     // opt-in (FBB_DEVICE_LOOP=1) and covered by the parity tests.
     const char* dlp = getenv("FBB_DEVICE_LOOP");
     ctx->device_loop = dlp && dlp[0] == '1';
+    const char* sm = getenv("FBB_SUMMARY");
+    ctx->summary_by_place = !(sm && std::string(sm) == "copy");
     const char* chk = getenv("FBB_CHECK");
     ctx->check = chk && chk[0] == '1';
     return ctx;

@@ -499,8 +499,12 @@ __device__ __forceinline__ void copy_rows(int rows, int width, Load load, Store 
 // pool size the host does not know); otherwise one group per CTA -- the plain form,
 // measurably faster (19 vs 26 us per 262K-child round) when the host sizes the grid.
 template <bool kGridStride>
+// summary (non-null, one-group form only): the last CTA past the counting copies the
+// round's counters (and the leaf schedule) into this mapped host RoundState, which
+// replaces the summary download (one stream operation less per round).
 __global__ void __launch_bounds__(kPlaceThreads) place_kernel(DevTables t, const Pool* __restrict__ pool,
-                                                              int cmax, RoundState* rs, ChunkOut out) {
+                                                              int cmax, RoundState* rs, ChunkOut out,
+                                                              RoundState* summary) {
     const int n = t.n, m = t.m, W = t.W;
     __shared__ int s_row0[kPlaceChunks + 1];  // CTA-local exclusive survivor offsets
     __shared__ int s_seg[kPlaceChunks];
@@ -576,9 +580,23 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(DevTables t, const
     }
     const int R = s_row0[nch];
     if (tid == 0 && R) atomicAdd((unsigned long long*)&rs->total, (unsigned long long)R);
+    if (!kGridStride && summary && tid < max(nch, 1)) __threadfence();  // this CTA's counts, device-wide
     for (int c = 0; c < nch; ++c)
         for (int row = s_row0[c] + tid; row < s_row0[c + 1]; row += kPlaceThreads) s_rc[row] = (uint8_t)c;
     __syncthreads();
+    if (!kGridStride && summary) {
+        __shared__ int s_last;
+        if (tid == 0) s_last = atomicAdd(&rs->place_done, 1u) == gridDim.x - 1;
+        __syncthreads();
+        if (s_last) {  // every CTA's counts are in: publish the summary
+            __threadfence();
+            const int words = (int)((offsetof(RoundState, seg_surv) + (size_t)pool->nseg * 8) / 8);
+            const unsigned long long* src = reinterpret_cast<const unsigned long long*>(rs);
+            unsigned long long* dst = reinterpret_cast<unsigned long long*>(summary);
+            for (int i = tid; i < words; i += kPlaceThreads) dst[i] = __ldcg(src + i);
+            for (int i = tid; i < t.n; i += kPlaceThreads) summary->schedule[i] = __ldcg(rs->schedule + i);
+        }
+    }
     auto src_row = [&](int row) { const int c = s_rc[row]; return (c0 + c) * (int64_t)cmax + (row - s_row0[c]); };
     auto dst_row = [&](int row) { const int c = s_rc[row]; return s_dst[c] + (row - s_row0[c]); };
     // Each array moves row by row in the widest unit that divides its row size (rows of
@@ -723,11 +741,12 @@ cudaError_t launch_leaf_schedule(const DevTables& t, const Pool* d_pool, RoundSt
 namespace fbb {
 
 cudaError_t launch_place(const DevTables& t, const K2Config& cfg, const Pool* d_pool,
-                         const Pool& h_pool, RoundState* rs, ChunkOut out, cudaStream_t stream) {
+                         const Pool& h_pool, RoundState* rs, ChunkOut out, cudaStream_t stream,
+                         RoundState* summary) {
     if (h_pool.nchunks == 0) return cudaSuccess;
     const int64_t blocks = (h_pool.nchunks + kPlaceChunks - 1) / kPlaceChunks;
     place_kernel<false><<<(unsigned)blocks, kPlaceThreads, (size_t)cfg.cmax * kPlaceChunks, stream>>>(
-        t, d_pool, cfg.cmax, rs, out);
+        t, d_pool, cfg.cmax, rs, out, summary);
     return cudaGetLastError();
 }
 
@@ -757,7 +776,7 @@ cudaError_t launch_round_device(const DevTables& t, const K2Config& cfg, const P
                                                                                  rs, out);
     if (k2_end) cudaEventRecord(k2_end, stream);
     place_kernel<true><<<148 * 2, kPlaceThreads, (size_t)cfg.cmax * kPlaceChunks, stream>>>(t, d_pool, cfg.cmax, rs,
-                                                                                      out);
+                                                                                      out, nullptr);
     e = cudaGetLastError();
     return e;
 }

@@ -164,6 +164,8 @@ struct RoundState {
     int32_t found;                // leaf schedule written (value < ub)
     uint32_t ticket;              // next chunk to claim
     int64_t total;                // survivors of the pool
+    uint32_t place_done;          // place CTAs past their counting (the last one publishes)
+    uint32_t pad;
     int64_t seg_surv[kMaxSegments];
     int32_t schedule[kMaxJobs];
 };
@@ -192,7 +194,8 @@ cudaError_t launch_k2_internal(const DevTables& t, const K2Config& cfg, const Po
 // Every chunk's survivors moved, in batch order, to its segment's dst; per-segment
 // and pool survivor totals added to `rs` (zeroed before the round).
 cudaError_t launch_place(const DevTables& t, const K2Config& cfg, const Pool* d_pool,
-                         const Pool& h_pool, RoundState* rs, ChunkOut out, cudaStream_t stream);
+                         const Pool& h_pool, RoundState* rs, ChunkOut out, cudaStream_t stream,
+                         RoundState* summary = nullptr);
 // Schedule of the best leaf when it beats ub (before the parents are recycled).
 cudaError_t launch_leaf_schedule(const DevTables& t, const Pool* d_pool, RoundState* rs,
                                  int32_t ub, cudaStream_t stream);
