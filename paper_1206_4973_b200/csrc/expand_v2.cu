@@ -310,7 +310,7 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
     // compute), and the next ticket is claimed during setup, so a chunk costs one
     // barrier less.  At 3 CTAs/SM (96 registers) the staging loads stay direct.
     constexpr bool kPipe = OCC == 2 && N != 32;  // (N = 32: the prefetch registers spill)
-    constexpr int kPpcCt = N <= 32 ? 43 : 16;                  // >= parents per chunk
+    constexpr int kPpcCt = N <= 32 ? 64 : 16;                  // >= parents per chunk (cmax / 3)
     constexpr int kPfPre = (kPpcCt * N + 191) / 192;           // prefix bytes per thread
     constexpr int kPfHead = (kPpcCt * M + 191) / 192;          // heads per thread
     uint32_t pf_pre[kPipe ? kPfPre : 1];
@@ -652,8 +652,15 @@ bool k2_v2_config(const DevTables& t, int device, K2Config* out) {
     // 16x2 grouped Phase B, m in {5, 10} at 3 CTAs/SM; FBB_K2_OCC=2|3 overrides
     const char* occ_env = getenv("FBB_K2_OCC");
     const int occ = occ_env ? (occ_env[0] == '2' ? 2 : 3) : (m == 20 ? 2 : 3);
-    c.cmax = occ == 3 ? 112 : 128;
     const int NN = n <= 20 ? 20 : (n <= 32 ? 32 : 64);
+    // children per chunk, measured (profiles/r01_k2_iterations.md): larger chunks amortise
+    // the per-chunk setup and barriers while the CTAs per SM hold -- Ta021 (m = 20, 2
+    // CTAs/SM) 128 -> 160: +3.9 %, 192 drops to 1 CTA/SM; Ta001 (m = 5, 3 CTAs/SM)
+    // 112 -> 192: +7 %; the wide variant (n > 32) stays at 128 (160: -22 %)
+    c.cmax = NN == 64 ? (occ == 3 ? 112 : 128) : (occ == 3 ? 192 : 160);
+    if (const char* cm = getenv("FBB_K2_CMAX")) c.cmax = std::max(32, std::min(192, atoi(cm)));
+    // the per-parent u16 offset tables address up to (cmax + dummy rows) Mq rows
+    while (c.cmax > 32 && (size_t)(c.cmax + v2_dummy_rows(t.P)) * v2_row_bytes(m) > 65535) c.cmax -= 16;
     c.variant = occ * 10000 + NN * 100 + m;
     c.ppc_cap = NN <= 32 ? 0 : v2_ppc_cap(NN);
     c.jm_in_smem = false;

@@ -1,11 +1,8 @@
-for i in 1 2 3; do
-  for V in old new; do
-    if [ $V = old ]; then export FBB_SUMMARY=copy; else unset FBB_SUMMARY; fi
-    for I in ta021 ta001; do
-    python bench.py --instance $I --no-e2e --no-cpu-baseline 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.readline()); print('$V $I', round(d['value']/1e6,1), round(d['ms_per_step']*1e3,2))"
-    done
+for i in 1 2; do
+  for C in 112 128 144 160 176 192; do
+    FBB_K2_CMAX=$C python bench.py --instance ta001 --no-e2e --no-cpu-baseline 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.readline()); print('ta001 cmax $C', round(d['value']/1e6,1), round(d['ms_per_step']*1e3,2), round(d['roofline']['k2_share_of_round'],3))"
   done
 done
-unset FBB_SUMMARY
-python scripts/diag_e2e.py ta021
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -1
+for C in 128 160; do
+FBB_K2_CMAX=$C python bench.py --instance ta051 --no-e2e --no-cpu-baseline 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.readline()); print('ta051 cmax $C', round(d['value']/1e6,1), round(d['ms_per_step']*1e3,2))"
+done
