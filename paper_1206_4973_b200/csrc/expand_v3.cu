@@ -388,6 +388,8 @@ bool k2_v3_config(const DevTables& t, int device, K2Config* out) {
     const int NW = n <= 128 ? 4 : 8;
     c.cmax = ((n + 31) / 32) * 32;          // one parent's children always fit a chunk
     c.threads = NW <= 4 ? 192 : 256;        // >= cmax (Phase B: a child per thread), >= P
+    if (const char* cm = getenv("FBB_K2_CMAX"))
+        c.cmax = std::max(c.cmax, std::min(c.threads, (atoi(cm) / 32) * 32));
     c.ppc_cap = kV3Ppc;
     c.variant = 100000 + NW * 100 + m;
     c.jm_in_smem = false;
