@@ -900,6 +900,9 @@ fbb_ctx* fbb_create(int device, const int32_t* p, int n, int m) {
             if (k2_v2_config(ctx->dt, device, &kc)) ctx->k2 = kc;
             else if (k2_v3_config(ctx->dt, device, &kc)) ctx->k2 = kc;
         }
+        // a variant that could not be configured must not leave its error behind for the
+        // next launch check (cudaGetLastError)
+        (void)cudaGetLastError();
     }
     int max_smem = 0;
     cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
