@@ -71,12 +71,14 @@ struct V2Layout {
 __host__ __device__ inline int v2_rw(int N) { return N <= 32 ? 32 : 64; }
 // Parents per chunk: the wide variant caps them at 16 so that its per-parent arrays
 // leave room for 2 CTAs per SM (its 64-position rows take 48 KB).
-__host__ __device__ inline int v2_ppc_cap(int N) { return N <= 32 ? (1 << 20) : 16; }
+// Measured: 32 at 2 CTAs/SM (smaller per-parent arrays and prefetch registers, +3 % at
+// Ta021), none at 3 CTAs/SM (Ta001 -2.3 % with it), 16 for the wide variant.
+__host__ __device__ inline int v2_ppc_cap(int N, int occ) { return N <= 32 ? (occ == 2 ? 32 : (1 << 20)) : 16; }
 
-__host__ __device__ inline V2Layout v2_layout(int n, int m, int P, int cmax, int threads, int N) {
+__host__ __device__ inline V2Layout v2_layout(int n, int m, int P, int cmax, int threads, int N, int occ) {
     V2Layout L;
     L.ppc_max = cmax / 3 > 0 ? cmax / 3 : 1;
-    if (L.ppc_max > v2_ppc_cap(N)) L.ppc_max = v2_ppc_cap(N);
+    if (L.ppc_max > v2_ppc_cap(N, occ)) L.ppc_max = v2_ppc_cap(N, occ);
     L.rowb = v2_row_bytes(m);
     size_t o = 0;
     L.row = o;  o = b16(o + (size_t)N * P * 4);  // rows padded to N positions
@@ -156,7 +158,7 @@ __device__ __forceinline__ int32_t scan_block(uint32_t row_sa, uint32_t slo, uin
     for (int i = 0; i < NB; ++i) e[i] = lds_u32(row_sa + (uint32_t)(i * P * 4));
     uint32_t at[NB];
 #pragma unroll
-    for (int i = 0; i < NB; ++i) at[i] = base_sa + lds_u16(off_sa + (e[i] & (WIDE ? 63u : 31u)) * 2u);
+    for (int i = 0; i < NB; ++i) at[i] = base_sa + (lds_u16(off_sa + (e[i] & (WIDE ? 63u : 31u)) * 2u) << 4);
     int32_t D = D0, PM = PM0;
     int32_t pm[NB], ce[NB], ndm[NB];
 #pragma unroll
@@ -205,8 +207,8 @@ __device__ __forceinline__ void scan_pair16(uint32_t row_sa, uint32_t s0, uint32
     for (int i = 0; i < NB; ++i) {
         const uint32_t e = lds_u32(row_sa + (uint32_t)(i * P * 4));
         const uint32_t code2 = (e & 31u) * 2u;
-        at0[i] = base0 + lds_u16(off0 + code2);
-        at1[i] = base1 + lds_u16(off1 + code2);
+        at0[i] = base0 + (lds_u16(off0 + code2) << 4);  // tables hold offsets / 16
+        at1[i] = base1 + (lds_u16(off1 + code2) << 4);
         const uint32_t f0 = __funnelshift_l(0u, s0, e), f1 = __funnelshift_l(0u, s1, e);
         uint32_t m2, c2, d2;
         asm("prmt.b32 %0, %1, %2, 0xFFBB;" : "=r"(m2) : "r"(f0), "r"(f1));  // 0xFFFF where scheduled
@@ -243,7 +245,7 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
     constexpr bool kDual16 = OCC == 2 && N == 20;  // Phase A: two parents per thread, 16x2
     extern __shared__ __align__(16) unsigned char smem[];
     const int n = t.n, W = t.W;
-    const V2Layout L = v2_layout(n, M, P, cmax, blockDim.x, N);
+    const V2Layout L = v2_layout(n, M, P, cmax, blockDim.x, N, OCC);
     uint64_t* s_um = (uint64_t*)(smem + L.um);  // unscheduled jobs of each parent
     constexpr int RW = N <= 32 ? 32 : 64;
     uint16_t* s_off = (uint16_t*)(smem + L.rank);  // per parent: Mq byte offset of each job code
@@ -310,7 +312,7 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
     // compute), and the next ticket is claimed during setup, so a chunk costs one
     // barrier less.  At 3 CTAs/SM (96 registers) the staging loads stay direct.
     constexpr bool kPipe = OCC == 2 && N != 32;  // (N = 32: the prefetch registers spill)
-    constexpr int kPpcCt = N <= 32 ? 64 : 16;                  // >= parents per chunk (cmax / 3)
+    constexpr int kPpcCt = N <= 32 ? 32 : 16;                  // >= parents per chunk (v2_ppc_cap)
     constexpr int kPfPre = (kPpcCt * N + 191) / 192;           // prefix bytes per thread
     constexpr int kPfHead = (kPpcCt * M + 191) / 192;          // heads per thread
     uint32_t pf_pre[kPipe ? kPfPre : 1];
@@ -320,7 +322,7 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
         s_ = v2_find_segment(pool, first_seg, c);
         const Segment& g_ = pool->seg[s_];
         depth_ = g_.depth;
-        const int ppc_ = min(cmax / (n - depth_), v2_ppc_cap(N));
+        const int ppc_ = min(cmax / (n - depth_), v2_ppc_cap(N, OCC));
         p0_ = (c - g_.chunk_base) * ppc_;
         np_ = (int)(g_.count - p0_ < ppc_ ? g_.count - p0_ : ppc_);
     };
@@ -406,7 +408,7 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
             }
             __syncthreads();
         }
-        // per parent and job code: byte offset of the job's child row in Mq relative to
+        // per parent and job code: offset (/16) of the job's child row in Mq relative to
         // the parent's first child row (rank of the job among U), or of the dummy row
         // for a scheduled / absent job
         for (int x = tid; x < np * RW; x += bd) {
@@ -415,7 +417,7 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
             const uint64_t um = s_um[pp];
             const bool in = j < n && ((um >> j) & 1ull);
             const int row = in ? __popcll(um & ((1ull << j) - 1ull)) : cmax + pp % v2_dummy_rows(P) - pp * r;
-            s_off[x] = (uint16_t)(row * L.rowb);
+            s_off[x] = (uint16_t)(row * L.rowb / 16);  // rows are 16-byte multiples
         }
         // per (parent, machine): load, two smallest tails (+ argmin, smallest job on ties)
         for (int x = tid; x < np * M; x += bd) {
@@ -660,11 +662,11 @@ bool k2_v2_config(const DevTables& t, int device, K2Config* out) {
     c.cmax = NN == 64 ? (occ == 3 ? 112 : 128) : (occ == 3 ? 192 : 160);
     if (const char* cm = getenv("FBB_K2_CMAX")) c.cmax = std::max(32, std::min(192, atoi(cm)));
     // the per-parent u16 offset tables address up to (cmax + dummy rows) Mq rows
-    while (c.cmax > 32 && (size_t)(c.cmax + v2_dummy_rows(t.P)) * v2_row_bytes(m) > 65535) c.cmax -= 16;
+    while (c.cmax > 32 && (size_t)(c.cmax + v2_dummy_rows(t.P)) * v2_row_bytes(m) / 16 > 65535) c.cmax -= 16;
     c.variant = occ * 10000 + NN * 100 + m;
-    c.ppc_cap = NN <= 32 ? 0 : v2_ppc_cap(NN);
+    c.ppc_cap = v2_ppc_cap(NN, occ) < (1 << 20) ? v2_ppc_cap(NN, occ) : 0;
     c.jm_in_smem = false;
-    c.smem = v2_layout(n, m, t.P, c.cmax, c.threads, NN).total;
+    c.smem = v2_layout(n, m, t.P, c.cmax, c.threads, NN, occ).total;
     cudaError_t e;
     switch (c.variant) {
         case 22005: e = v2_setup<20, 5, 2>(t, c, device); break;
