@@ -725,7 +725,8 @@ def main():
     alg_bytes = (branched * node_b) + survivors * (2 * node_b + 4)  # parents in, survivors staged+pushed
     k2_s = k2_ms / 1e3
     roofline = {
-        "bound": "int32-alu", "kernel": "k2_internal_kernel (fused expand+bound+prune)",
+        "bound": "int32-alu",
+        "kernel": (k2_traffic(inst_name) or {}).get("kernel", "K2") + " (fused expand+bound+prune+compact)",
         "achieved": ops / k2_s / 1e9 if k2_s > 0 else 0.0, "peak": int_peak, "unit": "Gop/s",
         "frac": (ops / k2_s / 1e9) / int_peak if k2_s > 0 else 0.0,
         "traffic": (k2_traffic(inst_name) or {}).get("bytes_per_launch"),
