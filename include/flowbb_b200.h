@@ -68,7 +68,8 @@ typedef struct {
     int64_t pruned;    /* internal children eliminated (lb >= incumbent) */
     int64_t leaves;    /* complete children */
     int32_t incumbent; /* incumbent after the round (frozen: best leaf < UB, else UB) */
-    float k2_ms;       /* device time of the internal-children K2 launch (CUDA events) */
+    float k2_ms;       /* device time of the internal-children K2 launch (first CTA start ..
+                          last CTA end on the device clock; CUDA events with FBB_PDL=0) */
     int64_t pending;   /* pending nodes after the round */
     float round_ms;    /* device time of the round, pool upload .. summary download */
     int32_t launches;  /* kernels this library launched for the round */
@@ -76,7 +77,7 @@ typedef struct {
     float sync_ms;     /* part of host_ms spent waiting for the device */
     int64_t h2d_bytes; /* host -> device bytes of the round (host-resident explorer) */
     int64_t d2h_bytes; /* device -> host bytes of the round (host-resident explorer) */
-    float place_ms;    /* device time of place_kernel + the round summary download */
+    float place_ms;    /* place_kernel + summary time (CUDA events, FBB_PDL=0 only; else -1) */
     int32_t reserved;
 } fbb_round_t;
 

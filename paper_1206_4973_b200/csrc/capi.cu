@@ -351,7 +351,11 @@ int run_pool(fbb_ctx* ctx, Pool& pool, int first_internal, int32_t ub, int froze
                  ctx->st_seg.as<int32_t>()};
     CK(launch_k2_internal(ctx->dt, ctx->k2, dp, pool, first_internal, ub, frozen, rs, out, st),
        "K2 internal");
-    CK(cudaEventRecord(ctx->ev[2], st), "event");
+    // place_kernel is a programmatic dependent of K2 (scheduled onto SMs as K2's CTAs
+    // retire; FBB_PDL=0: plain stream order); no event may sit between the two, so K2's
+    // time then comes from the device clock stamps K2 leaves in the round state
+    static const bool pdl = [] { const char* e = getenv("FBB_PDL"); return !(e && e[0] == '0'); }();
+    if (!pdl) CK(cudaEventRecord(ctx->ev[2], st), "event");
     // with internal chunks, place_kernel's last CTA writes the round summary straight into
     // the pinned (UVA-mapped) h_round; otherwise one download of the counters (and, after
     // a leaf round, the schedule behind them)
@@ -370,9 +374,15 @@ int run_pool(fbb_ctx* ctx, Pool& pool, int first_internal, int32_t ub, int froze
     ctx->last_sync_ms = std::chrono::duration<float, std::milli>(std::chrono::steady_clock::now() - t_sync).count();
     if (ctx->h_round.as<RoundState>()->found < 0)
         return ctx->fail(FBB_E_STATE, "corrupt pending node (unscheduled-job count mismatch)");
-    cudaEventElapsedTime(&ctx->last_k2_ms, ctx->ev[1], ctx->ev[2]);
+    if (pdl) {
+        const RoundState* hr = ctx->h_round.as<RoundState>();
+        ctx->last_k2_ms = hr->k2_t1 && hr->k2_t0_inv ? (float)((double)(hr->k2_t1 - ~hr->k2_t0_inv) * 1e-6) : 0.f;
+    } else {
+        cudaEventElapsedTime(&ctx->last_k2_ms, ctx->ev[1], ctx->ev[2]);
+    }
     cudaEventElapsedTime(&ctx->last_round_ms, ctx->ev[0], ctx->ev[3]);
-    cudaEventElapsedTime(&ctx->last_place_ms, ctx->ev[2], ctx->ev[3]);  // place + summary download
+    if (pdl) ctx->last_place_ms = -1.f;
+    else cudaEventElapsedTime(&ctx->last_place_ms, ctx->ev[2], ctx->ev[3]);  // place + summary download
     ctx->last_launches = launches;
     return FBB_OK;
 }

@@ -91,6 +91,8 @@ __global__ void __launch_bounds__(128) k2_internal_kernel(DevTables t, const Poo
                                                          int first_seg, int cmax, int32_t ub,
                                                          int frozen, RoundState* rs,
                                                          ChunkOut out) {
+    asm volatile("griddepcontrol.launch_dependents;");  // place_kernel may be scheduled early
+    k2_stamp_begin(rs);
     extern __shared__ __align__(16) unsigned char smem[];
     const int n = t.n, m = t.m, P = t.P, W = t.W;
     const int W32 = (n + 31) / 32;
@@ -348,6 +350,7 @@ __global__ void __launch_bounds__(128) k2_internal_kernel(DevTables t, const Poo
             __syncthreads();
         }
     }
+    k2_stamp_end(rs);
 }
 
 // Children of parents at depth >= n-2 are complete schedules: bound = makespan
@@ -514,6 +517,8 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(DevTables t, const
     __shared__ int64_t s_red[2][kPlaceThreads / 32];
     __shared__ int s_need;                     // prefix bytes that matter: max child depth
     extern __shared__ uint8_t s_rc[];          // chunk of each row (cmax * kPlaceChunks)
+    // launched as a programmatic dependent of K2 (FBB_PDL=1): wait for its completion
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t nchunks = pool->nchunks;
     for (int64_t c0 = (int64_t)blockIdx.x * kPlaceChunks; c0 < nchunks;
@@ -745,6 +750,20 @@ cudaError_t launch_place(const DevTables& t, const K2Config& cfg, const Pool* d_
                          RoundState* summary) {
     if (h_pool.nchunks == 0) return cudaSuccess;
     const int64_t blocks = (h_pool.nchunks + kPlaceChunks - 1) / kPlaceChunks;
+    static const bool pdl = [] { const char* e = getenv("FBB_PDL"); return !(e && e[0] == '0'); }();
+    if (pdl) {
+        cudaLaunchConfig_t lc = {};
+        lc.gridDim = dim3((unsigned)blocks);
+        lc.blockDim = dim3(kPlaceThreads);
+        lc.dynamicSmemBytes = (size_t)cfg.cmax * kPlaceChunks;
+        lc.stream = stream;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        lc.attrs = at;
+        lc.numAttrs = 1;
+        return cudaLaunchKernelEx(&lc, place_kernel<false>, t, d_pool, cfg.cmax, rs, out, summary);
+    }
     place_kernel<false><<<(unsigned)blocks, kPlaceThreads, (size_t)cfg.cmax * kPlaceChunks, stream>>>(
         t, d_pool, cfg.cmax, rs, out, summary);
     return cudaGetLastError();

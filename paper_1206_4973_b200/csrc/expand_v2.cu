@@ -244,6 +244,10 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
     constexpr bool kGroupedB = OCC == 2;
     constexpr bool kDual16 = OCC == 2 && N == 20;  // Phase A: two parents per thread, 16x2
     extern __shared__ __align__(16) unsigned char smem[];
+    // programmatic dependent launch: place_kernel may be scheduled onto SMs as this grid's
+    // CTAs retire (it waits for the grid's completion before reading anything)
+    asm volatile("griddepcontrol.launch_dependents;");
+    k2_stamp_begin(rs);
     const int n = t.n, W = t.W;
     const V2Layout L = v2_layout(n, M, P, cmax, blockDim.x, N, OCC);
     uint64_t* s_um = (uint64_t*)(smem + L.um);  // unscheduled jobs of each parent
@@ -628,6 +632,7 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
             chunk = claim_chunk(rs, c_begin, s_slot);
         }
     }
+    k2_stamp_end(rs);
 }
 
 template <int N, int M, int OCC>

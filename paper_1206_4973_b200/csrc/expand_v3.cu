@@ -108,6 +108,8 @@ template <int NW, int M>
 __global__ void __launch_bounds__(NW <= 4 ? 192 : 256, NW <= 4 ? 3 : 2)
     k2_v3_kernel(DevTables t, const Pool* __restrict__ pool, int first_seg, int cmax, int32_t ub,
                  int frozen, RoundState* rs, ChunkOut out) {
+    asm volatile("griddepcontrol.launch_dependents;");  // place_kernel may be scheduled early
+    k2_stamp_begin(rs);
     constexpr int P = M * (M - 1) / 2;
     constexpr int N = 32 * NW;
     extern __shared__ __align__(16) unsigned char smem[];
@@ -365,6 +367,7 @@ __global__ void __launch_bounds__(NW <= 4 ? 192 : 256, NW <= 4 ? 3 : 2)
             out.lb[o] = mylb;
         }
     }
+    k2_stamp_end(rs);
 }
 
 template <int NW, int M>

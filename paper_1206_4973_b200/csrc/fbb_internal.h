@@ -166,6 +166,8 @@ struct RoundState {
     int64_t total;                // survivors of the pool
     uint32_t place_done;          // place CTAs past their counting (the last one publishes)
     uint32_t pad;
+    unsigned long long k2_t0_inv; // ~(first K2 CTA start), %globaltimer ns (0 = none)
+    unsigned long long k2_t1;     // last K2 CTA end, %globaltimer ns
     int64_t seg_surv[kMaxSegments];
     int32_t schedule[kMaxJobs];
 };

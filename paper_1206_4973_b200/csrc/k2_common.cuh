@@ -25,6 +25,22 @@ __device__ __forceinline__ int find_segment_lb(const Pool* __restrict__ pool, in
     return lo;
 }
 
+// K2's span on the device clock (%globaltimer, ns): with place_kernel launched as its
+// programmatic dependent no CUDA event can sit between the two kernels, so the K2 time
+// of a round is the first CTA start .. last CTA end recorded here.
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void k2_stamp_begin(RoundState* rs) {
+    if (threadIdx.x == 0) atomicMax(&rs->k2_t0_inv, ~global_ns());
+}
+__device__ __forceinline__ void k2_stamp_end(RoundState* rs) {
+    __syncthreads();
+    if (threadIdx.x == 0) atomicMax(&rs->k2_t1, global_ns());
+}
+
 // Claims the next chunk for the CTA (all threads return the same value).
 __device__ inline int64_t claim_chunk(RoundState* rs, int64_t c_begin, int64_t* s_slot) {
     __syncthreads();  // previous chunk fully consumed
