@@ -737,6 +737,10 @@ def main():
         "hbm": {"achieved": alg_bytes / k2_s / 1e9 if k2_s > 0 else 0.0, "peak": hbm_peak,
                 "unit": "GB/s", "frac": (alg_bytes / k2_s / 1e9) / hbm_peak if k2_s > 0 else 0.0},
         "k2_share_of_round": k2_ms / dev_ms if dev_ms > 0 else 0.0,
+        "k2_time_source": ("CUDA events around K2 (FBB_PDL=0)" if os.environ.get("FBB_PDL") == "0" else
+                           "device clock (%globaltimer) stamps in the round state: first K2 CTA start .. "
+                           "last K2 CTA end (place_kernel is K2's programmatic dependent launch, so no "
+                           "event can sit between them); rounds themselves are CUDA-event timed"),
     }
     cpu = None
     if not args.no_cpu_baseline and world == 1:
