@@ -332,12 +332,19 @@ int run_pool(fbb_ctx* ctx, Pool& pool, int first_internal, int32_t ub, int froze
     size_t pool_bytes = offsetof(Pool, seg) + (size_t)pool.nseg * sizeof(Segment);
     std::memcpy((char*)ctx->h_rp.p + kPoolOff, &pool, pool_bytes);
     int launches = 0;
+    static const bool pdl = [] { const char* e = getenv("FBB_PDL"); return !(e && e[0] == '0'); }();
+    bool has_leaf = pool.nseg > 0 && pool.seg[0].depth >= n - 2;
+    // without leaf kernels in between, the upload is a one-CTA kernel and K2 its
+    // programmatic dependent (K2's prologue overlaps the upload); else one DMA copy
+    const bool kernel_upload = pdl && !has_leaf;
     CK(cudaEventRecord(ctx->ev[0], st), "event");
-    // one copy uploads the pool and zeroes the round state (counters, ticket, leaf key)
-    CK(cudaMemcpyAsync(ctx->d_rp.p, ctx->h_rp.p, kPoolOff + pool_bytes, cudaMemcpyHostToDevice, st), "pool H2D");
+    // one upload carries the pool and zeroes the round state (counters, ticket, leaf key)
+    if (kernel_upload)
+        CK(launch_pool_upload(ctx->h_rp.p, ctx->d_rp.p, (int)((kPoolOff + pool_bytes + 7) / 8), st), "pool upload");
+    else
+        CK(cudaMemcpyAsync(ctx->d_rp.p, ctx->h_rp.p, kPoolOff + pool_bytes, cudaMemcpyHostToDevice, st), "pool H2D");
     const Pool* dp = (const Pool*)((char*)ctx->d_rp.p + kPoolOff);
     RoundState* rs = ctx->d_rp.as<RoundState>();
-    bool has_leaf = pool.nseg > 0 && pool.seg[0].depth >= n - 2;
     if (has_leaf) {
         // leaves, then the best leaf's schedule -- before K2 recycles the leaf
         // parents' slots (bucket n-2 receives the next segment's survivors)
@@ -345,16 +352,15 @@ int run_pool(fbb_ctx* ctx, Pool& pool, int first_internal, int32_t ub, int froze
         CK(launch_leaf_schedule(ctx->dt, dp, rs, ub, st), "leaf schedule");
         launches += 2;
     }
-    CK(cudaEventRecord(ctx->ev[1], st), "event");
+    if (!pdl) CK(cudaEventRecord(ctx->ev[1], st), "event");
     bool has_internal = first_internal < pool.nseg && pool.nchunks > 0;
     ChunkOut out{ctx->staging.view(), ctx->st_lb.as<int32_t>(), ctx->st_count.as<int32_t>(),
                  ctx->st_seg.as<int32_t>()};
-    CK(launch_k2_internal(ctx->dt, ctx->k2, dp, pool, first_internal, ub, frozen, rs, out, st),
+    CK(launch_k2_internal(ctx->dt, ctx->k2, dp, pool, first_internal, ub, frozen, rs, out, st, kernel_upload),
        "K2 internal");
     // place_kernel is a programmatic dependent of K2 (scheduled onto SMs as K2's CTAs
     // retire; FBB_PDL=0: plain stream order); no event may sit between the two, so K2's
     // time then comes from the device clock stamps K2 leaves in the round state
-    static const bool pdl = [] { const char* e = getenv("FBB_PDL"); return !(e && e[0] == '0'); }();
     if (!pdl) CK(cudaEventRecord(ctx->ev[2], st), "event");
     // with internal chunks, place_kernel's last CTA writes the round summary straight into
     // the pinned (UVA-mapped) h_round; otherwise one download of the counters (and, after

@@ -92,7 +92,6 @@ __global__ void __launch_bounds__(128) k2_internal_kernel(DevTables t, const Poo
                                                          int frozen, RoundState* rs,
                                                          ChunkOut out) {
     asm volatile("griddepcontrol.launch_dependents;");  // place_kernel may be scheduled early
-    k2_stamp_begin(rs);
     extern __shared__ __align__(16) unsigned char smem[];
     const int n = t.n, m = t.m, P = t.P, W = t.W;
     const int W32 = (n + 31) / 32;
@@ -128,6 +127,8 @@ __global__ void __launch_bounds__(128) k2_internal_kernel(DevTables t, const Poo
     // incumbent for internal children: min(UB, batch leaf minimum) unless frozen
     // the round's bound, semantics and first internal segment come from the pool
     // (written by the host, or by the device-side planner of the batched explorer loop)
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // the pool upload kernel (PDL)
+    k2_stamp_begin(rs);
     ub = pool->ub;
     frozen = pool->frozen;
     first_seg = pool->first_internal;
@@ -717,21 +718,31 @@ cudaError_t launch_k2_leaves(const DevTables& t, const Pool* d_pool, const Pool&
 
 cudaError_t launch_k2_internal(const DevTables& t, const K2Config& cfg, const Pool* d_pool,
                                const Pool& h_pool, int first_seg, int32_t ub, int frozen,
-                               RoundState* rs, ChunkOut out, cudaStream_t stream) {
+                               RoundState* rs, ChunkOut out, cudaStream_t stream, bool pdl) {
     if (first_seg >= h_pool.nseg) return cudaSuccess;
     int64_t nch = h_pool.nchunks - h_pool.seg[first_seg].chunk_base;
     if (nch <= 0) return cudaSuccess;
     int blocks = (int)(nch < cfg.blocks ? nch : cfg.blocks);
     if (cfg.variant >= 100000)
-        return launch_k2_v3(t, cfg, d_pool, first_seg, blocks, ub, frozen, rs, out, stream);
+        return launch_k2_v3(t, cfg, d_pool, first_seg, blocks, ub, frozen, rs, out, stream, pdl);
     if (cfg.variant != 0)
-        return launch_k2_v2(t, cfg, d_pool, first_seg, blocks, ub, frozen, rs, out, stream);
-    if (cfg.jm_in_smem)
-        k2_internal_kernel<true><<<blocks, cfg.threads, cfg.smem, stream>>>(t, d_pool, first_seg, cfg.cmax,
-                                                                            ub, frozen, rs, out);
-    else
-        k2_internal_kernel<false><<<blocks, cfg.threads, cfg.smem, stream>>>(t, d_pool, first_seg, cfg.cmax,
-                                                                             ub, frozen, rs, out);
+        return launch_k2_v2(t, cfg, d_pool, first_seg, blocks, ub, frozen, rs, out, stream, pdl);
+    return launch_pdl(cfg.jm_in_smem ? k2_internal_kernel<true> : k2_internal_kernel<false>, dim3(blocks),
+                      dim3(cfg.threads), cfg.smem, stream, pdl, t, d_pool, first_seg, cfg.cmax, ub, frozen, rs,
+                      out);
+}
+
+namespace {
+__global__ void pool_upload_kernel(const volatile unsigned long long* __restrict__ src,
+                                   unsigned long long* __restrict__ dst, int words) {
+    asm volatile("griddepcontrol.launch_dependents;");  // K2 may start its prologue now
+    for (int i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
+}
+}  // namespace
+
+cudaError_t launch_pool_upload(const void* h_src, void* d_dst, int words, cudaStream_t stream) {
+    pool_upload_kernel<<<1, 256, 0, stream>>>((const volatile unsigned long long*)h_src,
+                                              (unsigned long long*)d_dst, words);
     return cudaGetLastError();
 }
 

@@ -247,7 +247,6 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
     // programmatic dependent launch: place_kernel may be scheduled onto SMs as this grid's
     // CTAs retire (it waits for the grid's completion before reading anything)
     asm volatile("griddepcontrol.launch_dependents;");
-    k2_stamp_begin(rs);
     const int n = t.n, W = t.W;
     const V2Layout L = v2_layout(n, M, P, cmax, blockDim.x, N, OCC);
     uint64_t* s_um = (uint64_t*)(smem + L.um);  // unscheduled jobs of each parent
@@ -297,6 +296,8 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
 
     // the round's bound, semantics and first internal segment come from the pool
     // (written by the host, or by the device-side planner of the batched explorer loop)
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // the pool upload kernel (PDL)
+    k2_stamp_begin(rs);
     ub = pool->ub;
     frozen = pool->frozen;
     first_seg = pool->first_internal;
@@ -701,12 +702,11 @@ bool k2_v2_config(const DevTables& t, int device, K2Config* out) {
 
 cudaError_t launch_k2_v2(const DevTables& t, const K2Config& cfg, const Pool* d_pool, int first_seg,
                          int blocks, int32_t ub, int frozen, RoundState* rs, ChunkOut out,
-                         cudaStream_t stream) {
+                         cudaStream_t stream, bool pdl) {
 #define V2_CASE(NN, MM, OO)                                                                   \
     case OO * 10000 + NN * 100 + MM:                                                          \
-        k2_v2_kernel<NN, MM, OO><<<blocks, cfg.threads, cfg.smem, stream>>>(                   \
-            t, d_pool, first_seg, cfg.cmax, ub, frozen, rs, out);                             \
-        break;
+        return launch_pdl(k2_v2_kernel<NN, MM, OO>, dim3(blocks), dim3(cfg.threads), cfg.smem, stream, pdl, \
+                          t, d_pool, first_seg, cfg.cmax, ub, frozen, rs, out);
     switch (cfg.variant) {
         V2_CASE(20, 5, 2)
         V2_CASE(20, 10, 2)

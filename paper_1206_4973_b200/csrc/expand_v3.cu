@@ -109,7 +109,6 @@ __global__ void __launch_bounds__(NW <= 4 ? 192 : 256, NW <= 4 ? 3 : 2)
     k2_v3_kernel(DevTables t, const Pool* __restrict__ pool, int first_seg, int cmax, int32_t ub,
                  int frozen, RoundState* rs, ChunkOut out) {
     asm volatile("griddepcontrol.launch_dependents;");  // place_kernel may be scheduled early
-    k2_stamp_begin(rs);
     constexpr int P = M * (M - 1) / 2;
     constexpr int N = 32 * NW;
     extern __shared__ __align__(16) unsigned char smem[];
@@ -135,6 +134,8 @@ __global__ void __launch_bounds__(NW <= 4 ? 192 : 256, NW <= 4 ? 3 : 2)
 
     // the round's bound, semantics and first internal segment come from the pool
     // (written by the host, or by the device-side planner of the batched explorer loop)
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // the pool upload kernel (PDL)
+    k2_stamp_begin(rs);
     ub = pool->ub;
     frozen = pool->frozen;
     first_seg = pool->first_internal;
@@ -414,12 +415,11 @@ bool k2_v3_config(const DevTables& t, int device, K2Config* out) {
 
 cudaError_t launch_k2_v3(const DevTables& t, const K2Config& cfg, const Pool* d_pool, int first_seg,
                          int blocks, int32_t ub, int frozen, RoundState* rs, ChunkOut out,
-                         cudaStream_t stream) {
+                         cudaStream_t stream, bool pdl) {
 #define V3_CASE(NW, MM)                                                                      \
     case 100000 + NW * 100 + MM:                                                             \
-        k2_v3_kernel<NW, MM><<<blocks, cfg.threads, cfg.smem, stream>>>(t, d_pool, first_seg, \
-                                                                       cfg.cmax, ub, frozen, rs, out); \
-        break;
+        return launch_pdl(k2_v3_kernel<NW, MM>, dim3(blocks), dim3(cfg.threads), cfg.smem, stream, pdl, t, \
+                          d_pool, first_seg, cfg.cmax, ub, frozen, rs, out);
     switch (cfg.variant) {
         V3_CASE(4, 5)
         V3_CASE(4, 10)

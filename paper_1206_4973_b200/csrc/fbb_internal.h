@@ -177,13 +177,13 @@ constexpr size_t kRoundStateHead = offsetof(RoundState, schedule);
 bool k2_v2_config(const DevTables& t, int device, K2Config* out);
 cudaError_t launch_k2_v2(const DevTables& t, const K2Config& cfg, const Pool* d_pool, int first_seg,
                          int blocks, int32_t ub, int frozen, RoundState* rs, ChunkOut out,
-                         cudaStream_t stream);
+                         cudaStream_t stream, bool pdl = false);
 
 // 64 < n <= 256, m in {5,10,20}: rows through L1, RMW scans; false when not applicable.
 bool k2_v3_config(const DevTables& t, int device, K2Config* out);
 cudaError_t launch_k2_v3(const DevTables& t, const K2Config& cfg, const Pool* d_pool, int first_seg,
                          int blocks, int32_t ub, int frozen, RoundState* rs, ChunkOut out,
-                         cudaStream_t stream);
+                         cudaStream_t stream, bool pdl = false);
 
 // Leaves (parents at depth >= n-2): batch minimum (value, first position).
 cudaError_t launch_k2_leaves(const DevTables& t, const Pool* d_pool, const Pool& h_pool,
@@ -192,7 +192,10 @@ cudaError_t launch_k2_leaves(const DevTables& t, const Pool* d_pool, const Pool&
 // survivors compacted per chunk into `out`.
 cudaError_t launch_k2_internal(const DevTables& t, const K2Config& cfg, const Pool* d_pool,
                                const Pool& h_pool, int first_seg, int32_t ub, int frozen,
-                               RoundState* rs, ChunkOut out, cudaStream_t stream);
+                               RoundState* rs, ChunkOut out, cudaStream_t stream, bool pdl = false);
+// Uploads `words` 8-byte words from pinned host memory (UVA) to the device with one CTA:
+// the round's zeroed state + pool, as a kernel so that K2 can be its programmatic dependent.
+cudaError_t launch_pool_upload(const void* h_src, void* d_dst, int words, cudaStream_t stream);
 // Every chunk's survivors moved, in batch order, to its segment's dst; per-segment
 // and pool survivor totals added to `rs` (zeroed before the round).
 cudaError_t launch_place(const DevTables& t, const K2Config& cfg, const Pool* d_pool,
@@ -234,6 +237,25 @@ cudaError_t launch_loop_close(const DevTables& t, LoopState* ls, const Pool* poo
 cudaError_t launch_round_device(const DevTables& t, const K2Config& cfg, const Pool* d_pool,
                                 RoundState* rs, ChunkOut out, cudaStream_t stream, cudaEvent_t k2_begin,
                                 cudaEvent_t k2_end);
+
+// Launches kern<<<grid, block, smem, st>>>(args...), as a programmatic dependent of the
+// previous kernel in the stream when pdl (the kernel must griddepcontrol.wait before it
+// reads that kernel's output).
+template <class... KArgs, class... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              bool pdl, Args... args) {
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = grid;
+    lc.blockDim = block;
+    lc.dynamicSmemBytes = smem;
+    lc.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&lc, kern, static_cast<KArgs>(args)...);
+}
 
 // Chunk geometry of a segment: parents per chunk.
 __host__ __device__ inline int parents_per_chunk(int n, int depth, int cmax, int ppc_cap) {
