@@ -334,9 +334,10 @@ int run_pool(fbb_ctx* ctx, Pool& pool, int first_internal, int32_t ub, int froze
     int launches = 0;
     static const bool pdl = [] { const char* e = getenv("FBB_PDL"); return !(e && e[0] == '0'); }();
     bool has_leaf = pool.nseg > 0 && pool.seg[0].depth >= n - 2;
-    // without leaf kernels in between, the upload is a one-CTA kernel and K2 its
-    // programmatic dependent (K2's prologue overlaps the upload); else one DMA copy
-    const bool kernel_upload = pdl && !has_leaf;
+    // the upload is a one-CTA kernel and the round's kernels form a programmatic-
+    // dependent-launch chain (upload -> [leaves -> leaf schedule] -> K2 -> place): each
+    // one's prologue overlaps its predecessor; FBB_PDL=0: DMA copy and plain stream order
+    const bool kernel_upload = pdl;
     CK(cudaEventRecord(ctx->ev[0], st), "event");
     // one upload carries the pool and zeroes the round state (counters, ticket, leaf key)
     if (kernel_upload)
@@ -348,8 +349,8 @@ int run_pool(fbb_ctx* ctx, Pool& pool, int first_internal, int32_t ub, int froze
     if (has_leaf) {
         // leaves, then the best leaf's schedule -- before K2 recycles the leaf
         // parents' slots (bucket n-2 receives the next segment's survivors)
-        CK(launch_k2_leaves(ctx->dt, dp, pool, 0, rs, st), "K2 leaves");
-        CK(launch_leaf_schedule(ctx->dt, dp, rs, ub, st), "leaf schedule");
+        CK(launch_k2_leaves(ctx->dt, dp, pool, 0, rs, st, kernel_upload), "K2 leaves");
+        CK(launch_leaf_schedule(ctx->dt, dp, rs, ub, st, kernel_upload), "leaf schedule");
         launches += 2;
     }
     if (!pdl) CK(cudaEventRecord(ctx->ev[1], st), "event");

@@ -358,6 +358,8 @@ __global__ void __launch_bounds__(128) k2_internal_kernel(DevTables t, const Poo
 // (bound.hpp:95).  Thread per child; batch-minimum (value, position) by atomicMin.
 __global__ void k2_leaf_kernel(DevTables t, const Pool* __restrict__ pool, int seg_index,
                                RoundState* rs) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // the pool upload (PDL chain)
+    asm volatile("griddepcontrol.launch_dependents;");
     const int n = t.n, m = t.m, W = t.W;
     if (pool->nseg <= seg_index || pool->seg[seg_index].depth < n - 2) return;  // no leaves
     const Segment& sg = pool->seg[seg_index];
@@ -418,6 +420,8 @@ __global__ void k2_leaf_kernel(DevTables t, const Pool* __restrict__ pool, int s
 // parents' storage is recycled by the push.
 __global__ void leaf_schedule_kernel(DevTables t, const Pool* __restrict__ pool, RoundState* rs,
                                      int32_t ub) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // the leaf kernel (PDL chain)
+    asm volatile("griddepcontrol.launch_dependents;");
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     ub = pool->ub;
     if (pool->nseg == 0 || pool->seg[0].depth < t.n - 2) {  // no leaves this round
@@ -706,14 +710,13 @@ K2Config k2_config(const DevTables& t, int device) {
 }
 
 cudaError_t launch_k2_leaves(const DevTables& t, const Pool* d_pool, const Pool& h_pool,
-                             int seg_index, RoundState* rs, cudaStream_t stream) {
+                             int seg_index, RoundState* rs, cudaStream_t stream, bool pdl) {
     const Segment& sg = h_pool.seg[seg_index];
     int64_t nc = sg.count * (t.n - sg.depth);
     if (nc <= 0) return cudaSuccess;
     int blocks = (int)((nc + 255) / 256);
     if (blocks > 4096) blocks = 4096;
-    k2_leaf_kernel<<<blocks, 256, 0, stream>>>(t, d_pool, seg_index, rs);
-    return cudaGetLastError();
+    return launch_pdl(k2_leaf_kernel, dim3(blocks), dim3(256), 0, stream, pdl, t, d_pool, seg_index, rs);
 }
 
 cudaError_t launch_k2_internal(const DevTables& t, const K2Config& cfg, const Pool* d_pool,
@@ -747,9 +750,8 @@ cudaError_t launch_pool_upload(const void* h_src, void* d_dst, int words, cudaSt
 }
 
 cudaError_t launch_leaf_schedule(const DevTables& t, const Pool* d_pool, RoundState* rs,
-                                 int32_t ub, cudaStream_t stream) {
-    leaf_schedule_kernel<<<1, 32, 0, stream>>>(t, d_pool, rs, ub);
-    return cudaGetLastError();
+                                 int32_t ub, cudaStream_t stream, bool pdl) {
+    return launch_pdl(leaf_schedule_kernel, dim3(1), dim3(32), 0, stream, pdl, t, d_pool, rs, ub);
 }
 
 }  // namespace fbb

@@ -187,7 +187,7 @@ cudaError_t launch_k2_v3(const DevTables& t, const K2Config& cfg, const Pool* d_
 
 // Leaves (parents at depth >= n-2): batch minimum (value, first position).
 cudaError_t launch_k2_leaves(const DevTables& t, const Pool* d_pool, const Pool& h_pool,
-                             int seg_index, RoundState* rs, cudaStream_t stream);
+                             int seg_index, RoundState* rs, cudaStream_t stream, bool pdl = false);
 // Internal children: bound, prune against min(ub, leaf minimum) (frozen: ub),
 // survivors compacted per chunk into `out`.
 cudaError_t launch_k2_internal(const DevTables& t, const K2Config& cfg, const Pool* d_pool,
@@ -203,7 +203,7 @@ cudaError_t launch_place(const DevTables& t, const K2Config& cfg, const Pool* d_
                          RoundState* summary = nullptr);
 // Schedule of the best leaf when it beats ub (before the parents are recycled).
 cudaError_t launch_leaf_schedule(const DevTables& t, const Pool* d_pool, RoundState* rs,
-                                 int32_t ub, cudaStream_t stream);
+                                 int32_t ub, cudaStream_t stream, bool pdl = false);
 
 // ---- batched explorer loop (explorer_loop.cu): rounds planned and closed on the device --
 constexpr int kLoopMax = 64;  // rounds per batch
