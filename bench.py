@@ -167,6 +167,20 @@ def measured_peaks():
         return {}
 
 
+def explore_config(args, inst_name, world, tuner_desc=None):
+    """The `config` of an explorer line -- identical in both arms (same workload)."""
+    n, m, _, ub = INSTANCES[inst_name]
+    return {"workload": f"{inst_name} {n}x{m} frozen UB {ub}, root pushed, prefill to a full pool, "
+                        f"then rounds at pool target "
+                        f"{'set by the adaptive tuner' if args.tuner else args.target}; step = one "
+                        f"explorer round (select + expand/bound/prune + push)",
+            "instance": inst_name,
+            "pool_target": tuner_desc if (args.tuner and tuner_desc) else
+                           ("adaptive" if args.tuner else args.target),
+            "ub": ub, "parallelism": f"dp{world}",
+            "l2": "flushed between timed rounds (256 MiB write)"}
+
+
 def reference_arm(args, inst_name):
     rank, world, _ = dist_env()
     if rank != 0:
@@ -195,17 +209,14 @@ def reference_arm(args, inst_name):
             "e2e": {"value": value, "unit": "bounded subproblems/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}), flush=True)
         return
-    cfg = {"workload": f"{inst_name} {n}x{m} frozen UB {ub}, root pushed, pool target "
-                       f"{args.target}, step = one explorer round",
-           "instance": inst_name, "pool_target": args.target, "ub": ub,
-           "parallelism": "host threads"}
+    cfg = explore_config(args, inst_name, world)
     if os.path.exists(REF_SO):
         ref = Ref()
         cores = ref.detect_units()
         p = ref.generate_instance(n, m, seed)
         # each step is one full reference round (~1 s at 262K children on 16 cores): the
         # timed steps stop after ~60 s so the arm ends within a few minutes at any K
-        pre, rounds, secs = ref.bench_rounds(p, ub, args.target, min(args.warmup, 3), args.steps,
+        pre, rounds, secs = ref.bench_rounds(p, ub, args.target, args.warmup, args.steps,
                                              cores, max_seconds=args.ref_seconds)
         kind = "reference"
     else:  # the C restatement, single thread (reference not compiled on this host)
@@ -228,7 +239,8 @@ def reference_arm(args, inst_name):
             "cpu_baseline": {"value": value, "unit": "bounded subproblems/s", "cores": cores,
                              "kind": kind,
                              "sample": f"{len(secs)} rounds after {pre} prefill + {args.warmup} "
-                                       f"warm-up rounds, {bounded} bounded nodes"},
+                                       f"warm-up rounds, {bounded} bounded nodes; the reference "
+                                       f"explorer (BackendSet over {cores} host threads)"},
             "e2e": {"value": value, "unit": "bounded subproblems/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0},
             "rounds": [list(r) for r in rounds]}
@@ -404,7 +416,7 @@ def bound_stress(args, inst_name):
                    "mean_unscheduled": n_u, "parallelism": f"dp{world} (own pool per GPU)",
                    "l2": f"pool {cnt * node_b / 2**30:.2f} GiB > L2 (126 MB), no flush needed"},
         "e2e": e2e,
-        "roofline": {"bound": "int32-alu", "kernel": "k1_bound_kernel (bound-only)",
+        "roofline": {"bound": "int32-alu", "kernel": ctx.kernels().split()[0][3:] + " (bound-only K1)",
                      "achieved": achieved, "peak": int_peak, "unit": "Gop/s",
                      "frac": achieved / int_peak, "traffic": None,
                      "ops_per_node": ops_per_node,
@@ -674,8 +686,8 @@ def main():
             torch.distributed.barrier()
         e_rounds, e_tim, e_secs = [], [], 0.0
         if pxe is None and tuner is None:
-            # one C-ABI call runs the K rounds (batched on the device, no per-round host
-            # round trip); the host tree is read and written over the link every round
+            # one C-ABI call runs the K rounds (host-planned, one stream sync per round);
+            # the host tree is read and written over the link every round
             w0 = time.perf_counter()
             e_rounds, e_tim = ctx.explorer_run([T], args.steps, timing=True)
             e_secs = time.perf_counter() - w0
@@ -726,7 +738,7 @@ def main():
     k2_s = k2_ms / 1e3
     roofline = {
         "bound": "int32-alu",
-        "kernel": (k2_traffic(inst_name) or {}).get("kernel", "K2") + " (fused expand+bound+prune+compact)",
+        "kernel": ctx.kernels().split()[1][3:] + " (fused expand+bound+prune+compact)",
         "achieved": ops / k2_s / 1e9 if k2_s > 0 else 0.0, "peak": int_peak, "unit": "Gop/s",
         "frac": (ops / k2_s / 1e9) / int_peak if k2_s > 0 else 0.0,
         "traffic": (k2_traffic(inst_name) or {}).get("bytes_per_launch"),
@@ -757,18 +769,10 @@ def main():
         "ms_per_step": dev_ms_max / max(1, steps_done),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
         "data": "synthetic (Taillard generator, published seed; no dataset)",
-        "config": {"workload": f"{inst_name} {n}x{m} frozen UB {ub}, root pushed, prefill to a "
-                               f"full pool, then rounds at pool target "
-                               f"{'set by the adaptive tuner' if tuner else T}; step = one explorer "
-                               f"round (select + K2 expand/bound/prune/compact + push)",
-                   "instance": inst_name,
-                   "pool_target": (f"adaptive: tuner best {tuner.best_batch()} "
-                                   f"(phase {tuner.phase().name})") if tuner else T,
-                   "ub": ub,
-                   "parallelism": (f"dp{world}: pending-tree slices per GPU, per-round "
-                                   "incumbent/pending all_gather + rebalancing (NCCL)")
-                                  if world > 1 else "dp1",
-                   "l2": "flushed between timed rounds (256 MiB write)"},
+        "config": explore_config(args, inst_name, world),
+        "tuner": ({"best_batch": tuner.best_batch(), "phase": tuner.phase().name,
+                   "targets": [r[0] for r in rounds]} if tuner else None),
+        "kernels": ctx.kernels(),
         "wall_value": bounded_all / wall_max if wall_max > 0 else 0.0,
         "wall_breakdown_ms_per_step": {
             "round_wall": 1e3 * wall / max(1, len(rounds)),

@@ -211,6 +211,11 @@ int fbb_tuner_phase(const fbb_tuner* t); /* 0 doubling, 1 refining, 2 fixed */
 int64_t fbb_tuner_best_batch(const fbb_tuner* t);
 double fbb_tuner_best_throughput(const fbb_tuner* t);
 
+/* The kernel variants this context launches, as one line of text, e.g.
+ * "K1=k1v2_kernel<8,4> K2=k2_v3_kernel<4,20> cmax=224 ppc_cap=16 blocks=444"
+ * (measurement labels; copies up to cap-1 bytes). */
+int fbb_kernels(fbb_ctx* ctx, char* buf, size_t cap);
+
 /* Library build identification (sm arch, git-less version string). */
 const char* fbb_version(void);
 

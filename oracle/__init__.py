@@ -285,6 +285,10 @@ class Ref:
         L.ref_resolve.argtypes = [C.c_int, C.c_int, _i32p, C.c_int32, C.c_int64, _i32p, _i32p,
                                   _i64p, C.c_int, C.c_int64, C.c_int, C.POINTER(Result),
                                   C.c_void_p, C.c_int64, C.POINTER(C.c_double)]
+        L.ref_resolve_drain.argtypes = [C.c_int, C.c_int, _i32p, C.c_int32, C.c_int64, _i32p,
+                                        _i32p, _i64p, C.c_int, C.c_int64, C.c_int,
+                                        C.POINTER(Result), C.c_int64, _i32p, _i32p,
+                                        C.POINTER(C.c_int64)]
         L.ref_solve_trace.argtypes = [C.c_int, C.c_int, _i32p, C.c_int32, _i64p, C.c_int,
                                       C.c_int64, C.c_int, C.POINTER(Result), _i32p, C.c_void_p,
                                       C.c_int64]
@@ -399,6 +403,24 @@ class Ref:
             raise RuntimeError("ref_resolve failed")
         rounds = [trace[i].as_tuple() for i in range(min(res.rounds, max_trace))] if trace else []
         return res.as_dict(), rounds, secs.value
+
+    def resolve_drain(self, p, ub, roots, targets=(1,), budget=0, backends=1, cap=1 << 22):
+        """resolve() stopped by `budget`, then PendingTree::drain (pending.hpp:41-50) of what
+        is left: (result dict, [prefix of every pending node, drain order])."""
+        n, m = p.shape
+        pre, dep = pack_prefixes(n, roots)
+        t, nt = _targets(targets)
+        res = Result()
+        dp = np.zeros(cap * n, np.int32)
+        dd = np.zeros(cap, np.int32)
+        cnt = C.c_int64(0)
+        rc = self.lib.ref_resolve_drain(n, m, np.ascontiguousarray(p, np.int32).ravel(), ub,
+                                        len(roots), pre, dep, t, nt, budget, backends,
+                                        C.byref(res), cap, dp, dd, C.byref(cnt))
+        if rc != 0:
+            raise RuntimeError(f"ref_resolve_drain failed ({rc}, pending {cnt.value})")
+        dp = dp.reshape(cap, n)
+        return res.as_dict(), [list(map(int, dp[i, : dd[i]])) for i in range(cnt.value)]
 
     def solve_trace(self, p, initial_ub=-1, targets=(1,), budget=0, backends=1, max_trace=0):
         n, m = p.shape

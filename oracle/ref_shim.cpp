@@ -140,10 +140,15 @@ int ref_branch(int n, int m, const int32_t* p, const int32_t* prefix, int depth,
 // bench.hpp:63-114 resolve_workload's loop, call for call (fill_buffer,
 // BackendSet::evaluate, the frozen prune), with a per-round target schedule
 // and a bounded-node budget checked after each round.
-int ref_resolve(int n, int m, const int32_t* p, int32_t ub, int64_t nroots,
-                const int32_t* roots_prefix, const int32_t* roots_depth, const int64_t* targets,
-                int ntargets, int64_t budget, int backends, orc_result* res, orc_round* trace,
-                int64_t max_trace, double* seconds) {
+// With drain_cap >= 0, the pending tree left by a budget stop is drained
+// (PendingTree::drain, pending.hpp:41-50: shallowest bucket first, insertion order)
+// into drain_prefix (n int32 per node) / drain_depth; *drain_count = its size.
+static int resolve_impl(int n, int m, const int32_t* p, int32_t ub, int64_t nroots,
+                        const int32_t* roots_prefix, const int32_t* roots_depth,
+                        const int64_t* targets, int ntargets, int64_t budget, int backends,
+                        orc_result* res, orc_round* trace, int64_t max_trace, double* seconds,
+                        int64_t drain_cap, int32_t* drain_prefix, int32_t* drain_depth,
+                        int64_t* drain_count) {
     try {
         Instance inst = make_instance(n, m, p);
         BackendSet set(backends, wide_descriptor());
@@ -193,10 +198,37 @@ int ref_resolve(int n, int m, const int32_t* p, int32_t ub, int64_t nroots,
         res->found = best.has_value();
         res->optimum = best ? *best : -1;
         res->pending = static_cast<int64_t>(pending.size());
+        if (drain_cap >= 0) {
+            std::vector<Node> left = pending.drain();
+            *drain_count = static_cast<int64_t>(left.size());
+            if (static_cast<int64_t>(left.size()) > drain_cap) return -2;
+            for (std::size_t i = 0; i < left.size(); ++i) {
+                drain_depth[i] = left[i].depth();
+                for (int d = 0; d < left[i].depth(); ++d) drain_prefix[i * n + d] = left[i].prefix[d];
+            }
+        }
         return 0;
     } catch (const std::exception&) {
         return -1;
     }
+}
+
+int ref_resolve(int n, int m, const int32_t* p, int32_t ub, int64_t nroots,
+                const int32_t* roots_prefix, const int32_t* roots_depth, const int64_t* targets,
+                int ntargets, int64_t budget, int backends, orc_result* res, orc_round* trace,
+                int64_t max_trace, double* seconds) {
+    return resolve_impl(n, m, p, ub, nroots, roots_prefix, roots_depth, targets, ntargets, budget,
+                        backends, res, trace, max_trace, seconds, -1, nullptr, nullptr, nullptr);
+}
+
+int ref_resolve_drain(int n, int m, const int32_t* p, int32_t ub, int64_t nroots,
+                      const int32_t* roots_prefix, const int32_t* roots_depth,
+                      const int64_t* targets, int ntargets, int64_t budget, int backends,
+                      orc_result* res, int64_t drain_cap, int32_t* drain_prefix,
+                      int32_t* drain_depth, int64_t* drain_count) {
+    return resolve_impl(n, m, p, ub, nroots, roots_prefix, roots_depth, targets, ntargets, budget,
+                        backends, res, nullptr, 0, nullptr, drain_cap, drain_prefix, drain_depth,
+                        drain_count);
 }
 
 // search.hpp:124-174 solve()'s loop, call for call (BackendSet::evaluate,

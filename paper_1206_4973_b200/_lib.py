@@ -25,7 +25,7 @@ EXPORTED = (
     "fbb_explorer_pending", "fbb_explorer_set_residency", "fbb_explorer_set_incumbent",
     "fbb_explorer_best", "fbb_explorer_take", "fbb_explorer_push", "fbb_tuner_create", "fbb_tuner_destroy", "fbb_tuner_target",
     "fbb_tuner_observe", "fbb_tuner_phase", "fbb_tuner_best_batch",
-    "fbb_tuner_best_throughput", "fbb_version",
+    "fbb_tuner_best_throughput", "fbb_version", "fbb_kernels",
 )
 
 
@@ -133,6 +133,7 @@ def load_library(path: str = LIB_PATH):
     L.fbb_tuner_best_throughput.argtypes = [_vp]
     L.fbb_tuner_best_throughput.restype = C.c_double
     L.fbb_version.restype = C.c_char_p
+    L.fbb_kernels.argtypes = [_vp, C.c_char_p, C.c_size_t]
     _lib = L
     return L
 

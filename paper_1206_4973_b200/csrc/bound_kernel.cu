@@ -43,7 +43,8 @@ __host__ __device__ inline K1Layout k1_layout(int n, int m, int P, int tile, boo
 
 // kJmSmem: the Johnson table is staged in shared memory; when it does not fit next
 // to the tile (n*P*4 > ~half the opt-in maximum, e.g. 256x20) it is read through L1.
-template <bool kOneWord, bool kJmSmem>
+// kWide: the unpacked rows (DevTables::jw) for instances outside the packed range.
+template <bool kOneWord, bool kJmSmem, bool kWide>
 __global__ void __launch_bounds__(256) k1_bound_kernel(DevTables t, int tile,
                                                       const uint64_t* __restrict__ masks,
                                                       const int32_t* __restrict__ heads,
@@ -53,7 +54,7 @@ __global__ void __launch_bounds__(256) k1_bound_kernel(DevTables t, int tile,
     const int n = t.n, m = t.m, P = t.P, W = t.W;
     const int W32 = (n + 31) / 32;
     const K1Layout L = k1_layout(n, m, P, tile, kJmSmem);
-    const uint32_t* s_jm = kJmSmem ? (const uint32_t*)(smem + L.jm) : t.jm;
+    const uint32_t* s_jm = (kJmSmem && !kWide) ? (const uint32_t*)(smem + L.jm) : t.jm;
     int32_t* s_pk = (int32_t*)(smem + L.pk);
     int32_t* s_p = (int32_t*)(smem + L.p);
     int32_t* s_tl = (int32_t*)(smem + L.tl);
@@ -65,7 +66,7 @@ __global__ void __launch_bounds__(256) k1_bound_kernel(DevTables t, int tile,
     const int tid = threadIdx.x, bd = blockDim.x;
 
     // stage the instance constants once per CTA
-    if (kJmSmem)
+    if (kJmSmem && !kWide)
         for (int x = tid; x < n * P; x += bd) ((uint32_t*)(smem + L.jm))[x] = t.jm[x];
     for (int x = tid; x < P; x += bd) s_pk[x] = (int32_t)t.pair_k[x] | ((int32_t)t.pair_l[x] << 16);
     for (int x = tid; x < n * m; x += bd) {
@@ -116,7 +117,16 @@ __global__ void __launch_bounds__(256) k1_bound_kernel(DevTables t, int tile,
             int kl = s_pk[q];
             int k = kl & 0xFFFF, l = kl >> 16;
             int32_t D = 0, M = INT_MIN / 2;
-            if (kOneWord) {
+            if constexpr (kWide) {
+                const uint32_t* um = s_um + tt * W32;
+                for (int i = 0; i < n; ++i) {
+                    const int4 w = __ldg(t.jw + (size_t)i * P + q);
+                    if ((um[w.x >> 5] >> (w.x & 31)) & 1u) {
+                        M = max(M, D + w.z);
+                        D += w.y;
+                    }
+                }
+            } else if (kOneWord) {
                 const uint32_t um = s_um[tt];
 #pragma unroll 4
                 for (int i = 0; i < n; ++i) {
@@ -168,8 +178,11 @@ K1Config k1_config(const DevTables& t, int device) {
     if (!c.jm_in_smem) c.smem = k1_layout(t.n, t.m, t.P, c.tile, false).total;
     int sms = 148, per_sm = 1;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    auto kern = t.n <= 32 ? (c.jm_in_smem ? k1_bound_kernel<true, true> : k1_bound_kernel<true, false>)
-                          : (c.jm_in_smem ? k1_bound_kernel<false, true> : k1_bound_kernel<false, false>);
+    c.wide = !(t.safe16 & kTablesPacked);
+    if (c.wide) c.jm_in_smem = false, c.smem = k1_layout(t.n, t.m, t.P, c.tile, false).total;
+    auto kern = c.wide ? k1_bound_kernel<false, false, true>
+                : t.n <= 32 ? (c.jm_in_smem ? k1_bound_kernel<true, true, false> : k1_bound_kernel<true, false, false>)
+                            : (c.jm_in_smem ? k1_bound_kernel<false, true, false> : k1_bound_kernel<false, false, false>);
     // the attribute is per kernel, not per context: allow the device maximum once
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, c.threads, c.smem);
@@ -185,13 +198,15 @@ cudaError_t launch_k1(const DevTables& t, const K1Config& cfg, const uint64_t* m
     if (cfg.variant != 0) return launch_k1v2(t, cfg, masks, heads, depth, count, lb, stream);
     int64_t ntiles = (count + cfg.tile - 1) / cfg.tile;
     int blocks = (int)(ntiles < cfg.blocks ? ntiles : cfg.blocks);
-#define K1_LAUNCH(ONE, SM)                                                                      \
-    k1_bound_kernel<ONE, SM><<<blocks, cfg.threads, cfg.smem, stream>>>(t, cfg.tile, masks, heads, \
-                                                                       depth, count, lb)
-    if (t.n <= 32) {
-        if (cfg.jm_in_smem) K1_LAUNCH(true, true); else K1_LAUNCH(true, false);
+#define K1_LAUNCH(ONE, SM, WIDE)                                                                      \
+    k1_bound_kernel<ONE, SM, WIDE><<<blocks, cfg.threads, cfg.smem, stream>>>(t, cfg.tile, masks, heads, \
+                                                                             depth, count, lb)
+    if (cfg.wide) {
+        K1_LAUNCH(false, false, true);
+    } else if (t.n <= 32) {
+        if (cfg.jm_in_smem) K1_LAUNCH(true, true, false); else K1_LAUNCH(true, false, false);
     } else {
-        if (cfg.jm_in_smem) K1_LAUNCH(false, true); else K1_LAUNCH(false, false);
+        if (cfg.jm_in_smem) K1_LAUNCH(false, true, false); else K1_LAUNCH(false, false, false);
     }
 #undef K1_LAUNCH
     return cudaGetLastError();

@@ -727,9 +727,16 @@ int explorer_run_batched(fbb_ctx* ctx, const int64_t* targets, int ntargets, int
             const int64_t ri = r + i;
             tmax = std::max<int64_t>(tmax, targets[ri < ntargets ? ri : ntargets - 1]);
         }
-        // staging for the largest pool of the batch: a chunk holds >= cmax/2 children
+        // staging for the largest pool of the batch, worst case: every internal segment
+        // (r >= 3) at its fewest children per chunk, min(cmax / r, ppc_cap) * r, plus one
+        // partial chunk per segment; fill_buffer overshoots the target by < n children
         const int cmax = ctx->k2.cmax;
-        const int64_t chunks = 2 * tmax / cmax + n + 2;
+        int64_t cpc_min = cmax;
+        for (int r = 3; r <= n; ++r) {
+            const int ppc = parents_per_chunk(n, n - r, cmax, ctx->k2.ppc_cap);
+            cpc_min = std::min<int64_t>(cpc_min, (int64_t)std::max(ppc, 1) * r);
+        }
+        const int64_t chunks = (tmax + n + cpc_min - 1) / std::max<int64_t>(cpc_min, 1) + n + 2;
         CK(store_ensure(ctx, ctx->staging, chunks * cmax, 0), "staging");
         CK(ctx->st_lb.ensure((size_t)chunks * cmax * 4), "staging");
         CK(ctx->st_count.ensure((size_t)chunks * 4), "staging");
@@ -753,6 +760,7 @@ int explorer_run_batched(fbb_ctx* ctx, const int64_t* targets, int ntargets, int
         hl->cmax = cmax;
         hl->ppc_cap = ctx->k2.ppc_cap;
         hl->nrounds = R;
+        hl->chunk_cap = (int32_t)std::min<int64_t>(chunks, INT32_MAX);
         for (int i = 0; i < n; ++i) hl->schedule[i] = ctx->schedule[i];
         LoopState* dl = ctx->d_loop.as<LoopState>();
         Pool* dp = ctx->d_pool.as<Pool>();
@@ -776,6 +784,7 @@ int explorer_run_batched(fbb_ctx* ctx, const int64_t* targets, int ntargets, int
         const float sync_ms = std::chrono::duration<float, std::milli>(w1 - t_sync).count();
         const float wall_ms = std::chrono::duration<float, std::milli>(w1 - w0).count();
         if (hl->stop == 4) return ctx->fail(FBB_E_STATE, "corrupt pending node (unscheduled-job count mismatch)");
+        if (hl->stop == 5) return ctx->fail(FBB_E_STATE, "device loop: staging smaller than a planned pool");
         int valid = 0;
         while (valid < R && hl->rec[valid].valid) ++valid;
         const int64_t nb = (int64_t)node_bytes(ctx);
@@ -832,7 +841,26 @@ int explorer_run_batched(fbb_ctx* ctx, const int64_t* targets, int ntargets, int
 // =========================================================================================
 extern "C" {
 
-const char* fbb_version(void) { return "flowbb-b200 0.1 (sm_100a)"; }
+const char* fbb_version(void) { return "flowbb-b200 0.2 (sm_100a)"; }
+
+int fbb_kernels(fbb_ctx* ctx, char* buf, size_t cap) {
+    if (!ctx || !buf || cap == 0) return FBB_E_ARG;
+    char k1[64], k2[64];
+    const K1Config& a = ctx->k1;
+    if (a.variant == 0)
+        std::snprintf(k1, sizeof k1, "k1_bound_kernel<%d,%d,%d>", ctx->dt.n <= 32 && !a.wide, a.jm_in_smem, a.wide);
+    else std::snprintf(k1, sizeof k1, "k1v2_kernel<%d,4>", a.variant);
+    const K2Config& b = ctx->k2;
+    if (b.variant >= 100000)
+        std::snprintf(k2, sizeof k2, "k2_v3_kernel<%d,%d>", (b.variant / 100) % 100, b.variant % 100);
+    else if (b.variant != 0)
+        std::snprintf(k2, sizeof k2, "k2_v2_kernel<%d,%d,%d>", (b.variant / 100) % 100, b.variant % 100,
+                      b.variant / 10000);
+    else
+        std::snprintf(k2, sizeof k2, "k2_internal_kernel<%d,%d>", b.jm_in_smem, b.wide);
+    std::snprintf(buf, cap, "K1=%s K2=%s cmax=%d ppc_cap=%d blocks=%d", k1, k2, b.cmax, b.ppc_cap, b.blocks);
+    return FBB_OK;
+}
 
 fbb_ctx* fbb_create(int device, const int32_t* p, int n, int m) {
     auto fail = [&](int code, const std::string& m_) -> fbb_ctx* {

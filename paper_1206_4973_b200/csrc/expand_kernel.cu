@@ -28,6 +28,7 @@
 // (integrate lowers the incumbent mid-batch; leaves precede every internal
 // child in a pool because the leaf-producing bucket is the deepest one).
 #include <climits>
+#include <type_traits>
 
 #include "k2_common.cuh"
 
@@ -44,8 +45,9 @@ struct K2Layout {
     int ppc_max, pst, mst;
 };
 
+// mq_bytes: 2 (int16 M', the safe16 instances) or 4 (kWide: int32 M')
 __host__ __device__ inline K2Layout k2_layout(int n, int m, int P, int cmax, int threads,
-                                              bool jm_in_smem) {
+                                              bool jm_in_smem, int mq_bytes = 2) {
     K2Layout L;
     int W32 = (n + 31) / 32;
     L.ppc_max = cmax / 3 > 0 ? cmax / 3 : 1;
@@ -64,7 +66,7 @@ __host__ __device__ inline K2Layout k2_layout(int n, int m, int P, int cmax, int
     L.min1 = o; o = a16(o + (size_t)L.ppc_max * m * 4);
     L.min2 = o; o = a16(o + (size_t)L.ppc_max * m * 4);
     L.amin = o; o = a16(o + (size_t)L.ppc_max * m * 4);
-    L.Mq = o;   o = a16(o + (size_t)cmax * L.pst * 2);
+    L.Mq = o;   o = a16(o + (size_t)cmax * L.pst * mq_bytes);
     L.cR = o;   o = a16(o + (size_t)cmax * L.mst * 4);
     L.cL = o;   o = a16(o + (size_t)cmax * L.mst * 4);
     L.pre = o;  o = a16(o + (size_t)L.ppc_max * n);
@@ -86,7 +88,10 @@ __device__ inline bool um_test(const uint32_t* um, int j) { return (um[j >> 5] >
 
 // kJmSmem: the Johnson table is staged in shared memory (n*P*4 bytes); for the
 // largest instances (200x20: 152 KB) it is read through L1/L2 instead.
-template <bool kJmSmem>
+// kWide: instances outside the packed / 16-bit ranges (DevTables::safe16): the unpacked
+// rows (DevTables::jw) and int32 M' -- the reference's plain int arithmetic
+// (bound.hpp:27-44, 79-90) for any instance whose total processing time fits int32.
+template <bool kJmSmem, bool kWide>
 __global__ void __launch_bounds__(128) k2_internal_kernel(DevTables t, const Pool* __restrict__ pool,
                                                          int first_seg, int cmax, int32_t ub,
                                                          int frozen, RoundState* rs,
@@ -95,8 +100,10 @@ __global__ void __launch_bounds__(128) k2_internal_kernel(DevTables t, const Poo
     extern __shared__ __align__(16) unsigned char smem[];
     const int n = t.n, m = t.m, P = t.P, W = t.W;
     const int W32 = (n + 31) / 32;
-    const K2Layout L = k2_layout(n, m, P, cmax, blockDim.x, kJmSmem);
-    const uint32_t* s_jm = kJmSmem ? (const uint32_t*)(smem + L.jm) : t.jm;
+    using MqT = typename std::conditional<kWide, int32_t, int16_t>::type;
+    constexpr int32_t kNegA = kWide ? -(1 << 29) : kNeg;  // -inf: |D|, c <= 2^30 (total check)
+    const K2Layout L = k2_layout(n, m, P, cmax, blockDim.x, kJmSmem && !kWide, (int)sizeof(MqT));
+    const uint32_t* s_jm = (kJmSmem && !kWide) ? (const uint32_t*)(smem + L.jm) : t.jm;
     int32_t* s_pk = (int32_t*)(smem + L.pk);
     int32_t* s_p = (int32_t*)(smem + L.p);
     int32_t* s_tl = (int32_t*)(smem + L.tl);
@@ -108,7 +115,7 @@ __global__ void __launch_bounds__(128) k2_internal_kernel(DevTables t, const Poo
     int32_t* s_min1 = (int32_t*)(smem + L.min1);
     int32_t* s_min2 = (int32_t*)(smem + L.min2);
     int32_t* s_amin = (int32_t*)(smem + L.amin);
-    int16_t* s_Mq = (int16_t*)(smem + L.Mq);
+    MqT* s_Mq = (MqT*)(smem + L.Mq);
     int32_t* s_cR = (int32_t*)(smem + L.cR);
     int32_t* s_cL = (int32_t*)(smem + L.cL);
     uint8_t* s_pre = (uint8_t*)(smem + L.pre);
@@ -117,13 +124,27 @@ __global__ void __launch_bounds__(128) k2_internal_kernel(DevTables t, const Poo
     const int tid = threadIdx.x, bd = blockDim.x, lane = tid & 31, warp = tid >> 5;
     const int nwarps = bd >> 5;
 
-    if (kJmSmem)
+    if (kJmSmem && !kWide)
         for (int x = tid; x < n * P; x += bd) ((uint32_t*)(smem + L.jm))[x] = t.jm[x];
     for (int x = tid; x < P; x += bd) s_pk[x] = (int32_t)t.pair_k[x] | ((int32_t)t.pair_l[x] << 16);
     for (int x = tid; x < n * m; x += bd) {
         s_p[x] = t.p[x];
         s_tl[x] = t.tails[x];
     }
+    // Johnson row entry (job, d, c) of position i, pair q
+    auto entry = [&](int i, int q, int& j, int32_t& d, int32_t& c) {
+        if constexpr (kWide) {
+            const int4 w = __ldg(t.jw + (size_t)i * P + q);
+            j = w.x;
+            d = w.y;
+            c = w.z;
+        } else {
+            const uint32_t e = s_jm[i * P + q];
+            j = entry_job(e);
+            d = entry_d(e);
+            c = entry_c(e);
+        }
+    };
     // incumbent for internal children: min(UB, batch leaf minimum) unless frozen
     // the round's bound, semantics and first internal segment come from the pool
     // (written by the host, or by the device-side planner of the batched explorer loop)
@@ -238,28 +259,32 @@ __global__ void __launch_bounds__(128) k2_internal_kernel(DevTables t, const Poo
             int pp = x / P, q = x - pp * P;
             const uint32_t* um = s_um + pp * W32;
             const uint8_t* rank = s_rank + pp * n;
-            int16_t* Mq = s_Mq + (size_t)(pp * r) * L.pst + q;
-            int32_t D = 0, PM = kNeg;
+            MqT* Mq = s_Mq + (size_t)(pp * r) * L.pst + q;
+            // int16 M' (safe16 instances: every M' fits; -inf clamps to -32768, which
+            // loses to R_l since R_k <= R_l); int32 M' in the kWide form
+            constexpr int32_t kLo = kWide ? INT_MIN : -32768;
+            int32_t D = 0, PM = kNegA;
             for (int i = 0; i < n; ++i) {
-                uint32_t e = s_jm[i * P + q];
-                int j = entry_job(e);
+                int j;
+                int32_t dj, cj;
+                entry(i, q, j, dj, cj);
                 if (um_test(um, j)) {
-                    Mq[rank[j] * L.pst] = (int16_t)max(PM, -32768);  // exclusive prefix max
-                    PM = max(PM, D + entry_c(e));
-                    D += entry_d(e);
+                    Mq[rank[j] * L.pst] = (MqT)max(PM, kLo);  // exclusive prefix max
+                    PM = max(PM, D + cj);
+                    D += dj;
                 }
             }
-            int32_t SM = kNeg;
+            int32_t SM = kNegA;
             for (int i = n - 1; i >= 0; --i) {
-                uint32_t e = s_jm[i * P + q];
-                int j = entry_job(e);
+                int j;
+                int32_t dj, cj;
+                entry(i, q, j, dj, cj);
                 if (um_test(um, j)) {
-                    int dj = entry_d(e);
                     D -= dj;  // D_<i
-                    int16_t* slot = Mq + rank[j] * L.pst;
+                    MqT* slot = Mq + rank[j] * L.pst;
                     int32_t v = max((int32_t)*slot, SM - dj);
-                    *slot = (int16_t)max(v, -32768);
-                    SM = max(SM, D + entry_c(e));
+                    *slot = (MqT)max(v, kLo);
+                    SM = max(SM, D + cj);
                 }
             }
         }
@@ -281,7 +306,7 @@ __global__ void __launch_bounds__(128) k2_internal_kernel(DevTables t, const Poo
                 cL[k] = lc;
                 lb = max(lb, prev + lc);  // one-machine term (bound.hpp:61-74)
             }
-            const int16_t* Mq = s_Mq + (size_t)c * L.pst;
+            const MqT* Mq = s_Mq + (size_t)c * L.pst;
             for (int q = 0; q < P; ++q) {
                 int kl = s_pk[q];
                 int k = kl & 0xFFFF, l = kl >> 16;
@@ -356,18 +381,33 @@ __global__ void __launch_bounds__(128) k2_internal_kernel(DevTables t, const Poo
 
 // Children of parents at depth >= n-2 are complete schedules: bound = makespan
 // (bound.hpp:95).  Thread per child; batch-minimum (value, position) by atomicMin.
-__global__ void k2_leaf_kernel(DevTables t, const Pool* __restrict__ pool, int seg_index,
+// A pool has at most two leaf segments, both ahead of every internal one (segments
+// are depth-descending): parents at depth n-1 (children complete at once) and at
+// depth n-2 (children auto-completed, search.hpp:48-55).  Pending trees built by the
+// search itself never hold depth n-1 nodes, but fbb_explorer_reset / push and
+// fbb_expand_bound_prune accept them.
+__device__ __forceinline__ int leaf_segments(const Pool* __restrict__ pool, int n) {
+    int k = 0;
+    while (k < 2 && k < pool->nseg && pool->seg[k].depth >= n - 2) ++k;
+    return k;
+}
+
+__global__ void k2_leaf_kernel(DevTables t, const Pool* __restrict__ pool, int /*unused*/,
                                RoundState* rs) {
     asm volatile("griddepcontrol.wait;" ::: "memory");  // the pool upload (PDL chain)
     asm volatile("griddepcontrol.launch_dependents;");
     const int n = t.n, m = t.m, W = t.W;
-    if (pool->nseg <= seg_index || pool->seg[seg_index].depth < n - 2) return;  // no leaves
-    const Segment& sg = pool->seg[seg_index];
-    const int depth = sg.depth;
-    const int r = n - depth;
-    const int64_t nc = sg.count * r;
-    for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < nc;
-         c += (int64_t)gridDim.x * blockDim.x) {
+    const int nls = leaf_segments(pool, n);
+    if (nls == 0) return;  // no leaves
+    const int64_t nc0 = pool->seg[0].count * (n - pool->seg[0].depth);
+    const int64_t nct = nc0 + (nls > 1 ? pool->seg[1].count * (n - pool->seg[1].depth) : 0);
+    for (int64_t cc = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; cc < nct;
+         cc += (int64_t)gridDim.x * blockDim.x) {
+        const int si = cc < nc0 ? 0 : 1;
+        const Segment& sg = pool->seg[si];
+        const int64_t c = si == 0 ? cc : cc - nc0;
+        const int depth = sg.depth;
+        const int r = n - depth;
         int64_t pp = c / r;
         int rk = (int)(c - pp * r);
         int64_t node = sg.first + sg.step * pp;
@@ -417,28 +457,29 @@ __global__ void k2_leaf_kernel(DevTables t, const Pool* __restrict__ pool, int s
 }
 
 // Writes the schedule of the batch's best leaf (if it beats ub) before the
-// parents' storage is recycled by the push.
+// parents' storage is recycled by the push.  A corrupt-node flag (found < 0, set by
+// the leaf kernel) is kept for the host to report.
 __global__ void leaf_schedule_kernel(DevTables t, const Pool* __restrict__ pool, RoundState* rs,
                                      int32_t ub) {
     asm volatile("griddepcontrol.wait;" ::: "memory");  // the leaf kernel (PDL chain)
     asm volatile("griddepcontrol.launch_dependents;");
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (rs->found < 0) return;
     ub = pool->ub;
-    if (pool->nseg == 0 || pool->seg[0].depth < t.n - 2) {  // no leaves this round
-        rs->found = 0;
-        return;
-    }
+    const int n = t.n;
+    const int nls = leaf_segments(pool, n);
     unsigned long long inv = rs->leaf_inv;
     unsigned long long key = ~inv;
     int32_t* schedule = rs->schedule;
     int32_t* found = &rs->found;
-    if (inv == 0ull || (int32_t)(key >> 32) >= ub) {
+    if (nls == 0 || inv == 0ull || (int32_t)(key >> 32) >= ub) {  // no (improving) leaf
         *found = 0;
         return;
     }
-    const int n = t.n, W = t.W;
     int64_t pos = (int64_t)(key & 0xFFFFFFFFull);
-    const Segment& sg = pool->seg[0];  // leaves only come from the first (deepest) segment
+    // the leaf's segment: the first or (depth n-2 behind depth n-1) the second one
+    const int si = nls > 1 && pos >= pool->seg[1].child_base ? 1 : 0;
+    const Segment& sg = pool->seg[si];
     const int r = n - sg.depth;
     int64_t c = pos - sg.child_base;
     int64_t pp = c / r;
@@ -691,14 +732,17 @@ K2Config k2_config(const DevTables& t, int device) {
     c.threads = 128;
     int n = t.n;
     c.cmax = n <= 128 ? 128 : ((n + 31) / 32) * 32;
+    c.wide = !(t.safe16 & kSafeM16);  // outside the packed / int16 ranges: int32 form
     int max_smem = 0;
     cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
-    c.smem = k2_layout(t.n, t.m, t.P, c.cmax, c.threads, true).total;
-    c.jm_in_smem = c.smem <= (size_t)max_smem / 2;  // keep >= 2 CTAs per SM
-    if (!c.jm_in_smem) c.smem = k2_layout(t.n, t.m, t.P, c.cmax, c.threads, false).total;
+    const int mqb = c.wide ? 4 : 2;
+    c.smem = k2_layout(t.n, t.m, t.P, c.cmax, c.threads, !c.wide, mqb).total;
+    c.jm_in_smem = !c.wide && c.smem <= (size_t)max_smem / 2;  // keep >= 2 CTAs per SM
+    if (!c.jm_in_smem) c.smem = k2_layout(t.n, t.m, t.P, c.cmax, c.threads, false, mqb).total;
     int sms = 148, per_sm = 1;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    auto kern = c.jm_in_smem ? k2_internal_kernel<true> : k2_internal_kernel<false>;
+    auto kern = c.wide ? k2_internal_kernel<false, true>
+                       : (c.jm_in_smem ? k2_internal_kernel<true, false> : k2_internal_kernel<false, false>);
     // the attribute is per kernel, not per context: allow the device maximum once
     int optin = 0;
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
@@ -711,8 +755,10 @@ K2Config k2_config(const DevTables& t, int device) {
 
 cudaError_t launch_k2_leaves(const DevTables& t, const Pool* d_pool, const Pool& h_pool,
                              int seg_index, RoundState* rs, cudaStream_t stream, bool pdl) {
-    const Segment& sg = h_pool.seg[seg_index];
-    int64_t nc = sg.count * (t.n - sg.depth);
+    int64_t nc = 0;  // children of every leaf segment (at most two, from the first)
+    for (int s = 0; s < 2 && s < h_pool.nseg && h_pool.seg[s].depth >= t.n - 2; ++s)
+        nc += h_pool.seg[s].count * (t.n - h_pool.seg[s].depth);
+    (void)seg_index;
     if (nc <= 0) return cudaSuccess;
     int blocks = (int)((nc + 255) / 256);
     if (blocks > 4096) blocks = 4096;
@@ -730,7 +776,9 @@ cudaError_t launch_k2_internal(const DevTables& t, const K2Config& cfg, const Po
         return launch_k2_v3(t, cfg, d_pool, first_seg, blocks, ub, frozen, rs, out, stream, pdl);
     if (cfg.variant != 0)
         return launch_k2_v2(t, cfg, d_pool, first_seg, blocks, ub, frozen, rs, out, stream, pdl);
-    return launch_pdl(cfg.jm_in_smem ? k2_internal_kernel<true> : k2_internal_kernel<false>, dim3(blocks),
+    return launch_pdl(cfg.wide ? k2_internal_kernel<false, true>
+                               : (cfg.jm_in_smem ? k2_internal_kernel<true, false> : k2_internal_kernel<false, false>),
+                      dim3(blocks),
                       dim3(cfg.threads), cfg.smem, stream, pdl, t, d_pool, first_seg, cfg.cmax, ub, frozen, rs,
                       out);
 }
@@ -800,12 +848,15 @@ cudaError_t launch_round_device(const DevTables& t, const K2Config& cfg, const P
         e = launch_k2_v3(t, cfg, d_pool, 0, cfg.blocks, 0, 0, rs, out, stream);
     else if (cfg.variant != 0)
         e = launch_k2_v2(t, cfg, d_pool, 0, cfg.blocks, 0, 0, rs, out, stream);
+    else if (cfg.wide)
+        k2_internal_kernel<false, true><<<cfg.blocks, cfg.threads, cfg.smem, stream>>>(t, d_pool, 0, cfg.cmax, 0,
+                                                                                       0, rs, out);
     else if (cfg.jm_in_smem)
-        k2_internal_kernel<true><<<cfg.blocks, cfg.threads, cfg.smem, stream>>>(t, d_pool, 0, cfg.cmax, 0, 0,
-                                                                                rs, out);
+        k2_internal_kernel<true, false><<<cfg.blocks, cfg.threads, cfg.smem, stream>>>(t, d_pool, 0, cfg.cmax, 0,
+                                                                                       0, rs, out);
     else
-        k2_internal_kernel<false><<<cfg.blocks, cfg.threads, cfg.smem, stream>>>(t, d_pool, 0, cfg.cmax, 0, 0,
-                                                                                 rs, out);
+        k2_internal_kernel<false, false><<<cfg.blocks, cfg.threads, cfg.smem, stream>>>(t, d_pool, 0, cfg.cmax, 0,
+                                                                                        0, rs, out);
     if (k2_end) cudaEventRecord(k2_end, stream);
     place_kernel<true><<<148 * 2, kPlaceThreads, (size_t)cfg.cmax * kPlaceChunks, stream>>>(t, d_pool, cfg.cmax, rs,
                                                                                       out, nullptr);

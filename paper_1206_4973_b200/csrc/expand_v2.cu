@@ -659,8 +659,14 @@ bool k2_v2_config(const DevTables& t, int device, K2Config* out) {
     // measured (profiles/r01_reading.md): m = 20 runs fastest at 2 CTAs/SM with the
     // 16x2 grouped Phase B, m in {5, 10} at 3 CTAs/SM; FBB_K2_OCC=2|3 overrides
     const char* occ_env = getenv("FBB_K2_OCC");
-    const int occ = occ_env ? (occ_env[0] == '2' ? 2 : 3) : (m == 20 ? 2 : 3);
-    const int NN = n <= 20 ? 20 : (n <= 32 ? 32 : 64);
+    int occ = occ_env ? (occ_env[0] == '2' ? 2 : 3) : (m == 20 ? 2 : 3);
+    int NN = n <= 20 ? 20 : (n <= 32 ? 32 : 64);
+    // 16-bit intermediates must be exact for this instance (DevTables::safe16): every M'
+    // is stored as int16; the 2-CTA grouped Phase B adds Lc_l + M' in 16x2; the two-parent
+    // scan (N = 20 at 2 CTAs/SM) runs D, D + c and its -16384 neutral in 16x2
+    if (!(t.safe16 & kSafeM16)) return false;
+    if (occ == 2 && !(t.safe16 & kSafeLcM16)) occ = 3;
+    if (NN == 20 && occ == 2 && !(t.safe16 & kSafeDual16)) NN = 32;
     // children per chunk, measured (profiles/r01_k2_iterations.md): larger chunks amortise
     // the per-chunk setup and barriers while the CTAs per SM hold -- Ta021 (m = 20, 2
     // CTAs/SM) 128 -> 160: +3.9 %, 192 drops to 1 CTA/SM; Ta001 (m = 5, 3 CTAs/SM)

@@ -388,6 +388,7 @@ cudaError_t v3_setup(K2Config& c, int device) {
 bool k2_v3_config(const DevTables& t, int device, K2Config* out) {
     const int m = t.m, n = t.n;
     if (n <= 64 || n > 256 || !(m == 5 || m == 10 || m == 20) || !t.rowv3) return false;
+    if (!(t.safe16 & kSafeM16)) return false;  // M' is stored as int16 (DevTables::safe16)
     K2Config c;
     const int NW = n <= 128 ? 4 : 8;
     c.cmax = ((n + 31) / 32) * 32;          // one parent's children always fit a chunk

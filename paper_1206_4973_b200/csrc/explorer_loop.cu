@@ -93,6 +93,10 @@ __global__ void loop_plan_kernel(DevTables t, LoopState* ls, Pool* pool, RoundSt
         const int ppc = parents_per_chunk(n, sg.depth, cmax, ls->ppc_cap);
         chunk += (sg.count + ppc - 1) / ppc;
     }
+    if (chunk > ls->chunk_cap) {  // the host sized staging for the worst case: never taken
+        ls->stop = 5;
+        return;  // nseg stays 0: nothing of this round runs
+    }
     for (int s = 0; s < nseg; ++s) rs->seg_surv[s] = 0;
     pool->first_internal = first_internal;
     pool->nchunks = chunk;

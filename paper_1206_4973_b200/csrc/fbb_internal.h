@@ -52,14 +52,33 @@ struct DevTables {
     // bits 16..31 c -- membership and the child slot come from a per-parent table
     // indexed by j, so no code/shift field is needed.  Null when rowpk is.
     uint32_t* rowv3;
+    // Unpacked Johnson rows (n*P, [i][q]): {job, d, c, 0} as int32 -- any instance whose
+    // total processing time fits int32 arithmetic; read by the kWide kernels.  Null unless
+    // some kernel needs it (values outside the packed or the int16 ranges).
+    int4* jw;
+    // Which 16-bit intermediates are exact for this instance (build_host_tables' range
+    // analysis): kSafeM16 = every M' fits int16, kSafeLcM16 = every Lc_l + M'_kl fits int16,
+    // kSafeDual16 = the 16x2 two-parent scan (D, D + c, the -16384 neutral) fits.
+    int32_t safe16;
 };
+constexpr int32_t kSafeM16 = 1, kSafeLcM16 = 2, kSafeDual16 = 4;
+constexpr int32_t kTablesPacked = 8;  // safe16 bit: jm holds the packed rows
 
 // Host copy of the same tables (for tests of the table builder).
 struct HostTables {
     int n = 0, m = 0, P = 0, W = 0;
-    int max_abs_d = 0;  // max |p[j][k] - p[j][l]| over pairs
+    int64_t max_abs_d = 0;  // max |p[j][k] - p[j][l]| over pairs
+    bool packed = true;     // every entry fits pack_entry (|d| <= 255, c < 2^14)
+    // Range analysis of the max-plus intermediates (bound.hpp:27-44 in the form of
+    // fbb_internal.h's pack_entry comment), over every unscheduled set U:
+    //   D_<i in [sum of negative d, sum of positive d] of the pair,  c in [0, max c],
+    //   so M' = max(D_<i + c_i) <= m_hi = max_q (sum_j max(d,0) + max_j c) and >= m_lo,
+    //   and Lc_l = load_l - p[x][l] + min tail_l <= lc_max = max_l (sum_j p[j][l] + max_j tail).
+    int64_t m_hi = 0, m_lo = 0, lc_max = 0;
+    int32_t safe16 = 0;     // kSafe* bits derived from the above
     std::vector<int32_t> p, tails;
-    std::vector<uint32_t> jm;
+    std::vector<uint32_t> jm;   // packed rows (zeros when !packed)
+    std::vector<int32_t> jw;    // unpacked rows, 4 int32 per entry {job, d, c, 0}
     std::vector<int16_t> pair_k, pair_l;
 };
 
@@ -67,13 +86,16 @@ struct HostTables {
 // (group, key, job) -- group 0 if a+lag < lag+b, ascending a+lag, else
 // group 1 descending lag+b -- which is the order std::stable_sort gives over
 // the ascending unscheduled list (bound.hpp:28-36) restricted to any subset.
-// Returns FBB_E_RANGE when a value does not fit the packed entry.
+// Returns FBB_E_RANGE only when the instance exceeds int32 arithmetic (total
+// processing time > 2^30) or the device limits (n <= 256, m <= 64); instances whose
+// values do not fit the packed / 16-bit forms run the kWide kernels.
 int build_host_tables(const int32_t* p, int n, int m, HostTables* out, std::string* why);
 int upload_tables(const HostTables& h, DevTables* d, std::string* why);
 void free_tables(DevTables* d);
 
 // ---- K1 ----------------------------------------------------------------------------------
 struct K1Config {
+    bool wide = false;   // k1_bound_kernel over DevTables::jw (unpacked rows)
     int threads = 256;
     int tile = 32;       // nodes per tile
     bool jm_in_smem = true;
@@ -137,6 +159,7 @@ struct Pool {
 };
 
 struct K2Config {
+    bool wide = false;   // generic kernel with int32 Mq over DevTables::jw
     int threads = 128;
     int cmax = 128;      // children per chunk (>= n)
     bool jm_in_smem = true;
@@ -222,10 +245,11 @@ struct LoopState {
     int64_t targets[kLoopMax];        // pool target of each round of the batch
     int64_t tot_bounded, budget;      // cumulative bounded count; stop when >= budget (> 0)
     int32_t incumbent, best, found, frozen;
-    int32_t stop;                     // 0 running, 1 pending empty, 2 budget, 3 bucket too small
+    int32_t stop;                     // 0 running, 1 pending empty, 2 budget, 3 bucket too small,
+                                      // 4 corrupt node, 5 staging too small (never, by sizing)
     int32_t need_depth;               // stop == 3: the bucket that must grow ...
     int64_t need_rows;                // ... to at least this many rows
-    int32_t cmax, ppc_cap, nrounds, pad;
+    int32_t cmax, ppc_cap, nrounds, chunk_cap;  // chunk_cap: staging chunks available
     int32_t schedule[kMaxJobs];       // incumbent schedule (solve mode)
     LoopRecord rec[kLoopMax];
 };

@@ -9,6 +9,7 @@
 // input (= job index) order.
 #include <algorithm>
 #include <climits>
+#include <cstring>
 #include <numeric>
 
 #include "fbb_internal.h"
@@ -53,14 +54,19 @@ int build_host_tables(const int32_t* p, int n, int m, HostTables* out, std::stri
         }
     const int P = h.P;
     h.jm.assign((size_t)n * std::max(P, 1), 0);
+    h.jw.assign((size_t)n * std::max(P, 1) * 4, 0);
     std::vector<int> order(n);
-    std::vector<int32_t> a(n), b(n), lag(n);
+    std::vector<int64_t> a(n), b(n), lag(n);
+    h.packed = true;
+    h.max_abs_d = 0;
+    h.m_hi = 0;
+    h.m_lo = 0;
     for (int q = 0; q < P; ++q) {
         int k = h.pair_k[q], l = h.pair_l[q];
         for (int j = 0; j < n; ++j) {
             a[j] = h.p[(size_t)j * m + k];
             b[j] = h.p[(size_t)j * m + l];
-            lag[j] = h.tails[(size_t)j * m + k] - h.p[(size_t)j * m + l] - h.tails[(size_t)j * m + l];
+            lag[j] = (int64_t)h.tails[(size_t)j * m + k] - h.p[(size_t)j * m + l] - h.tails[(size_t)j * m + l];
         }
         std::iota(order.begin(), order.end(), 0);
         // bound.hpp:30-36 comparator; stable_sort over ascending job index
@@ -71,24 +77,48 @@ int build_host_tables(const int32_t* p, int n, int m, HostTables* out, std::stri
             if (fi) return a[i] + lag[i] < a[j] + lag[j];
             return lag[i] + b[i] > lag[j] + b[j];
         });
+        int64_t spos = 0, sneg = 0, cmax = 0;
         for (int i = 0; i < n; ++i) {
             int j = order[i];
-            int d = a[j] - b[j];
-            int c = a[j] + lag[j];
-            if (d < -256 || d > 255 || c < 0 || c >= (1 << 14)) {
-                *why = "processing times outside the packed Johnson-table range "
-                       "(need |p[j][k]-p[j][l]| <= 255 and sum of a pair span < 16384)";
-                return FBB_E_RANGE;
-            }
-            h.jm[(size_t)i * P + q] = pack_entry(j, d, c);
-            h.max_abs_d = std::max(h.max_abs_d, d < 0 ? -d : d);
+            int64_t d = a[j] - b[j];
+            int64_t c = a[j] + lag[j];  // = sum_{k <= u < l} p[j][u] >= 0
+            if (d < -256 || d > 255 || c < 0 || c >= (1 << 14)) h.packed = false;
+            else h.jm[(size_t)i * P + q] = pack_entry(j, (int)d, (int)c);
+            int32_t* w = &h.jw[((size_t)i * P + q) * 4];
+            w[0] = j;
+            w[1] = (int32_t)d;
+            w[2] = (int32_t)c;
+            h.max_abs_d = std::max<int64_t>(h.max_abs_d, d < 0 ? -d : d);
+            (d > 0 ? spos : sneg) += d;
+            cmax = std::max(cmax, c);
+        }
+        h.m_hi = std::max(h.m_hi, spos + cmax);
+        h.m_lo = std::min(h.m_lo, sneg);
+    }
+    if (!h.packed) std::fill(h.jm.begin(), h.jm.end(), 0u);
+    h.lc_max = 0;
+    for (int l = 0; l < m; ++l) {
+        int64_t load = 0, tmax = 0;
+        for (int j = 0; j < n; ++j) {
+            load += h.p[(size_t)j * m + l];
+            tmax = std::max<int64_t>(tmax, h.tails[(size_t)j * m + l]);
+        }
+        h.lc_max = std::max(h.lc_max, load + tmax);
+    }
+    // 16-bit intermediates (see DevTables::safe16); every bound is exact in int32
+    h.safe16 = h.packed ? kTablesPacked : 0;
+    if (h.packed && h.m_hi <= 32767 && h.m_lo >= -32767) {
+        h.safe16 |= kSafeM16;
+        if (h.lc_max + h.m_hi <= 32767) {
+            h.safe16 |= kSafeLcM16;
+            if (h.m_hi <= 16383 && h.m_lo >= -16383) h.safe16 |= kSafeDual16;
         }
     }
     // every head / bound fits int32 comfortably; check the worst makespan
     int64_t total = 0;
     for (int32_t v : h.p) total += v;
     if (total > (int64_t)1 << 30) {
-        *why = "total processing time too large for int32 arithmetic";
+        *why = "total processing time too large for int32 arithmetic (sum of p > 2^30)";
         return FBB_E_RANGE;
     }
     return FBB_OK;
@@ -116,7 +146,16 @@ int upload_tables(const HostTables& h, DevTables* d, std::string* why) {
         *why = std::string("table upload: ") + cudaGetErrorString(e);
         return FBB_E_CUDA;
     }
-    if (h.max_abs_d <= 127) {
+    d->safe16 = h.safe16;
+    if (!h.packed || !(h.safe16 & kSafeM16)) {  // some kernel runs the unpacked int32 form
+        std::vector<int4> w(h.jw.size() / 4);
+        std::memcpy(w.data(), h.jw.data(), w.size() * sizeof(int4));
+        if ((e = upload(&d->jw, w)) != cudaSuccess) {
+            *why = std::string("table upload: ") + cudaGetErrorString(e);
+            return FBB_E_CUDA;
+        }
+    }
+    if (h.packed && h.max_abs_d <= 127) {
         std::vector<uint32_t> rp(h.jm.size());
         for (size_t x = 0; x < h.jm.size(); ++x) {
             const uint32_t e = h.jm[x];
@@ -149,6 +188,7 @@ void free_tables(DevTables* d) {
     cudaFree(d->pair_l);
     cudaFree(d->rowpk);
     cudaFree(d->rowv3);
+    cudaFree(d->jw);
     *d = DevTables{};
 }
 

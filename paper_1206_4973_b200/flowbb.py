@@ -221,6 +221,12 @@ class Context:
         self._check(self.L.fbb_descriptor(self.h, C.byref(d)))
         return BackendDescriptor(d.grain, d.base_units, d.max_batch)
 
+    def kernels(self) -> str:
+        """The kernel variants this context launches (fbb_kernels)."""
+        buf = C.create_string_buffer(256)
+        self._check(self.L.fbb_kernels(self.h, buf, 256))
+        return buf.value.decode()
+
     # K1 ----------------------------------------------------------------------------------
     def bound(self, batch: NodeBatch) -> np.ndarray:
         cnt = len(batch)
@@ -551,12 +557,14 @@ class ResolutionResult:
     exhausted: bool = True
 
 
-def _drive(ctx: Context, targets, autotune, window, probes, budget, max_rounds):
+def _drive(ctx: Context, targets, autotune, window, probes, budget, max_rounds, tuner=None):
     """Round loop on the device explorer: fixed target schedule (one C call), or the
-    tuner observing each round's wall time (search.hpp:155-165)."""
+    tuner observing each round's wall time (search.hpp:155-165).  `tuner`: one that
+    already observed earlier rounds (solve's root round)."""
     if not autotune:
         return ctx.explorer_run(targets, max_rounds, budget), None
-    tuner = Tuner(ctx.descriptor(), window, probes)
+    if tuner is None:
+        tuner = Tuner(ctx.descriptor(), window, probes)
     rounds = []
     while len(rounds) < max_rounds:
         t0 = time.perf_counter()
@@ -606,12 +614,17 @@ def solve(inst: Instance, initial_ub: Optional[int] = None, fixed_batch: Optiona
     updates, deepest-first LIFO selection)."""
     ctx = context_for(inst, device)
     ctx.explorer_set_residency(pending_on_host)
+    # the tuner exists before the root round and observes it (batch of 1), as
+    # search.hpp:139-165 does: its first window closes on the reference's iteration
+    tuner = Tuner(ctx.descriptor(), window, probes) if autotune else None
     t0 = time.perf_counter()
     r0 = ctx.explorer_start_solve(initial_ub)
+    if tuner is not None:
+        tuner.observe(r0[2], max(time.perf_counter() - t0, 1e-9))
     if targets is None:
         d = ctx.descriptor()
         targets = [fixed_batch if fixed_batch else d.grain * d.base_units]
-    rounds, _ = _drive(ctx, targets, autotune, window, probes, budget, max_rounds)
+    rounds, _ = _drive(ctx, targets, autotune, window, probes, budget, max_rounds, tuner)
     st = ctx.explorer_state()
     sol = Solution()
     sol.optimum = st["incumbent"]

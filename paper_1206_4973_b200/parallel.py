@@ -160,13 +160,15 @@ class ParallelExplorer:
         for donor, rcv, k in plan:
             if self.rank == donor:
                 nodes = self.port.take(k)
-                buf = np.full((k, self.n + 1), -1, np.int16)
+                # int32 rows: torch's NCCL backend has no 16-bit integer type (c10d
+                # NCCLUtils datatype map: int8/uint8/int32/int64/float types only)
+                buf = np.full((k, self.n + 1), -1, np.int32)
                 for i, pr in enumerate(nodes):
                     buf[i, 0] = len(pr)
                     buf[i, 1:1 + len(pr)] = pr
                 self.dist.send(t.from_numpy(buf).to(self.device), rcv, group=self.group)
             elif self.rank == rcv:
-                buf = t.zeros((k, self.n + 1), dtype=t.int16, device=self.device)
+                buf = t.zeros((k, self.n + 1), dtype=t.int32, device=self.device)
                 self.dist.recv(buf, donor, group=self.group)
                 rows = buf.cpu().numpy()
                 self.port.push([list(map(int, r[1:1 + r[0]])) for r in rows if r[0] >= 0])

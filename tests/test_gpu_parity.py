@@ -166,6 +166,59 @@ def test_k2_solve_mode_prunes_with_batch_leaf_min(oracle):
             assert best is None
 
 
+@pytest.mark.parametrize("frozen", [False, True])
+def test_k2_two_leaf_segments(oracle, frozen):
+    # parents at depth n-1 AND at depth n-2 (two leaf segments ahead of the internal ones):
+    # every leaf is evaluated, the batch minimum / first position / schedule come from
+    # either segment, and internal children prune against it (integrate, search.hpp:84-107)
+    rng = np.random.default_rng(17)
+    for trial in range(12):
+        n, m = (9, 4) if trial % 2 else (20, 20)
+        p = rng.integers(1, 60, size=(n, m)).astype(np.int32)
+        inst = inst_of(p)
+        d1 = [list(rng.permutation(n)[: n - 1]) for _ in range(int(rng.integers(1, 6)))]
+        d2 = [list(rng.permutation(n)[: n - 2]) for _ in range(int(rng.integers(1, 6)))]
+        shallow = sorted([list(rng.permutation(n)[: rng.integers(0, n - 2)]) for _ in range(6)],
+                         key=len, reverse=True)
+        parents = d1 + d2 + shallow
+        kids = []
+        for pr in parents:
+            kids += oracle.branch(p, pr)[0]
+        kn = fbb.nodes_from_prefixes(inst, kids)
+        klb = oracle.evaluate_batch(p, kn.masks, kn.heads, kn.depth)
+        leaf_vals = [int(v) for k, v in zip(kids, klb) if len(k) == n]
+        assert len(leaf_vals) == len(d1) + 2 * len(d2)
+        # ub between the two segments' best leaves whenever possible
+        ub = int(np.percentile(leaf_vals, 50 + 10 * (trial % 3))) + (trial % 2)
+        inc = ub if frozen else min([ub] + leaf_vals)
+        surv, slb, best, pos, sched, counts = fbb.Context(inst).expand_bound_prune(
+            fbb.nodes_from_prefixes(inst, parents), ub, frozen=frozen)
+        exp = [k for k, v in zip(kids, klb) if len(k) < n and v < inc]
+        assert surv.prefixes() == exp, trial
+        assert counts[5] == len(leaf_vals)
+        under = [v for v in leaf_vals if v < ub]
+        if under:
+            assert best == min(under), trial
+            first = next(i for i, (k, v) in enumerate(zip(kids, klb)) if len(k) == n and v == best)
+            assert pos == first and sched == [int(x) for x in kids[first]], trial
+        else:
+            assert best is None, trial
+
+
+def test_explorer_pushed_depth_n_minus_1_nodes(oracle):
+    # pending nodes at depth n-1 (accepted by fbb_explorer_reset / push) are leaves' parents
+    rng = np.random.default_rng(23)
+    n, m = 9, 4
+    p = rng.integers(1, 40, size=(n, m)).astype(np.int32)
+    inst = inst_of(p)
+    roots = [list(rng.permutation(n)[: d]) for d in (3, 7, 8, 8, 5, 7, 8)]
+    ub = 10 ** 6
+    full, gold = oracle.resolve(p, ub, roots, targets=[7], max_trace=64)
+    res = fbb.resolve_workload(inst, roots, ub, targets=[7])
+    assert [tuple(r) for r in res.rounds] == [tuple(r) for r in gold]
+    assert res.best == full["optimum"]
+
+
 def test_k2_rejects_non_pop_order():
     inst = fbb.generate_instance(8, 3, 1234)
     ctx = fbb.Context(inst)
@@ -253,18 +306,26 @@ def test_resolution_equivalent_across_batches_and_tuner(traces):
             assert r.nodes_bounded == runs[0].nodes_bounded
 
 
-def test_explorer_pending_matches_oracle_drain(oracle):
-    # after a budget stop, the device pending tree equals the reference's (drain order)
-    inst = fbb.generate_instance(20, 5, 873654221)
-    fbb.resolve_workload(inst, [[]], 1279, targets=[4096], budget=50_000)
-    ctx = fbb.flowbb.context_for(inst)
-    got = ctx.explorer_pending()
+@pytest.mark.parametrize("on_host", [False, True])
+def test_explorer_pending_matches_reference_drain(on_host):
+    # after a budget stop, the device pending tree equals the reference's PendingTree,
+    # node for node in PendingTree::drain order (pending.hpp:41-50)
     from oracle import Ref
     try:
         ref = Ref()
     except FileNotFoundError:
         pytest.skip("oracle/_ref not built on this host")
-    assert len(got) == ctx.explorer_state()["pending"]
+    for (n, m, seed, ub, tgt, budget) in [(20, 5, 873654221, 1279, 4096, 50_000),
+                                         (20, 20, 479340445, 2297, 16384, 400_000),
+                                         (50, 20, 1539989115, 3847, 8192, 100_000)]:
+        inst = fbb.generate_instance(n, m, seed)
+        fbb.resolve_workload(inst, [[]], ub, targets=[tgt], budget=budget, pending_on_host=on_host)
+        ctx = fbb.flowbb.context_for(inst)
+        got = ctx.explorer_pending()
+        res, want = ref.resolve_drain(inst.p, ub, [[]], targets=[tgt], budget=budget)
+        assert res["bounded"] == ctx.explorer_state()["bounded"]
+        assert len(got) == len(want) == ctx.explorer_state()["pending"] > 0
+        assert got == want, f"{n}x{m}: pending tree differs from the reference drain"
 
 
 def test_solve_small_kats():
