@@ -210,6 +210,12 @@ int fbb_tuner_observe(fbb_tuner* t, int64_t nodes_bounded, double elapsed_second
 int fbb_tuner_phase(const fbb_tuner* t); /* 0 doubling, 1 refining, 2 fixed */
 int64_t fbb_tuner_best_batch(const fbb_tuner* t);
 double fbb_tuner_best_throughput(const fbb_tuner* t);
+/* Tuner::set_trace (autotune.hpp:112-113): called once per closed window with the
+ * window index, the measured batch, its throughput and the decision text
+ * ("double to B" | "refine at B" | "fix at B"); fn == NULL disables it. */
+typedef void (*fbb_tuner_trace_fn)(void* user, int window, int64_t batch, double throughput,
+                                   const char* decision);
+int fbb_tuner_set_trace(fbb_tuner* t, fbb_tuner_trace_fn fn, void* user);
 
 /* The kernel variants this context launches, as one line of text, e.g.
  * "K1=k1v2_kernel<8,4> K2=k2_v3_kernel<4,20> cmax=224 ppc_cap=16 blocks=444"

@@ -323,6 +323,29 @@ class Ref:
     def detect_units(self):
         return int(self.lib.ref_detect_units())
 
+    def workload_text(self, p, ub, nodes, seed):
+        """The reference's save_workload(generate_workload(inst, ub, by_nodes(nodes), seed))."""
+        n, m = p.shape
+        buf = C.create_string_buffer(1 << 24)
+        self.lib.ref_workload_text.argtypes = [C.c_int, C.c_int, _i32p, C.c_int32, C.c_int64,
+                                               C.c_uint32, C.c_char_p, C.c_int64]
+        self.lib.ref_workload_text.restype = C.c_int64
+        k = self.lib.ref_workload_text(n, m, np.ascontiguousarray(p, np.int32).ravel(), ub, nodes,
+                                       seed, buf, 1 << 24)
+        if k < 0:
+            raise RuntimeError("ref_workload_text failed")
+        return buf.raw[:k].decode()
+
+    def tuner_trace(self, grain, units, max_batch, window, probes, peak):
+        """The reference Tuner's trace lines ("window batch decision") on the synthetic
+        curve x / (1 + (x / peak)^2), driven until fixed (ref_tuner_trace)."""
+        buf = C.create_string_buffer(1 << 16)
+        self.lib.ref_tuner_trace.argtypes = [C.c_int] * 5 + [C.c_double, C.c_char_p, C.c_int64]
+        k = self.lib.ref_tuner_trace(grain, units, max_batch, window, probes, peak, buf, 1 << 16)
+        if k < 0:
+            raise RuntimeError("ref_tuner_trace failed")
+        return buf.value.decode().splitlines()
+
     def generate_instance(self, n, m, seed):
         p = np.zeros(n * m, np.int32)
         if self.lib.ref_generate_instance(n, m, seed, p) != 0:

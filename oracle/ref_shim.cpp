@@ -399,4 +399,46 @@ int ref_bench_rounds(int n, int m, const int32_t* p, int32_t ub, int64_t target,
     }
 }
 
+// save_workload(generate_workload(...)) of the reference (workload.hpp:62-131) as text;
+// returns its length (or -2 when cap is too small).
+int64_t ref_workload_text(int n, int m, const int32_t* p, int32_t ub, int64_t nodes, uint32_t seed,
+                          char* out, int64_t cap) {
+    try {
+        Instance inst = make_instance(n, m, p);
+        std::string text = save_workload(generate_workload(inst, ub, CaptureCutoff::by_nodes(nodes), seed));
+        if ((int64_t)text.size() + 1 > cap) return -2;
+        std::memcpy(out, text.c_str(), text.size() + 1);
+        return (int64_t)text.size();
+    } catch (const std::exception&) {
+        return -1;
+    }
+}
+
+// The reference Tuner (autotune.hpp) with its trace hook, driven by the synthetic
+// unimodal throughput curve tp(x) = x / (1 + (x / peak)^2) (each observation bounds
+// target() nodes in target()/tp seconds) until fixed; the trace lines
+// "window batch decision" go to out (newline-separated).  Returns the line count.
+int ref_tuner_trace(int grain, int units, int max_batch, int window, int probes, double peak,
+                    char* out, int64_t cap) {
+    try {
+        Tuner tuner(BackendDescriptor{grain, units, max_batch}, window, probes);
+        std::string text;
+        int lines = 0;
+        tuner.set_trace([&](int w, int batch, double, const std::string& decision) {
+            text += std::to_string(w) + " " + std::to_string(batch) + " " + decision + "\n";
+            ++lines;
+        });
+        for (int it = 0; it < 10000 && tuner.phase() != TunerPhase::fixed; ++it) {
+            const double x = tuner.target();
+            const double tp = x / (1.0 + (x / peak) * (x / peak));
+            tuner.observe(tuner.target(), x / tp);
+        }
+        if ((int64_t)text.size() + 1 > cap) return -2;
+        std::memcpy(out, text.c_str(), text.size() + 1);
+        return lines;
+    } catch (const std::exception&) {
+        return -1;
+    }
+}
+
 }  // extern "C"

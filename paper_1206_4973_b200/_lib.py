@@ -25,7 +25,7 @@ EXPORTED = (
     "fbb_explorer_pending", "fbb_explorer_set_residency", "fbb_explorer_set_incumbent",
     "fbb_explorer_best", "fbb_explorer_take", "fbb_explorer_push", "fbb_tuner_create", "fbb_tuner_destroy", "fbb_tuner_target",
     "fbb_tuner_observe", "fbb_tuner_phase", "fbb_tuner_best_batch",
-    "fbb_tuner_best_throughput", "fbb_version", "fbb_kernels",
+    "fbb_tuner_best_throughput", "fbb_tuner_set_trace", "fbb_version", "fbb_kernels",
 )
 
 
@@ -80,6 +80,8 @@ _i64p = np.ctypeslib.ndpointer(dtype=np.int64, flags="C_CONTIGUOUS")
 _u64p = np.ctypeslib.ndpointer(dtype=np.uint64, flags="C_CONTIGUOUS")
 _u8p = np.ctypeslib.ndpointer(dtype=np.uint8, flags="C_CONTIGUOUS")
 _vp = C.c_void_p
+# fbb_tuner_trace_fn(user, window, batch, throughput, decision)
+TRACE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_int, C.c_int64, C.c_double, C.c_char_p)
 
 _lib = None
 
@@ -134,6 +136,7 @@ def load_library(path: str = LIB_PATH):
     L.fbb_tuner_best_throughput.restype = C.c_double
     L.fbb_version.restype = C.c_char_p
     L.fbb_kernels.argtypes = [_vp, C.c_char_p, C.c_size_t]
+    L.fbb_tuner_set_trace.argtypes = [_vp, TRACE_FN, _vp]
     _lib = L
     return L
 

@@ -15,6 +15,7 @@
 #include <cstdint>
 #include <deque>
 #include <set>
+#include <string>
 #include <vector>
 
 #include "flowbb_b200.h"
@@ -31,6 +32,9 @@ struct fbb_tuner {
     double best_throughput = -1.0;
     std::deque<int64_t> probes;
     std::set<int64_t> visited;
+    fbb_tuner_trace_fn trace = nullptr;  // Tuner::set_trace (autotune.hpp)
+    void* trace_user = nullptr;
+    int window_index = 0;
 
     int64_t target() const {
         switch (phase) {
@@ -57,19 +61,28 @@ struct fbb_tuner {
                 probes.push_back(c);
     }
 
-    void advance() {  // autotune.hpp:89-121
+    void advance(int64_t measured, double tp) {  // autotune.hpp:89-121
+        const char* what = "";
         if (phase == 0) {
             if (grain * units * 2 <= max_batch) {
                 units *= 2;
+                what = "double to ";
             } else {
                 build_probes();
                 phase = probes.empty() ? 2 : 1;
+                what = phase == 2 ? "fix at " : "refine at ";
             }
         } else if (phase == 1) {
             probes.pop_front();
             while (!probes.empty() && visited.count(probes.front())) probes.pop_front();
             if (probes.empty()) phase = 2;
+            what = phase == 2 ? "fix at " : "refine at ";
         }
+        if (trace) {  // the decision strings of the reference's trace
+            const std::string decision = std::string(what) + std::to_string(target());
+            trace(trace_user, window_index, measured, tp, decision.c_str());
+        }
+        ++window_index;
     }
 
     void observe(int64_t nodes, double seconds) {  // autotune.hpp:69-86
@@ -86,7 +99,7 @@ struct fbb_tuner {
         }
         window_nodes = 0;
         window_time = 0.0;
-        advance();
+        advance(measured, tp);
     }
 };
 
@@ -121,5 +134,12 @@ int fbb_tuner_observe(fbb_tuner* t, int64_t nodes_bounded, double elapsed_second
 int fbb_tuner_phase(const fbb_tuner* t) { return t ? t->phase : -1; }
 int64_t fbb_tuner_best_batch(const fbb_tuner* t) { return t ? t->best_batch : 0; }
 double fbb_tuner_best_throughput(const fbb_tuner* t) { return t ? t->best_throughput : -1.0; }
+
+int fbb_tuner_set_trace(fbb_tuner* t, fbb_tuner_trace_fn fn, void* user) {
+    if (!t) return FBB_E_ARG;
+    t->trace = fn;
+    t->trace_user = user;
+    return FBB_OK;
+}
 
 }  // extern "C"

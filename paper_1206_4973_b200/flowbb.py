@@ -515,6 +515,14 @@ class Tuner:
     def best_throughput(self) -> float:
         return float(self.L.fbb_tuner_best_throughput(self.h))
 
+    def set_trace(self, fn) -> None:
+        """Tuner::set_trace (autotune.hpp): fn(window, batch, throughput, decision) per
+        closed window; None disables it."""
+        from ._lib import TRACE_FN
+
+        self._trace = TRACE_FN(lambda _u, w, b, tp, d: fn(w, b, tp, d.decode())) if fn else None
+        self.L.fbb_tuner_set_trace(self.h, self._trace or TRACE_FN(), None)
+
 
 # ---------------------------------------------------------------------------------------------
 # L4/L6: explorer drivers (search.hpp solve, bench.hpp resolve_workload)

@@ -213,7 +213,7 @@ def test_explorer_pushed_depth_n_minus_1_nodes(oracle):
     inst = inst_of(p)
     roots = [list(rng.permutation(n)[: d]) for d in (3, 7, 8, 8, 5, 7, 8)]
     ub = 10 ** 6
-    full, gold = oracle.resolve(p, ub, roots, targets=[7], max_trace=64)
+    full, gold = oracle.resolve(p, ub, roots, targets=[7], max_trace=4096)
     res = fbb.resolve_workload(inst, roots, ub, targets=[7])
     assert [tuple(r) for r in res.rounds] == [tuple(r) for r in gold]
     assert res.best == full["optimum"]

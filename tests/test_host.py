@@ -175,3 +175,27 @@ def test_tuner_b200_descriptor_grid():
         seen.append(t.target())
         t.observe(t.target(), 1.0)
     assert seen == [37888, 75776, 151552, 303104]
+
+
+@pytest.mark.parametrize("desc,window,probes,peak", [((256, 4, 65536), 5, 2, 9000.0),
+                                                     ((64, 3, 5000), 2, 3, 700.0),
+                                                     ((1, 1, 16384), 1, 2, 3000.0),
+                                                     ((160, 296, 1 << 24), 2, 2, 2.0e5)])
+def test_tuner_trace_matches_reference(desc, window, probes, peak):
+    # Tuner::set_trace (autotune.hpp): same window index, measured batch and decision text
+    # as the reference Tuner driven by the same synthetic curve
+    from oracle import Ref
+    try:
+        ref = Ref()
+    except FileNotFoundError:
+        pytest.skip("oracle/_ref not built on this host")
+    want = ref.tuner_trace(*desc, window, probes, peak)
+    got = []
+    t = fbb.Tuner(fbb.BackendDescriptor(*desc), window, probes)
+    t.set_trace(lambda w, b, tp, d: got.append(f"{w} {b} {d}"))
+    for _ in range(10000):
+        if t.phase() == fbb.TunerPhase.fixed:
+            break
+        x = float(t.target())
+        t.observe(t.target(), x / (x / (1.0 + (x / peak) ** 2)))
+    assert got == want and len(got) >= 3
