@@ -163,8 +163,11 @@ __global__ void __launch_bounds__(256) k1_bound_kernel(DevTables t, int tile,
 K1Config k1_config(const DevTables& t, int device) {
     K1Config c;
     {
-        const char* sel = getenv("FBB_K1");  // FBB_K1=v1 forces this kernel (A/B runs)
-        if (!(sel && std::string(sel) == "v1") && k1v2_config(t, device, &c)) return c;
+        // FBB_K1=v1 | v2 forces that kernel (A/B runs); default: v3, else v2, else v1
+        const char* sel = getenv("FBB_K1");
+        const std::string s = sel ? sel : "";
+        if (s != "v1" && s != "v2" && k1v3_config(t, device, &c)) return c;
+        if (s != "v1" && k1v2_config(t, device, &c)) return c;
         c = K1Config{};
     }
     c.threads = 256;
@@ -195,6 +198,7 @@ cudaError_t launch_k1(const DevTables& t, const K1Config& cfg, const uint64_t* m
                       const int32_t* heads, const int32_t* depth, int64_t count, int32_t* lb,
                       cudaStream_t stream) {
     if (count <= 0) return cudaSuccess;
+    if (cfg.variant >= 100) return launch_k1v3(t, cfg, masks, heads, depth, count, lb, stream);
     if (cfg.variant != 0) return launch_k1v2(t, cfg, masks, heads, depth, count, lb, stream);
     int64_t ntiles = (count + cfg.tile - 1) / cfg.tile;
     int blocks = (int)(ntiles < cfg.blocks ? ntiles : cfg.blocks);

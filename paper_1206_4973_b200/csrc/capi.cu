@@ -849,6 +849,7 @@ int fbb_kernels(fbb_ctx* ctx, char* buf, size_t cap) {
     const K1Config& a = ctx->k1;
     if (a.variant == 0)
         std::snprintf(k1, sizeof k1, "k1_bound_kernel<%d,%d,%d>", ctx->dt.n <= 32 && !a.wide, a.jm_in_smem, a.wide);
+    else if (a.variant >= 100) std::snprintf(k1, sizeof k1, "k1v3_kernel<%d>", a.variant - 100);
     else std::snprintf(k1, sizeof k1, "k1v2_kernel<%d,4>", a.variant);
     const K2Config& b = ctx->k2;
     if (b.variant >= 100000)

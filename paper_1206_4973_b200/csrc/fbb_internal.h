@@ -56,6 +56,12 @@ struct DevTables {
     // total processing time fits int32 arithmetic; read by the kWide kernels.  Null unless
     // some kernel needs it (values outside the packed or the int16 ranges).
     int4* jw;
+    // K1 v3 rows (n*P, [i][q]): bits 0..7 j, 8..15 d as int8, 16..31 c + k1_c0, and the
+    // two biases of its 16x2 chains (bound_v3.cu): k1_bias lifts the low half of D above
+    // zero, k1_c0 lifts every member's candidate above every non-member's.  Null unless
+    // kSafeK1x2.
+    uint32_t* rowk1;
+    int32_t k1_bias, k1_c0;
     // Which 16-bit intermediates are exact for this instance (build_host_tables' range
     // analysis): kSafeM16 = every M' fits int16, kSafeLcM16 = every Lc_l + M'_kl fits int16,
     // kSafeDual16 = the 16x2 two-parent scan (D, D + c, the -16384 neutral) fits.
@@ -63,6 +69,7 @@ struct DevTables {
 };
 constexpr int32_t kSafeM16 = 1, kSafeLcM16 = 2, kSafeDual16 = 4;
 constexpr int32_t kTablesPacked = 8;  // safe16 bit: jm holds the packed rows
+constexpr int32_t kSafeK1x2 = 16;     // K1's biased 16x2 chains fit (bound_v3.cu)
 
 // Host copy of the same tables (for tests of the table builder).
 struct HostTables {
@@ -75,6 +82,7 @@ struct HostTables {
     //   so M' = max(D_<i + c_i) <= m_hi = max_q (sum_j max(d,0) + max_j c) and >= m_lo,
     //   and Lc_l = load_l - p[x][l] + min tail_l <= lc_max = max_l (sum_j p[j][l] + max_j tail).
     int64_t m_hi = 0, m_lo = 0, lc_max = 0;
+    int64_t spos_max = 0;   // max_q sum_j max(d, 0)
     int32_t safe16 = 0;     // kSafe* bits derived from the above
     std::vector<int32_t> p, tails;
     std::vector<uint32_t> jm;   // packed rows (zeros when !packed)
@@ -99,7 +107,8 @@ struct K1Config {
     int threads = 256;
     int tile = 32;       // nodes per tile
     bool jm_in_smem = true;
-    int variant = 0;     // 0: k1_bound_kernel; 1/2/8: k1v2_kernel<NW> (bound_v2.cu)
+    int variant = 0;     // 0: k1_bound_kernel; 1/2/8: k1v2_kernel<NW> (bound_v2.cu);
+                         // 100 + NW: k1v3_kernel<NW> (bound_v3.cu)
     int blocks = 0;      // persistent grid
     size_t smem = 0;
 };
@@ -112,6 +121,13 @@ cudaError_t launch_k1(const DevTables& t, const K1Config& cfg, const uint64_t* m
 // the instance does not qualify (|d| > 127, m > 20, n > 256).
 bool k1v2_config(const DevTables& t, int device, K1Config* out);
 cudaError_t launch_k1v2(const DevTables& t, const K1Config& cfg, const uint64_t* masks,
+                        const int32_t* heads, const int32_t* depth, int64_t count, int32_t* lb,
+                        cudaStream_t stream);
+
+// K1 v3 (bound_v3.cu): 16x2 SIMD chains, 16 nodes per row sweep; false when the instance
+// does not qualify (no rowv3, m > 20, n > 256, or not kSafeK1x2).  variant = 100 + NW.
+bool k1v3_config(const DevTables& t, int device, K1Config* out);
+cudaError_t launch_k1v3(const DevTables& t, const K1Config& cfg, const uint64_t* masks,
                         const int32_t* heads, const int32_t* depth, int64_t count, int32_t* lb,
                         cudaStream_t stream);
 

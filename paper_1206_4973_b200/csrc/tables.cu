@@ -61,6 +61,7 @@ int build_host_tables(const int32_t* p, int n, int m, HostTables* out, std::stri
     h.max_abs_d = 0;
     h.m_hi = 0;
     h.m_lo = 0;
+    h.spos_max = 0;
     for (int q = 0; q < P; ++q) {
         int k = h.pair_k[q], l = h.pair_l[q];
         for (int j = 0; j < n; ++j) {
@@ -93,10 +94,12 @@ int build_host_tables(const int32_t* p, int n, int m, HostTables* out, std::stri
             cmax = std::max(cmax, c);
         }
         h.m_hi = std::max(h.m_hi, spos + cmax);
+        h.spos_max = std::max(h.spos_max, spos);
         h.m_lo = std::min(h.m_lo, sneg);
     }
     if (!h.packed) std::fill(h.jm.begin(), h.jm.end(), 0u);
     h.lc_max = 0;
+    int64_t load_max = 0, tail_max = 0;
     for (int l = 0; l < m; ++l) {
         int64_t load = 0, tmax = 0;
         for (int j = 0; j < n; ++j) {
@@ -104,9 +107,16 @@ int build_host_tables(const int32_t* p, int n, int m, HostTables* out, std::stri
             tmax = std::max<int64_t>(tmax, h.tails[(size_t)j * m + l]);
         }
         h.lc_max = std::max(h.lc_max, load + tmax);
+        load_max = std::max(load_max, load);
+        tail_max = std::max(tail_max, tmax);
     }
     // 16-bit intermediates (see DevTables::safe16); every bound is exact in int32
     h.safe16 = h.packed ? kTablesPacked : 0;
+    // K1 v3: low halves of D lifted by 1 - m_lo, candidates by 1 + spos_max (bound_v3.cu)
+    // and the one-machine loads / tails as unsigned 16-bit halves
+    if (h.packed && h.max_abs_d <= 127 && (1 - h.m_lo) + (1 + h.spos_max) + h.m_hi <= 32767 &&
+        load_max <= 65535 && tail_max < 65535)
+        h.safe16 |= kSafeK1x2;
     if (h.packed && h.m_hi <= 32767 && h.m_lo >= -32767) {
         h.safe16 |= kSafeM16;
         if (h.lc_max + h.m_hi <= 32767) {
@@ -176,6 +186,19 @@ int upload_tables(const HostTables& h, DevTables* d, std::string* why) {
             *why = std::string("table upload: ") + cudaGetErrorString(e);
             return FBB_E_CUDA;
         }
+        if (h.safe16 & kSafeK1x2) {
+            d->k1_bias = (int32_t)(1 - h.m_lo);
+            d->k1_c0 = (int32_t)(1 + h.spos_max);
+            for (size_t x = 0; x < h.jm.size(); ++x) {
+                const uint32_t en = h.jm[x];
+                rp[x] = (uint32_t)entry_job(en) | ((uint32_t)(entry_d(en) & 0xFF) << 8) |
+                        ((uint32_t)(entry_c(en) + d->k1_c0) << 16);
+            }
+            if ((e = upload(&d->rowk1, rp)) != cudaSuccess) {
+                *why = std::string("table upload: ") + cudaGetErrorString(e);
+                return FBB_E_CUDA;
+            }
+        }
     }
     return FBB_OK;
 }
@@ -188,6 +211,7 @@ void free_tables(DevTables* d) {
     cudaFree(d->pair_l);
     cudaFree(d->rowpk);
     cudaFree(d->rowv3);
+    cudaFree(d->rowk1);
     cudaFree(d->jw);
     *d = DevTables{};
 }

@@ -371,22 +371,28 @@ def test_synth_pool_and_k1_device_vs_oracle(oracle, nm):
     assert np.array_equal(dl.cpu().numpy(), lb)
 
 
-@pytest.mark.parametrize("nm", [(20, 20), (50, 10), (200, 20), (20, 7), (100, 5), (65, 2), (130, 3)])
-def test_k1_v1_and_v2_agree(oracle, nm, monkeypatch):
-    """Both K1 kernels (the smem-table v1 and the packed-row v2) give the oracle's bounds."""
+@pytest.mark.parametrize("nm", [(20, 20), (50, 10), (200, 20), (20, 7), (100, 5), (65, 2), (130, 3),
+                                (256, 20), (33, 20), (128, 4), (9, 2)])
+def test_k1_v1_v2_v3_agree(oracle, nm, monkeypatch):
+    """The three K1 kernels (smem-table v1, packed-row v2, 16x2 SIMD v3) give the oracle's
+    bounds; pools mix every depth (leaves included) and a ragged last tile."""
     n, m = nm
     rng = np.random.default_rng(n * 100 + m)
     inst = inst_of(rng.integers(1, 100, size=(n, m)).astype(np.int32))
-    prefixes = [list(rng.permutation(n)[: rng.integers(0, n + 1)]) for _ in range(300)]
+    prefixes = [list(rng.permutation(n)[: rng.integers(0, n + 1)]) for _ in range(301)]
     nodes = fbb.nodes_from_prefixes(inst, prefixes)
     ref = oracle.evaluate_batch(inst.p, nodes.masks, nodes.heads, nodes.depth)
     got = {}
-    for sel in ("v1", "v2"):
+    for sel in ("v1", "v2", "v3"):
         monkeypatch.setenv("FBB_K1", sel)
         ctx = fbb.Context(inst)
+        kern = ctx.kernels()
         got[sel] = ctx.bound(nodes)
         ctx.close()
-    assert np.array_equal(got["v1"], ref) and np.array_equal(got["v2"], ref)
+        if sel == "v3" and m <= 20:
+            assert "k1v3_kernel" in kern, kern
+    for sel in got:
+        assert np.array_equal(got[sel], ref), sel
 
 
 def test_k2_generic_and_specialised_agree(monkeypatch):
