@@ -61,6 +61,8 @@ def parse():
     ap.add_argument("--tuner", action="store_true",
                     help="adaptive pool size (autotune.hpp) instead of a fixed --target")
     ap.add_argument("--tuner-window", type=int, default=4)
+    ap.add_argument("--exchange-every", type=int, default=4,
+                    help="N > 1: explorer rounds per rank exchange (one library call each)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-seconds", type=float, default=60.0,
                     help="time cap of the reference arm's timed rounds")
@@ -178,7 +180,9 @@ def explore_config(args, inst_name, world, tuner_desc=None):
             "pool_target": tuner_desc if (args.tuner and tuner_desc) else
                            ("adaptive" if args.tuner else args.target),
             "ub": ub, "parallelism": f"dp{world}",
-            "l2": "flushed between timed rounds (256 MiB write)"}
+            "l2": "flushed between timed rounds (256 MiB write)" if world == 1 else
+                  f"flushed between timed exchange steps of {args.exchange_every} rounds "
+                  f"(256 MiB write)"}
 
 
 def reference_arm(args, inst_name):
@@ -479,10 +483,10 @@ def exhaust(args, inst_name):
     else:
         from paper_1206_4973_b200.parallel import DevicePort, ParallelExplorer
 
-        px = ParallelExplorer(DevicePort(ctx, frozen=True), n, device=coll_dev, balance_every=4)
+        px = ParallelExplorer(DevicePort(ctx, frozen=True), n, device=coll_dev, balance_every=2,
+                              exchange_every=args.exchange_every)
         while px.step(args.target):
-            if px.port.last_timing:
-                dev_ms += px.port.last_timing["round_ms"]
+            dev_ms += sum(x["round_ms"] for x in px.port.last_timings)
             if time.perf_counter() - t0 > args.max_seconds:
                 break
         rounds, transfers = len(px.res.rounds), px.res.transfers
@@ -590,7 +594,7 @@ def main():
         if world == 1:
             return None
         return ParallelExplorer(DevicePort(ctx, frozen=True), n, device=coll_dev,
-                                balance_every=4)
+                                balance_every=2, exchange_every=args.exchange_every)
 
     px = make_px()
 
@@ -611,18 +615,19 @@ def main():
         return r, t
 
     def px_round(px, tgt):
+        """One exchange step: px.exchange_every rounds in one library call, then the rank
+        exchange (charged to the step's last round)."""
         before = len(px.res.rounds)
         x0 = px.res.exchange_seconds
         px.step(tgt)
         r = px.res.rounds[before:]
-        t = [px.port.last_timing] if r else []
+        t = [dict(x) for x in px.port.last_timings] if r else []
+        xm = 1e3 * (px.res.exchange_seconds - x0)
         if t:
-            t[0] = dict(t[0])
-            t[0]["exchange_ms"] = 1e3 * (px.res.exchange_seconds - x0)
+            t[-1]["exchange_ms"] = xm
         else:
             t = [{"round_ms": 0.0, "k2_ms": 0.0, "launches": 0, "host_ms": 0.0, "sync_ms": 0.0,
-                  "h2d_bytes": 0, "d2h_bytes": 0,
-                  "exchange_ms": 1e3 * (px.res.exchange_seconds - x0)}]
+                  "h2d_bytes": 0, "d2h_bytes": 0, "exchange_ms": xm}]
         return r, t
 
     # ---- device-resident explorer: W warm-up rounds, K timed rounds -------------------------
@@ -635,6 +640,8 @@ def main():
     sampler = ClockSampler(dev) if rank == 0 and not os.environ.get("FBB_NO_CLOCKS") else None
     rounds, timing, wall, flush_s = [], [], 0.0, 0.0
     for _ in range(args.steps):
+        if len(rounds) >= args.steps:  # N > 1: a step of px runs exchange_every rounds
+            break
         f0 = time.perf_counter()
         flush.fill_(rank + len(rounds) % 7)  # L2 flush (> 126 MB) between timed rounds
         torch.cuda.synchronize()
@@ -693,6 +700,8 @@ def main():
             e_secs = time.perf_counter() - w0
         else:
             for _ in range(args.steps):
+                if len(e_rounds) >= args.steps:
+                    break
                 w0 = time.perf_counter()
                 r, t = one_round(True, pxe)
                 e_secs += time.perf_counter() - w0

@@ -199,6 +199,61 @@ int fbb_explorer_take(fbb_ctx* ctx, int64_t k, uint8_t* prefix, int32_t* depth, 
  * resetting it (the receiving side of fbb_explorer_take). */
 int fbb_explorer_push(fbb_ctx* ctx, const uint8_t* prefix, const int32_t* depth, int64_t count);
 
+/* ---- device group: one process, G devices, the exchange inside the library ------------
+ * The single-process form of the multi-GPU explorer (SURVEY 8(b) "fbb_group_create(devs[],
+ * G)"; the paper's Type-1 split of one host over the GPUs of a box, with
+ * the reference's BackendSet(k) over k devices, backend.hpp:142-158).  Each member is an
+ * ordinary context (device ids may repeat) driven by its own host thread; every step runs
+ * `rounds_per_step` explorer rounds on all members concurrently, then the library
+ * exchanges, on the calling thread:
+ *   - solve mode: the minimum incumbent over members becomes every member's pruning
+ *     bound (the UB min-allreduce; fbb_explorer_set_incumbent),
+ *   - every `balance_every` steps: a starving member (pending < target / n) receives
+ *     half the difference (<= 65536 nodes) from the richest member, shallowest pending
+ *     nodes first (fbb_explorer_take -> fbb_explorer_push), the same deterministic plan
+ *     as the multi-process driver (paper_1206_4973_b200/parallel.py plan_transfers).
+ * Frozen exploration is partition-invariant (bench.hpp:60-62): the summed counts to
+ * exhaustion equal one context's. */
+typedef struct fbb_group fbb_group;
+
+typedef struct {
+    int64_t steps;         /* exchange steps run by this call */
+    int64_t rounds;        /* explorer rounds summed over members */
+    int64_t branched, bounded, pruned, leaves;  /* totals over members since the reset */
+    int64_t pending;       /* pending nodes over members after the call */
+    int64_t transfers;     /* nodes moved between members by this call */
+    int32_t incumbent;     /* group incumbent (frozen: best leaf < UB, else UB) */
+    int32_t found;         /* a leaf below the initial UB was found */
+    double seconds;        /* wall time of the call */
+    double device_ms_max;  /* max over members of their summed round device time */
+    double exchange_ms;    /* wall time spent in the exchanges (calling thread) */
+} fbb_group_stats_t;
+
+/* Creates one context per entry of devices[0..G) over the same instance (p job-major,
+ * n x m).  NULL on failure (fbb_last_error(NULL, ...) says why). */
+fbb_group* fbb_group_create(const int* devices, int G, const int32_t* p_jobmajor, int n, int m);
+void fbb_group_destroy(fbb_group* g);
+int fbb_group_size(const fbb_group* g);
+/* Member i's context (owned by the group): its fbb_explorer_* counters stay per member. */
+fbb_ctx* fbb_group_context(fbb_group* g, int i);
+/* Last error of the group: the failing member's status, index and message. */
+int fbb_group_last_error(const fbb_group* g, int* member, char* msg, size_t cap);
+/* Resets every member: the nodes are split into G contiguous slices (split_slices,
+ * backend.hpp:73-84), slice i pushed in order onto member i; incumbent `ub`. */
+int fbb_group_reset(fbb_group* g, const uint8_t* prefix, const int32_t* depth, int64_t count,
+                    int32_t ub, int frozen);
+/* solve()'s root round (search.hpp:131-153) on member 0 (ub < 0: identity makespan);
+ * the other members start empty with the same incumbent and are fed by rebalancing. */
+int fbb_group_start_solve(fbb_group* g, int32_t ub);
+/* Runs exchange steps with pool target `target` per member until every member's
+ * pending tree is empty, max_steps steps ran, or the summed bounded count reached
+ * `budget` (> 0).  stats may be NULL. */
+int fbb_group_run(fbb_group* g, int64_t target, int64_t max_steps, int rounds_per_step,
+                  int balance_every, int64_t budget, fbb_group_stats_t* stats);
+/* Group best leaf: min over members of (value, member index); returns 1 and its value
+ * (and, in solve mode, its schedule) when found, else 0 with *value = INT32_MAX. */
+int fbb_group_best(fbb_group* g, int32_t* value, int32_t* schedule);
+
 /* ---- adaptive pool-size tuner (autotune.hpp:35-156), re-derived descriptor ----------- */
 typedef struct fbb_tuner fbb_tuner;
 fbb_tuner* fbb_tuner_create(int32_t grain, int32_t base_units, int64_t max_batch, int window,

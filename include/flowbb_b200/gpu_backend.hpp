@@ -341,6 +341,69 @@ inline flowbb::Report run_experiment(const GpuBackend& gpu, const flowbb::Worklo
     return report;
 }
 
+// The multi-GPU explorer of one process over fbb_group_* (include/flowbb_b200.h): the
+// reference's solve / resolve_workload (search.hpp:124-174, bench.hpp:63-114) with each
+// GPU exploring its own share of the pending tree, the incumbent min-exchanged between
+// steps and starving GPUs fed subtrees.  Frozen exploration gives the
+// reference's node counts for any GPU count (bench.hpp:60-62).
+class GpuGroupExplorer {
+public:
+    GpuGroupExplorer(const flowbb::Instance& inst, const std::vector<int>& devices) : n_(inst.jobs()) {
+        std::vector<int32_t> p((std::size_t)inst.jobs() * inst.machines());
+        for (int j = 0; j < inst.jobs(); ++j)
+            for (int k = 0; k < inst.machines(); ++k) p[(std::size_t)j * inst.machines() + k] = inst.p(j, k);
+        g_ = fbb_group_create(devices.data(), (int)devices.size(), p.data(), inst.jobs(), inst.machines());
+        if (!g_) {
+            int dev = -1;
+            std::string m = detail::last_error(nullptr, &dev);
+            throw flowbb::BackendError{dev < 0 ? 0 : dev, m};
+        }
+    }
+    ~GpuGroupExplorer() { fbb_group_destroy(g_); }
+    GpuGroupExplorer(const GpuGroupExplorer&) = delete;
+    GpuGroupExplorer& operator=(const GpuGroupExplorer&) = delete;
+
+    // resolve_workload's start (bench.hpp:80-85): the snapshot nodes, frozen incumbent
+    void reset(const std::vector<flowbb::Node>& nodes, int ub, bool frozen = true) {
+        std::vector<uint8_t> pre(std::max<std::size_t>(nodes.size(), 1) * n_);
+        std::vector<int32_t> dep(std::max<std::size_t>(nodes.size(), 1));
+        for (std::size_t i = 0; i < nodes.size(); ++i) {
+            dep[i] = nodes[i].depth();
+            for (int d = 0; d < nodes[i].depth(); ++d) pre[i * n_ + d] = static_cast<uint8_t>(nodes[i].prefix[d]);
+        }
+        check(fbb_group_reset(g_, pre.data(), dep.data(), (int64_t)nodes.size(), ub, frozen ? 1 : 0));
+    }
+    // solve's start (search.hpp:131-153); ub < 0: the identity makespan
+    void start_solve(int ub = -1) { check(fbb_group_start_solve(g_, ub)); }
+    fbb_group_stats_t run(std::int64_t target, std::int64_t max_steps = INT64_MAX, int rounds_per_step = 4,
+                          int balance_every = 1, std::int64_t budget = 0) {
+        fbb_group_stats_t st;
+        check(fbb_group_run(g_, target, max_steps, rounds_per_step, balance_every, budget, &st));
+        return st;
+    }
+    // the group's best leaf (value, schedule when solving), if any
+    std::optional<std::pair<int, flowbb::Permutation>> best() {
+        int32_t v = 0;
+        std::vector<int32_t> s(n_, -1);
+        int f = fbb_group_best(g_, &v, s.data());
+        if (f < 0) check(f);
+        if (!f) return std::nullopt;
+        return std::make_pair((int)v, flowbb::Permutation(s.begin(), s.end()));
+    }
+    int size() const { return fbb_group_size(g_); }
+
+private:
+    void check(int rc) {
+        if (rc == FBB_OK) return;
+        int member = -1;
+        char buf[512] = {0};
+        fbb_group_last_error(g_, &member, buf, sizeof buf);
+        throw flowbb::BackendError{member < 0 ? 0 : member, buf};
+    }
+    fbb_group* g_ = nullptr;
+    int n_;
+};
+
 }  // namespace flowbb_b200
 
 

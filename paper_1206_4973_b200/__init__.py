@@ -25,6 +25,7 @@ from .flowbb import (  # noqa: F401
     BackendDescriptor,
     BackendSet,
     Context,
+    DeviceGroup,
     GpuBackend,
     Instance,
     NodeBatch,

@@ -26,6 +26,9 @@ EXPORTED = (
     "fbb_explorer_best", "fbb_explorer_take", "fbb_explorer_push", "fbb_tuner_create", "fbb_tuner_destroy", "fbb_tuner_target",
     "fbb_tuner_observe", "fbb_tuner_phase", "fbb_tuner_best_batch",
     "fbb_tuner_best_throughput", "fbb_tuner_set_trace", "fbb_version", "fbb_kernels",
+    "fbb_group_create", "fbb_group_destroy", "fbb_group_size", "fbb_group_context",
+    "fbb_group_last_error", "fbb_group_reset", "fbb_group_start_solve", "fbb_group_run",
+    "fbb_group_best",
 )
 
 
@@ -73,6 +76,19 @@ class RoundRec(C.Structure):
     def as_tuple(self):
         return (self.target, self.branched, self.bounded, self.inserted, self.pruned,
                 self.leaves, self.incumbent, self.pending)
+
+
+class GroupStats(C.Structure):
+    """fbb_group_stats_t"""
+
+    _fields_ = [("steps", C.c_int64), ("rounds", C.c_int64), ("branched", C.c_int64),
+                ("bounded", C.c_int64), ("pruned", C.c_int64), ("leaves", C.c_int64),
+                ("pending", C.c_int64), ("transfers", C.c_int64), ("incumbent", C.c_int32),
+                ("found", C.c_int32), ("seconds", C.c_double), ("device_ms_max", C.c_double),
+                ("exchange_ms", C.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
 
 
 _i32p = np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS")
@@ -137,6 +153,19 @@ def load_library(path: str = LIB_PATH):
     L.fbb_version.restype = C.c_char_p
     L.fbb_kernels.argtypes = [_vp, C.c_char_p, C.c_size_t]
     L.fbb_tuner_set_trace.argtypes = [_vp, TRACE_FN, _vp]
+    L.fbb_group_create.argtypes = [_i32p, C.c_int, _i32p, C.c_int, C.c_int]
+    L.fbb_group_create.restype = _vp
+    L.fbb_group_destroy.argtypes = [_vp]
+    L.fbb_group_destroy.restype = None
+    L.fbb_group_size.argtypes = [_vp]
+    L.fbb_group_context.argtypes = [_vp, C.c_int]
+    L.fbb_group_context.restype = _vp
+    L.fbb_group_last_error.argtypes = [_vp, C.POINTER(C.c_int), C.c_char_p, C.c_size_t]
+    L.fbb_group_reset.argtypes = [_vp, _u8p, _i32p, C.c_int64, C.c_int32, C.c_int]
+    L.fbb_group_start_solve.argtypes = [_vp, C.c_int32]
+    L.fbb_group_run.argtypes = [_vp, C.c_int64, C.c_int64, C.c_int, C.c_int, C.c_int64,
+                                C.POINTER(GroupStats)]
+    L.fbb_group_best.argtypes = [_vp, C.POINTER(C.c_int32), _i32p]
     _lib = L
     return L
 

@@ -16,8 +16,8 @@ from typing import Optional, Sequence
 
 import numpy as np
 
-from ._lib import (FBB_OK, BackendError, Descriptor, RoundRec, _i64p, check, last_error,
-                   load_library)
+from ._lib import (FBB_OK, BackendError, Descriptor, GroupStats, RoundRec, _i64p, check,
+                   last_error, load_library)
 
 # ---------------------------------------------------------------------------------------------
 # L0: instance model (instance.hpp)
@@ -475,6 +475,82 @@ class BackendSet:
 # ---------------------------------------------------------------------------------------------
 # L5: tuner (autotune.hpp)
 # ---------------------------------------------------------------------------------------------
+
+
+class DeviceGroup:
+    """fbb_group_*: the multi-device explorer inside one process (the paper's split of one
+    host's pools over its GPUs; BackendSet(k) over k devices,
+    backend.hpp:142-158).  Member i is a full context (`context(i)`); the library runs
+    every member's rounds on its own host thread and exchanges the incumbent (solve) and
+    pending subtrees between steps.  Device ids may repeat (tests on one GPU)."""
+
+    def __init__(self, inst: Instance, devices: Sequence[int]):
+        L = self.L = load_library()
+        self.inst = inst
+        self.n, self.m = inst.p.shape
+        devs = np.ascontiguousarray(np.asarray(list(devices), np.int32))
+        h = L.fbb_group_create(devs, len(devs), np.ascontiguousarray(inst.p.ravel()), self.n, self.m)
+        if not h:
+            status, _, msg = last_error(None)
+            if status == -1:
+                raise ValueError(msg or "invalid group")
+            raise BackendError(int(devs[0]) if len(devs) else -1, msg, status)
+        self.h = h
+        self.devices = [int(d) for d in devs]
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.fbb_group_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc):
+        if rc != FBB_OK:
+            member = C.c_int(-1)
+            buf = C.create_string_buffer(512)
+            status = self.L.fbb_group_last_error(self.h, C.byref(member), buf, 512)
+            msg = buf.value.decode(errors="replace")
+            if status == -1:
+                raise ValueError(msg)
+            raise BackendError(member.value, msg, status)
+
+    def size(self) -> int:
+        return self.L.fbb_group_size(self.h)
+
+    def reset(self, nodes, ub: int, frozen: bool = True):
+        """Splits the nodes (NodeBatch or prefixes) into size() contiguous slices."""
+        if not isinstance(nodes, NodeBatch):
+            nodes = nodes_from_prefixes(self.inst, nodes) if len(nodes) else NodeBatch.empty(self.inst)
+        cnt = len(nodes)
+        pre = np.ascontiguousarray(nodes.prefix.ravel()) if cnt else np.zeros(1, np.uint8)
+        dep = np.ascontiguousarray(nodes.depth) if cnt else np.zeros(1, np.int32)
+        self._check(self.L.fbb_group_reset(self.h, pre, dep, cnt, int(ub), 1 if frozen else 0))
+
+    def start_solve(self, ub: Optional[int] = None):
+        self._check(self.L.fbb_group_start_solve(self.h, -1 if ub is None else int(ub)))
+
+    def run(self, target: int, max_steps: int = 1 << 40, rounds_per_step: int = 4,
+            balance_every: int = 1, budget: int = 0) -> dict:
+        st = GroupStats()
+        self._check(self.L.fbb_group_run(self.h, int(target), int(max_steps), int(rounds_per_step),
+                                         int(balance_every), int(budget), C.byref(st)))
+        return st.as_dict()
+
+    def best(self):
+        """(value, schedule) of the group's best leaf, or (None, None)."""
+        v = C.c_int32(0)
+        sched = np.zeros(max(self.n, 1), np.int32)
+        found = self.L.fbb_group_best(self.h, C.byref(v), sched)
+        if found < 0:
+            self._check(found)
+        if not found:
+            return None, None
+        return v.value, [int(x) for x in sched[: self.n]]
 
 
 class TunerPhase(enum.IntEnum):

@@ -15,8 +15,10 @@ subtree), and per round the ranks exchange only
     largest unexplored subtrees) of the richest rank, as (depth, prefix) rows.
 
 Both ride on ONE all_gather of a [incumbent, pending, bounded] triple per rank per
-round (NCCL over NVLink on GPUs, gloo in the CPU tests); rebalancing adds a
-send/recv pair per transfer every `balance_every` rounds.  The explorer behind a
+exchange step of `exchange_every` rounds (NCCL over NVLink on GPUs, gloo in the
+CPU tests); rebalancing adds a send/recv pair per transfer every `balance_every`
+steps.  Every tensor that crosses a collective is int32 or int64: torch's NCCL
+backend has no 16-bit integer type.  The explorer behind a
 rank is any object with the `ExplorerPort` methods -- the device explorer in
 production (`DevicePort`), a CPU model in the tests.
 """
@@ -32,7 +34,7 @@ INT32_MAX = 2**31 - 1
 
 
 class ExplorerPort(Protocol):
-    def round(self, target: int):  # -> round tuple (target, branched, bounded, ...) or None
+    def run(self, target: int, max_rounds: int):  # -> list of round tuples (may be empty)
         ...
 
     def pending(self) -> int:
@@ -55,33 +57,55 @@ class ExplorerPort(Protocol):
 
 
 class DevicePort:
-    """ExplorerPort over a device context (fbb_explorer_*)."""
+    """ExplorerPort over a device context (fbb_explorer_*).
+
+    `run` hands R rounds to ONE fbb_explorer_run call (host-planned rounds back to back
+    on the library's stream, no Python between them); the pending size and incumbent
+    come from the last round record and are tracked across take/push, so a rank makes
+    one explorer_state call at construction and none per round."""
 
     def __init__(self, ctx, frozen: bool):
         self.ctx, self.frozen = ctx, frozen
         self.last_timing = None
+        self.last_timings = []
+        st = ctx.explorer_state()
+        self._pend = st["pending"]
+        self._inc = st["incumbent"]
+
+    def run(self, target: int, max_rounds: int = 1):
+        if self._pend <= 0:
+            self.last_timings, self.last_timing = [], None
+            return []
+        r, t = self.ctx.explorer_run([target], max_rounds, timing=True)
+        self.last_timings = t
+        self.last_timing = t[-1] if t else None
+        if r:
+            self._inc, self._pend = int(r[-1][6]), int(r[-1][7])
+        return r
 
     def round(self, target: int):
-        r, t = self.ctx.explorer_run([target], 1, timing=True)
-        self.last_timing = t[0] if t else None
+        r = self.run(target, 1)
         return r[0] if r else None
 
     def pending(self) -> int:
-        return self.ctx.explorer_state()["pending"]
+        return self._pend
 
     def take(self, k: int):
-        return self.ctx.explorer_take(k)
+        out = self.ctx.explorer_take(k)
+        self._pend -= len(out)
+        return out
 
     def push(self, prefixes):
         self.ctx.explorer_push(prefixes)
+        self._pend += len(prefixes)
 
     def incumbent(self) -> int:
-        st = self.ctx.explorer_state()
-        return st["incumbent"] if not self.frozen else INT32_MAX
+        return self._inc if not self.frozen else INT32_MAX
 
     def set_incumbent(self, v: int) -> None:
-        if not self.frozen:
+        if not self.frozen and v < self._inc:
             self.ctx.explorer_set_incumbent(v)
+            self._inc = int(v)
 
     def best(self):
         return self.ctx.explorer_best()
@@ -125,10 +149,18 @@ class ParallelResult:
 
 
 class ParallelExplorer:
-    """Runs synchronous rounds on every rank with the per-round exchange above."""
+    """Runs synchronous exchange steps on every rank: `exchange_every` explorer rounds
+    (one fbb_explorer_run call on a device port), then the rank exchange above.
+
+    Exchanging every R rounds instead of every round keeps the collective (a ~20-50 us
+    all_gather plus its host sync) off R-1 of every R rounds of ~120 us; the price is
+    that an incumbent found on one rank prunes on the others up to R rounds later
+    (solve mode only -- still exact, since the incumbent only lowers), and that a rank
+    whose tree runs dry idles until the next exchange feeds it."""
 
     def __init__(self, port: ExplorerPort, n_jobs: int, group=None, device=None,
-                 balance_every: int = 4, low_water: Optional[int] = None, max_transfer: int = 1 << 16):
+                 balance_every: int = 4, low_water: Optional[int] = None, max_transfer: int = 1 << 16,
+                 exchange_every: int = 1):
         import torch
         import torch.distributed as dist
 
@@ -138,6 +170,7 @@ class ParallelExplorer:
         self.world = dist.get_world_size(group)
         self.device = device if device is not None else "cpu"
         self.balance_every = max(1, balance_every)
+        self.exchange_every = max(1, exchange_every)
         self.low_water = low_water
         self.max_transfer = max_transfer
         self.res = ParallelResult()
@@ -175,10 +208,24 @@ class ParallelExplorer:
             self.res.transfers += k
 
     # -- driver --------------------------------------------------------------------------------
+    def _run_local(self, target: int, rounds: int):
+        if self.port.pending() <= 0:
+            return []
+        run = getattr(self.port, "run", None)
+        if run is not None:
+            return list(run(target, rounds))
+        out = []  # a port with a one-round interface only
+        while len(out) < rounds and self.port.pending() > 0:
+            rec = self.port.round(target)
+            if rec is None:
+                break
+            out.append(rec)
+        return out
+
     def step(self, target: int) -> bool:
-        """One synchronous round on every rank; False once every rank's pending is empty."""
-        rec = self.port.round(target) if self.port.pending() > 0 else None
-        if rec is not None:
+        """`exchange_every` rounds on every rank, then one exchange; False once every
+        rank's pending is empty."""
+        for rec in self._run_local(target, self.exchange_every):
             self.res.rounds.append(tuple(rec))
             self._bounded_local += int(rec[2])
         t0 = time.perf_counter()

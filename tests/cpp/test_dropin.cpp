@@ -172,6 +172,40 @@ int main() {
         }
         std::printf("ok generate_workload byte-identical; run_experiment GPU == sequential CPU\n");
     }
+    // 7. GpuGroupExplorer (fbb_group_*): frozen exhaustion over 2 and 3 members (one GPU,
+    //    repeated device ids) == the reference resolve_workload; solve == reference optimum
+    {
+        std::mt19937 rng(91);
+        for (int trial = 0; trial < 4; ++trial) {
+            Instance inst = testutil::random_instance(rng, 9 + trial, 4 + trial % 3);
+            SolveConfig sc;
+            sc.fixed_batch = 64;
+            sc.descriptor = BackendDescriptor{1, 1, 1 << 20};
+            Solution ref = solve(inst, sc);
+            const int ub = ref.optimum + 12;
+            WorkloadSnapshot snap{inst, {Node::root(inst)}, ub, 0u, CaptureCutoff::by_nodes(0)};
+            BenchConfig bc;
+            bc.batch = 32;
+            ResolutionResult cpu = resolve_workload(snap, bc);
+            for (int G : {2, 3}) {
+                flowbb_b200::GpuGroupExplorer grp(inst, std::vector<int>(G, 0));
+                grp.reset(snap.nodes, ub, true);
+                fbb_group_stats_t st = grp.run(32, INT64_MAX, 2, 1);
+                CHECK(st.pending == 0, "group exhausted");
+                CHECK(st.bounded == cpu.nodes_bounded, "group frozen bounded == reference");
+                auto b = grp.best();
+                CHECK(b.has_value() == cpu.best.has_value() && (!b || b->first == *cpu.best),
+                      "group frozen best leaf == reference");
+                flowbb_b200::GpuGroupExplorer sg(inst, std::vector<int>(G, 0));
+                sg.start_solve(-1);
+                fbb_group_stats_t ss = sg.run(16, INT64_MAX, 2, 1);
+                auto sb = sg.best();
+                CHECK(ss.pending == 0 && sb && sb->first == ref.optimum, "group solve optimum");
+                CHECK(sb && makespan(inst, sb->second) == ref.optimum, "group solve schedule");
+            }
+        }
+        std::printf("ok GpuGroupExplorer: frozen counts == reference resolve, solve optimum (G in {2,3})\n");
+    }
     std::printf(failures ? "FAILED %d\n" : "ALL PASS\n", failures);
     return failures ? 1 : 0;
 }

@@ -69,29 +69,56 @@ def test_frontier_partition_is_count_invariant(world, oracle):
 
 # ---- the multi-GPU driver (paper_1206_4973_b200.parallel) over gloo ---------------------------
 
-def _parallel_worker(rank, world, port, p, ub, frozen, roots_by_rank, target, q):
+# torch's NCCL process group accepts only these element types (c10d NCCLUtils.hpp
+# getNcclDataType: kChar, kByte, kBool, kInt, kLong, kHalf, kFloat, kDouble, kBFloat16 and
+# the float8 types); gloo is laxer, so the CPU tests enforce NCCL's map themselves.
+NCCL_DTYPES = {torch.int8, torch.uint8, torch.bool, torch.int32, torch.int64, torch.float16,
+               torch.float32, torch.float64, torch.bfloat16}
+
+
+def strict_nccl_dtypes():
+    """Wraps the torch.distributed calls the multi-GPU driver uses so that a tensor NCCL
+    would reject raises here too (the round-1 int16 rebalancing rows passed gloo and would
+    have failed their first NCCL send)."""
+    def wrap(fn):
+        def checked(*a, **kw):
+            for x in a:
+                for t in (x if isinstance(x, (list, tuple)) else [x]):
+                    if isinstance(t, torch.Tensor) and t.dtype not in NCCL_DTYPES:
+                        raise TypeError(f"{fn.__name__}: dtype {t.dtype} is not supported by NCCL")
+            return fn(*a, **kw)
+        return checked
+    saved = {}
+    for name in ("send", "recv", "all_gather", "all_reduce", "broadcast"):
+        saved[name] = getattr(dist, name)
+        setattr(dist, name, wrap(saved[name]))
+    return saved
+
+
+def _parallel_worker(rank, world, port, p, ub, frozen, roots_by_rank, target, q, every=1):
     sys.path.insert(0, ROOT)
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
+    strict_nccl_dtypes()
     from model_port import OraclePort
     from oracle import Oracle
     from paper_1206_4973_b200.parallel import ParallelExplorer
 
     ex = ParallelExplorer(OraclePort(Oracle(), p, ub, frozen, roots_by_rank[rank]), p.shape[0],
-                          balance_every=1)
+                          balance_every=1, exchange_every=every)
     res = ex.run([target])
     q.put((rank, res.bounded, res.best, res.schedule, res.transfers, res.exhausted,
            sum(r[2] for r in res.rounds)))
     dist.destroy_process_group()
 
 
-def _run_parallel(world, p, ub, frozen, roots_by_rank, target=16):
+def _run_parallel(world, p, ub, frozen, roots_by_rank, target=16, every=1):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = 29600 + (os.getpid() % 1000)
+    port = 29600 + (os.getpid() % 1000) + 7 * every
     procs = [ctx.Process(target=_parallel_worker,
-                         args=(r, world, port, p, ub, frozen, roots_by_rank, target, q))
+                         args=(r, world, port, p, ub, frozen, roots_by_rank, target, q, every))
              for r in range(world)]
     for pr in procs:
         pr.start()
@@ -112,8 +139,25 @@ def test_plan_transfers_is_deterministic_and_conserving():
     assert plan_transfers([0, 400], 10, 64) == [(1, 0, 64)]     # capped
 
 
-@pytest.mark.parametrize("world", [2])
-def test_parallel_frozen_exploration_is_partition_invariant(world, oracle):
+def test_strict_dtype_wrapper_rejects_int16():
+    """The dtype guard itself: an int16 tensor (what round 1 sent) is refused."""
+    calls = []
+    orig = dist.send
+    dist.send = lambda *a, **k: calls.append(a)
+    saved = strict_nccl_dtypes()
+    try:
+        with pytest.raises(TypeError):
+            dist.send(torch.zeros(3, dtype=torch.int16), 1)
+        dist.send(torch.zeros(3, dtype=torch.int32), 1)
+        assert len(calls) == 1
+    finally:
+        for name, fn in saved.items():
+            setattr(dist, name, fn)
+        dist.send = orig
+
+
+@pytest.mark.parametrize("world,every", [(2, 1), (2, 3)])
+def test_parallel_frozen_exploration_is_partition_invariant(world, every, oracle):
     """Frozen UB, all work on rank 0 at the start: rebalancing feeds rank 1, and the total
     bounded count over ranks equals the single-explorer resolve (bench.hpp:60-62)."""
     rng = np.random.default_rng(11)
@@ -121,7 +165,7 @@ def test_parallel_frozen_exploration_is_partition_invariant(world, oracle):
     opt, _, _ = oracle.solve(p, -1, targets=[64])
     ub = opt["optimum"] + 8
     single, _ = oracle.resolve(p, ub, [[]], targets=[16])
-    out = _run_parallel(world, p, ub, True, [[[]], []])
+    out = _run_parallel(world, p, ub, True, [[[]], []], every=every)
     assert all(o[1] == single["bounded"] for o in out)          # gathered total, every rank
     assert sum(o[6] for o in out) == single["bounded"]          # per-rank work adds up
     assert all(o[5] for o in out)                               # exhausted everywhere
