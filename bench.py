@@ -47,10 +47,12 @@ def parse():
     ap.add_argument("--instance", default="ta021")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--mode", default="explore", choices=["explore", "bound", "exhaust"],
+    ap.add_argument("--mode", default="explore", choices=["explore", "bound", "exhaust", "solve"],
                     help="explore: explorer rounds (configs 1-4); bound: K1 bound-only passes "
                          "over a synthetic pool in HBM (config 5, bounding stress); exhaust: "
-                         "explore the whole tree (time-to-explore / proof of optimality)")
+                         "explore the whole tree (time-to-explore / proof of optimality); solve: "
+                         "solve() from the identity-permutation UB (config 1 in the reference's "
+                         "own mode), to optimality or --max-seconds")
     ap.add_argument("--ub", type=int, default=None,
                     help="--mode exhaust: frozen UB (default: the instance's UB + 1, so the "
                          "optimum is found and proven)")
@@ -249,6 +251,28 @@ def reference_arm(args, inst_name):
                     "d2h_bytes_per_step": 0},
             "rounds": [list(r) for r in rounds]}
     print(json.dumps(line), flush=True)
+
+
+def reference_api_e2e(target, steps):
+    """The same workload driven through the calls a reference C++ user makes, with the
+    reference's own PendingTree of heap Nodes on the host (tests/cpp/bench_dropin.cpp, built
+    against the unmodified reference headers): gpu_round (K2 per round) and the reference
+    resolve loop over GpuBackendSet (K1 per round).  None when the binary was not built."""
+    import subprocess
+
+    exe = os.path.join(ROOT, "tests", "cpp", "bin", "dropin_bench")
+    if not os.path.exists(exe):
+        return None
+    try:
+        out = subprocess.run([exe, str(target), str(steps)], capture_output=True, text=True,
+                             timeout=600)
+        d = json.loads(out.stdout.strip().splitlines()[-1])
+    except Exception as e:  # noqa: BLE001
+        return {"error": str(e)}
+    d["unit"] = "bounded subproblems/s"
+    d["timing"] = ("wall clock of the timed rounds, host Node packing/unpacking, PendingTree "
+                   "pushes/pops and transfers included")
+    return d
 
 
 def cpu_baseline(inst_name, target, sample_nodes):
@@ -531,8 +555,79 @@ def exhaust(args, inst_name):
         torch.distributed.destroy_process_group()
 
 
+def solve_mode(args, inst_name):
+    """BASELINE configs[0] in the reference's own mode: solve() (search.hpp:124-174) from the
+    identity-permutation makespan (search.hpp:131-137), strict-improvement incumbent with
+    mid-batch updates, deepest-first LIFO selection at a fixed pool target, until the pending
+    tree is empty (optimality proven) or --max-seconds.  Beside it, the reference's own
+    solve() on the host cores (oracle/_ref, BackendSet over all threads) for a bounded node
+    sample at the same pool target: its rate and the incumbent it reached."""
+    import torch
+
+    torch.cuda.set_device(0)
+    import paper_1206_4973_b200 as fbb
+
+    n, m, seed, _ = INSTANCES[inst_name]
+    inst = fbb.generate_instance(n, m, seed)
+    ctx = fbb.Context(inst, 0)
+    sampler = ClockSampler(0) if not os.environ.get("FBB_NO_CLOCKS") else None
+    t0 = time.perf_counter()
+    r0 = ctx.explorer_start_solve(None)
+    dev_ms, rounds, trace = 0.0, 1, []
+    while True:
+        r, t = ctx.explorer_run([args.target], 500, timing=True)
+        dev_ms += sum(x["round_ms"] for x in t)
+        rounds += len(r)
+        st = ctx.explorer_state()
+        trace.append((round(time.perf_counter() - t0, 3), st["bounded"], st["incumbent"]))
+        if st["pending"] == 0 or not r or time.perf_counter() - t0 > args.max_seconds:
+            break
+    wall = time.perf_counter() - t0
+    clocks = sampler.result() if sampler else None
+    st = ctx.explorer_state()
+    done = st["pending"] == 0
+    sched = st["schedule"]
+    cpu = None
+    if not args.no_cpu_baseline:
+        from oracle import REF_SO, Ref
+
+        if os.path.exists(REF_SO):
+            ref = Ref()
+            cores = ref.detect_units()
+            p = ref.generate_instance(n, m, seed)
+            w0 = time.perf_counter()
+            res, _, _ = ref.solve_trace(p, -1, targets=[args.target], budget=args.cpu_sample,
+                                        backends=cores, max_trace=1)
+            secs = time.perf_counter() - w0
+            cpu = {"value": res["bounded"] / secs, "unit": "bounded subproblems/s", "cores": cores,
+                   "kind": "reference",
+                   "sample": f"reference solve() from the identity UB, pool target {args.target}, "
+                             f"first {res['bounded']} bounded nodes in {secs:.1f} s; incumbent "
+                             f"reached {res['optimum']}"}
+    line = {
+        "metric": METRIC, "value": st["bounded"] / wall, "unit": "bounded subproblems/s",
+        "n_gpus": 1, "steps": rounds, "warmup": 0, "ms_per_step": 1e3 * wall / max(1, rounds),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic (Taillard generator, published seed; no dataset)",
+        "config": {"workload": f"{inst_name} {n}x{m} solve() from the identity-permutation "
+                               f"makespan, pool target {args.target}, to proven optimality "
+                               f"(pending tree empty) or {args.max_seconds:.0f} s",
+                   "instance": inst_name, "pool_target": args.target, "parallelism": "dp1"},
+        "explore_seconds": wall, "device_seconds": dev_ms / 1e3, "exhausted": done,
+        "optimum": st["incumbent"] if done else None, "incumbent": st["incumbent"],
+        "schedule": sched, "schedule_makespan": fbb.makespan(inst, sched) if sched else None,
+        "initial_ub": r0[6], "bounded": st["bounded"], "branched": st["branched"],
+        "pruned": st["pruned"], "leaves": st["leaves"], "incumbent_trace": trace[:200],
+        "cpu_baseline": cpu, "clocks": clocks, "gpu_launches": rounds * 3,
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
+    if args.mode == "solve":
+        solve_mode(args, args.instance)
+        return
     if args.mode == "exhaust":
         exhaust(args, args.instance)
         return
@@ -763,6 +858,9 @@ def main():
                            "last K2 CTA end (place_kernel is K2's programmatic dependent launch, so no "
                            "event can sit between them); rounds themselves are CUDA-event timed"),
     }
+    ref_api = None
+    if not args.no_e2e and world == 1 and inst_name == "ta021" and not args.tuner:
+        ref_api = reference_api_e2e(T, min(args.steps, 20))
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         try:
@@ -789,7 +887,8 @@ def main():
             "library_sync_wait": sum(t["sync_ms"] for t in timing) / max(1, len(timing)),
             "device_events": dev_ms / max(1, len(timing)),
             "l2_flush_untimed": 1e3 * flush_s / max(1, len(rounds))},
-        "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,
+        "e2e": e2e, "e2e_reference_api": ref_api, "roofline": roofline, "cpu_baseline": cpu,
+        "clocks": clocks,
         "gpu_launches": int(launches_all),
         "rounds": [list(r) for r in rounds],
         "prefill_rounds": len(prefill),

@@ -175,6 +175,24 @@ static std::mutex g_err_mu;
 static std::string g_create_err = "";
 static int g_create_status = FBB_OK;
 
+// What a captured batch graph bakes in: its length and the buffers its kernels and copies
+// address (bucket storage travels in the uploaded LoopState, so bucket growth needs no
+// recapture).
+struct LoopGraphKey {
+    int rounds = 0;
+    const void* p[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    LoopGraphKey() = default;
+    LoopGraphKey(int r, const void* a, const void* b, const void* c, const void* d, const void* e,
+                 const void* f, const void* g, const void* h)
+        : rounds(r), p{a, b, c, d, e, f, g, h} {}
+    bool operator==(const LoopGraphKey& o) const {
+        if (rounds != o.rounds) return false;
+        for (int i = 0; i < 8; ++i)
+            if (p[i] != o.p[i]) return false;
+        return true;
+    }
+};
+
 struct fbb_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -201,7 +219,8 @@ struct fbb_ctx {
     // batched device-planned explorer loop (explorer_loop.cu)
     DBuf d_loop;
     HBuf h_loop;
-    std::vector<cudaEvent_t> loop_ev;  // 4 per round of a batch
+    cudaGraphExec_t loop_graph = nullptr;  // the captured batch (explorer_run_batched)
+    LoopGraphKey loop_graph_key{};
     bool device_loop = false;          // FBB_DEVICE_LOOP=1: batched device-planned rounds
     float last_k2_ms = 0.f, last_round_ms = 0.f, last_sync_ms = 0.f, last_place_ms = 0.f;
     int last_launches = 0;
@@ -708,11 +727,6 @@ int explorer_run_batched(fbb_ctx* ctx, const int64_t* targets, int ntargets, int
     cudaStream_t st = ctx->stream;
     int64_t r = 0;
     if (done) *done = 0;
-    if ((int)ctx->loop_ev.size() < 4 * kLoopMax) {
-        ctx->loop_ev.resize(4 * kLoopMax, nullptr);
-        for (cudaEvent_t& e : ctx->loop_ev)
-            if (!e) CK(cudaEventCreate(&e), "event");
-    }
     CK(ctx->d_loop.ensure(sizeof(LoopState)), "loop state");
     CK(ctx->h_loop.ensure(sizeof(LoopState)), "loop state");
     CK(ctx->d_pool.ensure(sizeof(Pool)), "pool");
@@ -768,16 +782,43 @@ int explorer_run_batched(fbb_ctx* ctx, const int64_t* targets, int ntargets, int
         ChunkOut out{ctx->staging.view(), ctx->st_lb.as<int32_t>(), ctx->st_count.as<int32_t>(),
                      ctx->st_seg.as<int32_t>()};
         const auto w0 = std::chrono::steady_clock::now();
-        CK(cudaMemcpyAsync(dl, hl, offsetof(LoopState, rec), cudaMemcpyHostToDevice, st), "loop H2D");
-        for (int i = 0; i < R; ++i) {
-            cudaEvent_t* ev = &ctx->loop_ev[4 * i];
-            CK(cudaEventRecord(ev[0], st), "event");
-            CK(launch_loop_plan(ctx->dt, dl, dp, rs, i, st), "plan");
-            CK(launch_round_device(ctx->dt, ctx->k2, dp, rs, out, st, ev[1], ev[2]), "round");
-            CK(launch_loop_close(ctx->dt, dl, dp, rs, i, st), "close");
-            CK(cudaEventRecord(ev[3], st), "event");
+        // the batch: state upload, R x (plan, leaves, leaf schedule, K2, place, close), state
+        // download -- every kernel a programmatic dependent of the one before, the whole
+        // sequence one CUDA graph (captured once per batch length and staging buffers, then
+        // replayed: one host call per batch)
+        auto enqueue = [&](bool pdl) -> cudaError_t {
+            cudaError_t e = cudaMemcpyAsync(dl, hl, offsetof(LoopState, rec), cudaMemcpyHostToDevice, st);
+            for (int i = 0; i < R && e == cudaSuccess; ++i) {
+                if ((e = launch_loop_plan(ctx->dt, dl, dp, rs, i, st, pdl && i > 0)) != cudaSuccess) break;
+                if ((e = launch_round_device(ctx->dt, ctx->k2, dp, rs, out, st, pdl)) != cudaSuccess) break;
+                e = launch_loop_close(ctx->dt, dl, dp, rs, i, st, pdl);
+            }
+            if (e == cudaSuccess) e = cudaMemcpyAsync(hl, dl, sizeof(LoopState), cudaMemcpyDeviceToHost, st);
+            return e;
+        };
+        static const bool use_graph = [] { const char* e = getenv("FBB_LOOP_GRAPH"); return !(e && e[0] == '0'); }();
+        static const bool loop_pdl = [] { const char* e = getenv("FBB_PDL"); return !(e && e[0] == '0'); }();
+        if (use_graph) {
+            const LoopGraphKey key{R, out.nodes.masks, out.nodes.heads, out.nodes.prefix, out.lb, out.count,
+                                   out.seg, dl, hl};
+            if (!ctx->loop_graph || !(ctx->loop_graph_key == key)) {
+                if (ctx->loop_graph) cudaGraphExecDestroy(ctx->loop_graph);
+                ctx->loop_graph = nullptr;
+                cudaGraph_t g = nullptr;
+                CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "loop capture");
+                cudaError_t ce = enqueue(loop_pdl);
+                cudaError_t ee = cudaStreamEndCapture(st, &g);
+                CK(ce, "loop capture");
+                CK(ee, "loop capture");
+                ce = cudaGraphInstantiate(&ctx->loop_graph, g, 0);
+                cudaGraphDestroy(g);
+                CK(ce, "loop graph instantiate");
+                ctx->loop_graph_key = key;
+            }
+            CK(cudaGraphLaunch(ctx->loop_graph, st), "loop graph");
+        } else {
+            CK(enqueue(loop_pdl), "loop batch");
         }
-        CK(cudaMemcpyAsync(hl, dl, sizeof(LoopState), cudaMemcpyDeviceToHost, st), "loop D2H");
         const auto t_sync = std::chrono::steady_clock::now();
         CK(cudaStreamSynchronize(st), "batch");
         const auto w1 = std::chrono::steady_clock::now();
@@ -800,9 +841,12 @@ int explorer_run_batched(fbb_ctx* ctx, const int64_t* targets, int ntargets, int
             rec.leaves = lr.leaves;
             rec.incumbent = lr.incumbent;
             rec.pending = lr.pending;
-            cudaEvent_t* ev = &ctx->loop_ev[4 * i];
-            cudaEventElapsedTime(&rec.k2_ms, ev[1], ev[2]);
-            cudaEventElapsedTime(&rec.round_ms, ev[0], ev[3]);
+            // device clock: a round runs from its plan's start to the next round's plan
+            // start (the last one: to its close's end), so the rounds tile the batch
+            const unsigned long long t_next = i + 1 < valid ? hl->rec[i + 1].t0 : lr.t1;
+            rec.round_ms = (float)((double)(t_next - lr.t0) * 1e-6);
+            rec.k2_ms = lr.k2_t0 && lr.k2_t1 > lr.k2_t0 ? (float)((double)(lr.k2_t1 - lr.k2_t0) * 1e-6) : 0.f;
+            rec.place_ms = -1.f;
             rec.launches = 6;
             rec.host_ms = wall_ms / valid;
             rec.sync_ms = sync_ms / valid;
@@ -993,8 +1037,7 @@ void fbb_destroy(fbb_ctx* ctx) {
     ctx->h_rp.release();
     ctx->h_loop.release();
     ctx->d_loop.release();
-    for (cudaEvent_t ev : ctx->loop_ev)
-        if (ev) cudaEventDestroy(ev);
+    if (ctx->loop_graph) cudaGraphExecDestroy(ctx->loop_graph);
     for (cudaEvent_t ev : ctx->ev)
         if (ev) cudaEventDestroy(ev);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);

@@ -565,6 +565,7 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(DevTables t, const
     extern __shared__ uint8_t s_rc[];          // chunk of each row (cmax * kPlaceChunks)
     // launched as a programmatic dependent of K2 (FBB_PDL=1): wait for its completion
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;");  // the device loop's close kernel
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t nchunks = pool->nchunks;
     for (int64_t c0 = (int64_t)blockIdx.x * kPlaceChunks; c0 < nchunks;
@@ -838,30 +839,24 @@ namespace fbb {
 // round's plan from the device Pool / RoundState and exits when it has nothing to do,
 // so the grids are fixed and nothing here needs the host.
 cudaError_t launch_round_device(const DevTables& t, const K2Config& cfg, const Pool* d_pool,
-                                RoundState* rs, ChunkOut out, cudaStream_t stream, cudaEvent_t k2_begin,
-                                cudaEvent_t k2_end) {
-    k2_leaf_kernel<<<148 * 4, 256, 0, stream>>>(t, d_pool, 0, rs);
-    leaf_schedule_kernel<<<1, 32, 0, stream>>>(t, d_pool, rs, 0);
-    if (k2_begin) cudaEventRecord(k2_begin, stream);
-    cudaError_t e;
+                                RoundState* rs, ChunkOut out, cudaStream_t stream, bool pdl) {
+    // leaves: a one-wave grid-stride grid (most rounds have none and exit at once)
+    cudaError_t e = launch_pdl(k2_leaf_kernel, dim3(148), dim3(256), 0, stream, pdl, t, d_pool, 0, rs);
+    if (e != cudaSuccess) return e;
+    e = launch_pdl(leaf_schedule_kernel, dim3(1), dim3(32), 0, stream, pdl, t, d_pool, rs, 0);
+    if (e != cudaSuccess) return e;
     if (cfg.variant >= 100000)
-        e = launch_k2_v3(t, cfg, d_pool, 0, cfg.blocks, 0, 0, rs, out, stream);
+        e = launch_k2_v3(t, cfg, d_pool, 0, cfg.blocks, 0, 0, rs, out, stream, pdl);
     else if (cfg.variant != 0)
-        e = launch_k2_v2(t, cfg, d_pool, 0, cfg.blocks, 0, 0, rs, out, stream);
-    else if (cfg.wide)
-        k2_internal_kernel<false, true><<<cfg.blocks, cfg.threads, cfg.smem, stream>>>(t, d_pool, 0, cfg.cmax, 0,
-                                                                                       0, rs, out);
-    else if (cfg.jm_in_smem)
-        k2_internal_kernel<true, false><<<cfg.blocks, cfg.threads, cfg.smem, stream>>>(t, d_pool, 0, cfg.cmax, 0,
-                                                                                       0, rs, out);
+        e = launch_k2_v2(t, cfg, d_pool, 0, cfg.blocks, 0, 0, rs, out, stream, pdl);
     else
-        k2_internal_kernel<false, false><<<cfg.blocks, cfg.threads, cfg.smem, stream>>>(t, d_pool, 0, cfg.cmax, 0,
-                                                                                        0, rs, out);
-    if (k2_end) cudaEventRecord(k2_end, stream);
-    place_kernel<true><<<148 * 2, kPlaceThreads, (size_t)cfg.cmax * kPlaceChunks, stream>>>(t, d_pool, cfg.cmax, rs,
-                                                                                      out, nullptr);
-    e = cudaGetLastError();
-    return e;
+        e = launch_pdl(cfg.wide ? k2_internal_kernel<false, true>
+                                : (cfg.jm_in_smem ? k2_internal_kernel<true, false> : k2_internal_kernel<false, false>),
+                       dim3(cfg.blocks), dim3(cfg.threads), cfg.smem, stream, pdl, t, d_pool, 0, cfg.cmax, 0, 0,
+                       rs, out);
+    if (e != cudaSuccess) return e;
+    return launch_pdl(place_kernel<true>, dim3(148 * 2), dim3(kPlaceThreads), (size_t)cfg.cmax * kPlaceChunks,
+                      stream, pdl, t, d_pool, cfg.cmax, rs, out, (RoundState*)nullptr);
 }
 
 }  // namespace fbb

@@ -19,8 +19,20 @@ namespace fbb {
 
 namespace {
 
+__device__ __forceinline__ unsigned long long loop_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
 __global__ void loop_plan_kernel(DevTables t, LoopState* ls, Pool* pool, RoundState* rs, int round) {
+    // a programmatic dependent of the previous round's close kernel (or of the batch's
+    // state upload): wait for it before reading the loop state, then let the leaf kernel
+    // be scheduled
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;");
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    if (round < kLoopMax) ls->rec[round].t0 = loop_ns();
     const int n = t.n;
     pool->nseg = 0;
     pool->nchunks = 0;
@@ -29,6 +41,9 @@ __global__ void loop_plan_kernel(DevTables t, LoopState* ls, Pool* pool, RoundSt
     rs->found = 0;
     rs->ticket = 0u;
     rs->total = 0;
+    rs->place_done = 0u;
+    rs->k2_t0_inv = 0ull;
+    rs->k2_t1 = 0ull;
     pool->ub = ls->incumbent;
     pool->frozen = ls->frozen;
     pool->first_internal = 0;
@@ -108,11 +123,15 @@ __global__ void loop_plan_kernel(DevTables t, LoopState* ls, Pool* pool, RoundSt
 
 __global__ void loop_close_kernel(DevTables t, LoopState* ls, const Pool* pool, const RoundState* rs,
                                   int round) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // the round's place kernel
+    asm volatile("griddepcontrol.launch_dependents;");
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     const int n = t.n;
     LoopRecord& rec = ls->rec[round];
     rec.valid = 0;
     if (pool->nseg == 0) return;  // stopped before this round
+    rec.k2_t0 = rs->k2_t0_inv ? ~rs->k2_t0_inv : 0ull;
+    rec.k2_t1 = rs->k2_t1;
     if (rs->found < 0) {          // corrupt pending node (leaf kernel's check)
         ls->stop = 4;
         return;
@@ -159,20 +178,19 @@ __global__ void loop_close_kernel(DevTables t, LoopState* ls, const Pool* pool, 
     ls->tot_bounded += internal + leaves;
     if (pending == 0) ls->stop = 1;
     else if (ls->budget > 0 && ls->tot_bounded >= ls->budget) ls->stop = 2;
+    rec.t1 = loop_ns();
 }
 
 }  // namespace
 
 cudaError_t launch_loop_plan(const DevTables& t, LoopState* ls, Pool* pool, RoundState* rs, int round,
-                             cudaStream_t stream) {
-    loop_plan_kernel<<<1, 32, 0, stream>>>(t, ls, pool, rs, round);
-    return cudaGetLastError();
+                             cudaStream_t stream, bool pdl) {
+    return launch_pdl(loop_plan_kernel, dim3(1), dim3(32), 0, stream, pdl, t, ls, pool, rs, round);
 }
 
 cudaError_t launch_loop_close(const DevTables& t, LoopState* ls, const Pool* pool, const RoundState* rs,
-                              int round, cudaStream_t stream) {
-    loop_close_kernel<<<1, 32, 0, stream>>>(t, ls, pool, rs, round);
-    return cudaGetLastError();
+                              int round, cudaStream_t stream, bool pdl) {
+    return launch_pdl(loop_close_kernel, dim3(1), dim3(32), 0, stream, pdl, t, ls, pool, rs, round);
 }
 
 }  // namespace fbb

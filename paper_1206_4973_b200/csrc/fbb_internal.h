@@ -250,6 +250,9 @@ constexpr int kLoopMax = 64;  // rounds per batch
 struct LoopRecord {  // one round's counters (search.hpp:21-26, 75-79)
     int64_t target, branched, bounded, inserted, pruned, leaves, pending;
     int32_t incumbent, valid;
+    // device clock (%globaltimer, ns): plan start, close end, first K2 CTA start, last K2
+    // CTA end -- the per-round timing of a batch that has no events inside it
+    unsigned long long t0, t1, k2_t0, k2_t1;
 };
 
 // Device-resident explorer state for a batch of rounds.  The host writes the head
@@ -270,13 +273,14 @@ struct LoopState {
     LoopRecord rec[kLoopMax];
 };
 
+// pdl: each kernel of the batch is a programmatic dependent of the one before (every one
+// of them waits -- griddepcontrol.wait -- before it reads its predecessor's output)
 cudaError_t launch_loop_plan(const DevTables& t, LoopState* ls, Pool* pool, RoundState* rs, int round,
-                             cudaStream_t stream);
+                             cudaStream_t stream, bool pdl);
 cudaError_t launch_loop_close(const DevTables& t, LoopState* ls, const Pool* pool, const RoundState* rs,
-                              int round, cudaStream_t stream);
+                              int round, cudaStream_t stream, bool pdl);
 cudaError_t launch_round_device(const DevTables& t, const K2Config& cfg, const Pool* d_pool,
-                                RoundState* rs, ChunkOut out, cudaStream_t stream, cudaEvent_t k2_begin,
-                                cudaEvent_t k2_end);
+                                RoundState* rs, ChunkOut out, cudaStream_t stream, bool pdl);
 
 // Launches kern<<<grid, block, smem, st>>>(args...), as a programmatic dependent of the
 // previous kernel in the stream when pdl (the kernel must griddepcontrol.wait before it

@@ -468,3 +468,33 @@ def test_device_planned_loop_matches_reference(instances, traces, on_host, monke
         assert [r0] + rounds == [tuple(r) for r in case["rounds"]]
         assert st["incumbent"] == case["optimum"] and st["schedule"] == case["schedule"]
         ctx.close()
+
+
+# ---- >= 1 M-node traces at 50x20, 100x20, 200x20 (tests/golden/make_traces_large.py) ----------
+
+def _large_traces():
+    import json
+    import os
+
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "traces_large.json")
+    with open(path) as f:
+        return json.load(f)["resolve"]
+
+
+@pytest.mark.parametrize("mode", ["hbm", "host", "device_loop"])
+def test_explorer_large_traces_match_reference(instances, mode, monkeypatch):
+    """Per-round counts over >= 1 M bounded nodes (fixed pools and a tuner-shaped doubling
+    schedule) equal the reference explorer's at 50x20 (K2 v2 wide), 100x20 and 200x20
+    (K2 v3): HBM tree, host-resident tree, and the graph-captured device-planned loop."""
+    if mode == "device_loop":
+        monkeypatch.setenv("FBB_DEVICE_LOOP", "1")
+        monkeypatch.setenv("FBB_HOST_ROWS", "full")
+    for tr in _large_traces():
+        inst = inst_of(instance_p(instances, tr["instance"]))
+        ctx = fbb.Context(inst)
+        ctx.explorer_set_residency(mode == "host")
+        ctx.explorer_reset(fbb.NodeBatch.root(inst), tr["ub"], frozen=True)
+        rounds = ctx.explorer_run(tr["targets"], 1 << 20, tr["budget"])
+        assert rounds == [tuple(r) for r in tr["rounds"]], (tr["instance"], tr["targets"][:2], mode)
+        assert ctx.explorer_state()["bounded"] == tr["result"]["bounded"] >= 1_000_000
+        ctx.close()
