@@ -38,6 +38,28 @@ METRIC = "bounded subproblems/sec & explore time, Taillard 20x20/50x20, 1/2/4/8 
 INT32_LANES_PER_SM = 128  # ALU pipe 64 + FMA pipe 64 integer lanes / clk / SM (B300_MICROARCH)
 
 
+def int_peak_gops(clock_mhz):
+    """The integer roofline denominator, MEASURED on this pool's B200s by
+    scripts/micro/intpeak.cu (profiles/r02_intpeak.json): the best 32-bit integer issue
+    rate at full occupancy -- VIADDMNMX (ALU pipe) interleaved with IMAD (FMA pipe), 93.6
+    lane-instructions/clk/SM, i.e. what the K1/K2 instruction mix can issue at most -- in
+    Gop/s.  Falls back to the derived 148 x 128 lanes x clock when the file is missing."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_intpeak.json")) as f:
+            d = json.load(f)
+        mix = d["viaddmnmx+imad"]
+        return mix["gops"], {
+            "source": "measured: profiles/r02_intpeak.json (scripts/micro/intpeak.cu), "
+                      "VIADDMNMX+IMAD at 2048 threads/SM",
+            "lane_inst_per_clk_per_sm": mix["lane_inst_per_clk_per_sm"],
+            "single_pipe_gops": d["viaddmnmx"]["gops"],
+            "simd16x2_gops": d["viaddmnmx.s16x2"]["gops"],
+            "derived_gops": 148 * INT32_LANES_PER_SM * clock_mhz * 1e6 / 1e9}
+    except Exception:  # noqa: BLE001
+        g = 148 * INT32_LANES_PER_SM * clock_mhz * 1e6 / 1e9
+        return g, {"source": "derived: 148 SMs x 128 int32 lanes/clk x max SM clock"}
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -429,7 +451,7 @@ def bound_stress(args, inst_name):
     ops_per_node = 4 * P * n_u + 2 * m * n_u  # SURVEY 8(a) W_K1
     peaks = measured_peaks()
     clock_mhz = (clocks or {}).get("sm_max_mhz") or peaks.get("sm_max_mhz", 1965.0)
-    int_peak = 148 * INT32_LANES_PER_SM * clock_mhz * 1e6 / 1e9
+    int_peak, peak_src = int_peak_gops(clock_mhz)
     achieved = cnt * args.steps * ops_per_node / (ms / 1e3) / 1e9
     node_b = W * 8 + m * 4 + 4 + 4
     line = {
@@ -446,7 +468,7 @@ def bound_stress(args, inst_name):
         "e2e": e2e,
         "roofline": {"bound": "int32-alu", "kernel": ctx.kernels().split()[0][3:] + " (bound-only K1)",
                      "achieved": achieved, "peak": int_peak, "unit": "Gop/s",
-                     "frac": achieved / int_peak, "traffic": None,
+                     "frac": achieved / int_peak, "traffic": None, "peak_source": peak_src,
                      "ops_per_node": ops_per_node,
                      "hbm": {"achieved": cnt * args.steps * node_b / (ms / 1e3) / 1e9,
                              "peak": peaks.get("hbm_gbs", 6553.9), "unit": "GB/s"}},
@@ -833,7 +855,7 @@ def main():
     peaks = measured_peaks()
     hbm_peak = peaks.get("hbm_gbs", 6528.7)
     clock_mhz = (clocks or {}).get("sm_max_mhz") or peaks.get("sm_max_mhz", 1965.0)
-    int_peak = 148 * INT32_LANES_PER_SM * clock_mhz * 1e6 / 1e9  # Gop/s
+    int_peak, peak_src = int_peak_gops(clock_mhz)  # Gop/s
     internal = bounded - leaves
     # algorithmic int32 ops: per parent scan P*n, per child P*15 + 6m
     ops = P * (n * max(0, branched - leaves // 2) + 15 * internal) + 6 * m * bounded
@@ -848,8 +870,7 @@ def main():
         "traffic": (k2_traffic(inst_name) or {}).get("bytes_per_launch"),
         "traffic_source": k2_traffic(inst_name),
         "ops_per_child": ops / max(1, bounded),
-        "peak_note": "148 SMs x 128 int32 lanes/clk (alu+fma pipes) x max SM clock; derived, "
-                     "not measured (MEASURED_PEAKS has no integer figure)",
+        "peak_source": peak_src,
         "hbm": {"achieved": alg_bytes / k2_s / 1e9 if k2_s > 0 else 0.0, "peak": hbm_peak,
                 "unit": "GB/s", "frac": (alg_bytes / k2_s / 1e9) / hbm_peak if k2_s > 0 else 0.0},
         "k2_share_of_round": k2_ms / dev_ms if dev_ms > 0 else 0.0,
