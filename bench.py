@@ -81,10 +81,14 @@ def parse():
     ap.add_argument("--max-seconds", type=float, default=1800.0,
                     help="--mode exhaust: wall-clock cap")
     ap.add_argument("--pool", type=int, default=8_000_000,
-                    help="--mode bound: nodes in the synthetic pool")
+                    help="--mode bound: nodes in the synthetic pool (0: fill the GPU's free HBM)")
     ap.add_argument("--tuner", action="store_true",
                     help="adaptive pool size (autotune.hpp) instead of a fixed --target")
     ap.add_argument("--tuner-window", type=int, default=4)
+    ap.add_argument("--group", type=int, default=0,
+                    help="--mode exhaust, one process: explore with an fbb_group of this many "
+                         "members (the in-library multi-device explorer; members on GPUs "
+                         "0..G-1 when that many are visible, else all on GPU 0)")
     ap.add_argument("--exchange-every", type=int, default=4,
                     help="N > 1: explorer rounds per rank exchange (one library call each)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -298,7 +302,11 @@ def reference_api_e2e(target, steps):
 
 
 def cpu_baseline(inst_name, target, sample_nodes):
-    """The reference CPU explorer (oracle/_ref) on a bounded sample of the same workload."""
+    """The reference CPU explorer (oracle/_ref) on bounded samples of the same workload: all
+    host threads (BackendSet(k = nproc)) and one core (k = 1, the paper's Tcpu,
+    PAPER.md:353-354).  The samples scale with the per-node cost (~n): ~2e6 / n nodes on
+    one core, k/2 times that on k cores, rounds capped at the sample so that the first
+    round never dominates (100x20 / 200x20 nodes cost ~1-4 ms each on one core)."""
     from oracle import REF_SO, Oracle, Ref
 
     n, m, seed, ub = INSTANCES[inst_name]
@@ -306,20 +314,31 @@ def cpu_baseline(inst_name, target, sample_nodes):
         ref = Ref()
         cores = ref.detect_units()
         p = ref.generate_instance(n, m, seed)
-        res, rounds, secs = ref.resolve(p, ub, [[]], targets=[target], budget=sample_nodes,
-                                        backends=cores, max_trace=1)
-        kind = "reference"
-    else:
-        orc = Oracle()
-        p = orc.generate_instance(n, m, seed)
-        t0 = time.perf_counter()
-        res, _ = orc.resolve(p, ub, [[]], targets=[target], budget=sample_nodes // 20)
-        secs = time.perf_counter() - t0
-        cores, kind = 1, "port"
-    return {"value": res["bounded"] / secs, "unit": "bounded subproblems/s", "cores": cores,
-            "kind": kind, "sample": f"resolve from the root, target {target}, first "
-                                    f"{res['bounded']} bounded nodes ({res['rounds']} rounds, "
-                                    f"{secs:.1f} s)"}
+        one = max(2000, int(2e6 / n))
+        many = min(sample_nodes, max(one, one * cores // 2))
+        out = {}
+        for k, budget in ((cores, many), (1, one)):
+            tgt = min(target, budget)
+            t0 = time.perf_counter()
+            res, _, _ = ref.resolve(p, ub, [[]], targets=[tgt], budget=budget, backends=k,
+                                    max_trace=1)
+            secs = time.perf_counter() - t0
+            out[k] = {"value": res["bounded"] / secs, "unit": "bounded subproblems/s", "cores": k,
+                      "kind": "reference",
+                      "sample": f"reference resolve from the root, pool target {tgt}, first "
+                                f"{res['bounded']} bounded nodes ({res['rounds']} rounds, "
+                                f"{secs:.1f} s, BackendSet({k}))"}
+        line = dict(out[cores])
+        line["single_core"] = out[1]
+        return line
+    orc = Oracle()
+    p = orc.generate_instance(n, m, seed)
+    t0 = time.perf_counter()
+    res, _ = orc.resolve(p, ub, [[]], targets=[target], budget=sample_nodes // 20)
+    secs = time.perf_counter() - t0
+    return {"value": res["bounded"] / secs, "unit": "bounded subproblems/s", "cores": 1,
+            "kind": "port", "sample": f"C restatement, resolve from the root, target {target}, "
+                                      f"first {res['bounded']} bounded nodes ({secs:.1f} s)"}
 
 
 def ref_evaluate_timed(ref, p, prefixes_of, cores, target_s=10.0):
@@ -361,6 +380,10 @@ def bound_stress(args, inst_name):
     ctx = fbb.Context(inst, dev)
     cnt, W, P = args.pool, (n + 63) // 64, m * (m - 1) // 2
     cuda = f"cuda:{dev}"
+    if cnt <= 0:  # --pool 0: the largest pool that fits this GPU's free HBM (4 GiB headroom)
+        free_b, _ = torch.cuda.mem_get_info(dev)
+        cnt = max(1 << 20, int((free_b - (4 << 30)) // (W * 8 + m * 4 + 4 + 4)))
+        cnt -= cnt % 1024
     masks = torch.empty(cnt * W, dtype=torch.int64, device=cuda)
     heads = torch.empty(cnt * m, dtype=torch.int32, device=cuda)
     depth = torch.empty(cnt, dtype=torch.int32, device=cuda)
@@ -370,7 +393,7 @@ def bound_stress(args, inst_name):
     ctx.synth_pool(0x5EED + rank, cnt, 0, n - 1, masks.data_ptr(), heads.data_ptr(),
                    depth.data_ptr(), 0, stream)
     torch.cuda.synchronize()
-    n_u = float((n - depth.double()).mean())
+    n_u = n - float(depth.sum(dtype=torch.int64).item()) / cnt  # no pool-sized temporaries
 
     def one_pass():
         ctx.bound_device(masks.data_ptr(), heads.data_ptr(), depth.data_ptr(), cnt, lbs.data_ptr(),
@@ -464,6 +487,7 @@ def bound_stress(args, inst_name):
                                f"a synthetic pool of {cnt} nodes per GPU resident in HBM; step = "
                                f"one pass", "instance": inst_name, "pool_nodes": cnt,
                    "mean_unscheduled": n_u, "parallelism": f"dp{world} (own pool per GPU)",
+                   "pool_gib": cnt * node_b / 2**30,
                    "l2": f"pool {cnt * node_b / 2**30:.2f} GiB > L2 (126 MB), no flush needed"},
         "e2e": e2e,
         "roofline": {"bound": "int32-alu", "kernel": ctx.kernels().split()[0][3:] + " (bound-only K1)",
@@ -519,7 +543,17 @@ def exhaust(args, inst_name):
         torch.distributed.barrier()
     t0 = time.perf_counter()
     dev_ms, rounds, transfers = 0.0, 0, 0
-    if world == 1:
+    group = None
+    if world == 1 and args.group > 1:
+        G = args.group
+        devs = list(range(G)) if torch.cuda.device_count() >= G else [0] * G
+        group = fbb.DeviceGroup(inst, devs)
+        group.reset(fbb.NodeBatch.root(inst), ub, frozen=True)
+        t0 = time.perf_counter()
+        gs = group.run(args.target, max_steps=1 << 40, rounds_per_step=args.exchange_every,
+                       balance_every=1)
+        dev_ms, rounds, transfers = gs["device_ms_max"], gs["rounds"], gs["transfers"]
+    elif world == 1:
         while True:
             r, t = ctx.explorer_run([args.target], 2000, timing=True)
             dev_ms += sum(x["round_ms"] for x in t)
@@ -539,6 +573,10 @@ def exhaust(args, inst_name):
     wall = time.perf_counter() - t0
     clocks = sampler.result() if sampler else None
     st = ctx.explorer_state()
+    if group is not None:  # totals over the group's members
+        st = {"bounded": gs["bounded"], "branched": gs["branched"], "pruned": gs["pruned"],
+              "leaves": gs["leaves"], "pending": gs["pending"], "found": bool(gs["found"]),
+              "incumbent": gs["incumbent"]}
     best_mine = st["incumbent"] if st["found"] else 2**31 - 1
     tot = torch.tensor([st["bounded"], st["branched"], st["pruned"], st["leaves"], st["pending"]],
                        dtype=torch.int64, device=coll_dev)
@@ -563,10 +601,15 @@ def exhaust(args, inst_name):
             "config": {"workload": f"{inst_name} {n}x{m} exhaustive frozen-UB exploration from "
                                    f"the root at UB {ub}, pool target {args.target} per GPU",
                        "instance": inst_name, "ub": ub, "pool_target": args.target,
-                       "parallelism": f"dp{world}" + (" (pending-tree rebalancing)" if world > 1 else "")},
+                       "parallelism": (f"fbb_group of {args.group} members in one process"
+                                       if group is not None else
+                                       f"dp{world}" + (" (pending-tree rebalancing)" if world > 1 else ""))},
             "explore_seconds": wall_max, "device_seconds": dev_max, "exhausted": done,
             "bounded": bounded, "branched": branched, "pruned": pruned, "leaves": leaves,
             "nodes_moved_between_gpus": transfers, "best_leaf": int(best.item()) if found else None,
+            "group": ({"members": args.group, "devices": group.devices,
+                       "exchange_ms": gs["exchange_ms"], "steps": gs["steps"],
+                       "rounds_per_step": args.exchange_every} if group is not None else None),
             "proof": (f"optimum {int(best.item())}: no complete schedule below it exists"
                       if done and found else
                       f"no schedule below {ub}" if done else "time cap reached"),

@@ -1093,7 +1093,15 @@ int fbb_bound_device(fbb_ctx* ctx, const uint64_t* d_masks, const int32_t* d_hea
     if (count == 0) return FBB_OK;
     cudaSetDevice(ctx->device);
     cudaStream_t st = stream ? (cudaStream_t)stream : ctx->stream;
-    CK(launch_k1(ctx->dt, ctx->k1, d_masks, d_heads, d_depth, count, d_lb_out, st), "K1 launch");
+    // HBM-filling pools (billions of nodes): launches of at most 2^26 nodes, so every
+    // in-kernel node x row index stays within 32 bits
+    constexpr int64_t kSlice = int64_t(1) << 26;
+    const int W = ctx->dt.W, m = ctx->dt.m;
+    for (int64_t off = 0; off < count; off += kSlice) {
+        const int64_t k = std::min(kSlice, count - off);
+        CK(launch_k1(ctx->dt, ctx->k1, d_masks + off * W, d_heads + off * m, d_depth + off, k, d_lb_out + off, st),
+           "K1 launch");
+    }
     return FBB_OK;
 }
 

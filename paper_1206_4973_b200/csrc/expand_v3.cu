@@ -104,8 +104,10 @@ __device__ __forceinline__ Mins mins_merge(Mins x, Mins y) {
     return r;
 }
 
+// 4 CTAs/SM at n <= 128 (80 registers; chunk = one parent's r <= n children, cmax = n, so
+// the Mq rows fit 4 CTAs' shared memory), 2 at n <= 256
 template <int NW, int M>
-__global__ void __launch_bounds__(NW <= 4 ? 192 : 256, NW <= 4 ? 3 : 2)
+__global__ void __launch_bounds__(NW <= 4 ? 192 : 256, NW <= 4 ? 4 : 2)
     k2_v3_kernel(DevTables t, const Pool* __restrict__ pool, int first_seg, int cmax, int32_t ub,
                  int frozen, RoundState* rs, ChunkOut out) {
     asm volatile("griddepcontrol.launch_dependents;");  // place_kernel may be scheduled early
@@ -391,7 +393,7 @@ bool k2_v3_config(const DevTables& t, int device, K2Config* out) {
     if (!(t.safe16 & kSafeM16)) return false;  // M' is stored as int16 (DevTables::safe16)
     K2Config c;
     const int NW = n <= 128 ? 4 : 8;
-    c.cmax = ((n + 31) / 32) * 32;          // one parent's children always fit a chunk
+    c.cmax = n;                             // one parent's children always fit a chunk
     c.threads = NW <= 4 ? 192 : 256;        // >= cmax (Phase B: a child per thread), >= P
     if (const char* cm = getenv("FBB_K2_CMAX"))
         c.cmax = std::max(c.cmax, std::min(c.threads, (atoi(cm) / 32) * 32));

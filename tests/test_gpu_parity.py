@@ -498,3 +498,37 @@ def test_explorer_large_traces_match_reference(instances, mode, monkeypatch):
         assert rounds == [tuple(r) for r in tr["rounds"]], (tr["instance"], tr["targets"][:2], mode)
         assert ctx.explorer_state()["bounded"] == tr["result"]["bounded"] >= 1_000_000
         ctx.close()
+
+
+def test_tuner_schedule_replays_on_the_reference():
+    """Config 3 parity (SURVEY 7 hard part 4): the adaptive tuner (autotune.hpp:35-156 with
+    the B200 descriptor) picks each round's pool size from measured device time, so its
+    schedule is not reproducible -- but once recorded, the reference explorer driven with
+    the same per-round targets (oracle/_ref, the reference headers compiled in place) must
+    produce identical per-round counts on Ta051 (50x20, frozen UB)."""
+    import os
+
+    from oracle import REF_SO, Ref
+
+    if not os.path.exists(REF_SO):
+        pytest.skip("oracle/_ref not built")
+    inst = fbb.generate_instance(50, 20, 1539989115)
+    ctx = fbb.Context(inst)
+    ctx.explorer_reset(fbb.NodeBatch.root(inst), 3847, frozen=True)
+    tuner = fbb.Tuner(ctx.descriptor(), 1, 2)
+    rounds, total = [], 0
+    while total < 600_000:
+        r, t = ctx.explorer_run([tuner.target()], 1, timing=True)
+        if not r:
+            break
+        tuner.observe(r[0][2], max(t[0]["round_ms"], 1e-6) / 1e3)
+        rounds += r
+        total += r[0][2]
+    targets = [r[0] for r in rounds]
+    assert len(set(targets)) >= 2  # the tuner moved the pool size
+    ref = Ref()
+    res, gold, _ = ref.resolve(inst.p, 3847, [[]], targets=targets, budget=total,
+                               backends=ref.detect_units(), max_trace=1 << 12)
+    assert rounds == [tuple(x) for x in gold]
+    assert res["bounded"] == total
+    ctx.close()
