@@ -244,6 +244,7 @@ struct fbb_ctx {
                                 // mapped) host buckets; FBB_HOST_OUT=staged: device output + D2H
     int64_t last_h2d = 0, last_d2h = 0;
     bool summary_by_place = true;  // FBB_SUMMARY=copy: download the round summary instead
+    bool direct_place = true;      // FBB_DIRECT=0: always stage survivors + place_kernel
     bool check = false;  // FBB_CHECK=1: validate the pending tree after every round
 
     int fail(int code, const std::string& m) {
@@ -348,6 +349,19 @@ int run_pool(fbb_ctx* ctx, Pool& pool, int first_internal, int32_t ub, int froze
     pool.ub = ub;  // the round's bound, semantics and first internal segment travel with the pool
     pool.frozen = frozen;
     pool.first_internal = first_internal;
+    // direct placement (K2 writes the survivors to their bucket rows itself, no place
+    // kernel): single-wave pools of the v2 kernel into device buckets
+    pool.direct = 0;
+    pool.pad2 = 0;
+    pool.summary = nullptr;
+    if (ctx->direct_place && ctx->k2.variant != 0 && ctx->k2.variant < 100000 && !pool.host_dst &&
+        first_internal < pool.nseg && pool.nchunks > 0 && pool.nchunks <= ctx->k2.blocks) {
+        bool ok = true;
+        for (int s = first_internal; s < pool.nseg; ++s)
+            ok = ok && pool.seg[s].dst_base >= 0 && pool.seg[s].dst_lb == nullptr && pool.seg[s].dst.heads;
+        pool.direct = ok ? 1 : 0;
+    }
+    if (pool.direct && ctx->summary_by_place) pool.summary = ctx->h_round.as<RoundState>();
     size_t pool_bytes = offsetof(Pool, seg) + (size_t)pool.nseg * sizeof(Segment);
     std::memcpy((char*)ctx->h_rp.p + kPoolOff, &pool, pool_bytes);
     int launches = 0;
@@ -386,9 +400,10 @@ int run_pool(fbb_ctx* ctx, Pool& pool, int first_internal, int32_t ub, int froze
     // the pinned (UVA-mapped) h_round; otherwise one download of the counters (and, after
     // a leaf round, the schedule behind them)
     const bool publish = has_internal && ctx->summary_by_place;
-    CK(launch_place(ctx->dt, ctx->k2, dp, pool, rs, out, st, publish ? ctx->h_round.as<RoundState>() : nullptr),
-       "place");
-    launches += has_internal ? 2 : 0;  // K2 + place
+    if (!pool.direct)
+        CK(launch_place(ctx->dt, ctx->k2, dp, pool, rs, out, st, publish ? ctx->h_round.as<RoundState>() : nullptr),
+           "place");
+    launches += has_internal ? (pool.direct ? 1 : 2) : 0;  // K2 [+ place]
     if (!publish) {
         const size_t head = has_leaf ? offsetof(RoundState, schedule) + (size_t)n * 4
                                      : offsetof(RoundState, seg_surv) + (size_t)pool.nseg * 8;
@@ -775,6 +790,9 @@ int explorer_run_batched(fbb_ctx* ctx, const int64_t* targets, int ntargets, int
         hl->ppc_cap = ctx->k2.ppc_cap;
         hl->nrounds = R;
         hl->chunk_cap = (int32_t)std::min<int64_t>(chunks, INT32_MAX);
+        hl->direct_cap = (ctx->direct_place && ctx->k2.variant != 0 && ctx->k2.variant < 100000 &&
+                          !ctx->host_pending) ? ctx->k2.blocks : 0;
+        hl->pad3 = 0;
         for (int i = 0; i < n; ++i) hl->schedule[i] = ctx->schedule[i];
         LoopState* dl = ctx->d_loop.as<LoopState>();
         Pool* dp = ctx->d_pool.as<Pool>();
@@ -1009,6 +1027,8 @@ fbb_ctx* fbb_create(int device, const int32_t* p, int n, int m) {
     ctx->device_loop = dlp && dlp[0] == '1';
     const char* sm = getenv("FBB_SUMMARY");
     ctx->summary_by_place = !(sm && std::string(sm) == "copy");
+    const char* dir = getenv("FBB_DIRECT");
+    ctx->direct_place = !(dir && dir[0] == '0');
     const char* chk = getenv("FBB_CHECK");
     ctx->check = chk && chk[0] == '1';
     return ctx;

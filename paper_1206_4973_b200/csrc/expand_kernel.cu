@@ -566,6 +566,7 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(DevTables t, const
     // launched as a programmatic dependent of K2 (FBB_PDL=1): wait for its completion
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;");  // the device loop's close kernel
+    if (pool->direct) return;  // K2 placed the survivors itself (single-wave pool)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t nchunks = pool->nchunks;
     for (int64_t c0 = (int64_t)blockIdx.x * kPlaceChunks; c0 < nchunks;

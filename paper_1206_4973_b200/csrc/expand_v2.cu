@@ -94,7 +94,7 @@ __host__ __device__ inline V2Layout v2_layout(int n, int m, int P, int cmax, int
     L.p = o;    o = b16(o + (size_t)n * m * 4);
     L.tl = o;   o = b16(o + (size_t)n * m * 2);  // tails as int16
     L.pre = o;  o = b16(o + (size_t)L.ppc_max * v2_rw(N));
-    L.wsum = o; o = b16(o + (size_t)(threads / 32 + 2) * 8);
+    L.wsum = o; o = b16(o + (size_t)(threads / 32 + 2) * 8 + 16 * 8);  // + direct-placement sums
     L.total = o;
     return L;
 }
@@ -244,9 +244,6 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
     constexpr bool kGroupedB = OCC == 2;
     constexpr bool kDual16 = OCC == 2 && N == 20;  // Phase A: two parents per thread, 16x2
     extern __shared__ __align__(16) unsigned char smem[];
-    // programmatic dependent launch: place_kernel may be scheduled onto SMs as this grid's
-    // CTAs retire (it waits for the grid's completion before reading anything)
-    asm volatile("griddepcontrol.launch_dependents;");
     const int n = t.n, W = t.W;
     const V2Layout L = v2_layout(n, M, P, cmax, blockDim.x, N, OCC);
     uint64_t* s_um = (uint64_t*)(smem + L.um);  // unscheduled jobs of each parent
@@ -297,6 +294,12 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
     // the round's bound, semantics and first internal segment come from the pool
     // (written by the host, or by the device-side planner of the batched explorer loop)
     asm volatile("griddepcontrol.wait;" ::: "memory");  // the pool upload kernel (PDL)
+    // programmatic dependent launch: place_kernel may be scheduled onto SMs as this grid's
+    // CTAs retire (it waits for the grid's completion before reading anything) -- except
+    // under direct placement, where the dependents may not take SM room before every CTA
+    // of this grid is resident (its CTAs wait for each other)
+    const bool direct = pool->direct != 0;
+    if (!direct) asm volatile("griddepcontrol.launch_dependents;");
     k2_stamp_begin(rs);
     ub = pool->ub;
     frozen = pool->frozen;
@@ -356,7 +359,10 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
         }
         if (tid < np_ && !cpt_) pf_mask = g_.src.masks[(g_.first + g_.step * (p0_ + tid)) * W];
     };
-    int64_t chunk = claim_chunk(rs, c_begin, s_slot);
+    // direct placement: CTA i owns chunk c_begin + i (fixed-grid launches may have more
+    // CTAs than chunks; those have nothing to do)
+    int64_t chunk = direct ? c_begin + blockIdx.x : claim_chunk(rs, c_begin, s_slot);
+    if (direct && chunk >= c_end) return;
     if constexpr (kPipe) prefetch(chunk);
     while (chunk < c_end) {
         int s, depth, np;
@@ -399,7 +405,8 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
             }
         }
         __syncthreads();
-        if (kPipe && tid == 0) *s_slot = c_begin + (int64_t)atomicAdd(&rs->ticket, 1u);  // next chunk
+        if (kPipe && tid == 0)  // next chunk
+            *s_slot = direct ? c_end : c_begin + (int64_t)atomicAdd(&rs->ticket, 1u);
         if (compact) {  // heads and scheduled set folded from the staged prefixes
             if (tid < np) {
                 const uint8_t* pre = s_pre + tid * RW;
@@ -617,6 +624,22 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
             out.count[chunk] = tot;
             out.seg[chunk] = s;
         }
+        if (direct) {
+            // every chunk's count in (grid-wide), then this chunk's survivors straight to
+            // their bucket rows: segment base + survivors of the segment's earlier chunks
+            direct_arrive(rs, s, tot, c_end - c_begin);
+            asm volatile("griddepcontrol.launch_dependents;");
+            const int64_t before = direct_prefix(out.count, sg.chunk_base, chunk, (int64_t*)(s_wsum + 8));
+            if (keep) {
+                const int64_t o = sg.dst_base + before + woff + __popc(ballot & ((1u << lane) - 1u));
+                const NodeStore dst = sg.dst;
+                store_heads<M>(dst.heads + o * M, myR);
+                const uint64_t valid = n >= 64 ? ~0ull : ((1ull << n) - 1ull);
+                dst.masks[o * W] = (~s_um[mypp] & valid) | (1ull << myx);
+                store_prefix(dst.prefix + o * n, s_pre + mypp * RW, depth, myx, n);
+            }
+            break;  // one chunk per CTA
+        }
         if (keep) {
             const int64_t o = chunk * (int64_t)cmax + woff + __popc(ballot & ((1u << lane) - 1u));
             const NodeStore dst = out.nodes;
@@ -634,6 +657,7 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
         }
     }
     k2_stamp_end(rs);
+    if (direct) direct_finish(pool, rs, n, c_end - c_begin);
 }
 
 template <int N, int M, int OCC>

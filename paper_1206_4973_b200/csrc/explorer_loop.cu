@@ -42,6 +42,7 @@ __global__ void loop_plan_kernel(DevTables t, LoopState* ls, Pool* pool, RoundSt
     rs->ticket = 0u;
     rs->total = 0;
     rs->place_done = 0u;
+    rs->arrived = 0u;
     rs->k2_t0_inv = 0ull;
     rs->k2_t1 = 0ull;
     pool->ub = ls->incumbent;
@@ -118,6 +119,10 @@ __global__ void loop_plan_kernel(DevTables t, LoopState* ls, Pool* pool, RoundSt
     pool->nchildren = child;
     pool->pad = 0;
     pool->host_dst = 0;
+    // single-wave pools: K2 places the survivors itself (capi.cu run_pool, same rule)
+    pool->direct = (ls->direct_cap > 0 && chunk > 0 && chunk <= ls->direct_cap) ? 1 : 0;
+    pool->pad2 = 0;
+    pool->summary = nullptr;
     pool->nseg = nseg;
 }
 

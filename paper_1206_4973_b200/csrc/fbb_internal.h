@@ -162,6 +162,8 @@ struct Segment {
     int32_t* dst_lb;     // optional survivor bounds
 };
 
+struct RoundState;
+
 struct Pool {
     int nseg;
     int pad;             // always 0 (an opaque zero for the kernels)
@@ -171,6 +173,12 @@ struct Pool {
     int32_t frozen;      // resolve (1) or solve (0) semantics
     int32_t first_internal;  // first segment with internal children (nseg: none)
     int32_t host_dst;    // survivors go to pinned host buckets (place: contiguous 16-byte stores)
+    // direct placement (single-wave pools): K2 CTA i owns chunk first + i, all CTAs are
+    // co-resident, and after a grid-wide arrival count each writes its survivors straight
+    // to their batch-ordered bucket rows -- no staging, no place kernel
+    int32_t direct;
+    int32_t pad2;
+    RoundState* summary; // direct: the mapped host RoundState K2's CTA 0 publishes into (or null)
     Segment seg[kMaxSegments];
 };
 
@@ -204,7 +212,7 @@ struct RoundState {
     uint32_t ticket;              // next chunk to claim
     int64_t total;                // survivors of the pool
     uint32_t place_done;          // place CTAs past their counting (the last one publishes)
-    uint32_t pad;
+    uint32_t arrived;             // direct placement: K2 CTAs past their counts (grid barrier)
     unsigned long long k2_t0_inv; // ~(first K2 CTA start), %globaltimer ns (0 = none)
     unsigned long long k2_t1;     // last K2 CTA end, %globaltimer ns
     int64_t seg_surv[kMaxSegments];
@@ -269,6 +277,7 @@ struct LoopState {
     int32_t need_depth;               // stop == 3: the bucket that must grow ...
     int64_t need_rows;                // ... to at least this many rows
     int32_t cmax, ppc_cap, nrounds, chunk_cap;  // chunk_cap: staging chunks available
+    int32_t direct_cap, pad3;         // > 0: pools of at most this many chunks use direct placement
     int32_t schedule[kMaxJobs];       // incumbent schedule (solve mode)
     LoopRecord rec[kLoopMax];
 };

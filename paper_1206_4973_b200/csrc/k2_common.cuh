@@ -103,6 +103,64 @@ __device__ __forceinline__ void store_prefix(uint8_t* dp, const uint8_t* sp, int
     }
 }
 
+// Direct placement (Pool::direct): the grid-wide arrival of every chunk's counts.  Thread
+// 0 of each CTA adds its chunk's survivors to the segment / pool totals, releases them
+// (gpu-scope fence) and counts itself in; then waits until all `nchunks` chunks are in.
+// Every CTA of the grid is resident (the host enables the mode only for single-wave pools,
+// and K2 triggers its programmatic dependents only after this barrier), so the spin ends.
+__device__ __forceinline__ void direct_arrive(RoundState* rs, int s, int tot, int64_t nchunks) {
+    if (threadIdx.x == 0) {
+        if (tot) {
+            atomicAdd((unsigned long long*)&rs->seg_surv[s], (unsigned long long)tot);
+            atomicAdd((unsigned long long*)&rs->total, (unsigned long long)tot);
+        }
+        __threadfence();
+        atomicAdd(&rs->arrived, 1u);
+        uint32_t v;
+        for (;;) {
+            asm volatile("ld.acquire.gpu.u32 %0, [%1];" : "=r"(v) : "l"(&rs->arrived) : "memory");
+            if ((int64_t)v >= nchunks) break;
+            __nanosleep(64);
+        }
+    }
+    __syncthreads();
+}
+
+// Survivors of chunks [lo, hi) (their counts are final after direct_arrive): a block-wide
+// sum of L2 reads; every thread gets the result.
+__device__ __forceinline__ int64_t direct_prefix(const int32_t* count, int64_t lo, int64_t hi,
+                                                 int64_t* s_red) {
+    int64_t v = 0;
+    for (int64_t c = lo + threadIdx.x; c < hi; c += blockDim.x) v += __ldcg(count + c);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    int64_t t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s_red[w];
+    return t;
+}
+
+// Direct placement, at the end of a CTA's chunk (after its K2 end stamp): the last CTA
+// publishes the round summary into the mapped host RoundState, as place_kernel's last CTA
+// does in the staged form.
+__device__ __forceinline__ void direct_finish(const Pool* pool, RoundState* rs, int n, int64_t nchunks) {
+    __shared__ int s_last;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = (int64_t)atomicAdd(&rs->place_done, 1u) == nchunks - 1;
+    }
+    __syncthreads();
+    RoundState* summary = pool->summary;
+    if (!s_last || summary == nullptr) return;
+    __threadfence();
+    const int words = (int)((offsetof(RoundState, seg_surv) + (size_t)pool->nseg * 8) / 8);
+    const unsigned long long* src = reinterpret_cast<const unsigned long long*>(rs);
+    unsigned long long* dst = reinterpret_cast<unsigned long long*>(summary);
+    for (int i = threadIdx.x; i < words; i += blockDim.x) dst[i] = __ldcg(src + i);
+    for (int i = threadIdx.x; i < n; i += blockDim.x) summary->schedule[i] = __ldcg(rs->schedule + i);
+}
+
 __device__ __forceinline__ void leaf_offer(RoundState* rs, int32_t value, int64_t pos) {
     // min over (value, position) == max over its complement; 0 means "none yet"
     unsigned long long key = ((unsigned long long)(uint32_t)value << 32) | (uint32_t)pos;

@@ -532,3 +532,26 @@ def test_tuner_schedule_replays_on_the_reference():
     assert rounds == [tuple(x) for x in gold]
     assert res["bounded"] == total
     ctx.close()
+
+
+@pytest.mark.parametrize("device_loop", ["0", "1"])
+def test_direct_placement_matches_staged(device_loop, monkeypatch):
+    """Single-wave pools: K2 writes its survivors straight to the bucket rows after a
+    grid-wide count (Pool::direct) instead of staging them for place_kernel.  Same rounds
+    and the same pending tree as the staged path, at pool sizes on both sides of the
+    one-wave limit, in solve mode (leaf rounds, mid-batch incumbent) and frozen mode."""
+    monkeypatch.setenv("FBB_DEVICE_LOOP", device_loop)
+    inst = fbb.generate_instance(20, 20, 479340445)
+    out = {}
+    for direct in ("0", "1"):
+        monkeypatch.setenv("FBB_DIRECT", direct)
+        ctx = fbb.Context(inst)
+        res = []
+        for targets in ([512], [4096], [16384, 40000, 4096], [100000]):
+            ctx.explorer_reset(fbb.NodeBatch.root(inst), 2297, frozen=True)
+            res.append((ctx.explorer_run(targets, 40), ctx.explorer_pending()))
+        r0 = ctx.explorer_start_solve(None)
+        res.append(([r0] + ctx.explorer_run([2048], 60), ctx.explorer_state()["schedule"]))
+        out[direct] = res
+        ctx.close()
+    assert out["0"] == out["1"]
