@@ -800,17 +800,17 @@ int explorer_run_batched(fbb_ctx* ctx, const int64_t* targets, int ntargets, int
         ChunkOut out{ctx->staging.view(), ctx->st_lb.as<int32_t>(), ctx->st_count.as<int32_t>(),
                      ctx->st_seg.as<int32_t>()};
         const auto w0 = std::chrono::steady_clock::now();
-        // the batch: state upload, R x (plan, leaves, leaf schedule, K2, place, close), state
+        // the batch: state upload, R x (step, leaves, leaf schedule, K2, place), step, state
         // download -- every kernel a programmatic dependent of the one before, the whole
         // sequence one CUDA graph (captured once per batch length and staging buffers, then
         // replayed: one host call per batch)
         auto enqueue = [&](bool pdl) -> cudaError_t {
             cudaError_t e = cudaMemcpyAsync(dl, hl, offsetof(LoopState, rec), cudaMemcpyHostToDevice, st);
             for (int i = 0; i < R && e == cudaSuccess; ++i) {
-                if ((e = launch_loop_plan(ctx->dt, dl, dp, rs, i, st, pdl && i > 0)) != cudaSuccess) break;
-                if ((e = launch_round_device(ctx->dt, ctx->k2, dp, rs, out, st, pdl)) != cudaSuccess) break;
-                e = launch_loop_close(ctx->dt, dl, dp, rs, i, st, pdl);
+                if ((e = launch_loop_step(ctx->dt, dl, dp, rs, i, false, st, pdl && i > 0)) != cudaSuccess) break;
+                e = launch_round_device(ctx->dt, ctx->k2, dp, rs, out, st, pdl);
             }
+            if (e == cudaSuccess) e = launch_loop_step(ctx->dt, dl, dp, rs, R, true, st, pdl);
             if (e == cudaSuccess) e = cudaMemcpyAsync(hl, dl, sizeof(LoopState), cudaMemcpyDeviceToHost, st);
             return e;
         };
@@ -865,7 +865,7 @@ int explorer_run_batched(fbb_ctx* ctx, const int64_t* targets, int ntargets, int
             rec.round_ms = (float)((double)(t_next - lr.t0) * 1e-6);
             rec.k2_ms = lr.k2_t0 && lr.k2_t1 > lr.k2_t0 ? (float)((double)(lr.k2_t1 - lr.k2_t0) * 1e-6) : 0.f;
             rec.place_ms = -1.f;
-            rec.launches = 6;
+            rec.launches = 5;
             rec.host_ms = wall_ms / valid;
             rec.sync_ms = sync_ms / valid;
             rec.h2d_bytes = ctx->host_pending ? lr.branched * nb : 0;

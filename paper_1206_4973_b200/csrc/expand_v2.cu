@@ -665,8 +665,13 @@ cudaError_t v2_setup(const DevTables& t, K2Config& c, int device) {
     int optin = 0, sms = 148, per_sm = 1;
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    cudaError_t e = cudaFuncSetAttribute(k2_v2_kernel<N, M, OCC>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+    // dynamic + static shared memory must fit the opt-in limit (direct placement keeps a
+    // few bytes of static shared memory)
+    cudaFuncAttributes fa;
+    cudaError_t e = cudaFuncGetAttributes(&fa, k2_v2_kernel<N, M, OCC>);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(k2_v2_kernel<N, M, OCC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             optin - (int)fa.sharedSizeBytes);
     if (e != cudaSuccess) return e;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_v2_kernel<N, M, OCC>, c.threads, c.smem);
     c.blocks = sms * (per_sm < 1 ? 1 : per_sm);

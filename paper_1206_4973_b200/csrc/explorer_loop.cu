@@ -1,13 +1,14 @@
 // explorer_loop.cu -- the explorer round planned and closed on the device, so that a
 // batch of rounds runs back to back without the host (fbb_explorer_run).
 //
-//   plan  (1 thread)   fill_buffer (search.hpp:64-73) on the bucket sizes: pop the
+//   step  (1 warp)     closes the previous round, then plans this one:
+//   plan               fill_buffer (search.hpp:64-73) on the bucket sizes: pop the
 //                      deepest bucket tops, LIFO, until the children reach the target;
 //                      lay out segments and chunks exactly as the host planner does
 //                      (capi.cu layout_pool); point each segment at its source and
 //                      destination buckets; reset the round state.
 //   round              leaves, leaf schedule, K2, place (expand_kernel.cu)
-//   close (1 thread)   integrate / frozen prune bookkeeping (search.hpp:84-107,
+//   close              integrate / frozen prune bookkeeping (search.hpp:84-107,
 //                      bench.hpp:96-106): bucket sizes, incumbent and schedule, the
 //                      round's counters, stop conditions (empty tree, node budget).
 // A round whose destination bucket is too small is not started: the batch stops with
@@ -25,13 +26,9 @@ __device__ __forceinline__ unsigned long long loop_ns() {
     return t;
 }
 
-__global__ void loop_plan_kernel(DevTables t, LoopState* ls, Pool* pool, RoundState* rs, int round) {
-    // a programmatic dependent of the previous round's close kernel (or of the batch's
-    // state upload): wait for it before reading the loop state, then let the leaf kernel
-    // be scheduled
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    asm volatile("griddepcontrol.launch_dependents;");
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+// plan of round `round` (thread 0; cnt = the block's shared copy of the bucket sizes)
+__device__ void plan_round(const DevTables& t, LoopState* ls, Pool* pool, RoundState* rs, int round,
+                           const int64_t* cnt) {
     if (round < kLoopMax) ls->rec[round].t0 = loop_ns();
     const int n = t.n;
     pool->nseg = 0;
@@ -54,7 +51,7 @@ __global__ void loop_plan_kernel(DevTables t, LoopState* ls, Pool* pool, RoundSt
     int64_t have = 0;
     int nseg = 0;
     for (int d = n; d >= 0 && have < target; --d) {
-        const int64_t c = ls->cnt[d];
+        const int64_t c = cnt[d];
         if (c == 0) continue;
         const int r = n - d;
         const int64_t k = min(c, (target - have + r - 1) / r);
@@ -81,7 +78,7 @@ __global__ void loop_plan_kernel(DevTables t, LoopState* ls, Pool* pool, RoundSt
             sg.dst_base = 0;
             continue;
         }
-        int64_t after = ls->cnt[d + 1];
+        int64_t after = cnt[d + 1];
         for (int s2 = 0; s2 < s; ++s2)
             if (pool->seg[s2].depth == d + 1) after -= pool->seg[s2].count;
         const int64_t worst = after + sg.count * (n - d);
@@ -126,11 +123,9 @@ __global__ void loop_plan_kernel(DevTables t, LoopState* ls, Pool* pool, RoundSt
     pool->nseg = nseg;
 }
 
-__global__ void loop_close_kernel(DevTables t, LoopState* ls, const Pool* pool, const RoundState* rs,
-                                  int round) {
-    asm volatile("griddepcontrol.wait;" ::: "memory");  // the round's place kernel
-    asm volatile("griddepcontrol.launch_dependents;");
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+// integrate bookkeeping of round `round` (thread 0; updates the shared bucket sizes)
+__device__ void close_round(const DevTables& t, LoopState* ls, const Pool* pool, const RoundState* rs,
+                            int round, int64_t* cnt) {
     const int n = t.n;
     LoopRecord& rec = ls->rec[round];
     rec.valid = 0;
@@ -146,13 +141,13 @@ __global__ void loop_close_kernel(DevTables t, LoopState* ls, const Pool* pool, 
         const Segment& sg = pool->seg[s];
         const int64_t kids = sg.count * (n - sg.depth);
         branched += sg.count;
-        ls->cnt[sg.depth] -= sg.count;  // pops (the bucket tops)
+        cnt[sg.depth] -= sg.count;  // pops (the bucket tops)
         if (sg.depth >= n - 2) leaves += kids;
         else internal += kids;
     }
     for (int s = 0; s < pool->nseg; ++s) {  // pushes, batch order
         const Segment& sg = pool->seg[s];
-        if (sg.depth < n - 2) ls->cnt[sg.depth + 1] += rs->seg_surv[s];
+        if (sg.depth < n - 2) cnt[sg.depth + 1] += rs->seg_surv[s];
     }
     if (leaves > 0 && rs->leaf_inv != 0ull) {
         const int32_t v = (int32_t)((~rs->leaf_inv) >> 32);
@@ -170,7 +165,7 @@ __global__ void loop_close_kernel(DevTables t, LoopState* ls, const Pool* pool, 
         }
     }
     int64_t pending = 0;
-    for (int d = 0; d <= n; ++d) pending += ls->cnt[d];
+    for (int d = 0; d <= n; ++d) pending += cnt[d];
     rec.target = ls->targets[round];
     rec.branched = branched;
     rec.bounded = internal + leaves;
@@ -186,16 +181,36 @@ __global__ void loop_close_kernel(DevTables t, LoopState* ls, const Pool* pool, 
     rec.t1 = loop_ns();
 }
 
-}  // namespace
 
-cudaError_t launch_loop_plan(const DevTables& t, LoopState* ls, Pool* pool, RoundState* rs, int round,
-                             cudaStream_t stream, bool pdl) {
-    return launch_pdl(loop_plan_kernel, dim3(1), dim3(32), 0, stream, pdl, t, ls, pool, rs, round);
+// One kernel between two rounds of a batch: the integrate bookkeeping of round - 1 and the
+// plan of round (either may be absent: round 0 has nothing to close, round == nrounds
+// nothing to plan).  One warp: the bucket sizes move to shared memory with parallel
+// loads, thread 0 runs the sequential parts over that copy, the warp writes it back.
+__global__ void loop_step_kernel(DevTables t, LoopState* ls, Pool* pool, RoundState* rs, int round,
+                                 int last) {
+    // a programmatic dependent of the previous round's place kernel (or of the batch's
+    // state upload): wait for it before reading anything, then let the leaf kernel be
+    // scheduled
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;");
+    __shared__ int64_t s_cnt[kMaxJobs + 1];
+    const int n = t.n, lane = threadIdx.x;
+    for (int d = lane; d <= n; d += 32) s_cnt[d] = ls->cnt[d];
+    __syncwarp();
+    if (lane == 0) {
+        if (round > 0) close_round(t, ls, pool, rs, round - 1, s_cnt);
+        if (!last) plan_round(t, ls, pool, rs, round, s_cnt);
+    }
+    __syncwarp();
+    for (int d = lane; d <= n; d += 32) ls->cnt[d] = s_cnt[d];
 }
 
-cudaError_t launch_loop_close(const DevTables& t, LoopState* ls, const Pool* pool, const RoundState* rs,
-                              int round, cudaStream_t stream, bool pdl) {
-    return launch_pdl(loop_close_kernel, dim3(1), dim3(32), 0, stream, pdl, t, ls, pool, rs, round);
+}  // namespace
+
+cudaError_t launch_loop_step(const DevTables& t, LoopState* ls, Pool* pool, RoundState* rs, int round,
+                             bool last, cudaStream_t stream, bool pdl) {
+    return launch_pdl(loop_step_kernel, dim3(1), dim3(32), 0, stream, pdl, t, ls, pool, rs, round,
+                      last ? 1 : 0);
 }
 
 }  // namespace fbb

@@ -284,10 +284,9 @@ struct LoopState {
 
 // pdl: each kernel of the batch is a programmatic dependent of the one before (every one
 // of them waits -- griddepcontrol.wait -- before it reads its predecessor's output)
-cudaError_t launch_loop_plan(const DevTables& t, LoopState* ls, Pool* pool, RoundState* rs, int round,
-                             cudaStream_t stream, bool pdl);
-cudaError_t launch_loop_close(const DevTables& t, LoopState* ls, const Pool* pool, const RoundState* rs,
-                              int round, cudaStream_t stream, bool pdl);
+// close of round - 1 (round > 0) + plan of round (!last), one single-warp kernel
+cudaError_t launch_loop_step(const DevTables& t, LoopState* ls, Pool* pool, RoundState* rs, int round,
+                             bool last, cudaStream_t stream, bool pdl);
 cudaError_t launch_round_device(const DevTables& t, const K2Config& cfg, const Pool* d_pool,
                                 RoundState* rs, ChunkOut out, cudaStream_t stream, bool pdl);
 

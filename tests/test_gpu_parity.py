@@ -555,3 +555,16 @@ def test_direct_placement_matches_staged(device_loop, monkeypatch):
         out[direct] = res
         ctx.close()
     assert out["0"] == out["1"]
+
+
+def test_kernel_variants_selected():
+    """The specialised kernels are the ones that run on the benchmark instances (a failed
+    kernel configuration would otherwise fall back to the generic kernels silently)."""
+    want = {(20, 20, 479340445): ("k1v3_kernel", "k2_v2_kernel<20,20,2>"),
+            (20, 5, 873654221): ("K1=", "k2_v2_kernel<20,5,3>"),
+            (50, 20, 1539989115): ("k1v3_kernel", "k2_v2_kernel<64,20,2>"),
+            (100, 20, 450926852): ("k1v3_kernel", "k2_v3_kernel<4,20>"),
+            (200, 20, 2013025619): ("k1v3_kernel", "k2_v3_kernel<8,20>")}
+    for (n, m, seed), (k1, k2) in want.items():
+        ks = fbb.Context(fbb.generate_instance(n, m, seed)).kernels()
+        assert k1 in ks and k2 in ks, ks
