@@ -733,7 +733,7 @@ int explorer_round(fbb_ctx* ctx, int64_t target, fbb_round_t* rec) {
 // explorer_round.  Used when the parents can be read in place (HBM buckets, or host
 // buckets read and written through the mapping).
 bool device_loop_ok(const fbb_ctx* ctx) {
-    return ctx->device_loop && (!ctx->host_pending || (ctx->mapped_in && ctx->mapped_out && !ctx->compact_rows));
+    return ctx->device_loop && (!ctx->host_pending || (ctx->mapped_in && ctx->mapped_out));
 }
 
 int explorer_run_batched(fbb_ctx* ctx, const int64_t* targets, int ntargets, int64_t max_rounds,
@@ -792,7 +792,7 @@ int explorer_run_batched(fbb_ctx* ctx, const int64_t* targets, int ntargets, int
         hl->chunk_cap = (int32_t)std::min<int64_t>(chunks, INT32_MAX);
         hl->direct_cap = (ctx->direct_place && ctx->k2.variant != 0 && ctx->k2.variant < 100000 &&
                           !ctx->host_pending) ? ctx->k2.blocks : 0;
-        hl->pad3 = 0;
+        hl->host_dst = ctx->host_pending ? 1 : 0;  // survivors written over the host link
         for (int i = 0; i < n; ++i) hl->schedule[i] = ctx->schedule[i];
         LoopState* dl = ctx->d_loop.as<LoopState>();
         Pool* dp = ctx->d_pool.as<Pool>();
@@ -846,7 +846,7 @@ int explorer_run_batched(fbb_ctx* ctx, const int64_t* targets, int ntargets, int
         if (hl->stop == 5) return ctx->fail(FBB_E_STATE, "device loop: staging smaller than a planned pool");
         int valid = 0;
         while (valid < R && hl->rec[valid].valid) ++valid;
-        const int64_t nb = (int64_t)node_bytes(ctx);
+        const int64_t nb = (int64_t)row_bytes(ctx, ctx->host_pending && ctx->compact_rows);
         for (int i = 0; i < valid; ++i) {
             const LoopRecord& lr = hl->rec[i];
             fbb_round_t rec;
@@ -868,7 +868,7 @@ int explorer_run_batched(fbb_ctx* ctx, const int64_t* targets, int ntargets, int
             rec.launches = 5;
             rec.host_ms = wall_ms / valid;
             rec.sync_ms = sync_ms / valid;
-            rec.h2d_bytes = ctx->host_pending ? lr.branched * nb : 0;
+            rec.h2d_bytes = ctx->host_pending ? lr.branched * nb : 0;  // rows of the host tree
             rec.d2h_bytes = ctx->host_pending ? lr.inserted * nb : 0;
             ctx->tot_branched += lr.branched;
             ctx->tot_bounded += lr.bounded;

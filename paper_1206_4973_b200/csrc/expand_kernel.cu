@@ -777,7 +777,8 @@ cudaError_t launch_k2_internal(const DevTables& t, const K2Config& cfg, const Po
     if (cfg.variant >= 100000)
         return launch_k2_v3(t, cfg, d_pool, first_seg, blocks, ub, frozen, rs, out, stream, pdl);
     if (cfg.variant != 0)
-        return launch_k2_v2(t, cfg, d_pool, first_seg, blocks, ub, frozen, rs, out, stream, pdl);
+        return launch_k2_v2(t, cfg, d_pool, first_seg, blocks, h_pool.direct ? 1 : 0, frozen, rs, out, stream,
+                            pdl);
     return launch_pdl(cfg.wide ? k2_internal_kernel<false, true>
                                : (cfg.jm_in_smem ? k2_internal_kernel<true, false> : k2_internal_kernel<false, false>),
                       dim3(blocks),
@@ -849,7 +850,7 @@ cudaError_t launch_round_device(const DevTables& t, const K2Config& cfg, const P
     if (cfg.variant >= 100000)
         e = launch_k2_v3(t, cfg, d_pool, 0, cfg.blocks, 0, 0, rs, out, stream, pdl);
     else if (cfg.variant != 0)
-        e = launch_k2_v2(t, cfg, d_pool, 0, cfg.blocks, 0, 0, rs, out, stream, pdl);
+        e = launch_k2_v2(t, cfg, d_pool, 0, cfg.blocks, -1, 0, rs, out, stream, pdl);
     else
         e = launch_pdl(cfg.wide ? k2_internal_kernel<false, true>
                                 : (cfg.jm_in_smem ? k2_internal_kernel<true, false> : k2_internal_kernel<false, false>),

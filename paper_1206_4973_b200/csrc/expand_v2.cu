@@ -236,7 +236,7 @@ __device__ __forceinline__ void scan_pair16(uint32_t row_sa, uint32_t s0, uint32
 // OCC = target CTAs per SM: 2 -> up to 168 registers, 3 -> 112 (smaller chunks too)
 template <int N, int M, int OCC>
 __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool* __restrict__ pool,
-                                                   int first_seg, int cmax, int32_t ub, int frozen,
+                                                   int first_seg, int cmax, int place_hint, int frozen,
                                                    RoundState* rs, ChunkOut out) {
     constexpr int P = M * (M - 1) / 2;
     // Phase B: the 16x2 grouped form at 2 CTAs/SM (168 registers); at 3 CTAs/SM (96
@@ -244,6 +244,12 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
     constexpr bool kGroupedB = OCC == 2;
     constexpr bool kDual16 = OCC == 2 && N == 20;  // Phase A: two parents per thread, 16x2
     extern __shared__ __align__(16) unsigned char smem[];
+    // place_hint: 0 staged placement (known to the host), 1 direct, -1 read Pool::direct
+    // (device-planned loop).  Staged: place_kernel may be scheduled onto SMs as this
+    // grid's CTAs retire (programmatic dependent launch; it waits for the grid's
+    // completion before reading anything).  Direct: the dependents may not take SM room
+    // before every CTA of this grid is resident (its CTAs wait for each other).
+    if (place_hint == 0) asm volatile("griddepcontrol.launch_dependents;");
     const int n = t.n, W = t.W;
     const V2Layout L = v2_layout(n, M, P, cmax, blockDim.x, N, OCC);
     uint64_t* s_um = (uint64_t*)(smem + L.um);  // unscheduled jobs of each parent
@@ -294,14 +300,10 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
     // the round's bound, semantics and first internal segment come from the pool
     // (written by the host, or by the device-side planner of the batched explorer loop)
     asm volatile("griddepcontrol.wait;" ::: "memory");  // the pool upload kernel (PDL)
-    // programmatic dependent launch: place_kernel may be scheduled onto SMs as this grid's
-    // CTAs retire (it waits for the grid's completion before reading anything) -- except
-    // under direct placement, where the dependents may not take SM room before every CTA
-    // of this grid is resident (its CTAs wait for each other)
-    const bool direct = pool->direct != 0;
-    if (!direct) asm volatile("griddepcontrol.launch_dependents;");
+    const bool direct = place_hint < 0 ? pool->direct != 0 : place_hint == 1;
+    if (place_hint < 0 && !direct) asm volatile("griddepcontrol.launch_dependents;");
     k2_stamp_begin(rs);
-    ub = pool->ub;
+    const int32_t ub = pool->ub;
     frozen = pool->frozen;
     first_seg = pool->first_internal;
     if (first_seg >= pool->nseg) return;
@@ -736,12 +738,12 @@ bool k2_v2_config(const DevTables& t, int device, K2Config* out) {
 }
 
 cudaError_t launch_k2_v2(const DevTables& t, const K2Config& cfg, const Pool* d_pool, int first_seg,
-                         int blocks, int32_t ub, int frozen, RoundState* rs, ChunkOut out,
+                         int blocks, int place_hint, int frozen, RoundState* rs, ChunkOut out,
                          cudaStream_t stream, bool pdl) {
 #define V2_CASE(NN, MM, OO)                                                                   \
     case OO * 10000 + NN * 100 + MM:                                                          \
         return launch_pdl(k2_v2_kernel<NN, MM, OO>, dim3(blocks), dim3(cfg.threads), cfg.smem, stream, pdl, \
-                          t, d_pool, first_seg, cfg.cmax, ub, frozen, rs, out);
+                          t, d_pool, first_seg, cfg.cmax, place_hint, frozen, rs, out);
     switch (cfg.variant) {
         V2_CASE(20, 5, 2)
         V2_CASE(20, 10, 2)

@@ -115,7 +115,7 @@ __device__ void plan_round(const DevTables& t, LoopState* ls, Pool* pool, RoundS
     pool->nchunks = chunk;
     pool->nchildren = child;
     pool->pad = 0;
-    pool->host_dst = 0;
+    pool->host_dst = ls->host_dst;
     // single-wave pools: K2 places the survivors itself (capi.cu run_pool, same rule)
     pool->direct = (ls->direct_cap > 0 && chunk > 0 && chunk <= ls->direct_cap) ? 1 : 0;
     pool->pad2 = 0;

@@ -222,8 +222,10 @@ constexpr size_t kRoundStateHead = offsetof(RoundState, schedule);
 
 // n <= 32, m in {5,10,20}: the register/shared-row kernel; false when not applicable.
 bool k2_v2_config(const DevTables& t, int device, K2Config* out);
+// place_hint: 0 staged placement, 1 direct (Pool::direct, known to the host), -1 read it
+// from the pool (device-planned loop)
 cudaError_t launch_k2_v2(const DevTables& t, const K2Config& cfg, const Pool* d_pool, int first_seg,
-                         int blocks, int32_t ub, int frozen, RoundState* rs, ChunkOut out,
+                         int blocks, int place_hint, int frozen, RoundState* rs, ChunkOut out,
                          cudaStream_t stream, bool pdl = false);
 
 // 64 < n <= 256, m in {5,10,20}: rows through L1, RMW scans; false when not applicable.
@@ -277,7 +279,8 @@ struct LoopState {
     int32_t need_depth;               // stop == 3: the bucket that must grow ...
     int64_t need_rows;                // ... to at least this many rows
     int32_t cmax, ppc_cap, nrounds, chunk_cap;  // chunk_cap: staging chunks available
-    int32_t direct_cap, pad3;         // > 0: pools of at most this many chunks use direct placement
+    int32_t direct_cap;               // > 0: pools of at most this many chunks use direct placement
+    int32_t host_dst;                 // the buckets are pinned host memory (Pool::host_dst)
     int32_t schedule[kMaxJobs];       // incumbent schedule (solve mode)
     LoopRecord rec[kLoopMax];
 };

@@ -443,13 +443,14 @@ def test_host_tree_row_formats_match_hbm(nm_sel, monkeypatch):
     assert out["host"] == out["hbm"] and out["host_full"] == out["hbm"]
 
 
-@pytest.mark.parametrize("on_host", [False, True], ids=["pending_hbm", "pending_host"])
-def test_device_planned_loop_matches_reference(instances, traces, on_host, monkeypatch):
-    """The batched, device-planned explorer loop (FBB_DEVICE_LOOP=1) reproduces the
-    reference's per-round traces like the host-planned one (host-resident: full rows,
-    the form the device loop reads)."""
+@pytest.mark.parametrize("on_host,rows", [(False, "full"), (True, "full"), (True, "compact")],
+                         ids=["pending_hbm", "pending_host_full", "pending_host_compact"])
+def test_device_planned_loop_matches_reference(instances, traces, on_host, rows, monkeypatch):
+    """The batched, device-planned explorer loop (FBB_DEVICE_LOOP=1, one CUDA graph per
+    batch) reproduces the reference's per-round traces like the host-planned one, with the
+    tree in HBM or in pinned host memory (full rows, or prefix-only rows)."""
     monkeypatch.setenv("FBB_DEVICE_LOOP", "1")
-    monkeypatch.setenv("FBB_HOST_ROWS", "full")
+    monkeypatch.setenv("FBB_HOST_ROWS", rows)
     for tr in traces["resolve"][:4]:
         inst = inst_of(instance_p(instances, tr["instance"]))
         ctx = fbb.Context(inst)  # a fresh context picks up the environment
