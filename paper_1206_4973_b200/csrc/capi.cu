@@ -383,8 +383,7 @@ int run_pool(fbb_ctx* ctx, Pool& pool, int first_internal, int32_t ub, int froze
         // leaves, then the best leaf's schedule -- before K2 recycles the leaf
         // parents' slots (bucket n-2 receives the next segment's survivors)
         CK(launch_k2_leaves(ctx->dt, dp, pool, 0, rs, st, kernel_upload), "K2 leaves");
-        CK(launch_leaf_schedule(ctx->dt, dp, rs, ub, st, kernel_upload), "leaf schedule");
-        launches += 2;
+        launches += 1;  // its last CTA writes the best leaf's schedule
     }
     if (!pdl) CK(cudaEventRecord(ctx->ev[1], st), "event");
     bool has_internal = first_internal < pool.nseg && pool.nchunks > 0;
@@ -793,6 +792,8 @@ int explorer_run_batched(fbb_ctx* ctx, const int64_t* targets, int ntargets, int
         hl->direct_cap = (ctx->direct_place && ctx->k2.variant != 0 && ctx->k2.variant < 100000 &&
                           !ctx->host_pending) ? ctx->k2.blocks : 0;
         hl->host_dst = ctx->host_pending ? 1 : 0;  // survivors written over the host link
+        // every pool of the batch fits one wave (worst-case chunk count): K2 places them all
+        const bool all_direct = hl->direct_cap > 0 && chunks <= hl->direct_cap;
         for (int i = 0; i < n; ++i) hl->schedule[i] = ctx->schedule[i];
         LoopState* dl = ctx->d_loop.as<LoopState>();
         Pool* dp = ctx->d_pool.as<Pool>();
@@ -808,7 +809,7 @@ int explorer_run_batched(fbb_ctx* ctx, const int64_t* targets, int ntargets, int
             cudaError_t e = cudaMemcpyAsync(dl, hl, offsetof(LoopState, rec), cudaMemcpyHostToDevice, st);
             for (int i = 0; i < R && e == cudaSuccess; ++i) {
                 if ((e = launch_loop_step(ctx->dt, dl, dp, rs, i, false, st, pdl && i > 0)) != cudaSuccess) break;
-                e = launch_round_device(ctx->dt, ctx->k2, dp, rs, out, st, pdl);
+                e = launch_round_device(ctx->dt, ctx->k2, dp, rs, out, st, pdl, !all_direct);
             }
             if (e == cudaSuccess) e = launch_loop_step(ctx->dt, dl, dp, rs, R, true, st, pdl);
             if (e == cudaSuccess) e = cudaMemcpyAsync(hl, dl, sizeof(LoopState), cudaMemcpyDeviceToHost, st);
@@ -817,7 +818,7 @@ int explorer_run_batched(fbb_ctx* ctx, const int64_t* targets, int ntargets, int
         static const bool use_graph = [] { const char* e = getenv("FBB_LOOP_GRAPH"); return !(e && e[0] == '0'); }();
         static const bool loop_pdl = [] { const char* e = getenv("FBB_PDL"); return !(e && e[0] == '0'); }();
         if (use_graph) {
-            const LoopGraphKey key{R, out.nodes.masks, out.nodes.heads, out.nodes.prefix, out.lb, out.count,
+            const LoopGraphKey key{2 * R + (all_direct ? 1 : 0), out.nodes.masks, out.nodes.heads, out.nodes.prefix, out.lb, out.count,
                                    out.seg, dl, hl};
             if (!ctx->loop_graph || !(ctx->loop_graph_key == key)) {
                 if (ctx->loop_graph) cudaGraphExecDestroy(ctx->loop_graph);

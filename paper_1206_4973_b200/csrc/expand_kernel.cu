@@ -392,13 +392,11 @@ __device__ __forceinline__ int leaf_segments(const Pool* __restrict__ pool, int 
     return k;
 }
 
-__global__ void k2_leaf_kernel(DevTables t, const Pool* __restrict__ pool, int /*unused*/,
-                               RoundState* rs) {
-    asm volatile("griddepcontrol.wait;" ::: "memory");  // the pool upload (PDL chain)
-    asm volatile("griddepcontrol.launch_dependents;");
+// The leaf children of a pool, one per thread (grid-stride): makespan of the completion,
+// batch minimum (value, first position) by atomicMin.
+__device__ __forceinline__ void leaf_children(const DevTables& t, const Pool* __restrict__ pool, RoundState* rs,
+                                              int nls) {
     const int n = t.n, m = t.m, W = t.W;
-    const int nls = leaf_segments(pool, n);
-    if (nls == 0) return;  // no leaves
     const int64_t nc0 = pool->seg[0].count * (n - pool->seg[0].depth);
     const int64_t nct = nc0 + (nls > 1 ? pool->seg[1].count * (n - pool->seg[1].depth) : 0);
     for (int64_t cc = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; cc < nct;
@@ -456,16 +454,12 @@ __global__ void k2_leaf_kernel(DevTables t, const Pool* __restrict__ pool, int /
     }
 }
 
-// Writes the schedule of the batch's best leaf (if it beats ub) before the
-// parents' storage is recycled by the push.  A corrupt-node flag (found < 0, set by
-// the leaf kernel) is kept for the host to report.
-__global__ void leaf_schedule_kernel(DevTables t, const Pool* __restrict__ pool, RoundState* rs,
-                                     int32_t ub) {
-    asm volatile("griddepcontrol.wait;" ::: "memory");  // the leaf kernel (PDL chain)
-    asm volatile("griddepcontrol.launch_dependents;");
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+// Writes the schedule of the batch's best leaf (if it beats the pool's bound) before the
+// parents' storage is recycled by the push; run by the leaf kernel's last CTA.  A
+// corrupt-node flag (found < 0, set by the leaf kernel) is kept for the host to report.
+__device__ void write_leaf_schedule(const DevTables& t, const Pool* __restrict__ pool, RoundState* rs) {
     if (rs->found < 0) return;
-    ub = pool->ub;
+    const int32_t ub = pool->ub;
     const int n = t.n;
     const int nls = leaf_segments(pool, n);
     unsigned long long inv = rs->leaf_inv;
@@ -497,6 +491,28 @@ __global__ void leaf_schedule_kernel(DevTables t, const Pool* __restrict__ pool,
     schedule[sg.depth] = u[rk];
     if (r == 2) schedule[sg.depth + 1] = u[1 - rk];
     *found = 1;
+}
+
+__global__ void k2_leaf_kernel(DevTables t, const Pool* __restrict__ pool, int /*unused*/,
+                               RoundState* rs) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // the pool upload (PDL chain)
+    asm volatile("griddepcontrol.launch_dependents;");
+    const int n = t.n;
+    const int nls = leaf_segments(pool, n);
+    if (nls == 0) return;  // no leaves
+    leaf_children(t, pool, rs, nls);
+    // the last CTA out writes the best leaf's schedule (every CTA's offers are in)
+    __shared__ int s_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(&rs->leaf_done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last && threadIdx.x == 0) {
+        __threadfence();
+        write_leaf_schedule(t, pool, rs);
+    }
 }
 
 // Moves every chunk's survivors from its staging slot to its final, batch-ordered
@@ -800,10 +816,6 @@ cudaError_t launch_pool_upload(const void* h_src, void* d_dst, int words, cudaSt
     return cudaGetLastError();
 }
 
-cudaError_t launch_leaf_schedule(const DevTables& t, const Pool* d_pool, RoundState* rs,
-                                 int32_t ub, cudaStream_t stream, bool pdl) {
-    return launch_pdl(leaf_schedule_kernel, dim3(1), dim3(32), 0, stream, pdl, t, d_pool, rs, ub);
-}
 
 }  // namespace fbb
 
@@ -841,11 +853,9 @@ namespace fbb {
 // round's plan from the device Pool / RoundState and exits when it has nothing to do,
 // so the grids are fixed and nothing here needs the host.
 cudaError_t launch_round_device(const DevTables& t, const K2Config& cfg, const Pool* d_pool,
-                                RoundState* rs, ChunkOut out, cudaStream_t stream, bool pdl) {
+                                RoundState* rs, ChunkOut out, cudaStream_t stream, bool pdl, bool place) {
     // leaves: a one-wave grid-stride grid (most rounds have none and exit at once)
     cudaError_t e = launch_pdl(k2_leaf_kernel, dim3(148), dim3(256), 0, stream, pdl, t, d_pool, 0, rs);
-    if (e != cudaSuccess) return e;
-    e = launch_pdl(leaf_schedule_kernel, dim3(1), dim3(32), 0, stream, pdl, t, d_pool, rs, 0);
     if (e != cudaSuccess) return e;
     if (cfg.variant >= 100000)
         e = launch_k2_v3(t, cfg, d_pool, 0, cfg.blocks, 0, 0, rs, out, stream, pdl);
@@ -856,7 +866,7 @@ cudaError_t launch_round_device(const DevTables& t, const K2Config& cfg, const P
                                 : (cfg.jm_in_smem ? k2_internal_kernel<true, false> : k2_internal_kernel<false, false>),
                        dim3(cfg.blocks), dim3(cfg.threads), cfg.smem, stream, pdl, t, d_pool, 0, cfg.cmax, 0, 0,
                        rs, out);
-    if (e != cudaSuccess) return e;
+    if (e != cudaSuccess || !place) return e;  // !place: every pool of the batch is placed by K2
     return launch_pdl(place_kernel<true>, dim3(148 * 2), dim3(kPlaceThreads), (size_t)cfg.cmax * kPlaceChunks,
                       stream, pdl, t, d_pool, cfg.cmax, rs, out, (RoundState*)nullptr);
 }

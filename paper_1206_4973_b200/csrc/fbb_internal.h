@@ -213,6 +213,8 @@ struct RoundState {
     int64_t total;                // survivors of the pool
     uint32_t place_done;          // place CTAs past their counting (the last one publishes)
     uint32_t arrived;             // direct placement: K2 CTAs past their counts (grid barrier)
+    uint32_t leaf_done;           // leaf-kernel CTAs finished (the last one writes the schedule)
+    uint32_t pad_ls;
     unsigned long long k2_t0_inv; // ~(first K2 CTA start), %globaltimer ns (0 = none)
     unsigned long long k2_t1;     // last K2 CTA end, %globaltimer ns
     int64_t seg_surv[kMaxSegments];
@@ -251,8 +253,7 @@ cudaError_t launch_place(const DevTables& t, const K2Config& cfg, const Pool* d_
                          const Pool& h_pool, RoundState* rs, ChunkOut out, cudaStream_t stream,
                          RoundState* summary = nullptr);
 // Schedule of the best leaf when it beats ub (before the parents are recycled).
-cudaError_t launch_leaf_schedule(const DevTables& t, const Pool* d_pool, RoundState* rs,
-                                 int32_t ub, cudaStream_t stream, bool pdl = false);
+
 
 // ---- batched explorer loop (explorer_loop.cu): rounds planned and closed on the device --
 constexpr int kLoopMax = 64;  // rounds per batch
@@ -290,8 +291,10 @@ struct LoopState {
 // close of round - 1 (round > 0) + plan of round (!last), one single-warp kernel
 cudaError_t launch_loop_step(const DevTables& t, LoopState* ls, Pool* pool, RoundState* rs, int round,
                              bool last, cudaStream_t stream, bool pdl);
+// place == false: every pool of the batch is small enough for direct placement (K2 writes
+// the survivors itself), so the place kernel is left out
 cudaError_t launch_round_device(const DevTables& t, const K2Config& cfg, const Pool* d_pool,
-                                RoundState* rs, ChunkOut out, cudaStream_t stream, bool pdl);
+                                RoundState* rs, ChunkOut out, cudaStream_t stream, bool pdl, bool place);
 
 // Launches kern<<<grid, block, smem, st>>>(args...), as a programmatic dependent of the
 // previous kernel in the stream when pdl (the kernel must griddepcontrol.wait before it
