@@ -219,8 +219,9 @@ struct fbb_ctx {
     // batched device-planned explorer loop (explorer_loop.cu)
     DBuf d_loop;
     HBuf h_loop;
-    cudaGraphExec_t loop_graph = nullptr;  // the captured batch (explorer_run_batched)
-    LoopGraphKey loop_graph_key{};
+    // captured batches (explorer_run_batched), one per (length, buffers); lengths are
+    // powers of two, so a context captures at most a handful
+    std::vector<std::pair<LoopGraphKey, cudaGraphExec_t>> loop_graphs;
     bool device_loop = false;          // FBB_DEVICE_LOOP=1: batched device-planned rounds
     float last_k2_ms = 0.f, last_round_ms = 0.f, last_sync_ms = 0.f, last_place_ms = 0.f;
     int last_launches = 0;
@@ -805,38 +806,47 @@ int explorer_run_batched(fbb_ctx* ctx, const int64_t* targets, int ntargets, int
         // download -- every kernel a programmatic dependent of the one before, the whole
         // sequence one CUDA graph (captured once per batch length and staging buffers, then
         // replayed: one host call per batch)
-        auto enqueue = [&](bool pdl) -> cudaError_t {
+        // graph length: R rounded up to a power of two (the rounds past hl->nrounds plan
+        // nothing and every kernel of theirs exits at once)
+        int Rg = 1;
+        while (Rg < R) Rg <<= 1;
+        auto enqueue = [&](bool pdl, int rounds) -> cudaError_t {
             cudaError_t e = cudaMemcpyAsync(dl, hl, offsetof(LoopState, rec), cudaMemcpyHostToDevice, st);
-            for (int i = 0; i < R && e == cudaSuccess; ++i) {
+            for (int i = 0; i < rounds && e == cudaSuccess; ++i) {
                 if ((e = launch_loop_step(ctx->dt, dl, dp, rs, i, false, st, pdl && i > 0)) != cudaSuccess) break;
                 e = launch_round_device(ctx->dt, ctx->k2, dp, rs, out, st, pdl, !all_direct);
             }
-            if (e == cudaSuccess) e = launch_loop_step(ctx->dt, dl, dp, rs, R, true, st, pdl);
+            if (e == cudaSuccess) e = launch_loop_step(ctx->dt, dl, dp, rs, rounds, true, st, pdl);
             if (e == cudaSuccess) e = cudaMemcpyAsync(hl, dl, sizeof(LoopState), cudaMemcpyDeviceToHost, st);
             return e;
         };
         static const bool use_graph = [] { const char* e = getenv("FBB_LOOP_GRAPH"); return !(e && e[0] == '0'); }();
         static const bool loop_pdl = [] { const char* e = getenv("FBB_PDL"); return !(e && e[0] == '0'); }();
         if (use_graph) {
-            const LoopGraphKey key{2 * R + (all_direct ? 1 : 0), out.nodes.masks, out.nodes.heads, out.nodes.prefix, out.lb, out.count,
-                                   out.seg, dl, hl};
-            if (!ctx->loop_graph || !(ctx->loop_graph_key == key)) {
-                if (ctx->loop_graph) cudaGraphExecDestroy(ctx->loop_graph);
-                ctx->loop_graph = nullptr;
+            const LoopGraphKey key{2 * Rg + (all_direct ? 1 : 0), out.nodes.masks, out.nodes.heads,
+                                   out.nodes.prefix, out.lb, out.count, out.seg, dl, hl};
+            cudaGraphExec_t exec = nullptr;
+            for (auto& kv : ctx->loop_graphs)
+                if (kv.first == key) exec = kv.second;
+            if (!exec) {
+                if (ctx->loop_graphs.size() >= 16) {  // buffers moved many times: start over
+                    for (auto& kv : ctx->loop_graphs) cudaGraphExecDestroy(kv.second);
+                    ctx->loop_graphs.clear();
+                }
                 cudaGraph_t g = nullptr;
                 CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "loop capture");
-                cudaError_t ce = enqueue(loop_pdl);
+                cudaError_t ce = enqueue(loop_pdl, Rg);
                 cudaError_t ee = cudaStreamEndCapture(st, &g);
                 CK(ce, "loop capture");
                 CK(ee, "loop capture");
-                ce = cudaGraphInstantiate(&ctx->loop_graph, g, 0);
+                ce = cudaGraphInstantiate(&exec, g, 0);
                 cudaGraphDestroy(g);
                 CK(ce, "loop graph instantiate");
-                ctx->loop_graph_key = key;
+                ctx->loop_graphs.emplace_back(key, exec);
             }
-            CK(cudaGraphLaunch(ctx->loop_graph, st), "loop graph");
+            CK(cudaGraphLaunch(exec, st), "loop graph");
         } else {
-            CK(enqueue(loop_pdl), "loop batch");
+            CK(enqueue(loop_pdl, R), "loop batch");
         }
         const auto t_sync = std::chrono::steady_clock::now();
         CK(cudaStreamSynchronize(st), "batch");
@@ -1058,7 +1068,7 @@ void fbb_destroy(fbb_ctx* ctx) {
     ctx->h_rp.release();
     ctx->h_loop.release();
     ctx->d_loop.release();
-    if (ctx->loop_graph) cudaGraphExecDestroy(ctx->loop_graph);
+    for (auto& kv : ctx->loop_graphs) cudaGraphExecDestroy(kv.second);
     for (cudaEvent_t ev : ctx->ev)
         if (ev) cudaEventDestroy(ev);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
