@@ -234,7 +234,10 @@ __device__ __forceinline__ void scan_pair16(uint32_t row_sa, uint32_t s0, uint32
 
 
 // OCC = target CTAs per SM: 2 -> up to 168 registers, 3 -> 112 (smaller chunks too)
-template <int N, int M, int OCC>
+// DIR: false = staged placement only (the big-pool kernel, untouched by the direct path),
+// true = direct placement capable (single-wave pools; Pool::direct decides at run time when
+// place_hint < 0)
+template <int N, int M, int OCC, bool DIR>
 __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool* __restrict__ pool,
                                                    int first_seg, int cmax, int place_hint, int frozen,
                                                    RoundState* rs, ChunkOut out) {
@@ -249,7 +252,7 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
     // grid's CTAs retire (programmatic dependent launch; it waits for the grid's
     // completion before reading anything).  Direct: the dependents may not take SM room
     // before every CTA of this grid is resident (its CTAs wait for each other).
-    if (place_hint == 0) asm volatile("griddepcontrol.launch_dependents;");
+    if (!DIR) asm volatile("griddepcontrol.launch_dependents;");
     const int n = t.n, W = t.W;
     const V2Layout L = v2_layout(n, M, P, cmax, blockDim.x, N, OCC);
     uint64_t* s_um = (uint64_t*)(smem + L.um);  // unscheduled jobs of each parent
@@ -300,8 +303,8 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
     // the round's bound, semantics and first internal segment come from the pool
     // (written by the host, or by the device-side planner of the batched explorer loop)
     asm volatile("griddepcontrol.wait;" ::: "memory");  // the pool upload kernel (PDL)
-    const bool direct = place_hint < 0 ? pool->direct != 0 : place_hint == 1;
-    if (place_hint < 0 && !direct) asm volatile("griddepcontrol.launch_dependents;");
+    const bool direct = DIR && (place_hint < 0 ? pool->direct != 0 : place_hint == 1);
+    if (DIR && !direct) asm volatile("griddepcontrol.launch_dependents;");
     k2_stamp_begin(rs);
     const int32_t ub = pool->ub;
     frozen = pool->frozen;
@@ -363,8 +366,8 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
     };
     // direct placement: CTA i owns chunk c_begin + i (fixed-grid launches may have more
     // CTAs than chunks; those have nothing to do)
-    int64_t chunk = direct ? c_begin + blockIdx.x : claim_chunk(rs, c_begin, s_slot);
-    if (direct && chunk >= c_end) return;
+    int64_t chunk = (DIR && direct) ? c_begin + blockIdx.x : claim_chunk(rs, c_begin, s_slot);
+    if (DIR && direct && chunk >= c_end) return;
     if constexpr (kPipe) prefetch(chunk);
     while (chunk < c_end) {
         int s, depth, np;
@@ -408,7 +411,7 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
         }
         __syncthreads();
         if (kPipe && tid == 0)  // next chunk
-            *s_slot = direct ? c_end : c_begin + (int64_t)atomicAdd(&rs->ticket, 1u);
+            *s_slot = (DIR && direct) ? c_end : c_begin + (int64_t)atomicAdd(&rs->ticket, 1u);
         if (compact) {  // heads and scheduled set folded from the staged prefixes
             if (tid < np) {
                 const uint8_t* pre = s_pre + tid * RW;
@@ -626,7 +629,7 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
             out.count[chunk] = tot;
             out.seg[chunk] = s;
         }
-        if (direct) {
+        if (DIR && direct) {
             // every chunk's count in (grid-wide), then this chunk's survivors straight to
             // their bucket rows: segment base + survivors of the segment's earlier chunks
             direct_arrive(rs, s, tot, c_end - c_begin);
@@ -659,25 +662,36 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
         }
     }
     k2_stamp_end(rs);
-    if (direct) direct_finish(pool, rs, n, c_end - c_begin);
+    if (DIR && direct) direct_finish(pool, rs, n, c_end - c_begin);
 }
 
-template <int N, int M, int OCC>
-cudaError_t v2_setup(const DevTables& t, K2Config& c, int device) {
+template <int N, int M, int OCC, bool DIR>
+cudaError_t v2_setup_one(const DevTables& t, K2Config& c, int device) {
     int optin = 0, sms = 148, per_sm = 1;
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     // dynamic + static shared memory must fit the opt-in limit (direct placement keeps a
     // few bytes of static shared memory)
     cudaFuncAttributes fa;
-    cudaError_t e = cudaFuncGetAttributes(&fa, k2_v2_kernel<N, M, OCC>);
+    cudaError_t e = cudaFuncGetAttributes(&fa, k2_v2_kernel<N, M, OCC, DIR>);
     if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k2_v2_kernel<N, M, OCC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    e = cudaFuncSetAttribute(k2_v2_kernel<N, M, OCC, DIR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              optin - (int)fa.sharedSizeBytes);
     if (e != cudaSuccess) return e;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_v2_kernel<N, M, OCC>, c.threads, c.smem);
-    c.blocks = sms * (per_sm < 1 ? 1 : per_sm);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k2_v2_kernel<N, M, OCC, DIR>, c.threads, c.smem);
+    const int blocks = sms * (per_sm < 1 ? 1 : per_sm);
+    // the staged kernel's residency sets the grid; the direct one must hold a whole wave
+    // of the same size (its CTAs wait for each other)
+    if (!DIR) c.blocks = blocks;
+    else if (blocks < c.blocks) return cudaErrorInvalidConfiguration;
     return cudaSuccess;
+}
+
+template <int N, int M, int OCC>
+cudaError_t v2_setup(const DevTables& t, K2Config& c, int device) {
+    cudaError_t e = v2_setup_one<N, M, OCC, false>(t, c, device);
+    if (e != cudaSuccess) return e;
+    return v2_setup_one<N, M, OCC, true>(t, c, device);
 }
 
 }  // namespace
@@ -742,8 +756,11 @@ cudaError_t launch_k2_v2(const DevTables& t, const K2Config& cfg, const Pool* d_
                          cudaStream_t stream, bool pdl) {
 #define V2_CASE(NN, MM, OO)                                                                   \
     case OO * 10000 + NN * 100 + MM:                                                          \
-        return launch_pdl(k2_v2_kernel<NN, MM, OO>, dim3(blocks), dim3(cfg.threads), cfg.smem, stream, pdl, \
-                          t, d_pool, first_seg, cfg.cmax, place_hint, frozen, rs, out);
+        return place_hint == 0                                                                \
+                   ? launch_pdl(k2_v2_kernel<NN, MM, OO, false>, dim3(blocks), dim3(cfg.threads), cfg.smem, \
+                                stream, pdl, t, d_pool, first_seg, cfg.cmax, 0, frozen, rs, out)  \
+                   : launch_pdl(k2_v2_kernel<NN, MM, OO, true>, dim3(blocks), dim3(cfg.threads), cfg.smem, \
+                                stream, pdl, t, d_pool, first_seg, cfg.cmax, place_hint, frozen, rs, out);
     switch (cfg.variant) {
         V2_CASE(20, 5, 2)
         V2_CASE(20, 10, 2)
