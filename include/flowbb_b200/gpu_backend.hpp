@@ -110,8 +110,13 @@ public:
         if (nodes.empty()) return out;
         fbb_ctx* ctx = cache_->get(inst);
         const int n = inst.jobs(), m = inst.machines(), W = (n + 63) / 64;
-        std::vector<uint64_t> masks(nodes.size() * W);
-        std::vector<int32_t> heads(nodes.size() * m), depth(nodes.size());
+        thread_local std::vector<uint64_t> masks;  // reused across calls (no re-initialisation)
+        thread_local std::vector<int32_t> heads, depth;
+        if (depth.size() < nodes.size()) {
+            masks.resize(nodes.size() * W);
+            heads.resize(nodes.size() * m);
+            depth.resize(nodes.size());
+        }
         for (std::size_t i = 0; i < nodes.size(); ++i) {
             detail::pack(inst, nodes[i], &masks[i * W], &heads[i * m], nullptr);
             depth[i] = nodes[i].depth();
@@ -170,25 +175,35 @@ inline RoundCounts gpu_round(const GpuBackend& backend, const flowbb::Instance& 
                              std::size_t target, bool frozen, std::optional<int>* best = nullptr) {
     RoundCounts rc;
     const int n = inst.jobs(), m = inst.machines(), W = (n + 63) / 64;
-    std::vector<uint64_t> masks;
-    std::vector<int32_t> heads, depth;
-    std::vector<uint8_t> prefix;
+    // per-thread buffers reused across rounds (a 262 K-child round's output arrays are
+    // ~30 MB: value-initialising them every round cost more than the GPU round itself)
+    thread_local std::vector<uint64_t> masks, omask;
+    thread_local std::vector<int32_t> heads, depth, oheads, odepth, olb;
+    thread_local std::vector<uint8_t> prefix, oprefix;
+    depth.clear();
     std::size_t children = 0;
     while (children < target && !pending.empty()) {
         flowbb::Node node = pending.pop();
         ++rc.branched;
         std::size_t i = depth.size();
-        masks.resize((i + 1) * W);
-        heads.resize((i + 1) * m);
-        prefix.resize((i + 1) * n);
+        if (masks.size() < (i + 1) * W) {
+            masks.resize(2 * (i + 1) * W);
+            heads.resize(2 * (i + 1) * m);
+            prefix.resize(2 * (i + 1) * n);
+        }
         detail::pack(inst, node, &masks[i * W], &heads[i * m], &prefix[i * n]);
         depth.push_back(node.depth());
         children += static_cast<std::size_t>(n - node.depth());
     }
     if (depth.empty()) return rc;
-    std::vector<uint64_t> omask(children * W);
-    std::vector<int32_t> oheads(children * m), odepth(children), olb(children), sched(n);
-    std::vector<uint8_t> oprefix(children * n);
+    if (odepth.size() < children) {
+        omask.resize(children * W);
+        oheads.resize(children * m);
+        odepth.resize(children);
+        olb.resize(children);
+        oprefix.resize(children * n);
+    }
+    std::vector<int32_t> sched(n);
     int64_t count = 0, pos = 0;
     int32_t leaf_best = 0;
     fbb_round_t rec;
@@ -207,6 +222,7 @@ inline RoundCounts gpu_round(const GpuBackend& backend, const flowbb::Instance& 
     }
     for (int64_t i = 0; i < count; ++i) {
         flowbb::Node node = flowbb::Node::root(inst);
+        node.prefix.reserve(static_cast<std::size_t>(odepth[i]));
         for (int d = 0; d < odepth[i]; ++d) {
             int j = oprefix[i * n + d];
             node.prefix.push_back(j);
