@@ -887,6 +887,11 @@ def main():
                "d2h_bytes_per_step": sum(t["d2h_bytes"] for t in e_tim) // stepsd,
                "rounds_match_device_explorer": [tuple(r) for r in e_rounds] == [
                    tuple(r) for r in rounds[: len(e_rounds)]],
+               "per_round_ms": {"wall": 1e3 * e_secs / stepsd,
+                                "device": sum(t["round_ms"] for t in e_tim) / stepsd,
+                                "k2": sum(t["k2_ms"] for t in e_tim) / stepsd,
+                                "library_host": sum(t["host_ms"] for t in e_tim) / stepsd,
+                                "sync_wait": sum(t["sync_ms"] for t in e_tim) / stepsd},
                "timing": "wall clock of fbb_explorer_run over the K rounds with the pending tree in "
                          "pinned, device-mapped host memory (parents read and survivors written "
                          "over the host link every round)"}

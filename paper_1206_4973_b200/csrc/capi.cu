@@ -384,7 +384,7 @@ int run_pool(fbb_ctx* ctx, Pool& pool, int first_internal, int32_t ub, int froze
         // leaves, then the best leaf's schedule -- before K2 recycles the leaf
         // parents' slots (bucket n-2 receives the next segment's survivors)
         CK(launch_k2_leaves(ctx->dt, dp, pool, 0, rs, st, kernel_upload), "K2 leaves");
-        launches += 1;  // its last CTA writes the best leaf's schedule
+        launches += 2;  // leaves + the best leaf's schedule
     }
     if (!pdl) CK(cudaEventRecord(ctx->ev[1], st), "event");
     bool has_internal = first_internal < pool.nseg && pool.nchunks > 0;

@@ -455,7 +455,7 @@ __device__ __forceinline__ void leaf_children(const DevTables& t, const Pool* __
 }
 
 // Writes the schedule of the batch's best leaf (if it beats the pool's bound) before the
-// parents' storage is recycled by the push; run by the leaf kernel's last CTA.  A
+// parents' storage is recycled by the push.  A
 // corrupt-node flag (found < 0, set by the leaf kernel) is kept for the host to report.
 __device__ void write_leaf_schedule(const DevTables& t, const Pool* __restrict__ pool, RoundState* rs) {
     if (rs->found < 0) return;
@@ -501,18 +501,15 @@ __global__ void k2_leaf_kernel(DevTables t, const Pool* __restrict__ pool, int /
     const int nls = leaf_segments(pool, n);
     if (nls == 0) return;  // no leaves
     leaf_children(t, pool, rs, nls);
-    // the last CTA out writes the best leaf's schedule (every CTA's offers are in)
-    __shared__ int s_last;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence();
-        s_last = atomicAdd(&rs->leaf_done, 1u) == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (s_last && threadIdx.x == 0) {
-        __threadfence();
-        write_leaf_schedule(t, pool, rs);
-    }
+}
+
+// The best leaf's schedule, after every leaf CTA's offer is in: a one-thread programmatic
+// dependent of the leaf kernel.  (Having the leaf kernel's last CTA write it instead needs
+// a gpu-scope release per CTA -- measured +10 us per Ta001 leaf round of ~1000 CTAs.)
+__global__ void leaf_schedule_kernel(DevTables t, const Pool* __restrict__ pool, RoundState* rs) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // the leaf kernel (PDL chain)
+    asm volatile("griddepcontrol.launch_dependents;");
+    if (threadIdx.x == 0 && blockIdx.x == 0) write_leaf_schedule(t, pool, rs);
 }
 
 // Moves every chunk's survivors from its staging slot to its final, batch-ordered
@@ -780,7 +777,9 @@ cudaError_t launch_k2_leaves(const DevTables& t, const Pool* d_pool, const Pool&
     if (nc <= 0) return cudaSuccess;
     int blocks = (int)((nc + 255) / 256);
     if (blocks > 4096) blocks = 4096;
-    return launch_pdl(k2_leaf_kernel, dim3(blocks), dim3(256), 0, stream, pdl, t, d_pool, seg_index, rs);
+    cudaError_t e = launch_pdl(k2_leaf_kernel, dim3(blocks), dim3(256), 0, stream, pdl, t, d_pool, seg_index, rs);
+    if (e != cudaSuccess) return e;
+    return launch_pdl(leaf_schedule_kernel, dim3(1), dim3(32), 0, stream, pdl, t, d_pool, rs);
 }
 
 cudaError_t launch_k2_internal(const DevTables& t, const K2Config& cfg, const Pool* d_pool,
@@ -856,6 +855,8 @@ cudaError_t launch_round_device(const DevTables& t, const K2Config& cfg, const P
                                 RoundState* rs, ChunkOut out, cudaStream_t stream, bool pdl, bool place) {
     // leaves: a one-wave grid-stride grid (most rounds have none and exit at once)
     cudaError_t e = launch_pdl(k2_leaf_kernel, dim3(148), dim3(256), 0, stream, pdl, t, d_pool, 0, rs);
+    if (e != cudaSuccess) return e;
+    e = launch_pdl(leaf_schedule_kernel, dim3(1), dim3(32), 0, stream, pdl, t, d_pool, rs);
     if (e != cudaSuccess) return e;
     if (cfg.variant >= 100000)
         e = launch_k2_v3(t, cfg, d_pool, 0, cfg.blocks, 0, 0, rs, out, stream, pdl);

@@ -40,7 +40,6 @@ __device__ void plan_round(const DevTables& t, LoopState* ls, Pool* pool, RoundS
     rs->total = 0;
     rs->place_done = 0u;
     rs->arrived = 0u;
-    rs->leaf_done = 0u;
     rs->k2_t0_inv = 0ull;
     rs->k2_t1 = 0ull;
     pool->ub = ls->incumbent;

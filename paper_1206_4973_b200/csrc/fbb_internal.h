@@ -213,8 +213,6 @@ struct RoundState {
     int64_t total;                // survivors of the pool
     uint32_t place_done;          // place CTAs past their counting (the last one publishes)
     uint32_t arrived;             // direct placement: K2 CTAs past their counts (grid barrier)
-    uint32_t leaf_done;           // leaf-kernel CTAs finished (the last one writes the schedule)
-    uint32_t pad_ls;
     unsigned long long k2_t0_inv; // ~(first K2 CTA start), %globaltimer ns (0 = none)
     unsigned long long k2_t1;     // last K2 CTA end, %globaltimer ns
     int64_t seg_surv[kMaxSegments];
