@@ -94,6 +94,7 @@ __global__ void __launch_bounds__(kK3Threads, 4) k1v3_kernel(DevTables t, const 
     const uint32_t* __restrict__ rowq = t.rowk1 + q;
     const uint32_t tab_sa = (uint32_t)__cvta_generic_to_shared(s_tab) + (uint32_t)(g * n * kNP * 2);
     const int32_t bias = t.k1_bias, c0 = t.k1_c0;
+    const uint32_t half_b = (uint32_t)n * 16u;  // byte distance between the two table planes
 
     const int64_t ntiles = (count + T - 1) / T;
     for (int64_t ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
@@ -124,13 +125,16 @@ __global__ void __launch_bounds__(kK3Threads, 4) k1v3_kernel(DevTables t, const 
         }
         __syncthreads();
         // membership table: word (group gg, job j, u) = [j in U of node gg*16 + 2u] +
-        // 65536 [j in U of node gg*16 + 2u + 1]
+        // 65536 [j in U of node gg*16 + 2u + 1], stored as two 16-byte halves per job in
+        // separate planes, [gg][u / 4][j][u % 4]: the lanes of a warp (machine pairs at
+        // one Johnson position, i.e. random jobs) then spread their 128-bit loads over all
+        // 8 bank groups (j mod 8) instead of 4 (2j mod 8 with 32-byte job rows)
         for (int x = tid; x < G * n * 8; x += kK3Threads) {
             const int gg = x / (n * 8), rem = x - gg * n * 8, j = rem >> 3, u = rem & 7;
             const int node0 = gg * kNP + 2 * u;
             const uint32_t a = (~s_sched[node0 * NW + (j >> 5)] >> (j & 31)) & 1u;
             const uint32_t b = (~s_sched[(node0 + 1) * NW + (j >> 5)] >> (j & 31)) & 1u;
-            s_tab[x] = a | (b << 16);
+            s_tab[gg * n * 8 + (u >> 2) * n * 4 + j * 4 + (u & 3)] = a | (b << 16);
         }
         __syncthreads();  // membership table complete
         // one-machine terms (bound.hpp:61-74) over the same table, 16 nodes per thread:
@@ -153,7 +157,7 @@ __global__ void __launch_bounds__(kK3Threads, 4) k1v3_kernel(DevTables t, const 
                 for (int j = ch; j < n; j += C) {
                     const uint32_t pj = (uint32_t)__ldg(t.p + j * m + kk);
                     const uint32_t t2 = (uint32_t)__ldg(t.tails + j * m + kk) * 0x10001u;  // (t, t)
-                    const uint4 s0 = lds128(tg + (uint32_t)j * (kNP * 2)), s1 = lds128(tg + (uint32_t)j * (kNP * 2) + 16);
+                    const uint4 s0 = lds128(tg + (uint32_t)j * 16u), s1 = lds128(tg + (uint32_t)(j + n) * 16u);
                     const uint32_t sel[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
 #pragma unroll
                     for (int u = 0; u < kNP / 2; ++u) {
@@ -219,8 +223,8 @@ __global__ void __launch_bounds__(kK3Threads, 4) k1v3_kernel(DevTables t, const 
             for (int i = 0; i < n; ++i) {
                 rp += P;
                 const uint32_t en = i + 1 < n ? __ldg(rp) : 0u;  // next position
-                const uint32_t at = tab_sa + (e & 0xFFu) * (uint32_t)(kNP * 2);
-                const uint4 s0 = lds128(at), s1 = lds128(at + 16);
+                const uint32_t at = tab_sa + (e & 0xFFu) * 16u;
+                const uint4 s0 = lds128(at), s1 = lds128(at + half_b);
                 const uint32_t cb2 = prmt(e, 0x3232u);            // (c + c0, c + c0)
                 const int32_t d = (int32_t)prmt(e, 0x9991u);      // int8 d, sign-extended
                 const uint32_t sel[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};

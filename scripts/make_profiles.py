@@ -91,7 +91,7 @@ def bench_line(path):
 
 def main(tag):
     os.makedirs(PROF, exist_ok=True)
-    md = [f"# {tag} — measured on one B200 (gpurun), `scripts/gpu_full.sh`", ""]
+    md = [f"# {tag} — measured on one B200 (gpurun), `scripts/gpu_{tag}_final.sh`", ""]
     gpu = os.path.join(OUT, "gpu.txt")
     if os.path.exists(gpu):
         md += ["```", open(gpu).read().strip(), open(os.path.join(OUT, "nproc.txt")).read().strip(),
@@ -100,7 +100,7 @@ def main(tag):
            "| run | value (bounded/s) | ms/step | e2e (bounded/s) | K2 share | roofline frac | cpu baseline |",
            "|---|---|---|---|---|---|---|"]
     for f in ["bench.json", "bench_ref.json", "bench_ta001.json", "bench_ta051.json",
-              "bench_ta081.json", "bench_ta101.json"]:
+              "bench_ta081.json", "bench_ta101.json", "bench_ta051_tuner.json"]:
         d = bench_line(os.path.join(OUT, f))
         if not d:
             continue
@@ -112,7 +112,8 @@ def main(tag):
                   f"{cpu if cpu is None else f'{cpu:.4g}'} |")
         shutil.copy(os.path.join(OUT, f), os.path.join(PROF, f"{tag}_{f}"))
     header = False
-    for f in ["bench_bound_ta101.json", "bench_bound_ta021.json", "bench_bound_ref.json"]:
+    for f in ["bench_bound_ta101.json", "bench_bound_ta051.json", "bench_bound_ta021.json",
+              "bench_bound_ref.json"]:
         d = bench_line(os.path.join(OUT, f))
         if d:
             if not header:
@@ -145,7 +146,9 @@ def main(tag):
     for rep, title in [("prof_k2_final.ncu-rep", "K2 (v2, Ta021) and place"),
                        ("prof_k2v2_pool.ncu-rep", "K2 (v2) on a fixed 262K-child Ta021 pool (k2_pool_bench)"),
                        ("prof_k2v3_ta081.ncu-rep", "K2 (v3, Ta081)"),
-                       ("prof_k1v2_ta101.ncu-rep", "K1 (v2, 200x20 bound-only pool)")]:
+                       ("prof_k1v2_ta101.ncu-rep", "K1 (v2, 200x20 bound-only pool)"),
+                       ("prof_k1v3_ta101.ncu-rep", "K1 (v3, 200x20 bound-only pool of 1 M nodes)"),
+                       ("prof_k1v3_ta021.ncu-rep", "K1 (v3, 20x20 bound-only pool of 2 M nodes)")]:
         p = os.path.join(OUT, rep)
         if os.path.exists(p):
             md += ["", f"## ncu --set full: {title}", ncu_metrics(p)]
