@@ -636,22 +636,49 @@ def solve_mode(args, inst_name):
     inst = fbb.generate_instance(n, m, seed)
     ctx = fbb.Context(inst, 0)
     sampler = ClockSampler(0) if not os.environ.get("FBB_NO_CLOCKS") else None
+    group, gs = None, None
     t0 = time.perf_counter()
-    r0 = ctx.explorer_start_solve(None)
-    dev_ms, rounds, trace = 0.0, 1, []
-    while True:
-        r, t = ctx.explorer_run([args.target], 500, timing=True)
-        dev_ms += sum(x["round_ms"] for x in t)
-        rounds += len(r)
-        st = ctx.explorer_state()
-        trace.append((round(time.perf_counter() - t0, 3), st["bounded"], st["incumbent"]))
-        if st["pending"] == 0 or not r or time.perf_counter() - t0 > args.max_seconds:
-            break
+    if args.group > 1:
+        # the in-library multi-device explorer: member 0 bounds the root, the others are fed
+        # by rebalancing, and every step ends with the incumbent min-exchange (the paper's
+        # UB allreduce)
+        G = args.group
+        devs = list(range(G)) if torch.cuda.device_count() >= G else [0] * G
+        group = fbb.DeviceGroup(inst, devs)
+        t0 = time.perf_counter()
+        group.start_solve(None)
+        r0 = (1, 0, 1, 1, 0, 0, fbb.makespan(inst, list(range(n))), 1)
+        dev_ms, rounds, trace = 0.0, 1, []
+        while True:
+            gs = group.run(args.target, max_steps=100, rounds_per_step=args.exchange_every,
+                           balance_every=1)
+            dev_ms += gs["device_ms_max"]
+            rounds += gs["rounds"]
+            trace.append((round(time.perf_counter() - t0, 3), gs["bounded"], gs["incumbent"]))
+            if gs["pending"] == 0 or time.perf_counter() - t0 > args.max_seconds:
+                break
+    else:
+        r0 = ctx.explorer_start_solve(None)
+        dev_ms, rounds, trace = 0.0, 1, []
+        while True:
+            r, t = ctx.explorer_run([args.target], 500, timing=True)
+            dev_ms += sum(x["round_ms"] for x in t)
+            rounds += len(r)
+            st = ctx.explorer_state()
+            trace.append((round(time.perf_counter() - t0, 3), st["bounded"], st["incumbent"]))
+            if st["pending"] == 0 or not r or time.perf_counter() - t0 > args.max_seconds:
+                break
     wall = time.perf_counter() - t0
     clocks = sampler.result() if sampler else None
-    st = ctx.explorer_state()
+    if group is not None:
+        v, sched = group.best()
+        st = {"pending": gs["pending"], "incumbent": v if v is not None else gs["incumbent"],
+              "bounded": gs["bounded"], "branched": gs["branched"], "pruned": gs["pruned"],
+              "leaves": gs["leaves"]}
+    else:
+        st = ctx.explorer_state()
+        sched = st["schedule"]
     done = st["pending"] == 0
-    sched = st["schedule"]
     cpu = None
     if not args.no_cpu_baseline:
         from oracle import REF_SO, Ref
@@ -677,7 +704,10 @@ def solve_mode(args, inst_name):
         "config": {"workload": f"{inst_name} {n}x{m} solve() from the identity-permutation "
                                f"makespan, pool target {args.target}, to proven optimality "
                                f"(pending tree empty) or {args.max_seconds:.0f} s",
-                   "instance": inst_name, "pool_target": args.target, "parallelism": "dp1"},
+                   "instance": inst_name, "pool_target": args.target,
+                   "parallelism": (f"fbb_group of {args.group} members (incumbent min-exchange "
+                                   f"every {args.exchange_every} rounds)" if group is not None
+                                   else "dp1")},
         "explore_seconds": wall, "device_seconds": dev_ms / 1e3, "exhausted": done,
         "optimum": st["incumbent"] if done else None, "incumbent": st["incumbent"],
         "schedule": sched, "schedule_makespan": fbb.makespan(inst, sched) if sched else None,
