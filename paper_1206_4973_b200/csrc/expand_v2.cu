@@ -759,8 +759,8 @@ cudaError_t launch_k2_v2(const DevTables& t, const K2Config& cfg, const Pool* d_
         return place_hint == 0                                                                \
                    ? launch_pdl(k2_v2_kernel<NN, MM, OO, false>, dim3(blocks), dim3(cfg.threads), cfg.smem, \
                                 stream, pdl, t, d_pool, first_seg, cfg.cmax, 0, frozen, rs, out)  \
-                   : launch_pdl(k2_v2_kernel<NN, MM, OO, true>, dim3(blocks), dim3(cfg.threads), cfg.smem, \
-                                stream, pdl, t, d_pool, first_seg, cfg.cmax, place_hint, frozen, rs, out);
+                   : launch_coop(k2_v2_kernel<NN, MM, OO, true>, dim3(blocks), dim3(cfg.threads), cfg.smem, \
+                                 stream, pdl, t, d_pool, first_seg, cfg.cmax, place_hint, frozen, rs, out);
     switch (cfg.variant) {
         V2_CASE(20, 5, 2)
         V2_CASE(20, 10, 2)

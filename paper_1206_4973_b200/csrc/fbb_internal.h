@@ -313,6 +313,28 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
     return cudaLaunchKernelEx(&lc, kern, static_cast<KArgs>(args)...);
 }
 
+// Same, as a cooperative launch: the grid is gang-scheduled (all CTAs resident at once),
+// which the direct-placement K2 needs for its grid-wide count -- without it, two such grids
+// running concurrently (two contexts on one device) could each hold SMs while waiting for
+// CTAs of their own that cannot be scheduled.
+template <class... KArgs, class... Args>
+inline cudaError_t launch_coop(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                               bool pdl, Args... args) {
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = grid;
+    lc.blockDim = block;
+    lc.dynamicSmemBytes = smem;
+    lc.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = pdl ? 2 : 1;
+    return cudaLaunchKernelEx(&lc, kern, static_cast<KArgs>(args)...);
+}
+
 // Chunk geometry of a segment: parents per chunk.
 __host__ __device__ inline int parents_per_chunk(int n, int depth, int cmax, int ppc_cap) {
     int r = n - depth;

@@ -31,4 +31,21 @@ for n, m in [(20, 20), (20, 5), (50, 20), (100, 20), (12, 7)]:
         ctx.explorer_reset(fbb.NodeBatch.root(inst), 10**6, frozen=True)
         ctx.explorer_run([2048], n + 2 if n <= 20 else 3)
     ctx.close()
+    # direct placement (single-wave pools: K2 grid-wide count + direct bucket writes) and the
+    # device-planned graph batches, in solve mode (leaf rounds, incumbent updates)
+    for dl in ("0", "1"):
+        os.environ["FBB_DEVICE_LOOP"] = dl
+        ctx = fbb.Context(inst)
+        ctx.explorer_set_residency(False)
+        ctx.explorer_start_solve(None)
+        ctx.explorer_run([256, 1024], 12)
+        ctx.close()
+    os.environ["FBB_DEVICE_LOOP"] = "0"
     print("ok", n, m, flush=True)
+# the in-library multi-device group (two members on one device)
+inst = fbb.generate_instance(12, 6, 123)
+grp = fbb.DeviceGroup(inst, [0, 0])
+grp.reset(fbb.NodeBatch.root(inst), 10**6, frozen=True)
+grp.run(512, max_steps=3, rounds_per_step=2)
+grp.close()
+print("ok group", flush=True)

@@ -103,3 +103,28 @@ def test_device_ranks_solve_reaches_the_oracle_optimum(oracle):
     s = out[0][3]
     assert s is not None and sorted(s) == list(range(10))
     assert oracle.makespan(p, s) == opt["optimum"]
+
+
+@pytest.mark.timeout(600)
+def test_group_members_sharing_a_gpu_with_single_wave_pools():
+    """Two group members on one GPU run K2 concurrently; with ~200-chunk pools each round is
+    single-wave (direct placement: its CTAs wait for each other), but the two grids together
+    exceed the device.  The cooperative launch gang-schedules each grid, so neither can hold
+    SMs while waiting for its own unscheduled CTAs.  Totals to a node budget's exhaustion
+    equal one context's (frozen exploration is partition-invariant)."""
+    import paper_1206_4973_b200 as fbb
+
+    inst = fbb.generate_instance(20, 20, 479340445)
+    ub = 2230  # below the optimum 2297: a tree the GPU exhausts in seconds
+    one = fbb.Context(inst)
+    one.explorer_reset(fbb.NodeBatch.root(inst), ub, frozen=True)
+    one.explorer_run([30000], 1 << 20)
+    st1 = one.explorer_state()
+    one.close()
+    assert st1["pending"] == 0
+    grp = fbb.DeviceGroup(inst, [0, 0])
+    grp.reset(fbb.NodeBatch.root(inst), ub, frozen=True)
+    gs = grp.run(30000, rounds_per_step=2, balance_every=1)
+    assert gs["pending"] == 0 and gs["bounded"] == st1["bounded"]
+    assert gs["pruned"] == st1["pruned"] and gs["leaves"] == st1["leaves"]
+    grp.close()
