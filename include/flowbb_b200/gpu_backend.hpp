@@ -112,11 +112,10 @@ public:
         const int n = inst.jobs(), m = inst.machines(), W = (n + 63) / 64;
         thread_local std::vector<uint64_t> masks;  // reused across calls (no re-initialisation)
         thread_local std::vector<int32_t> heads, depth;
-        if (depth.size() < nodes.size()) {
-            masks.resize(nodes.size() * W);
-            heads.resize(nodes.size() * m);
-            depth.resize(nodes.size());
-        }
+        // each buffer sized on its own: W and m change with the instance
+        if (masks.size() < nodes.size() * W) masks.resize(nodes.size() * W);
+        if (heads.size() < nodes.size() * m) heads.resize(nodes.size() * m);
+        if (depth.size() < nodes.size()) depth.resize(nodes.size());
         for (std::size_t i = 0; i < nodes.size(); ++i) {
             detail::pack(inst, nodes[i], &masks[i * W], &heads[i * m], nullptr);
             depth[i] = nodes[i].depth();
@@ -186,23 +185,20 @@ inline RoundCounts gpu_round(const GpuBackend& backend, const flowbb::Instance& 
         flowbb::Node node = pending.pop();
         ++rc.branched;
         std::size_t i = depth.size();
-        if (masks.size() < (i + 1) * W) {
-            masks.resize(2 * (i + 1) * W);
-            heads.resize(2 * (i + 1) * m);
-            prefix.resize(2 * (i + 1) * n);
-        }
+        // each buffer sized on its own (n, m, W change with the instance)
+        if (masks.size() < (i + 1) * W) masks.resize(2 * (i + 1) * W);
+        if (heads.size() < (i + 1) * m) heads.resize(2 * (i + 1) * m);
+        if (prefix.size() < (i + 1) * n) prefix.resize(2 * (i + 1) * n);
         detail::pack(inst, node, &masks[i * W], &heads[i * m], &prefix[i * n]);
         depth.push_back(node.depth());
         children += static_cast<std::size_t>(n - node.depth());
     }
     if (depth.empty()) return rc;
-    if (odepth.size() < children) {
-        omask.resize(children * W);
-        oheads.resize(children * m);
-        odepth.resize(children);
-        olb.resize(children);
-        oprefix.resize(children * n);
-    }
+    if (omask.size() < children * W) omask.resize(children * W);
+    if (oheads.size() < children * m) oheads.resize(children * m);
+    if (odepth.size() < children) odepth.resize(children);
+    if (olb.size() < children) olb.resize(children);
+    if (oprefix.size() < children * n) oprefix.resize(children * n);
     std::vector<int32_t> sched(n);
     int64_t count = 0, pos = 0;
     int32_t leaf_best = 0;
