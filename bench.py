@@ -178,13 +178,13 @@ class ClockSampler:
 
 def k2_traffic(inst_name):
     """DRAM bytes (read + write) of one K2 launch from the committed ncu --set full capture
-    (profiles/r01_k2_dram.json), when one exists for this instance; else None."""
+    (profiles/r02_k2_dram.json), when one exists for this instance; else None."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r01_k2_dram.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r02_k2_dram.json")) as f:
             d = json.load(f)[inst_name]
         return {"bytes_per_launch": d["dram_read_bytes"] + d["dram_write_bytes"],
                 "children_per_launch": d["children_per_launch"], "kernel": d["kernel"],
-                "source": "ncu --set full, profiles/r01_k2_dram.json"}
+                "source": "ncu --set full, profiles/r02_k2_dram.json"}
     except Exception:  # noqa: BLE001
         return None
 
