@@ -368,6 +368,10 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
     // CTAs than chunks; those have nothing to do)
     int64_t chunk = (DIR && direct) ? c_begin + blockIdx.x : claim_chunk(rs, c_begin, s_slot);
     if (DIR && direct && chunk >= c_end) return;
+    // the prologue's row tables complete before any scan reads them: claim_chunk's barrier
+    // does this in the staged form (the row loads are non-volatile asm, which the compiler
+    // may hoist up to the nearest barrier -- racecheck caught them above the staging one)
+    if (DIR && direct) __syncthreads();
     if constexpr (kPipe) prefetch(chunk);
     while (chunk < c_end) {
         int s, depth, np;
