@@ -11,6 +11,7 @@
 //              (integrate, search.hpp:84-107 / bench.hpp:96-106).
 // Only the per-segment survivor counts and the leaf minimum come back.
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <climits>
 #include <cstdio>
@@ -172,6 +173,9 @@ struct Store {
 }  // namespace
 
 static std::mutex g_err_mu;
+// live contexts per device (this process): K2's direct placement is gang-scheduled (a
+// cooperative launch) only when another context may run kernels on the same device
+static std::atomic<int> g_ctx_on_device[64];
 static std::string g_create_err = "";
 static int g_create_status = FBB_OK;
 
@@ -823,7 +827,8 @@ int explorer_run_batched(fbb_ctx* ctx, const int64_t* targets, int ntargets, int
         static const bool use_graph = [] { const char* e = getenv("FBB_LOOP_GRAPH"); return !(e && e[0] == '0'); }();
         static const bool loop_pdl = [] { const char* e = getenv("FBB_PDL"); return !(e && e[0] == '0'); }();
         if (use_graph) {
-            const LoopGraphKey key{2 * Rg + (all_direct ? 1 : 0), out.nodes.masks, out.nodes.heads,
+            const LoopGraphKey key{4 * Rg + (all_direct ? 2 : 0) + (device_shared(ctx->device) ? 1 : 0),
+                                   out.nodes.masks, out.nodes.heads,
                                    out.nodes.prefix, out.lb, out.count, out.seg, dl, hl};
             cudaGraphExec_t exec = nullptr;
             for (auto& kv : ctx->loop_graphs)
@@ -911,6 +916,14 @@ int explorer_run_batched(fbb_ctx* ctx, const int64_t* targets, int ntargets, int
 
 }  // namespace
 
+namespace fbb {
+bool device_shared(int device) {
+    // FBB_COOP=1: always (e.g. several processes sharing a GPU through MPS)
+    static const bool force = [] { const char* e = getenv("FBB_COOP"); return e && e[0] == '1'; }();
+    return force || device < 0 || device >= 64 || g_ctx_on_device[device].load() > 1;
+}
+}  // namespace fbb
+
 // =========================================================================================
 extern "C" {
 
@@ -956,14 +969,17 @@ fbb_ctx* fbb_create(int device, const int32_t* p, int n, int m) {
                                     std::to_string(prop.major * 10 + prop.minor));
     fbb_ctx* ctx = new fbb_ctx();
     ctx->device = device;
+    if (device >= 0 && device < 64) g_ctx_on_device[device].fetch_add(1);
     std::string why;
     int rc = build_host_tables(p, n, m, &ctx->ht, &why);
     if (rc != FBB_OK) {
+        g_ctx_on_device[device].fetch_sub(1);
         delete ctx;
         return fail(rc, why);
     }
     cudaSetDevice(device);
     if ((e = cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking)) != cudaSuccess) {
+        g_ctx_on_device[device].fetch_sub(1);
         delete ctx;
         return fail(FBB_E_CUDA, std::string("stream: ") + cudaGetErrorString(e));
     }
@@ -1047,6 +1063,7 @@ fbb_ctx* fbb_create(int device, const int32_t* p, int n, int m) {
 
 void fbb_destroy(fbb_ctx* ctx) {
     if (!ctx) return;
+    if (ctx->device >= 0 && ctx->device < 64) g_ctx_on_device[ctx->device].fetch_sub(1);
     cudaSetDevice(ctx->device);
     free_tables(&ctx->dt);
     for (DBuf* b : {&ctx->k1_masks, &ctx->k1_heads, &ctx->k1_depth, &ctx->k1_lb, &ctx->out_lb,

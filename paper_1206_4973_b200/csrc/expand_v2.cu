@@ -758,13 +758,24 @@ bool k2_v2_config(const DevTables& t, int device, K2Config* out) {
 cudaError_t launch_k2_v2(const DevTables& t, const K2Config& cfg, const Pool* d_pool, int first_seg,
                          int blocks, int place_hint, int frozen, RoundState* rs, ChunkOut out,
                          cudaStream_t stream, bool pdl) {
+    // direct placement waits for every CTA of the grid: gang-schedule it (cooperative
+    // launch, ~2-3 us more per launch) whenever another context of this process may run
+    // kernels on the device concurrently; alone on the device, a single-wave grid that fits
+    // the occupancy-derived CTA count is resident as a whole anyway
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const bool coop = place_hint != 0 && device_shared(dev);
 #define V2_CASE(NN, MM, OO)                                                                   \
     case OO * 10000 + NN * 100 + MM:                                                          \
         return place_hint == 0                                                                \
                    ? launch_pdl(k2_v2_kernel<NN, MM, OO, false>, dim3(blocks), dim3(cfg.threads), cfg.smem, \
                                 stream, pdl, t, d_pool, first_seg, cfg.cmax, 0, frozen, rs, out)  \
-                   : launch_coop(k2_v2_kernel<NN, MM, OO, true>, dim3(blocks), dim3(cfg.threads), cfg.smem, \
-                                 stream, pdl, t, d_pool, first_seg, cfg.cmax, place_hint, frozen, rs, out);
+                   : coop ? launch_coop(k2_v2_kernel<NN, MM, OO, true>, dim3(blocks), dim3(cfg.threads), \
+                                        cfg.smem, stream, pdl, t, d_pool, first_seg, cfg.cmax, place_hint, \
+                                        frozen, rs, out)                                        \
+                          : launch_pdl(k2_v2_kernel<NN, MM, OO, true>, dim3(blocks), dim3(cfg.threads), \
+                                       cfg.smem, stream, pdl, t, d_pool, first_seg, cfg.cmax, place_hint, \
+                                       frozen, rs, out);
     switch (cfg.variant) {
         V2_CASE(20, 5, 2)
         V2_CASE(20, 10, 2)

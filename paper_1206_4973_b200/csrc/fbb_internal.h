@@ -313,6 +313,10 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
     return cudaLaunchKernelEx(&lc, kern, static_cast<KArgs>(args)...);
 }
 
+// More than one live context of this process on `device` (capi.cu): kernels of several
+// contexts may then run on it concurrently.
+bool device_shared(int device);
+
 // Same, as a cooperative launch: the grid is gang-scheduled (all CTAs resident at once),
 // which the direct-placement K2 needs for its grid-wide count -- without it, two such grids
 // running concurrently (two contexts on one device) could each hold SMs while waiting for
