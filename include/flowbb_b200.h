@@ -250,6 +250,14 @@ int fbb_group_start_solve(fbb_group* g, int32_t ub);
  * `budget` (> 0).  stats may be NULL. */
 int fbb_group_run(fbb_group* g, int64_t target, int64_t max_steps, int rounds_per_step,
                   int balance_every, int64_t budget, fbb_group_stats_t* stats);
+/* The group's (and paper_1206_4973_b200/parallel.py's) deterministic rebalancing plan over
+ * G pending sizes: receivers in ascending (pending, index) order below `low` take half the
+ * difference (<= cap) from the richest member above 2*low that has not donated yet.
+ * Writes up to G (donor, receiver, count) triples to plan (3*G int64) and their number to
+ * *count.  Host-only: a multi-process C++ driver computes the same plan on every rank. */
+int fbb_plan_transfers(const int64_t* pending, int G, int64_t low, int64_t cap, int64_t* plan,
+                       int* count);
+
 /* Group best leaf: min over members of (value, member index); returns 1 and its value
  * (and, in solve mode, its schedule) when found, else 0 with *value = INT32_MAX. */
 int fbb_group_best(fbb_group* g, int32_t* value, int32_t* schedule);

@@ -28,7 +28,7 @@ EXPORTED = (
     "fbb_tuner_best_throughput", "fbb_tuner_set_trace", "fbb_version", "fbb_kernels",
     "fbb_group_create", "fbb_group_destroy", "fbb_group_size", "fbb_group_context",
     "fbb_group_last_error", "fbb_group_reset", "fbb_group_start_solve", "fbb_group_run",
-    "fbb_group_best",
+    "fbb_group_best", "fbb_plan_transfers",
 )
 
 
@@ -166,6 +166,7 @@ def load_library(path: str = LIB_PATH):
     L.fbb_group_run.argtypes = [_vp, C.c_int64, C.c_int64, C.c_int, C.c_int, C.c_int64,
                                 C.POINTER(GroupStats)]
     L.fbb_group_best.argtypes = [_vp, C.POINTER(C.c_int32), _i32p]
+    L.fbb_plan_transfers.argtypes = [_i64p, C.c_int, C.c_int64, C.c_int64, _i64p, C.POINTER(C.c_int)]
     _lib = L
     return L
 

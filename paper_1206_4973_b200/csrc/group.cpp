@@ -313,6 +313,19 @@ int fbb_group_run(fbb_group* g, int64_t target, int64_t max_steps, int rounds_pe
     return FBB_OK;
 }
 
+int fbb_plan_transfers(const int64_t* pending, int G, int64_t low, int64_t cap, int64_t* plan,
+                       int* count) {
+    if (!pending || !plan || !count || G < 1) return FBB_E_ARG;
+    const std::vector<Transfer> p = plan_transfers(std::vector<int64_t>(pending, pending + G), low, cap);
+    for (size_t i = 0; i < p.size(); ++i) {
+        plan[3 * i] = p[i].donor;
+        plan[3 * i + 1] = p[i].receiver;
+        plan[3 * i + 2] = p[i].count;
+    }
+    *count = (int)p.size();
+    return FBB_OK;
+}
+
 int fbb_group_best(fbb_group* g, int32_t* value, int32_t* schedule) {
     if (!g) return FBB_E_ARG;
     int32_t best = INT32_MAX;

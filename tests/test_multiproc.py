@@ -190,3 +190,25 @@ def test_parallel_solve_reaches_the_optimum_with_ub_exchange(world, oracle):
     assert vals == {opt["optimum"]}
     s = out[0][3]
     assert s is not None and oracle.makespan(p, s) == opt["optimum"]
+
+
+def test_library_and_python_transfer_plans_agree():
+    """The in-library group (csrc/group.cpp) and the multi-process driver (parallel.py)
+    compute the same deterministic rebalancing plan from the same pending sizes."""
+    import ctypes as C
+
+    import paper_1206_4973_b200 as fbb
+    from paper_1206_4973_b200.parallel import plan_transfers
+
+    L = fbb.load_library()
+    rng = np.random.default_rng(17)
+    for trial in range(400):
+        G = int(rng.integers(1, 9))
+        pend = rng.integers(0, 3, size=G) * rng.integers(0, 5000, size=G)
+        low, cap = int(rng.integers(1, 600)), int(rng.integers(1, 2000))
+        out = np.zeros(3 * G, np.int64)
+        cnt = C.c_int(0)
+        assert L.fbb_plan_transfers(np.ascontiguousarray(pend, np.int64), G, low, cap, out,
+                                    C.byref(cnt)) == 0
+        lib = [tuple(int(x) for x in out[3 * i:3 * i + 3]) for i in range(cnt.value)]
+        assert lib == plan_transfers([int(x) for x in pend], low, cap), (pend, low, cap)
