@@ -152,6 +152,27 @@ def main(tag):
         p = os.path.join(OUT, rep)
         if os.path.exists(p):
             md += ["", f"## ncu --set full: {title}", ncu_metrics(p)]
+    extra = []
+    for f, title in [("solve_ta001.json", "Ta001 solve() from the identity UB, one context"),
+                     ("solve_ta001_group2.json", "Ta001 solve() over an fbb_group of 2 (GPU 0 twice)"),
+                     ("exhaust_group2.json", "Ta021 exhaustion at UB 2298 over an fbb_group of 2"),
+                     ("bench_bound_ta101_max.json", "Ta101 K1 over a pool filling the GPU's HBM")]:
+        d = bench_line(os.path.join(OUT, f))
+        if not d:
+            continue
+        keep = {k: d[k] for k in ("value", "explore_seconds", "device_seconds", "exhausted", "optimum",
+                                  "incumbent", "bounded", "group", "proof", "config", "cpu_baseline",
+                                  "roofline") if k in d}
+        extra += ["", f"### {title} (`{f}`)", "", "```json", json.dumps(keep, indent=1)[:3000], "```"]
+        shutil.copy(os.path.join(OUT, f), os.path.join(PROF, f"{tag}_{f}"))
+    if extra:
+        md += ["", "## other configs (solve, group, HBM-filling pool)"] + extra
+    for f in ["sanitize_memcheck.txt", "sanitize_racecheck.txt", "sanitize_synccheck.txt"]:
+        q = os.path.join(OUT, f)
+        if os.path.exists(q):
+            lines = open(q).read().strip().splitlines()
+            md += ["", f"## {f}", "", "```", "\n".join(lines[-8:]), "```"]
+            shutil.copy(q, os.path.join(PROF, f"{tag}_{f}"))
     out = os.path.join(PROF, f"{tag}_summary.md")
     with open(out, "w") as f:
         f.write("\n".join(md) + "\n")
