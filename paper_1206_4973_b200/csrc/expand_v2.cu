@@ -327,7 +327,12 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
     constexpr bool kPipe = OCC == 2 && N != 32;  // (N = 32: the prefetch registers spill)
     constexpr int kPpcCt = N <= 32 ? 32 : 16;                  // >= parents per chunk (v2_ppc_cap)
     constexpr int kPfPre = (kPpcCt * N + 191) / 192;           // prefix bytes per thread
+    constexpr int kPfPreW = (kPpcCt * (N / 4) + 191) / 192;    // prefix words per thread
     constexpr int kPfHead = (kPpcCt * M + 191) / 192;          // heads per thread
+    // n % 4 == 0 (Ta 20x5 / 20x10 / 20x20): prefix rows are word aligned everywhere (device
+    // buckets and host arena blocks are 256-byte aligned), so they are staged as 32-bit
+    // words -- a quarter of the loads, which matters most over the host link
+    const bool n4 = (n & 3) == 0;
     uint32_t pf_pre[kPipe ? kPfPre : 1];
     int32_t pf_head[kPipe ? kPfHead : 1];
     uint64_t pf_mask = 0;
@@ -346,12 +351,25 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
         chunk_geo(c, s_, depth_, np_, p0_);
         const Segment& g_ = pool->seg[s_];
         const bool cpt_ = g_.src.heads == nullptr;  // compact rows: prefixes only
+        if (n4) {
+            const int wpr = (depth_ + 3) >> 2;
+            const uint32_t* src32 = reinterpret_cast<const uint32_t*>(g_.src.prefix);
 #pragma unroll
-        for (int u = 0; u < kPfPre; ++u) {
-            const int x = tid + u * 192;
-            if (x < np_ * depth_) {
-                const int pp = x / depth_, i = x - pp * depth_;
-                pf_pre[u] = g_.src.prefix[(g_.first + g_.step * (p0_ + pp)) * n + i];
+            for (int u = 0; u < kPfPreW; ++u) {
+                const int x = tid + u * 192;
+                if (x < np_ * wpr) {
+                    const int pp = x / wpr, w = x - pp * wpr;
+                    pf_pre[u] = src32[((g_.first + g_.step * (p0_ + pp)) * n >> 2) + w];
+                }
+            }
+        } else {
+#pragma unroll
+            for (int u = 0; u < kPfPre; ++u) {
+                const int x = tid + u * 192;
+                if (x < np_ * depth_) {
+                    const int pp = x / depth_, i = x - pp * depth_;
+                    pf_pre[u] = g_.src.prefix[(g_.first + g_.step * (p0_ + pp)) * n + i];
+                }
             }
         }
 #pragma unroll
@@ -383,12 +401,24 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
         const uint64_t valid = n >= 64 ? ~0ull : ((1ull << n) - 1ull);
         const bool compact = sg.src.heads == nullptr;  // prefix-only rows (host-resident tree)
         if constexpr (kPipe) {
+            if (n4) {
+                const int wpr = (depth + 3) >> 2;
 #pragma unroll
-            for (int u = 0; u < kPfPre; ++u) {
-                const int x = tid + u * 192;
-                if (x < np * depth) {
-                    const int pp = x / depth, i = x - pp * depth;
-                    s_pre[pp * RW + i] = (uint8_t)pf_pre[u];
+                for (int u = 0; u < kPfPreW; ++u) {
+                    const int x = tid + u * 192;
+                    if (x < np * wpr) {
+                        const int pp = x / wpr, w = x - pp * wpr;
+                        reinterpret_cast<uint32_t*>(s_pre)[pp * (RW / 4) + w] = pf_pre[u];
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int u = 0; u < kPfPre; ++u) {
+                    const int x = tid + u * 192;
+                    if (x < np * depth) {
+                        const int pp = x / depth, i = x - pp * depth;
+                        s_pre[pp * RW + i] = (uint8_t)pf_pre[u];
+                    }
                 }
             }
 #pragma unroll
@@ -400,9 +430,19 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
         } else {
             const NodeStore src = sg.src;
             const int64_t first = sg.first, step = sg.step;
-            for (int x = tid; x < np * depth; x += bd) {
-                int pp = x / depth, i = x - pp * depth;
-                s_pre[pp * RW + i] = src.prefix[(first + step * (p0 + pp)) * n + i];
+            if (n4) {
+                const int wpr = (depth + 3) >> 2;
+                const uint32_t* src32 = reinterpret_cast<const uint32_t*>(src.prefix);
+                for (int x = tid; x < np * wpr; x += bd) {
+                    const int pp = x / wpr, w = x - pp * wpr;
+                    reinterpret_cast<uint32_t*>(s_pre)[pp * (RW / 4) + w] =
+                        src32[((first + step * (p0 + pp)) * n >> 2) + w];
+                }
+            } else {
+                for (int x = tid; x < np * depth; x += bd) {
+                    int pp = x / depth, i = x - pp * depth;
+                    s_pre[pp * RW + i] = src.prefix[(first + step * (p0 + pp)) * n + i];
+                }
             }
             for (int pp = tid; pp < np && !compact; pp += bd) {
                 int64_t node = first + step * (p0 + pp);
