@@ -113,6 +113,9 @@ __global__ void __launch_bounds__(NW <= 4 ? 192 : 256, NW <= 4 ? 4 : 2)
     asm volatile("griddepcontrol.launch_dependents;");  // place_kernel may be scheduled early
     constexpr int P = M * (M - 1) / 2;
     constexpr int N = 32 * NW;
+    // scan unroll (independent row / table loads in flight per thread): 16 where the
+    // 2-CTA variant's 128-register budget allows it, 8 under the 4-CTA 80-register cap
+    constexpr int kV3Unroll = NW <= 4 ? 8 : 16;
     extern __shared__ __align__(16) unsigned char smem[];
     const int n = t.n, W = t.W;
     const V3Layout L = v3_layout(M, P, cmax, blockDim.x, NW);
@@ -259,7 +262,7 @@ __global__ void __launch_bounds__(NW <= 4 ? 192 : 256, NW <= 4 ? 4 : 2)
                 const uint32_t base_sa =
                     (uint32_t)__cvta_generic_to_shared(s_Mq + (size_t)(pp * r) * L.rowb + 2 * q);
                 int32_t D = 0, PM = -32768;  // PM stays within int16 (stored as is)
-#pragma unroll 8
+#pragma unroll kV3Unroll
                 for (int i = 0; i < n; ++i) {
                     const uint32_t e = __ldg(rowq + i * P);
                     const uint32_t ent = v3_lds_u16(tab_sa + (e & 0xFFu) * 2u);
@@ -274,7 +277,7 @@ __global__ void __launch_bounds__(NW <= 4 ? 192 : 256, NW <= 4 ? 4 : 2)
                     D += dm;
                 }
                 int32_t SM = -32768;
-#pragma unroll 8
+#pragma unroll kV3Unroll
                 for (int i = n - 1; i >= 0; --i) {
                     const uint32_t e = __ldg(rowq + i * P);
                     const uint32_t ent = v3_lds_u16(tab_sa + (e & 0xFFu) * 2u);
