@@ -226,6 +226,7 @@ struct fbb_ctx {
     // captured batches (explorer_run_batched), one per (length, buffers); lengths are
     // powers of two, so a context captures at most a handful
     std::vector<std::pair<LoopGraphKey, cudaGraphExec_t>> loop_graphs;
+    cudaStream_t capture_stream = nullptr;  // captures the conditional loop body
     bool device_loop = false;          // FBB_DEVICE_LOOP=1: batched device-planned rounds
     float last_k2_ms = 0.f, last_round_ms = 0.f, last_sync_ms = 0.f, last_place_ms = 0.f;
     int last_launches = 0;
@@ -810,10 +811,6 @@ int explorer_run_batched(fbb_ctx* ctx, const int64_t* targets, int ntargets, int
         // download -- every kernel a programmatic dependent of the one before, the whole
         // sequence one CUDA graph (captured once per batch length and staging buffers, then
         // replayed: one host call per batch)
-        // graph length: R rounded up to a power of two (the rounds past hl->nrounds plan
-        // nothing and every kernel of theirs exits at once)
-        int Rg = 1;
-        while (Rg < R) Rg <<= 1;
         auto enqueue = [&](bool pdl, int rounds) -> cudaError_t {
             cudaError_t e = cudaMemcpyAsync(dl, hl, offsetof(LoopState, rec), cudaMemcpyHostToDevice, st);
             for (int i = 0; i < rounds && e == cudaSuccess; ++i) {
@@ -827,7 +824,11 @@ int explorer_run_batched(fbb_ctx* ctx, const int64_t* targets, int ntargets, int
         static const bool use_graph = [] { const char* e = getenv("FBB_LOOP_GRAPH"); return !(e && e[0] == '0'); }();
         static const bool loop_pdl = [] { const char* e = getenv("FBB_PDL"); return !(e && e[0] == '0'); }();
         if (use_graph) {
-            const LoopGraphKey key{4 * Rg + (all_direct ? 2 : 0) + (device_shared(ctx->device) ? 1 : 0),
+            // one graph for every batch length: state upload, a step planning round 0, then a
+            // conditional WHILE node whose body -- leaves, leaf schedule, K2, [place], step --
+            // repeats while the step planned another round (the round index lives in the loop
+            // state), then the state download
+            const LoopGraphKey key{(all_direct ? 2 : 0) + (device_shared(ctx->device) ? 1 : 0),
                                    out.nodes.masks, out.nodes.heads,
                                    out.nodes.prefix, out.lb, out.count, out.seg, dl, hl};
             cudaGraphExec_t exec = nullptr;
@@ -838,14 +839,43 @@ int explorer_run_batched(fbb_ctx* ctx, const int64_t* targets, int ntargets, int
                     for (auto& kv : ctx->loop_graphs) cudaGraphExecDestroy(kv.second);
                     ctx->loop_graphs.clear();
                 }
+                if (!ctx->capture_stream)
+                    CK(cudaStreamCreateWithFlags(&ctx->capture_stream, cudaStreamNonBlocking), "stream");
                 cudaGraph_t g = nullptr;
+                cudaGraphConditionalHandle cond;
+                cudaStreamCaptureStatus cs;
+                const cudaGraphNode_t* deps = nullptr;
+                size_t ndeps = 0;
+                cudaGraphNode_t cnode;
                 CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "loop capture");
-                cudaError_t ce = enqueue(loop_pdl, Rg);
-                cudaError_t ee = cudaStreamEndCapture(st, &g);
+                cudaError_t ce = cudaMemcpyAsync(dl, hl, offsetof(LoopState, rec), cudaMemcpyHostToDevice, st);
+                if (ce == cudaSuccess) ce = cudaStreamGetCaptureInfo(st, &cs, nullptr, &g, &deps, &ndeps);
+                if (ce == cudaSuccess) ce = cudaGraphConditionalHandleCreate(&cond, g, 0, 0);
+                if (ce == cudaSuccess) ce = launch_loop_step_dyn(ctx->dt, dl, dp, rs, cond, st, false);
+                if (ce == cudaSuccess) ce = cudaStreamGetCaptureInfo(st, &cs, nullptr, &g, &deps, &ndeps);
+                cudaGraphNodeParams cp = {};
+                cp.type = cudaGraphNodeTypeConditional;
+                cp.conditional.handle = cond;
+                cp.conditional.type = cudaGraphCondTypeWhile;
+                cp.conditional.size = 1;
+                if (ce == cudaSuccess) ce = cudaGraphAddNode(&cnode, g, deps, ndeps, &cp);
+                if (ce == cudaSuccess) {  // the loop body, captured on a second stream
+                    cudaStream_t bs = ctx->capture_stream;
+                    ce = cudaStreamBeginCaptureToGraph(bs, cp.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                                       cudaStreamCaptureModeRelaxed);
+                    if (ce == cudaSuccess) ce = launch_round_device(ctx->dt, ctx->k2, dp, rs, out, bs, loop_pdl, !all_direct);
+                    if (ce == cudaSuccess) ce = launch_loop_step_dyn(ctx->dt, dl, dp, rs, cond, bs, loop_pdl);
+                    cudaError_t be = cudaStreamEndCapture(bs, nullptr);
+                    if (ce == cudaSuccess) ce = be;
+                }
+                if (ce == cudaSuccess) ce = cudaStreamUpdateCaptureDependencies(st, &cnode, 1, cudaStreamSetCaptureDependencies);
+                if (ce == cudaSuccess) ce = cudaMemcpyAsync(hl, dl, sizeof(LoopState), cudaMemcpyDeviceToHost, st);
+                cudaGraph_t gg = nullptr;
+                cudaError_t ee = cudaStreamEndCapture(st, &gg);
                 CK(ce, "loop capture");
                 CK(ee, "loop capture");
-                ce = cudaGraphInstantiate(&exec, g, 0);
-                cudaGraphDestroy(g);
+                ce = cudaGraphInstantiate(&exec, gg, 0);
+                cudaGraphDestroy(gg);
                 CK(ce, "loop graph instantiate");
                 ctx->loop_graphs.emplace_back(key, exec);
             }
@@ -1086,6 +1116,7 @@ void fbb_destroy(fbb_ctx* ctx) {
     ctx->h_loop.release();
     ctx->d_loop.release();
     for (auto& kv : ctx->loop_graphs) cudaGraphExecDestroy(kv.second);
+    if (ctx->capture_stream) cudaStreamDestroy(ctx->capture_stream);
     for (cudaEvent_t ev : ctx->ev)
         if (ev) cudaEventDestroy(ev);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);

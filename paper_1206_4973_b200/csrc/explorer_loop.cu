@@ -205,7 +205,35 @@ __global__ void loop_step_kernel(DevTables t, LoopState* ls, Pool* pool, RoundSt
     for (int d = lane; d <= n; d += 32) ls->cnt[d] = s_cnt[d];
 }
 
+// The same step for a batch driven by a conditional WHILE node of the batch graph: the
+// round index lives in the loop state (ls->cur_round), and the kernel sets the loop
+// condition -- another iteration (leaves, K2, place, step) exactly when it planned a round.
+// One graph then serves every batch length.
+__global__ void loop_step_dyn_kernel(DevTables t, LoopState* ls, Pool* pool, RoundState* rs,
+                                     cudaGraphConditionalHandle cond) {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;");
+    __shared__ int64_t s_cnt[kMaxJobs + 1];
+    const int n = t.n, lane = threadIdx.x;
+    for (int d = lane; d <= n; d += 32) s_cnt[d] = ls->cnt[d];
+    __syncwarp();
+    if (lane == 0) {
+        const int round = ls->cur_round;
+        if (round > 0) close_round(t, ls, pool, rs, round - 1, s_cnt);
+        plan_round(t, ls, pool, rs, round, s_cnt);  // nothing planned past nrounds or a stop
+        ls->cur_round = round + 1;
+        cudaGraphSetConditional(cond, pool->nseg > 0 ? 1u : 0u);
+    }
+    __syncwarp();
+    for (int d = lane; d <= n; d += 32) ls->cnt[d] = s_cnt[d];
+}
+
 }  // namespace
+
+cudaError_t launch_loop_step_dyn(const DevTables& t, LoopState* ls, Pool* pool, RoundState* rs,
+                                 cudaGraphConditionalHandle cond, cudaStream_t stream, bool pdl) {
+    return launch_pdl(loop_step_dyn_kernel, dim3(1), dim3(32), 0, stream, pdl, t, ls, pool, rs, cond);
+}
 
 cudaError_t launch_loop_step(const DevTables& t, LoopState* ls, Pool* pool, RoundState* rs, int round,
                              bool last, cudaStream_t stream, bool pdl) {

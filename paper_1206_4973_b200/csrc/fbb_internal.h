@@ -279,6 +279,7 @@ struct LoopState {
     int64_t need_rows;                // ... to at least this many rows
     int32_t cmax, ppc_cap, nrounds, chunk_cap;  // chunk_cap: staging chunks available
     int32_t direct_cap;               // > 0: pools of at most this many chunks use direct placement
+    int32_t cur_round;                // conditional-graph batches: the round the next step closes / plans
     int32_t host_dst;                 // the buckets are pinned host memory (Pool::host_dst)
     int32_t schedule[kMaxJobs];       // incumbent schedule (solve mode)
     LoopRecord rec[kLoopMax];
@@ -286,6 +287,10 @@ struct LoopState {
 
 // pdl: each kernel of the batch is a programmatic dependent of the one before (every one
 // of them waits -- griddepcontrol.wait -- before it reads its predecessor's output)
+// the step of a batch driven by a conditional WHILE graph node (round index in the loop
+// state; sets the node's condition to "another round planned")
+cudaError_t launch_loop_step_dyn(const DevTables& t, LoopState* ls, Pool* pool, RoundState* rs,
+                                 cudaGraphConditionalHandle cond, cudaStream_t stream, bool pdl);
 // close of round - 1 (round > 0) + plan of round (!last), one single-warp kernel
 cudaError_t launch_loop_step(const DevTables& t, LoopState* ls, Pool* pool, RoundState* rs, int round,
                              bool last, cudaStream_t stream, bool pdl);
