@@ -227,7 +227,9 @@ struct fbb_ctx {
     // powers of two, so a context captures at most a handful
     std::vector<std::pair<LoopGraphKey, cudaGraphExec_t>> loop_graphs;
     cudaStream_t capture_stream = nullptr;  // captures the conditional loop body
-    bool device_loop = false;          // FBB_DEVICE_LOOP=1: batched device-planned rounds
+    // batched device-planned rounds (explorer_loop.cu): -1 (default) for calls of two rounds
+    // or more, FBB_DEVICE_LOOP=1 always, FBB_DEVICE_LOOP=0 never
+    int device_loop = -1;
     float last_k2_ms = 0.f, last_round_ms = 0.f, last_sync_ms = 0.f, last_place_ms = 0.f;
     int last_launches = 0;
 
@@ -737,8 +739,9 @@ int explorer_round(fbb_ctx* ctx, int64_t target, fbb_round_t* rec) {
 // with no host synchronisation inside a batch; same semantics and per-round records as
 // explorer_round.  Used when the parents can be read in place (HBM buckets, or host
 // buckets read and written through the mapping).
-bool device_loop_ok(const fbb_ctx* ctx) {
-    return ctx->device_loop && (!ctx->host_pending || (ctx->mapped_in && ctx->mapped_out));
+bool device_loop_ok(const fbb_ctx* ctx, int64_t max_rounds) {
+    const bool want = ctx->device_loop == 1 || (ctx->device_loop == -1 && max_rounds >= 2);
+    return want && (!ctx->host_pending || (ctx->mapped_in && ctx->mapped_out));
 }
 
 int explorer_run_batched(fbb_ctx* ctx, const int64_t* targets, int ntargets, int64_t max_rounds,
@@ -1077,11 +1080,12 @@ fbb_ctx* fbb_create(int device, const int32_t* p, int n, int m) {
     }
     explorer_clear(ctx);
     ctx->incumbent = INT_MAX;
-    // Measured (r01): the device-planned loop costs more device time per round (plan /
-    // close kernels and fixed-grid launches) than the host planner saves; it stays
-    // opt-in (FBB_DEVICE_LOOP=1) and covered by the parity tests.
+    // Measured (r02): a single round is cheapest host-planned (fewer, exactly sized
+    // launches: Ta021 262 K 121 vs 133 us of device time); a call of several rounds runs
+    // them as one conditional-graph batch with no host round trip (wall 160 vs 172 us per
+    // round with the tree in host memory, Ta021 e2e +7.5 %)
     const char* dlp = getenv("FBB_DEVICE_LOOP");
-    ctx->device_loop = dlp && dlp[0] == '1';
+    ctx->device_loop = !dlp ? -1 : (dlp[0] == '1' ? 1 : (dlp[0] == '0' ? 0 : -1));
     const char* sm = getenv("FBB_SUMMARY");
     ctx->summary_by_place = !(sm && std::string(sm) == "copy");
     const char* dir = getenv("FBB_DIRECT");
@@ -1427,7 +1431,8 @@ int fbb_explorer_run(fbb_ctx* ctx, const int64_t* targets, int ntargets, int64_t
     if (!ctx) return FBB_E_ARG;
     if (!targets || ntargets < 1) return ctx->fail(FBB_E_ARG, "need at least one target");
     cudaSetDevice(ctx->device);
-    if (device_loop_ok(ctx)) return explorer_run_batched(ctx, targets, ntargets, max_rounds, budget, rounds, done);
+    if (device_loop_ok(ctx, max_rounds))
+        return explorer_run_batched(ctx, targets, ntargets, max_rounds, budget, rounds, done);
     int64_t r = 0;
     if (done) *done = 0;
     while (r < max_rounds) {

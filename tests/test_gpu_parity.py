@@ -254,8 +254,14 @@ def test_k2_random_parents_vs_oracle(oracle):
 
 # ---- device-resident explorer ---------------------------------------------------------------
 
+@pytest.mark.parametrize("loop", ["auto", "0"], ids=["loop_auto", "host_planned"])
 @pytest.mark.parametrize("on_host", [False, True], ids=["pending_hbm", "pending_host"])
-def test_explorer_resolve_traces_match_reference(instances, traces, on_host):
+def test_explorer_resolve_traces_match_reference(instances, traces, on_host, loop, monkeypatch):
+    """Multi-round calls run as device-planned graph batches by default; FBB_DEVICE_LOOP=0
+    keeps every round host-planned.  Both reproduce the reference traces."""
+    if loop == "0":
+        monkeypatch.setenv("FBB_DEVICE_LOOP", "0")
+    fbb.flowbb._ctx_cache.clear()  # contexts read the switch when created
     for tr in traces["resolve"]:
         inst = inst_of(instance_p(instances, tr["instance"]))
         res = fbb.resolve_workload(inst, tr["roots"], tr["ub"], targets=tr["targets"],
@@ -266,8 +272,12 @@ def test_explorer_resolve_traces_match_reference(instances, traces, on_host):
         assert (res.best if res.best is not None else -1) == tr["result"]["optimum"]
 
 
+@pytest.mark.parametrize("loop", ["auto", "0"], ids=["loop_auto", "host_planned"])
 @pytest.mark.parametrize("on_host", [False, True], ids=["pending_hbm", "pending_host"])
-def test_explorer_solve_traces_match_reference(instances, traces, on_host):
+def test_explorer_solve_traces_match_reference(instances, traces, on_host, loop, monkeypatch):
+    if loop == "0":
+        monkeypatch.setenv("FBB_DEVICE_LOOP", "0")
+    fbb.flowbb._ctx_cache.clear()
     for tr in traces["solve"]:
         inst = inst_of(instance_p(instances, tr["instance"]))
         ub = None if tr["initial_ub"] < 0 else tr["initial_ub"]
