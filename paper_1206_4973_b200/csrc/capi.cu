@@ -226,7 +226,8 @@ struct fbb_ctx {
     // captured batches (explorer_run_batched), one per (length, buffers); lengths are
     // powers of two, so a context captures at most a handful
     std::vector<std::pair<LoopGraphKey, cudaGraphExec_t>> loop_graphs;
-    cudaStream_t capture_stream = nullptr;  // captures the conditional loop body
+    cudaStream_t capture_stream = nullptr;   // captures the conditional loop body ...
+    cudaStream_t capture_stream2 = nullptr;  // ... and the leaf branch inside it
     // batched device-planned rounds (explorer_loop.cu): -1 (default) for calls of two rounds
     // or more, FBB_DEVICE_LOOP=1 always, FBB_DEVICE_LOOP=0 never
     int device_loop = -1;
@@ -842,36 +843,58 @@ int explorer_run_batched(fbb_ctx* ctx, const int64_t* targets, int ntargets, int
                     for (auto& kv : ctx->loop_graphs) cudaGraphExecDestroy(kv.second);
                     ctx->loop_graphs.clear();
                 }
-                if (!ctx->capture_stream)
-                    CK(cudaStreamCreateWithFlags(&ctx->capture_stream, cudaStreamNonBlocking), "stream");
+                for (cudaStream_t* cs_ : {&ctx->capture_stream, &ctx->capture_stream2})
+                    if (!*cs_) CK(cudaStreamCreateWithFlags(cs_, cudaStreamNonBlocking), "stream");
+                // outer graph: state upload -> WHILE(loop_cond, starts at 1 every launch) ->
+                // state download.  Loop body: step (close the last round, plan the next, set
+                // both conditions) -> IF(leaf_cond) {leaf kernel -> leaf schedule} -> K2 ->
+                // [place].  Inside a body graph the kernels keep their programmatic edges
+                // except across the IF node (K2 waits for it in full).
                 cudaGraph_t g = nullptr;
-                cudaGraphConditionalHandle cond;
+                cudaGraphConditionalHandle loop_cond, leaf_cond;
                 cudaStreamCaptureStatus cs;
                 const cudaGraphNode_t* deps = nullptr;
                 size_t ndeps = 0;
-                cudaGraphNode_t cnode;
+                cudaGraphNode_t wnode, inode;
+                cudaGraphNodeParams wp = {}, ip = {};
                 CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "loop capture");
                 cudaError_t ce = cudaMemcpyAsync(dl, hl, sizeof(LoopState), cudaMemcpyHostToDevice, st);
                 if (ce == cudaSuccess) ce = cudaStreamGetCaptureInfo(st, &cs, nullptr, &g, &deps, &ndeps);
-                if (ce == cudaSuccess) ce = cudaGraphConditionalHandleCreate(&cond, g, 0, 0);
-                if (ce == cudaSuccess) ce = launch_loop_step_dyn(ctx->dt, dl, dp, rs, cond, st, false);
-                if (ce == cudaSuccess) ce = cudaStreamGetCaptureInfo(st, &cs, nullptr, &g, &deps, &ndeps);
-                cudaGraphNodeParams cp = {};
-                cp.type = cudaGraphNodeTypeConditional;
-                cp.conditional.handle = cond;
-                cp.conditional.type = cudaGraphCondTypeWhile;
-                cp.conditional.size = 1;
-                if (ce == cudaSuccess) ce = cudaGraphAddNode(&cnode, g, deps, ndeps, &cp);
-                if (ce == cudaSuccess) {  // the loop body, captured on a second stream
-                    cudaStream_t bs = ctx->capture_stream;
-                    ce = cudaStreamBeginCaptureToGraph(bs, cp.conditional.phGraph_out[0], nullptr, nullptr, 0,
-                                                       cudaStreamCaptureModeRelaxed);
-                    if (ce == cudaSuccess) ce = launch_round_device(ctx->dt, ctx->k2, dp, rs, out, bs, loop_pdl, !all_direct);
-                    if (ce == cudaSuccess) ce = launch_loop_step_dyn(ctx->dt, dl, dp, rs, cond, bs, loop_pdl);
+                if (ce == cudaSuccess) ce = cudaGraphConditionalHandleCreate(&loop_cond, g, 1, cudaGraphCondAssignDefault);
+                wp.type = cudaGraphNodeTypeConditional;
+                wp.conditional.handle = loop_cond;
+                wp.conditional.type = cudaGraphCondTypeWhile;
+                wp.conditional.size = 1;
+                if (ce == cudaSuccess) ce = cudaGraphAddNode(&wnode, g, deps, ndeps, &wp);
+                if (ce == cudaSuccess) {
+                    cudaGraph_t body = wp.conditional.phGraph_out[0];
+                    cudaStream_t bs = ctx->capture_stream, ls2 = ctx->capture_stream2;
+                    ce = cudaGraphConditionalHandleCreate(&leaf_cond, body, 0, 0);
+                    if (ce == cudaSuccess)
+                        ce = cudaStreamBeginCaptureToGraph(bs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed);
+                    if (ce == cudaSuccess)
+                        ce = launch_loop_step_dyn(ctx->dt, dl, dp, rs, loop_cond, leaf_cond, bs, false);
+                    cudaGraph_t bg = nullptr;
+                    if (ce == cudaSuccess) ce = cudaStreamGetCaptureInfo(bs, &cs, nullptr, &bg, &deps, &ndeps);
+                    ip.type = cudaGraphNodeTypeConditional;
+                    ip.conditional.handle = leaf_cond;
+                    ip.conditional.type = cudaGraphCondTypeIf;
+                    ip.conditional.size = 1;
+                    if (ce == cudaSuccess) ce = cudaGraphAddNode(&inode, bg, deps, ndeps, &ip);
+                    if (ce == cudaSuccess) {
+                        ce = cudaStreamBeginCaptureToGraph(ls2, ip.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                                           cudaStreamCaptureModeRelaxed);
+                        if (ce == cudaSuccess) ce = launch_round_leaves(ctx->dt, dp, rs, ls2, false, loop_pdl);
+                        cudaError_t le = cudaStreamEndCapture(ls2, nullptr);
+                        if (ce == cudaSuccess) ce = le;
+                    }
+                    if (ce == cudaSuccess) ce = cudaStreamUpdateCaptureDependencies(bs, &inode, 1, cudaStreamSetCaptureDependencies);
+                    if (ce == cudaSuccess)
+                        ce = launch_round_k2_place(ctx->dt, ctx->k2, dp, rs, out, bs, false, loop_pdl, !all_direct);
                     cudaError_t be = cudaStreamEndCapture(bs, nullptr);
                     if (ce == cudaSuccess) ce = be;
                 }
-                if (ce == cudaSuccess) ce = cudaStreamUpdateCaptureDependencies(st, &cnode, 1, cudaStreamSetCaptureDependencies);
+                if (ce == cudaSuccess) ce = cudaStreamUpdateCaptureDependencies(st, &wnode, 1, cudaStreamSetCaptureDependencies);
                 if (ce == cudaSuccess) ce = cudaMemcpyAsync(hl, dl, sizeof(LoopState), cudaMemcpyDeviceToHost, st);
                 cudaGraph_t gg = nullptr;
                 cudaError_t ee = cudaStreamEndCapture(st, &gg);
@@ -1121,6 +1144,7 @@ void fbb_destroy(fbb_ctx* ctx) {
     ctx->d_loop.release();
     for (auto& kv : ctx->loop_graphs) cudaGraphExecDestroy(kv.second);
     if (ctx->capture_stream) cudaStreamDestroy(ctx->capture_stream);
+    if (ctx->capture_stream2) cudaStreamDestroy(ctx->capture_stream2);
     for (cudaEvent_t ev : ctx->ev)
         if (ev) cudaEventDestroy(ev);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);

@@ -851,25 +851,36 @@ namespace fbb {
 // One round of the batched (device-planned) explorer loop: every kernel reads the
 // round's plan from the device Pool / RoundState and exits when it has nothing to do,
 // so the grids are fixed and nothing here needs the host.
-cudaError_t launch_round_device(const DevTables& t, const K2Config& cfg, const Pool* d_pool,
-                                RoundState* rs, ChunkOut out, cudaStream_t stream, bool pdl, bool place) {
-    // leaves: a one-wave grid-stride grid (most rounds have none and exit at once)
-    cudaError_t e = launch_pdl(k2_leaf_kernel, dim3(148), dim3(256), 0, stream, pdl, t, d_pool, 0, rs);
+cudaError_t launch_round_leaves(const DevTables& t, const Pool* d_pool, RoundState* rs, cudaStream_t stream,
+                                bool pdl_first, bool pdl) {
+    // a one-wave grid-stride grid (rounds without leaves exit at once)
+    cudaError_t e = launch_pdl(k2_leaf_kernel, dim3(148), dim3(256), 0, stream, pdl_first, t, d_pool, 0, rs);
     if (e != cudaSuccess) return e;
-    e = launch_pdl(leaf_schedule_kernel, dim3(1), dim3(32), 0, stream, pdl, t, d_pool, rs);
-    if (e != cudaSuccess) return e;
+    return launch_pdl(leaf_schedule_kernel, dim3(1), dim3(32), 0, stream, pdl, t, d_pool, rs);
+}
+
+cudaError_t launch_round_k2_place(const DevTables& t, const K2Config& cfg, const Pool* d_pool, RoundState* rs,
+                                  ChunkOut out, cudaStream_t stream, bool pdl_k2, bool pdl, bool place) {
+    cudaError_t e;
     if (cfg.variant >= 100000)
-        e = launch_k2_v3(t, cfg, d_pool, 0, cfg.blocks, 0, 0, rs, out, stream, pdl);
+        e = launch_k2_v3(t, cfg, d_pool, 0, cfg.blocks, 0, 0, rs, out, stream, pdl_k2);
     else if (cfg.variant != 0)
-        e = launch_k2_v2(t, cfg, d_pool, 0, cfg.blocks, -1, 0, rs, out, stream, pdl);
+        e = launch_k2_v2(t, cfg, d_pool, 0, cfg.blocks, -1, 0, rs, out, stream, pdl_k2);
     else
         e = launch_pdl(cfg.wide ? k2_internal_kernel<false, true>
                                 : (cfg.jm_in_smem ? k2_internal_kernel<true, false> : k2_internal_kernel<false, false>),
-                       dim3(cfg.blocks), dim3(cfg.threads), cfg.smem, stream, pdl, t, d_pool, 0, cfg.cmax, 0, 0,
+                       dim3(cfg.blocks), dim3(cfg.threads), cfg.smem, stream, pdl_k2, t, d_pool, 0, cfg.cmax, 0, 0,
                        rs, out);
     if (e != cudaSuccess || !place) return e;  // !place: every pool of the batch is placed by K2
     return launch_pdl(place_kernel<true>, dim3(148 * 2), dim3(kPlaceThreads), (size_t)cfg.cmax * kPlaceChunks,
                       stream, pdl, t, d_pool, cfg.cmax, rs, out, (RoundState*)nullptr);
+}
+
+cudaError_t launch_round_device(const DevTables& t, const K2Config& cfg, const Pool* d_pool,
+                                RoundState* rs, ChunkOut out, cudaStream_t stream, bool pdl, bool place) {
+    cudaError_t e = launch_round_leaves(t, d_pool, rs, stream, pdl, pdl);
+    if (e != cudaSuccess) return e;
+    return launch_round_k2_place(t, cfg, d_pool, rs, out, stream, pdl, pdl, place);
 }
 
 }  // namespace fbb

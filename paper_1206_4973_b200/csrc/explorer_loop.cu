@@ -205,12 +205,16 @@ __global__ void loop_step_kernel(DevTables t, LoopState* ls, Pool* pool, RoundSt
     for (int d = lane; d <= n; d += 32) ls->cnt[d] = s_cnt[d];
 }
 
-// The same step for a batch driven by a conditional WHILE node of the batch graph: the
-// round index lives in the loop state (ls->cur_round), and the kernel sets the loop
-// condition -- another iteration (leaves, K2, place, step) exactly when it planned a round.
-// One graph then serves every batch length.
+// The step of a batch driven by a conditional WHILE node of the batch graph, run first in
+// the loop body: it closes the round run by the previous iteration, plans the next one
+// and sets both conditions -- the WHILE node's (another iteration after this one: a round
+// was planned) and the body's IF node around the leaf kernels (the planned pool has leaf
+// segments).  The round index lives in the loop state (ls->cur_round), so one graph
+// serves every batch length; an iteration that plans nothing runs K2 / place as no-ops and
+// ends the loop.
 __global__ void loop_step_dyn_kernel(DevTables t, LoopState* ls, Pool* pool, RoundState* rs,
-                                     cudaGraphConditionalHandle cond) {
+                                     cudaGraphConditionalHandle loop_cond,
+                                     cudaGraphConditionalHandle leaf_cond) {
     asm volatile("griddepcontrol.wait;" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;");
     __shared__ int64_t s_cnt[kMaxJobs + 1];
@@ -222,7 +226,9 @@ __global__ void loop_step_dyn_kernel(DevTables t, LoopState* ls, Pool* pool, Rou
         if (round > 0) close_round(t, ls, pool, rs, round - 1, s_cnt);
         plan_round(t, ls, pool, rs, round, s_cnt);  // nothing planned past nrounds or a stop
         ls->cur_round = round + 1;
-        cudaGraphSetConditional(cond, pool->nseg > 0 ? 1u : 0u);
+        const bool planned = pool->nseg > 0;
+        cudaGraphSetConditional(leaf_cond, planned && pool->seg[0].depth >= n - 2 ? 1u : 0u);
+        cudaGraphSetConditional(loop_cond, planned ? 1u : 0u);
     }
     __syncwarp();
     for (int d = lane; d <= n; d += 32) ls->cnt[d] = s_cnt[d];
@@ -231,8 +237,10 @@ __global__ void loop_step_dyn_kernel(DevTables t, LoopState* ls, Pool* pool, Rou
 }  // namespace
 
 cudaError_t launch_loop_step_dyn(const DevTables& t, LoopState* ls, Pool* pool, RoundState* rs,
-                                 cudaGraphConditionalHandle cond, cudaStream_t stream, bool pdl) {
-    return launch_pdl(loop_step_dyn_kernel, dim3(1), dim3(32), 0, stream, pdl, t, ls, pool, rs, cond);
+                                 cudaGraphConditionalHandle loop_cond, cudaGraphConditionalHandle leaf_cond,
+                                 cudaStream_t stream, bool pdl) {
+    return launch_pdl(loop_step_dyn_kernel, dim3(1), dim3(32), 0, stream, pdl, t, ls, pool, rs, loop_cond,
+                      leaf_cond);
 }
 
 cudaError_t launch_loop_step(const DevTables& t, LoopState* ls, Pool* pool, RoundState* rs, int round,

@@ -290,7 +290,8 @@ struct LoopState {
 // the step of a batch driven by a conditional WHILE graph node (round index in the loop
 // state; sets the node's condition to "another round planned")
 cudaError_t launch_loop_step_dyn(const DevTables& t, LoopState* ls, Pool* pool, RoundState* rs,
-                                 cudaGraphConditionalHandle cond, cudaStream_t stream, bool pdl);
+                                 cudaGraphConditionalHandle loop_cond, cudaGraphConditionalHandle leaf_cond,
+                                 cudaStream_t stream, bool pdl);
 // close of round - 1 (round > 0) + plan of round (!last), one single-warp kernel
 cudaError_t launch_loop_step(const DevTables& t, LoopState* ls, Pool* pool, RoundState* rs, int round,
                              bool last, cudaStream_t stream, bool pdl);
@@ -298,6 +299,11 @@ cudaError_t launch_loop_step(const DevTables& t, LoopState* ls, Pool* pool, Roun
 // the survivors itself), so the place kernel is left out
 cudaError_t launch_round_device(const DevTables& t, const K2Config& cfg, const Pool* d_pool,
                                 RoundState* rs, ChunkOut out, cudaStream_t stream, bool pdl, bool place);
+// its two halves, for graphs that put the leaf kernels under a conditional node
+cudaError_t launch_round_leaves(const DevTables& t, const Pool* d_pool, RoundState* rs, cudaStream_t stream,
+                                bool pdl_first, bool pdl);
+cudaError_t launch_round_k2_place(const DevTables& t, const K2Config& cfg, const Pool* d_pool, RoundState* rs,
+                                  ChunkOut out, cudaStream_t stream, bool pdl_k2, bool pdl, bool place);
 
 // Launches kern<<<grid, block, smem, st>>>(args...), as a programmatic dependent of the
 // previous kernel in the stream when pdl (the kernel must griddepcontrol.wait before it
