@@ -631,16 +631,49 @@ def solve_mode(args, inst_name):
     sample at the same pool target: its rate and the incumbent it reached."""
     import torch
 
-    torch.cuda.set_device(0)
+    rank, world, local = dist_env()
+    dev = local if world > 1 and not os.environ.get("FBB_SAME_GPU") else 0
+    torch.cuda.set_device(dev)
+    backend = os.environ.get("FBB_DIST_BACKEND", "nccl")
+    coll_dev = f"cuda:{dev}" if backend == "nccl" else "cpu"
+    if world > 1:
+        import torch.distributed as dist
+
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
     import paper_1206_4973_b200 as fbb
 
     n, m, seed, _ = INSTANCES[inst_name]
     inst = fbb.generate_instance(n, m, seed)
-    ctx = fbb.Context(inst, 0)
-    sampler = ClockSampler(0) if not os.environ.get("FBB_NO_CLOCKS") else None
-    group, gs = None, None
+    ctx = fbb.Context(inst, dev)
+    sampler = ClockSampler(dev) if rank == 0 and not os.environ.get("FBB_NO_CLOCKS") else None
+    group, gs, px = None, None, None
     t0 = time.perf_counter()
-    if args.group > 1:
+    if world > 1:
+        # one process per GPU (torchrun): rank 0 bounds the root, the other ranks start
+        # empty with the same incumbent and are fed by rebalancing; every exchange step
+        # min-allreduces the incumbent (the paper's UB allreduce, PAPER.md:300-308)
+        from paper_1206_4973_b200.parallel import DevicePort, ParallelExplorer
+
+        if rank == 0:
+            r0 = ctx.explorer_start_solve(None)
+        else:
+            ident = fbb.makespan(inst, list(range(n)))
+            ctx.explorer_reset(fbb.NodeBatch.empty(inst), ident, frozen=False)
+            r0 = (1, 0, 1, 1, 0, 0, ident, 1)
+        px = ParallelExplorer(DevicePort(ctx, frozen=False), n, device=coll_dev, balance_every=1,
+                              exchange_every=args.exchange_every)
+        dev_ms, rounds, trace = 0.0, 1, []
+        while px.step(args.target):
+            dev_ms += sum(x["round_ms"] for x in px.port.last_timings)
+            if time.perf_counter() - t0 > args.max_seconds:
+                break
+        res = px.finish()
+        rounds += len(px.res.rounds)
+        trace.append((round(time.perf_counter() - t0, 3), res.bounded, res.best))
+    elif args.group > 1:
         # the in-library multi-device explorer: member 0 bounds the root, the others are fed
         # by rebalancing, and every step ends with the incumbent min-exchange (the paper's
         # UB allreduce, PAPER.md:300-308)
@@ -672,7 +705,23 @@ def solve_mode(args, inst_name):
                 break
     wall = time.perf_counter() - t0
     clocks = sampler.result() if sampler else None
-    if group is not None:
+    if px is not None:
+        st0 = ctx.explorer_state()
+        tot = torch.tensor([st0["bounded"], st0["branched"], st0["pruned"], st0["leaves"],
+                            st0["pending"]], dtype=torch.int64, device=coll_dev)
+        mx = torch.tensor([wall, dev_ms / 1e3], dtype=torch.float64, device=coll_dev)
+        torch.distributed.all_reduce(tot, op=torch.distributed.ReduceOp.SUM)
+        torch.distributed.all_reduce(mx, op=torch.distributed.ReduceOp.MAX)
+        b, br, pr, lv, pe = (int(x) for x in tot.cpu().tolist())
+        wall, dev_s = (float(x) for x in mx.cpu().tolist())
+        dev_ms = 1e3 * dev_s
+        st = {"pending": pe, "incumbent": px.res.best if px.res.best is not None else r0[6],
+              "bounded": b, "branched": br, "pruned": pr, "leaves": lv}
+        sched = px.res.schedule
+        torch.distributed.destroy_process_group()
+        if rank != 0:
+            return
+    elif group is not None:
         v, sched = group.best()
         st = {"pending": gs["pending"], "incumbent": v if v is not None else gs["incumbent"],
               "bounded": gs["bounded"], "branched": gs["branched"], "pruned": gs["pruned"],
@@ -682,7 +731,7 @@ def solve_mode(args, inst_name):
         sched = st["schedule"]
     done = st["pending"] == 0
     cpu = None
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and world == 1:
         from oracle import REF_SO, Ref
 
         if os.path.exists(REF_SO):
@@ -700,7 +749,7 @@ def solve_mode(args, inst_name):
                              f"reached {res['optimum']}"}
     line = {
         "metric": METRIC, "value": st["bounded"] / wall, "unit": "bounded subproblems/s",
-        "n_gpus": 1, "steps": rounds, "warmup": 0, "ms_per_step": 1e3 * wall / max(1, rounds),
+        "n_gpus": world, "steps": rounds, "warmup": 0, "ms_per_step": 1e3 * wall / max(1, rounds),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int32",
         "data": "synthetic (Taillard generator, published seed; no dataset)",
         "config": {"workload": f"{inst_name} {n}x{m} solve() from the identity-permutation "
@@ -709,7 +758,9 @@ def solve_mode(args, inst_name):
                    "instance": inst_name, "pool_target": args.target,
                    "parallelism": (f"fbb_group of {args.group} members (incumbent min-exchange "
                                    f"every {args.exchange_every} rounds)" if group is not None
-                                   else "dp1")},
+                                   else f"dp{world}" + (f" (incumbent min-allreduce every "
+                                                         f"{args.exchange_every} rounds)"
+                                                         if world > 1 else ""))},
         "explore_seconds": wall, "device_seconds": dev_ms / 1e3, "exhausted": done,
         "optimum": st["incumbent"] if done else None, "incumbent": st["incumbent"],
         "schedule": sched, "schedule_makespan": fbb.makespan(inst, sched) if sched else None,
