@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(NW <= 4 ? 192 : 256, NW <= 4 ? 4 : 2)
     constexpr int N = 32 * NW;
     // scan unroll (independent row / table loads in flight per thread): 16 where the
     // 2-CTA variant's 128-register budget allows it, 8 under the 4-CTA 80-register cap
-    constexpr int kV3Unroll = NW <= 4 ? 8 : 16;
+    constexpr int kV3Unroll = 16;
     extern __shared__ __align__(16) unsigned char smem[];
     const int n = t.n, W = t.W;
     const V3Layout L = v3_layout(M, P, cmax, blockDim.x, NW);
