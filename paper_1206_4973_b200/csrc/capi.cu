@@ -779,7 +779,7 @@ int explorer_run_batched(fbb_ctx* ctx, const int64_t* targets, int ntargets, int
         CK(ctx->st_lb.ensure((size_t)chunks * cmax * 4), "staging");
         CK(ctx->st_count.ensure((size_t)chunks * 4), "staging");
         CK(ctx->st_seg.ensure((size_t)chunks * 4), "staging");
-        std::memset(hl, 0, sizeof(LoopState));  // records too: a batch that stops early leaves later ones unwritten
+        std::memset(hl, 0, offsetof(LoopState, rec));  // (the first step clears the records)
         for (int d = 0; d <= n; ++d) {
             hl->cnt[d] = ctx->cnt[d];
             hl->cap[d] = ctx->bucket[d].cap;
@@ -816,7 +816,7 @@ int explorer_run_batched(fbb_ctx* ctx, const int64_t* targets, int ntargets, int
         // sequence one CUDA graph (captured once per batch length and staging buffers, then
         // replayed: one host call per batch)
         auto enqueue = [&](bool pdl, int rounds) -> cudaError_t {
-            cudaError_t e = cudaMemcpyAsync(dl, hl, sizeof(LoopState), cudaMemcpyHostToDevice, st);
+            cudaError_t e = cudaMemcpyAsync(dl, hl, offsetof(LoopState, rec), cudaMemcpyHostToDevice, st);
             for (int i = 0; i < rounds && e == cudaSuccess; ++i) {
                 if ((e = launch_loop_step(ctx->dt, dl, dp, rs, i, false, st, pdl && i > 0)) != cudaSuccess) break;
                 e = launch_round_device(ctx->dt, ctx->k2, dp, rs, out, st, pdl, !all_direct);
@@ -858,7 +858,7 @@ int explorer_run_batched(fbb_ctx* ctx, const int64_t* targets, int ntargets, int
                 cudaGraphNode_t wnode, inode;
                 cudaGraphNodeParams wp = {}, ip = {};
                 CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal), "loop capture");
-                cudaError_t ce = cudaMemcpyAsync(dl, hl, sizeof(LoopState), cudaMemcpyHostToDevice, st);
+                cudaError_t ce = cudaMemcpyAsync(dl, hl, offsetof(LoopState, rec), cudaMemcpyHostToDevice, st);
                 if (ce == cudaSuccess) ce = cudaStreamGetCaptureInfo(st, &cs, nullptr, &g, &deps, &ndeps);
                 if (ce == cudaSuccess) ce = cudaGraphConditionalHandleCreate(&loop_cond, g, 1, cudaGraphCondAssignDefault);
                 wp.type = cudaGraphNodeTypeConditional;

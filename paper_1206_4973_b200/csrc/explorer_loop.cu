@@ -196,6 +196,10 @@ __global__ void loop_step_kernel(DevTables t, LoopState* ls, Pool* pool, RoundSt
     __shared__ int64_t s_cnt[kMaxJobs + 1];
     const int n = t.n, lane = threadIdx.x;
     for (int d = lane; d <= n; d += 32) s_cnt[d] = ls->cnt[d];
+    // a batch starts with every record invalid (rounds it never reaches stay so; the
+    // host uploads only the state head)
+    if (round == 0)
+        for (int i = lane; i < kLoopMax; i += 32) ls->rec[i].valid = 0;
     __syncwarp();
     if (lane == 0) {
         if (round > 0) close_round(t, ls, pool, rs, round - 1, s_cnt);
@@ -220,6 +224,8 @@ __global__ void loop_step_dyn_kernel(DevTables t, LoopState* ls, Pool* pool, Rou
     __shared__ int64_t s_cnt[kMaxJobs + 1];
     const int n = t.n, lane = threadIdx.x;
     for (int d = lane; d <= n; d += 32) s_cnt[d] = ls->cnt[d];
+    if (ls->cur_round == 0)  // a batch starts with every record invalid (see loop_step_kernel)
+        for (int i = lane; i < kLoopMax; i += 32) ls->rec[i].valid = 0;
     __syncwarp();
     if (lane == 0) {
         const int round = ls->cur_round;

@@ -264,8 +264,9 @@ struct LoopRecord {  // one round's counters (search.hpp:21-26, 75-79)
     unsigned long long t0, t1, k2_t0, k2_t1;
 };
 
-// Device-resident explorer state for a batch of rounds.  The host writes all of it (the
-// records zeroed) before a batch and reads the whole struct back after it.
+// Device-resident explorer state for a batch of rounds.  The host writes the head
+// (everything before `rec`; the batch's first step kernel clears the records) before a
+// batch and reads the whole struct back after it.
 struct LoopState {
     int64_t cnt[kMaxJobs + 1];        // pending bucket sizes
     int64_t cap[kMaxJobs + 1];        // their capacities (rows)
