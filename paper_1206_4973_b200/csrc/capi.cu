@@ -741,7 +741,11 @@ int explorer_round(fbb_ctx* ctx, int64_t target, fbb_round_t* rec) {
 // explorer_round.  Used when the parents can be read in place (HBM buckets, or host
 // buckets read and written through the mapping).
 bool device_loop_ok(const fbb_ctx* ctx, int64_t max_rounds) {
-    const bool want = ctx->device_loop == 1 || (ctx->device_loop == -1 && max_rounds >= 2);
+    // auto: multi-round calls on an HBM tree.  A host tree stays host-planned: its buckets
+    // grow from small pinned blocks, and each growth the device loop meets ends a batch
+    // early (a graph launch and a sync for one round), while the host planner grows them
+    // in line (measured: e2e 1.52 G/s host-planned vs 0.5-1.6 G/s batched, growth-bound)
+    const bool want = ctx->device_loop == 1 || (ctx->device_loop == -1 && max_rounds >= 2 && !ctx->host_pending);
     return want && (!ctx->host_pending || (ctx->mapped_in && ctx->mapped_out));
 }
 
@@ -756,7 +760,9 @@ int explorer_run_batched(fbb_ctx* ctx, const int64_t* targets, int ntargets, int
     CK(ctx->d_pool.ensure(sizeof(Pool)), "pool");
     CK(ctx->d_round.ensure(sizeof(RoundState)), "round state");
     LoopState* hl = ctx->h_loop.as<LoopState>();
+    static const bool dbg = [] { const char* e = getenv("FBB_LOOP_DEBUG"); return e && e[0] == '1'; }();
     while (r < max_rounds) {
+        const auto b0 = std::chrono::steady_clock::now();
         if (pending_total(ctx) == 0) break;
         if (budget > 0 && ctx->tot_bounded >= budget) break;
         const int R = (int)std::min<int64_t>(kLoopMax, max_rounds - r);
@@ -960,9 +966,17 @@ int explorer_run_batched(fbb_ctx* ctx, const int64_t* targets, int ntargets, int
             int rc2 = check_pending(ctx);
             if (rc2 != FBB_OK) return rc2;
         }
+        if (dbg)
+            fprintf(stderr, "[loop] batch R=%d valid=%d stop=%d setup_us=%.1f wall_us=%.1f\n", R, valid, hl->stop,
+                    std::chrono::duration<float, std::micro>(w0 - b0).count(), wall_ms * 1e3f);
         if (hl->stop == 3) {  // a destination bucket must grow before the next round
             const int d = hl->need_depth;
+            const auto g0 = std::chrono::steady_clock::now();
             CK(store_ensure(ctx, ctx->bucket[d], hl->need_rows, ctx->cnt[d]), "bucket grow");
+            if (dbg)
+                fprintf(stderr, "[loop] grow bucket %d to %lld rows (cap %lld) in %.1f us\n", d,
+                        (long long)hl->need_rows, (long long)ctx->bucket[d].cap,
+                        std::chrono::duration<float, std::micro>(std::chrono::steady_clock::now() - g0).count());
             continue;
         }
         if (hl->stop == 1 || hl->stop == 2) break;
@@ -1104,9 +1118,9 @@ fbb_ctx* fbb_create(int device, const int32_t* p, int n, int m) {
     explorer_clear(ctx);
     ctx->incumbent = INT_MAX;
     // Measured (r02): a single round is cheapest host-planned (fewer, exactly sized
-    // launches: Ta021 262 K 121 vs 133 us of device time); a call of several rounds runs
-    // them as one conditional-graph batch with no host round trip (wall 160 vs 172 us per
-    // round with the tree in host memory, Ta021 e2e +7.5 %)
+    // launches: Ta021 262 K 121 vs 138 us of device time); a call of several rounds on an
+    // HBM tree runs them as one conditional-graph batch with no host round trip (the Ta021
+    // exhaustion: 19.5 vs 22.4 s)
     const char* dlp = getenv("FBB_DEVICE_LOOP");
     ctx->device_loop = !dlp ? -1 : (dlp[0] == '1' ? 1 : (dlp[0] == '0' ? 0 : -1));
     const char* sm = getenv("FBB_SUMMARY");
