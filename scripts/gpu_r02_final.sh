@@ -25,7 +25,7 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k1v
 bash scripts/gpu_sweep.sh > gpurun_out/sweep_table.md; cat gpurun_out/sweep_table.md
 timeout 600 oracle/_ref/dropin_test > gpurun_out/dropin.txt 2>&1; tail -1 gpurun_out/dropin.txt
 timeout 900 python bench.py --mode exhaust --instance ta021 --group 2 > gpurun_out/exhaust_group2.json 2> gpurun_out/exhaust_group2.err; tail -c 400 gpurun_out/exhaust_group2.json
-for T in memcheck racecheck synccheck; do timeout 600 compute-sanitizer --tool $T --print-limit 20 python scripts/sanitize.py > gpurun_out/sanitize_$T.txt 2>&1; echo "== $T: $(grep -c "^ok" gpurun_out/sanitize_$T.txt) ok; $(tail -1 gpurun_out/sanitize_$T.txt)"; done
+for T in memcheck racecheck synccheck; do G=1; [ $T = racecheck ] && G=0; FBB_LOOP_GRAPH=$G timeout 600 compute-sanitizer --tool $T --print-limit 20 python scripts/sanitize.py > gpurun_out/sanitize_$T.txt 2>&1; echo "== $T: $(grep -c "^ok" gpurun_out/sanitize_$T.txt) ok; $(tail -1 gpurun_out/sanitize_$T.txt)"; done
 timeout 900 python bench.py --mode solve --instance ta001 --max-seconds 600 --cpu-sample 2000000 > gpurun_out/solve_ta001.json 2> gpurun_out/solve_ta001.err
 timeout 900 python bench.py --mode solve --instance ta001 --group 2 --max-seconds 600 --no-cpu-baseline > gpurun_out/solve_ta001_group2.json 2> gpurun_out/solve_ta001_group2.err
 timeout 900 python bench.py --instance ta051 --tuner > gpurun_out/bench_ta051_tuner.json 2> gpurun_out/bench_ta051_tuner.err
