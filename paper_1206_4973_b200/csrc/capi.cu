@@ -1129,6 +1129,8 @@ fbb_ctx* fbb_create(int device, const int32_t* p, int n, int m) {
     ctx->direct_place = !(dir && dir[0] == '0');
     const char* chk = getenv("FBB_CHECK");
     ctx->check = chk && chk[0] == '1';
+    preload_round_kernels();  // kernels load lazily: not inside the first round or graph capture
+    preload_loop_kernels();
     return ctx;
 }
 

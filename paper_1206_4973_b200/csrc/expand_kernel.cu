@@ -851,6 +851,15 @@ namespace fbb {
 // One round of the batched (device-planned) explorer loop: every kernel reads the
 // round's plan from the device Pool / RoundState and exits when it has nothing to do,
 // so the grids are fixed and nothing here needs the host.
+void preload_round_kernels() {
+    cudaFuncAttributes a;
+    cudaFuncGetAttributes(&a, k2_leaf_kernel);
+    cudaFuncGetAttributes(&a, leaf_schedule_kernel);
+    cudaFuncGetAttributes(&a, place_kernel<false>);
+    cudaFuncGetAttributes(&a, place_kernel<true>);
+    cudaFuncGetAttributes(&a, pool_upload_kernel);
+}
+
 cudaError_t launch_round_leaves(const DevTables& t, const Pool* d_pool, RoundState* rs, cudaStream_t stream,
                                 bool pdl_first, bool pdl) {
     // a one-wave grid-stride grid (rounds without leaves exit at once)

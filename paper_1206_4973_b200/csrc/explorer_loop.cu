@@ -242,6 +242,14 @@ __global__ void loop_step_dyn_kernel(DevTables t, LoopState* ls, Pool* pool, Rou
 
 }  // namespace
 
+// Loads the loop kernels now (CUDA loads kernels lazily, at first launch -- which would
+// otherwise land inside the first batch's graph capture).
+void preload_loop_kernels() {
+    cudaFuncAttributes a;
+    cudaFuncGetAttributes(&a, loop_step_kernel);
+    cudaFuncGetAttributes(&a, loop_step_dyn_kernel);
+}
+
 cudaError_t launch_loop_step_dyn(const DevTables& t, LoopState* ls, Pool* pool, RoundState* rs,
                                  cudaGraphConditionalHandle loop_cond, cudaGraphConditionalHandle leaf_cond,
                                  cudaStream_t stream, bool pdl) {

@@ -300,6 +300,9 @@ cudaError_t launch_loop_step(const DevTables& t, LoopState* ls, Pool* pool, Roun
 // the survivors itself), so the place kernel is left out
 cudaError_t launch_round_device(const DevTables& t, const K2Config& cfg, const Pool* d_pool,
                                 RoundState* rs, ChunkOut out, cudaStream_t stream, bool pdl, bool place);
+// Load the explorer's kernels at context creation (CUDA loads kernels lazily, at first use)
+void preload_round_kernels();
+void preload_loop_kernels();
 // its two halves, for graphs that put the leaf kernels under a conditional node
 cudaError_t launch_round_leaves(const DevTables& t, const Pool* d_pool, RoundState* rs, cudaStream_t stream,
                                 bool pdl_first, bool pdl);
