@@ -320,6 +320,10 @@ int layout_pool(const fbb_ctx* ctx, Pool& pool) {
     pool.pad = 0;  // read by the kernels as an opaque zero
     int64_t child = 0, chunk = 0;
     int first_internal = pool.nseg;
+    // small pools of the register-row kernel spread over the whole K2 wave
+    const bool v2 = ctx->k2.variant != 0 && ctx->k2.variant < 100000;
+    pool.ppc_lim = v2 ? spread_ppc(pool.seg, pool.nseg, n, cmax, ctx->k2.ppc_cap, ctx->k2.blocks) : 0;
+    const int cap = round_ppc_cap(ctx->k2.ppc_cap, pool.ppc_lim);
     for (int s = 0; s < pool.nseg; ++s) {
         Segment& sg = pool.seg[s];
         int r = n - sg.depth;
@@ -328,7 +332,7 @@ int layout_pool(const fbb_ctx* ctx, Pool& pool) {
         sg.chunk_base = chunk;
         if (sg.depth >= n - 2) continue;  // leaves: no chunks
         if (first_internal == pool.nseg) first_internal = s;
-        int ppc = parents_per_chunk(n, sg.depth, cmax, ctx->k2.ppc_cap);
+        int ppc = parents_per_chunk(n, sg.depth, cmax, cap);
         chunk += (sg.count + ppc - 1) / ppc;
     }
     pool.nchunks = chunk;
@@ -361,7 +365,6 @@ int run_pool(fbb_ctx* ctx, Pool& pool, int first_internal, int32_t ub, int froze
     // direct placement (K2 writes the survivors to their bucket rows itself, no place
     // kernel): single-wave pools of the v2 kernel into device buckets
     pool.direct = 0;
-    pool.pad2 = 0;
     pool.summary = nullptr;
     if (ctx->direct_place && ctx->k2.variant != 0 && ctx->k2.variant < 100000 && !pool.host_dst &&
         first_internal < pool.nseg && pool.nchunks > 0 && pool.nchunks <= ctx->k2.blocks) {
@@ -780,7 +783,9 @@ int explorer_run_batched(fbb_ctx* ctx, const int64_t* targets, int ntargets, int
             const int ppc = parents_per_chunk(n, n - r, cmax, ctx->k2.ppc_cap);
             cpc_min = std::min<int64_t>(cpc_min, (int64_t)std::max(ppc, 1) * r);
         }
-        const int64_t chunks = (tmax + n + cpc_min - 1) / std::max<int64_t>(cpc_min, 1) + n + 2;
+        int64_t chunks = (tmax + n + cpc_min - 1) / std::max<int64_t>(cpc_min, 1) + n + 2;
+        // small pools may be spread over up to k2.blocks chunks (spread_ppc)
+        if (ctx->k2.variant != 0 && ctx->k2.variant < 100000) chunks = std::max<int64_t>(chunks, ctx->k2.blocks);
         CK(store_ensure(ctx, ctx->staging, chunks * cmax, 0), "staging");
         CK(ctx->st_lb.ensure((size_t)chunks * cmax * 4), "staging");
         CK(ctx->st_count.ensure((size_t)chunks * 4), "staging");
@@ -808,6 +813,7 @@ int explorer_run_batched(fbb_ctx* ctx, const int64_t* targets, int ntargets, int
         hl->direct_cap = (ctx->direct_place && ctx->k2.variant != 0 && ctx->k2.variant < 100000 &&
                           !ctx->host_pending) ? ctx->k2.blocks : 0;
         hl->host_dst = ctx->host_pending ? 1 : 0;  // survivors written over the host link
+        hl->spread_blocks = (ctx->k2.variant != 0 && ctx->k2.variant < 100000) ? ctx->k2.blocks : 0;
         // every pool of the batch fits one wave (worst-case chunk count): K2 places them all
         const bool all_direct = hl->direct_cap > 0 && chunks <= hl->direct_cap;
         for (int i = 0; i < n; ++i) hl->schedule[i] = ctx->schedule[i];

@@ -319,6 +319,7 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
 
     const int64_t c_begin = pool->seg[first_seg].chunk_base;
     const int64_t c_end = pool->nchunks;
+    const int ppc_lim = pool->ppc_lim;
     // Chunk staging.  At 2 CTAs/SM the parents of the NEXT chunk are loaded into
     // registers while this chunk runs Phase A / B (software pipelining: the global --
     // or, host-resident, host-link -- latency of the staging loads hides behind
@@ -340,7 +341,8 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
         s_ = v2_find_segment(pool, first_seg, c);
         const Segment& g_ = pool->seg[s_];
         depth_ = g_.depth;
-        const int ppc_ = min(cmax / (n - depth_), v2_ppc_cap(N, OCC));
+        int ppc_ = min(cmax / (n - depth_), v2_ppc_cap(N, OCC));
+        if (ppc_lim > 0) ppc_ = min(ppc_, ppc_lim);  // small pools spread over the wave
         p0_ = (c - g_.chunk_base) * ppc_;
         np_ = (int)(g_.count - p0_ < ppc_ ? g_.count - p0_ : ppc_);
     };

@@ -95,6 +95,8 @@ __device__ void plan_round(const DevTables& t, LoopState* ls, Pool* pool, RoundS
     const int cmax = ls->cmax;
     int64_t child = 0, chunk = 0;
     int first_internal = nseg;
+    const int ppc_lim = spread_ppc(pool->seg, nseg, n, cmax, ls->ppc_cap, ls->spread_blocks);
+    const int cap = round_ppc_cap(ls->ppc_cap, ppc_lim);
     for (int s = 0; s < nseg; ++s) {
         Segment& sg = pool->seg[s];
         const int r = n - sg.depth;
@@ -103,7 +105,7 @@ __device__ void plan_round(const DevTables& t, LoopState* ls, Pool* pool, RoundS
         sg.chunk_base = chunk;
         if (sg.depth >= n - 2) continue;
         if (first_internal == nseg) first_internal = s;
-        const int ppc = parents_per_chunk(n, sg.depth, cmax, ls->ppc_cap);
+        const int ppc = parents_per_chunk(n, sg.depth, cmax, cap);
         chunk += (sg.count + ppc - 1) / ppc;
     }
     if (chunk > ls->chunk_cap) {  // the host sized staging for the worst case: never taken
@@ -118,7 +120,7 @@ __device__ void plan_round(const DevTables& t, LoopState* ls, Pool* pool, RoundS
     pool->host_dst = ls->host_dst;
     // single-wave pools: K2 places the survivors itself (capi.cu run_pool, same rule)
     pool->direct = (ls->direct_cap > 0 && chunk > 0 && chunk <= ls->direct_cap) ? 1 : 0;
-    pool->pad2 = 0;
+    pool->ppc_lim = ppc_lim;
     pool->summary = nullptr;
     pool->nseg = nseg;
 }

@@ -177,7 +177,7 @@ struct Pool {
     // co-resident, and after a grid-wide arrival count each writes its survivors straight
     // to their batch-ordered bucket rows -- no staging, no place kernel
     int32_t direct;
-    int32_t pad2;
+    int32_t ppc_lim;     // > 0: at most this many parents per chunk this round (spread_ppc)
     RoundState* summary; // direct: the mapped host RoundState K2's CTA 0 publishes into (or null)
     Segment seg[kMaxSegments];
 };
@@ -282,6 +282,7 @@ struct LoopState {
     int32_t direct_cap;               // > 0: pools of at most this many chunks use direct placement
     int32_t cur_round;                // conditional-graph batches: the round the next step closes / plans
     int32_t host_dst;                 // the buckets are pinned host memory (Pool::host_dst)
+    int32_t spread_blocks;            // > 0: small pools spread over this many K2 CTAs (spread_ppc)
     int32_t schedule[kMaxJobs];       // incumbent schedule (solve mode)
     LoopRecord rec[kLoopMax];
 };
@@ -359,6 +360,44 @@ __host__ __device__ inline int parents_per_chunk(int n, int depth, int cmax, int
     int r = n - depth;
     int ppc = r > 0 ? cmax / r : 1;
     return ppc_cap > 0 && ppc > ppc_cap ? ppc_cap : ppc;
+}
+// The tighter of the kernel's parents-per-chunk cap and a round's Pool::ppc_lim.
+__host__ __device__ inline int round_ppc_cap(int ppc_cap, int ppc_lim) {
+    return ppc_lim > 0 && (ppc_cap <= 0 || ppc_lim < ppc_cap) ? ppc_lim : ppc_cap;
+}
+// Small pools: when the internal parents of a round fill fewer chunks than the K2 grid has
+// resident CTAs (`blocks`), the chunks get fewer parents each, so that they spread over
+// the whole wave instead of leaving most SMs idle -- a single-wave round's time is one
+// chunk's serial chain (staging, tables, scans, bounds, compaction), so it shrinks with
+// the chunk.  Returns the smallest Pool::ppc_lim that keeps the round within `blocks`
+// chunks (0: none -- the pool already fills the wave).
+__host__ __device__ inline int64_t spread_chunks(const Segment* seg, int nseg, int n, int cmax, int cap) {
+    int64_t chunks = 0;
+    for (int s = 0; s < nseg; ++s) {
+        if (seg[s].depth >= n - 2) continue;  // leaves: no chunks
+        const int ppc = parents_per_chunk(n, seg[s].depth, cmax, cap);
+        chunks += (seg[s].count + ppc - 1) / ppc;
+    }
+    return chunks;
+}
+__host__ __device__ inline int spread_ppc(const Segment* seg, int nseg, int n, int cmax, int ppc_cap,
+                                          int blocks) {
+    if (blocks <= 0) return 0;
+    int64_t parents = 0;
+    int nint = 0, ppc_max = 0;
+    for (int s = 0; s < nseg; ++s) {
+        if (seg[s].depth >= n - 2) continue;
+        const int ppc = parents_per_chunk(n, seg[s].depth, cmax, ppc_cap);
+        parents += seg[s].count;
+        ppc_max = ppc > ppc_max ? ppc : ppc_max;
+        ++nint;
+    }
+    if (nint == 0 || spread_chunks(seg, nseg, n, cmax, ppc_cap) >= blocks || blocks <= nint) return 0;
+    // a lower bound (every segment at the cap), then up until the count fits
+    int64_t lim = (parents + (blocks - nint) - 1) / (blocks - nint);
+    if (lim < 1) lim = 1;
+    while (lim < ppc_max && spread_chunks(seg, nseg, n, cmax, (int)lim) > blocks) ++lim;
+    return lim < ppc_max ? (int)lim : 0;
 }
 
 }  // namespace fbb
