@@ -77,7 +77,8 @@ typedef struct {
     float sync_ms;     /* part of host_ms spent waiting for the device */
     int64_t h2d_bytes; /* host -> device bytes of the round (host-resident explorer) */
     int64_t d2h_bytes; /* device -> host bytes of the round (host-resident explorer) */
-    float place_ms;    /* place_kernel + summary time (CUDA events, FBB_PDL=0 only; else -1) */
+    float place_ms;    /* place_kernel + summary time (CUDA events, FBB_PDL=0 only; else -1); device-planned
+                          rounds: plan start .. first K2 CTA start (device clock) */
     int32_t reserved;
 } fbb_round_t;
 

@@ -839,7 +839,15 @@ int explorer_run_batched(fbb_ctx* ctx, const int64_t* targets, int ntargets, int
         };
         static const bool use_graph = [] { const char* e = getenv("FBB_LOOP_GRAPH"); return !(e && e[0] == '0'); }();
         static const bool loop_pdl = [] { const char* e = getenv("FBB_PDL"); return !(e && e[0] == '0'); }();
-        if (use_graph) {
+        static const bool persist = [] { const char* e = getenv("FBB_PERSIST"); return !(e && e[0] == '0'); }();
+        const bool pbk = persist && all_direct && ctx->k2.batch;
+        if (pbk) {
+            // every round of the batch fits one wave: ONE cooperative launch of the
+            // persistent K2 plans, runs and closes them all (expand_v2.cu, BATCH)
+            CK(cudaMemcpyAsync(dl, hl, offsetof(LoopState, rec), cudaMemcpyHostToDevice, st), "loop state");
+            CK(launch_k2_v2_batch(ctx->dt, ctx->k2, dl, dp, rs, out, st), "persistent batch");
+            CK(cudaMemcpyAsync(hl, dl, sizeof(LoopState), cudaMemcpyDeviceToHost, st), "loop state");
+        } else if (use_graph) {
             // one graph for every batch length: state upload, a step planning round 0, then a
             // conditional WHILE node whose body -- leaves, leaf schedule, K2, [place], step --
             // repeats while the step planned another round (the round index lives in the loop
@@ -948,8 +956,10 @@ int explorer_run_batched(fbb_ctx* ctx, const int64_t* targets, int ntargets, int
             const unsigned long long t_next = i + 1 < valid ? hl->rec[i + 1].t0 : lr.t1;
             rec.round_ms = (float)((double)(t_next - lr.t0) * 1e-6);
             rec.k2_ms = lr.k2_t0 && lr.k2_t1 > lr.k2_t0 ? (float)((double)(lr.k2_t1 - lr.k2_t0) * 1e-6) : 0.f;
-            rec.place_ms = -1.f;
-            rec.launches = 5;
+            // device-planned rounds: the lead-in, plan start .. first K2 CTA start (plan,
+            // the launch or barrier after it, the leaves)
+            rec.place_ms = lr.k2_t0 > lr.t0 ? (float)((double)(lr.k2_t0 - lr.t0) * 1e-6) : -1.f;
+            rec.launches = pbk ? (i == 0 ? 1 : 0) : 5;  // the persistent kernel: one per batch
             rec.host_ms = wall_ms / valid;
             rec.sync_ms = sync_ms / valid;
             rec.h2d_bytes = ctx->host_pending ? lr.branched * nb : 0;  // rows of the host tree
@@ -972,8 +982,23 @@ int explorer_run_batched(fbb_ctx* ctx, const int64_t* targets, int ntargets, int
             int rc2 = check_pending(ctx);
             if (rc2 != FBB_OK) return rc2;
         }
+        if (dbg && pbk && valid > 1) {  // where a persistent round's time goes (device clock)
+            double a = 0, b = 0, k = 0, s = 0, e = 0;
+            for (int i = 0; i + 1 < valid; ++i) {
+                const LoopRecord& q = hl->rec[i];
+                a += (double)(q.tp - q.t0);
+                b += (double)(q.tb - q.tp);
+                k += q.k2_t0 > q.tb ? (double)(q.k2_t0 - q.tb) : 0.0;
+                s += (double)(q.k2_t1 - q.k2_t0);
+                e += (double)(hl->rec[i + 1].t0 - q.k2_t1);
+            }
+            const double d = 1e3 * (valid - 1);
+            fprintf(stderr, "[loop] per round us: plan %.2f barrier %.2f to-K2 %.2f K2 %.2f K2-end..next plan %.2f\n",
+                    a / d, b / d, k / d, s / d, e / d);
+        }
         if (dbg)
-            fprintf(stderr, "[loop] batch R=%d valid=%d stop=%d setup_us=%.1f wall_us=%.1f\n", R, valid, hl->stop,
+            fprintf(stderr, "[loop] batch R=%d valid=%d stop=%d persistent=%d setup_us=%.1f wall_us=%.1f\n", R, valid,
+                    hl->stop, pbk ? 1 : 0,
                     std::chrono::duration<float, std::micro>(w0 - b0).count(), wall_ms * 1e3f);
         if (hl->stop == 3) {  // a destination bucket must grow before the next round
             const int d = hl->need_depth;
@@ -1021,7 +1046,8 @@ int fbb_kernels(fbb_ctx* ctx, char* buf, size_t cap) {
                       b.variant / 10000);
     else
         std::snprintf(k2, sizeof k2, "k2_internal_kernel<%d,%d>", b.jm_in_smem, b.wide);
-    std::snprintf(buf, cap, "K1=%s K2=%s cmax=%d ppc_cap=%d blocks=%d", k1, k2, b.cmax, b.ppc_cap, b.blocks);
+    std::snprintf(buf, cap, "K1=%s K2=%s cmax=%d ppc_cap=%d blocks=%d batch=%d", k1, k2, b.cmax, b.ppc_cap, b.blocks,
+                  b.batch ? 1 : 0);
     return FBB_OK;
 }
 

@@ -15,6 +15,7 @@
 #include <cstdlib>
 
 #include "k2_common.cuh"
+#include "loop_plan.cuh"
 
 namespace fbb {
 
@@ -189,6 +190,32 @@ __device__ __forceinline__ int32_t scan_block(uint32_t row_sa, uint32_t slo, uin
     return SM;
 }
 
+// Grid-wide barrier of the persistent batch kernel (cooperative launch: every CTA is
+// resident).  Thread 0 of each CTA releases the CTA's writes and arrives; the last one
+// resets the count and bumps the generation; the others spin on it with acquire loads.
+__device__ __forceinline__ void batch_grid_sync(uint32_t* count, uint32_t* gen) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t g0, g, old;
+        asm volatile("ld.relaxed.gpu.u32 %0, [%1];" : "=r"(g0) : "l"(gen) : "memory");
+        // arrive: release the CTA's writes (ordered before by the CTA barrier), and the
+        // last arriver acquires everyone's
+        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(count) : "memory");
+        if (old == gridDim.x - 1) {
+            asm volatile("st.relaxed.gpu.u32 [%0], 0;" ::"l"(count) : "memory");
+            asm volatile("st.release.gpu.u32 [%0], %1;" ::"l"(gen), "r"(g0 + 1u) : "memory");
+        } else {
+            // spin with relaxed loads (an acquire load invalidates the SM's L1, which would
+            // keep evicting the planning thread's working set on CTA 0's SM), then one fence
+            do {
+                asm volatile("ld.relaxed.gpu.u32 %0, [%1];" : "=r"(g) : "l"(gen) : "memory");
+            } while (g == g0);
+            asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        }
+    }
+    __syncthreads();
+}
+
 // Two parents per thread in 16x2 SIMD (n <= 20 at 2 CTAs/SM, where the 168-register
 // budget holds six 20-entry arrays): one row entry feeds both parents' max-plus chains,
 // each as one VIADDMNMX.S16x2 / VIADD.16x2.  Values fit int16 for n <= 20 (|D| <= 1960,
@@ -237,10 +264,16 @@ __device__ __forceinline__ void scan_pair16(uint32_t row_sa, uint32_t s0, uint32
 // DIR: false = staged placement only (the big-pool kernel, untouched by the direct path),
 // true = direct placement capable (single-wave pools; Pool::direct decides at run time when
 // place_hint < 0)
-template <int N, int M, int OCC, bool DIR>
-__global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool* __restrict__ pool,
+// BATCH: the persistent form -- one cooperative launch runs a whole device-planned batch:
+// per round CTA 0 closes the previous round and plans this one (loop_plan.cuh), a grid
+// barrier, [the leaves and the best leaf's schedule], K2 with direct placement, a grid
+// barrier.  The row tables stay staged (registers / shared memory) across the rounds and
+// no kernel is launched between them.  Every round must fit one wave (the host runs it
+// only when the batch's worst-case chunk count does).
+template <int N, int M, int OCC, bool DIR, bool BATCH = false>
+__global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool* __restrict__ pool_arg,
                                                    int first_seg, int cmax, int place_hint, int frozen,
-                                                   RoundState* rs, ChunkOut out) {
+                                                   RoundState* rs, ChunkOut out, LoopState* ls) {
     constexpr int P = M * (M - 1) / 2;
     // Phase B: the 16x2 grouped form at 2 CTAs/SM (168 registers); at 3 CTAs/SM (96
     // registers) the per-pair form over q-ordered Mq rows, which spills least there
@@ -300,6 +333,8 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
     for (int x = tid; x < (int)((cmax + v2_dummy_rows(P)) * L.rowb / 16); x += bd)  // padding slots stay 0
         ((uint4*)s_Mq)[x] = make_uint4(0u, 0u, 0u, 0u);
 
+    // one round over `pool` (the kernel's argument, or the batch's shared-memory copy)
+    auto k2_round = [&](const Pool* __restrict__ pool) {
     // the round's bound, semantics and first internal segment come from the pool
     // (written by the host, or by the device-side planner of the batched explorer loop)
     asm volatile("griddepcontrol.wait;" ::: "memory");  // the pool upload kernel (PDL)
@@ -312,7 +347,8 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
     if (first_seg >= pool->nseg) return;
     int32_t ub_eff = ub;
     if (!frozen) {
-        unsigned long long inv = rs->leaf_inv;
+        // (batch: written this kernel by other CTAs -- an L2 read)
+        unsigned long long inv = BATCH ? __ldcg(&rs->leaf_inv) : rs->leaf_inv;
         int32_t v = (int32_t)((~inv) >> 32);
         if (inv != 0ull && v < ub_eff) ub_eff = v;
     }
@@ -708,7 +744,65 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
         }
     }
     k2_stamp_end(rs);
-    if (DIR && direct) direct_finish(pool, rs, n, c_end - c_begin);
+    if (!BATCH && DIR && direct) direct_finish(pool, rs, n, c_end - c_begin);
+    };  // k2_round
+
+    if constexpr (!BATCH) {
+        k2_round(pool_arg);
+    } else {
+        // batch state: CTA 0 keeps the bucket sizes in shared memory for the whole batch;
+        // every CTA copies each round's plan (written by CTA 0 during this kernel, so read
+        // from L2, never through the read-only path) into shared memory
+        Pool* gpool = const_cast<Pool*>(pool_arg);
+        Pool* s_pool = (Pool*)(smem + L.total);
+        int64_t* s_cnt = (int64_t*)(smem + L.total + b16(offsetof(Pool, seg) + (size_t)(n + 1) * sizeof(Segment)));
+        int64_t* s_cap = s_cnt + (n + 1);
+        NodeStore* s_bucket = (NodeStore*)(s_cap + (n + 1));
+        const bool lead = blockIdx.x == 0 && tid == 0;
+        if (blockIdx.x == 0) {
+            for (int d = tid; d <= n; d += bd) s_cnt[d] = ls->cnt[d];
+            stage_buckets(ls, s_bucket, s_cap, n, tid, bd);
+            for (int i = tid; i < kLoopMax; i += bd) ls->rec[i].valid = 0;  // see loop_step_kernel
+        }
+        __syncthreads();
+        for (int round = 0;; ++round) {
+            if (blockIdx.x == 0) {  // CTA 0 closes and plans in its shared memory, then publishes
+                if (warp == 0) {
+                    if (round > 0) close_round(t, ls, s_pool, rs, round - 1, s_cnt, lane);
+                    __syncwarp();
+                    // nothing planned past nrounds or a stop
+                    plan_round(t, ls, s_pool, rs, round, s_cnt, LoopBuckets{s_bucket, s_cap}, lane);
+                }
+                if (lead) {
+                    if (s_pool->nseg > 0 && s_pool->nchunks > 0 && !s_pool->direct) {
+                        ls->stop = 5;  // more chunks than one wave: the host never plans such a batch
+                        s_pool->nseg = 0;
+                    }
+                    if (round < kLoopMax) ls->rec[round].tp = loop_ns();
+                }
+                __syncthreads();
+                pool_store(gpool, s_pool, s_pool->nseg, tid, bd);
+            }
+            batch_grid_sync(&ls->bar_count, &ls->bar_gen);
+            if (lead && round < kLoopMax) ls->rec[round].tb = loop_ns();
+            if (blockIdx.x != 0) pool_load(s_pool, gpool, __ldcg(&gpool->nseg), tid, bd);
+            __syncthreads();
+            const int nseg = s_pool->nseg;
+            if (nseg == 0) break;
+            if (s_pool->seg[0].depth >= n - 2) {
+                // leaves (search.hpp:48-55), then the best leaf's schedule before K2 recycles
+                // the leaf parents' slots
+                leaf_children(t, s_pool, rs, leaf_segments(s_pool, n));
+                batch_grid_sync(&ls->bar_count, &ls->bar_gen);
+                if (lead) write_leaf_schedule(t, s_pool, rs);
+                batch_grid_sync(&ls->bar_count, &ls->bar_gen);
+            }
+            k2_round(s_pool);
+            batch_grid_sync(&ls->bar_count, &ls->bar_gen);  // survivors written, counts final
+        }
+        if (blockIdx.x == 0)
+            for (int d = tid; d <= n; d += bd) ls->cnt[d] = s_cnt[d];
+    }
 }
 
 template <int N, int M, int OCC, bool DIR>
@@ -733,11 +827,42 @@ cudaError_t v2_setup_one(const DevTables& t, K2Config& c, int device) {
     return cudaSuccess;
 }
 
+// Shared memory of the persistent batch kernel: the round kernel's, + the round's plan
+// (Pool head and up to n + 1 segments) + CTA 0's bucket sizes, capacities and storage.
+inline size_t v2_batch_smem(size_t smem, int n) {
+    return smem + b16(offsetof(Pool, seg) + (size_t)(n + 1) * sizeof(Segment)) +
+           (size_t)(n + 1) * (8 + 8 + sizeof(NodeStore));  // + bucket sizes, capacities, storage
+}
+
+// The batch kernel is enabled when a whole grid of c.blocks CTAs is resident with its
+// larger shared memory (cooperative launch).
+template <int N, int M, int OCC>
+void v2_setup_batch(const DevTables& t, K2Config& c, int device) {
+    auto kern = k2_v2_kernel<N, M, OCC, true, true>;
+    int optin = 0, sms = 148, per_sm = 0, coop = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device);
+    cudaFuncAttributes fa;
+    c.batch = false;
+    c.batch_smem = v2_batch_smem(c.smem, t.n);
+    if (!coop || cudaFuncGetAttributes(&fa, kern) != cudaSuccess) return;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin - (int)fa.sharedSizeBytes) !=
+        cudaSuccess)
+        return;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, c.threads, c.batch_smem) != cudaSuccess) return;
+    c.batch = per_sm * sms >= c.blocks;
+}
+
 template <int N, int M, int OCC>
 cudaError_t v2_setup(const DevTables& t, K2Config& c, int device) {
     cudaError_t e = v2_setup_one<N, M, OCC, false>(t, c, device);
     if (e != cudaSuccess) return e;
-    return v2_setup_one<N, M, OCC, true>(t, c, device);
+    e = v2_setup_one<N, M, OCC, true>(t, c, device);
+    if (e != cudaSuccess) return e;
+    v2_setup_batch<N, M, OCC>(t, c, device);
+    (void)cudaGetLastError();  // a batch kernel that could not be configured leaves no error behind
+    return cudaSuccess;
 }
 
 }  // namespace
@@ -797,6 +922,38 @@ bool k2_v2_config(const DevTables& t, int device, K2Config* out) {
     return true;
 }
 
+cudaError_t launch_k2_v2_batch(const DevTables& t, const K2Config& cfg, LoopState* ls, Pool* d_pool,
+                               RoundState* rs, ChunkOut out, cudaStream_t stream) {
+    if (!cfg.batch) return cudaErrorInvalidValue;
+#define V2B_CASE(NN, MM, OO)                                                                     \
+    case OO * 10000 + NN * 100 + MM:                                                             \
+        return launch_coop(k2_v2_kernel<NN, MM, OO, true, true>, dim3(cfg.blocks), dim3(cfg.threads), \
+                           cfg.batch_smem, stream, false, t, (const Pool*)d_pool, 0, cfg.cmax, -1, 0, rs, \
+                           out, ls);
+    switch (cfg.variant) {
+        V2B_CASE(20, 5, 2)
+        V2B_CASE(20, 10, 2)
+        V2B_CASE(20, 20, 2)
+        V2B_CASE(32, 5, 2)
+        V2B_CASE(32, 10, 2)
+        V2B_CASE(32, 20, 2)
+        V2B_CASE(20, 5, 3)
+        V2B_CASE(20, 10, 3)
+        V2B_CASE(20, 20, 3)
+        V2B_CASE(32, 5, 3)
+        V2B_CASE(32, 10, 3)
+        V2B_CASE(32, 20, 3)
+        V2B_CASE(64, 5, 2)
+        V2B_CASE(64, 10, 2)
+        V2B_CASE(64, 20, 2)
+        V2B_CASE(64, 5, 3)
+        V2B_CASE(64, 10, 3)
+        V2B_CASE(64, 20, 3)
+        default: return cudaErrorInvalidValue;
+    }
+#undef V2B_CASE
+}
+
 cudaError_t launch_k2_v2(const DevTables& t, const K2Config& cfg, const Pool* d_pool, int first_seg,
                          int blocks, int place_hint, int frozen, RoundState* rs, ChunkOut out,
                          cudaStream_t stream, bool pdl) {
@@ -811,13 +968,14 @@ cudaError_t launch_k2_v2(const DevTables& t, const K2Config& cfg, const Pool* d_
     case OO * 10000 + NN * 100 + MM:                                                          \
         return place_hint == 0                                                                \
                    ? launch_pdl(k2_v2_kernel<NN, MM, OO, false>, dim3(blocks), dim3(cfg.threads), cfg.smem, \
-                                stream, pdl, t, d_pool, first_seg, cfg.cmax, 0, frozen, rs, out)  \
+                                stream, pdl, t, d_pool, first_seg, cfg.cmax, 0, frozen, rs, out, \
+                                (LoopState*)nullptr)                                              \
                    : coop ? launch_coop(k2_v2_kernel<NN, MM, OO, true>, dim3(blocks), dim3(cfg.threads), \
                                         cfg.smem, stream, pdl, t, d_pool, first_seg, cfg.cmax, place_hint, \
-                                        frozen, rs, out)                                        \
+                                        frozen, rs, out, (LoopState*)nullptr)                     \
                           : launch_pdl(k2_v2_kernel<NN, MM, OO, true>, dim3(blocks), dim3(cfg.threads), \
                                        cfg.smem, stream, pdl, t, d_pool, first_seg, cfg.cmax, place_hint, \
-                                       frozen, rs, out);
+                                       frozen, rs, out, (LoopState*)nullptr);
     switch (cfg.variant) {
         V2_CASE(20, 5, 2)
         V2_CASE(20, 10, 2)

@@ -192,6 +192,10 @@ struct K2Config {
     int ppc_cap = 0;     // > 0: at most this many parents per chunk
     int blocks = 0;
     size_t smem = 0;
+    // persistent batch kernel (k2_v2_kernel<..., BATCH>): a whole device-planned batch of
+    // single-wave rounds in one cooperative launch of `blocks` CTAs
+    bool batch = false;
+    size_t batch_smem = 0;
 };
 K2Config k2_config(const DevTables& t, int device);
 
@@ -224,6 +228,11 @@ constexpr size_t kRoundStateHead = offsetof(RoundState, schedule);
 bool k2_v2_config(const DevTables& t, int device, K2Config* out);
 // place_hint: 0 staged placement, 1 direct (Pool::direct, known to the host), -1 read it
 // from the pool (device-planned loop)
+// The persistent batch kernel: plans, runs (leaves, K2 with direct placement) and closes
+// rounds until the loop state stops it; every round must fit one wave (direct placement).
+struct LoopState;
+cudaError_t launch_k2_v2_batch(const DevTables& t, const K2Config& cfg, LoopState* ls, Pool* d_pool,
+                               RoundState* rs, ChunkOut out, cudaStream_t stream);
 cudaError_t launch_k2_v2(const DevTables& t, const K2Config& cfg, const Pool* d_pool, int first_seg,
                          int blocks, int place_hint, int frozen, RoundState* rs, ChunkOut out,
                          cudaStream_t stream, bool pdl = false);
@@ -262,6 +271,7 @@ struct LoopRecord {  // one round's counters (search.hpp:21-26, 75-79)
     // device clock (%globaltimer, ns): plan start, close end, first K2 CTA start, last K2
     // CTA end -- the per-round timing of a batch that has no events inside it
     unsigned long long t0, t1, k2_t0, k2_t1;
+    unsigned long long tp, tb;  // persistent batch kernel: plan end, CTA 0 past the plan's grid barrier
 };
 
 // Device-resident explorer state for a batch of rounds.  The host writes the head
@@ -283,6 +293,7 @@ struct LoopState {
     int32_t cur_round;                // conditional-graph batches: the round the next step closes / plans
     int32_t host_dst;                 // the buckets are pinned host memory (Pool::host_dst)
     int32_t spread_blocks;            // > 0: small pools spread over this many K2 CTAs (spread_ppc)
+    uint32_t bar_count, bar_gen;      // grid barrier of the persistent batch kernel (zeroed by the host)
     int32_t schedule[kMaxJobs];       // incumbent schedule (solve mode)
     LoopRecord rec[kLoopMax];
 };
@@ -371,12 +382,19 @@ __host__ __device__ inline int round_ppc_cap(int ppc_cap, int ppc_lim) {
 // chunk's serial chain (staging, tables, scans, bounds, compaction), so it shrinks with
 // the chunk.  Returns the smallest Pool::ppc_lim that keeps the round within `blocks`
 // chunks (0: none -- the pool already fills the wave).
+// ceil(a / b) for a >= 0, b > 0 -- in 32 bits when a fits: the device planner runs on one
+// thread, where a 64-bit division is a long dependent subroutine
+__host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) {
+    if (((uint64_t)a >> 31) == 0 && ((uint64_t)b >> 31) == 0)
+        return (int64_t)(((uint32_t)a + (uint32_t)b - 1u) / (uint32_t)b);
+    return (a + b - 1) / b;
+}
 __host__ __device__ inline int64_t spread_chunks(const Segment* seg, int nseg, int n, int cmax, int cap) {
     int64_t chunks = 0;
     for (int s = 0; s < nseg; ++s) {
         if (seg[s].depth >= n - 2) continue;  // leaves: no chunks
         const int ppc = parents_per_chunk(n, seg[s].depth, cmax, cap);
-        chunks += (seg[s].count + ppc - 1) / ppc;
+        chunks += ceil_div(seg[s].count, ppc);
     }
     return chunks;
 }
@@ -393,11 +411,16 @@ __host__ __device__ inline int spread_ppc(const Segment* seg, int nseg, int n, i
         ++nint;
     }
     if (nint == 0 || spread_chunks(seg, nseg, n, cmax, ppc_cap) >= blocks || blocks <= nint) return 0;
-    // a lower bound (every segment at the cap), then up until the count fits
-    int64_t lim = (parents + (blocks - nint) - 1) / (blocks - nint);
-    if (lim < 1) lim = 1;
-    while (lim < ppc_max && spread_chunks(seg, nseg, n, cmax, (int)lim) > blocks) ++lim;
-    return lim < ppc_max ? (int)lim : 0;
+    // the smallest cap whose chunk count fits (the count falls as the cap grows): binary
+    // search between a lower bound (every segment at the cap) and ppc_max (fits)
+    int64_t lo = ceil_div(parents, blocks - nint), hi = ppc_max;
+    if (lo < 1) lo = 1;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (spread_chunks(seg, nseg, n, cmax, (int)mid) > blocks) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo < ppc_max ? (int)lo : 0;
 }
 
 }  // namespace fbb

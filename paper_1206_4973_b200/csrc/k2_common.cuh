@@ -167,4 +167,118 @@ __device__ __forceinline__ void leaf_offer(RoundState* rs, int32_t value, int64_
     atomicMax(&rs->leaf_inv, ~key);
 }
 
+// Children of parents at depth >= n-2 are complete schedules: bound = makespan
+// (bound.hpp:95).  Thread per child; batch-minimum (value, position) by atomicMin.
+// A pool has at most two leaf segments, both ahead of every internal one (segments
+// are depth-descending): parents at depth n-1 (children complete at once) and at
+// depth n-2 (children auto-completed, search.hpp:48-55).  Pending trees built by the
+// search itself never hold depth n-1 nodes, but fbb_explorer_reset / push and
+// fbb_expand_bound_prune accept them.
+__device__ __forceinline__ int leaf_segments(const Pool* __restrict__ pool, int n) {
+    int k = 0;
+    while (k < 2 && k < pool->nseg && pool->seg[k].depth >= n - 2) ++k;
+    return k;
+}
+
+// The leaf children of a pool, one per thread (grid-stride): makespan of the completion,
+// batch minimum (value, first position) by atomicMin.
+__device__ __forceinline__ void leaf_children(const DevTables& t, const Pool* __restrict__ pool, RoundState* rs,
+                                              int nls) {
+    const int n = t.n, m = t.m, W = t.W;
+    const int64_t nc0 = pool->seg[0].count * (n - pool->seg[0].depth);
+    const int64_t nct = nc0 + (nls > 1 ? pool->seg[1].count * (n - pool->seg[1].depth) : 0);
+    for (int64_t cc = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; cc < nct;
+         cc += (int64_t)gridDim.x * blockDim.x) {
+        const int si = cc < nc0 ? 0 : 1;
+        const Segment& sg = pool->seg[si];
+        const int64_t c = si == 0 ? cc : cc - nc0;
+        const int depth = sg.depth;
+        const int r = n - depth;
+        int64_t pp = c / r;
+        int rk = (int)(c - pp * r);
+        int64_t node = sg.first + sg.step * pp;
+        // the unscheduled jobs in ascending order: x = rk-th, y = the other
+        int u[2] = {-1, -1}, cnt = 0;
+        int32_t prev = 0, h[kMaxMachines];
+        if (sg.src.heads) {
+            const uint64_t* mk = sg.src.masks + node * W;
+            for (int j = 0; j < n && cnt < 2; ++j)
+                if (!((mk[j >> 6] >> (j & 63)) & 1ull)) u[cnt++] = j;
+            for (int k = 0; k < m; ++k) h[k] = sg.src.heads[node * m + k];
+        } else {  // compact rows: heads and unscheduled jobs from the prefix
+            const uint8_t* pre = sg.src.prefix + node * n;
+            uint64_t sm[kMaxWords] = {0, 0, 0, 0};
+            for (int k = 0; k < m; ++k) h[k] = 0;
+            for (int i = 0; i < depth; ++i) {  // child_heads, instance.hpp:81-89
+                const int j = pre[i];
+                sm[j >> 6] |= 1ull << (j & 63);
+                prev = 0;
+                for (int k = 0; k < m; ++k) {
+                    prev = max(prev, h[k]) + t.p[j * m + k];
+                    h[k] = prev;
+                }
+            }
+            for (int j = 0; j < n && cnt < 2; ++j)
+                if (!((sm[j >> 6] >> (j & 63)) & 1ull)) u[cnt++] = j;
+        }
+        if (cnt < r) {  // a pending node must have exactly r unscheduled jobs
+            atomicExch(&rs->found, -1);
+            continue;
+        }
+        int x = u[rk], y = (r == 2) ? u[1 - rk] : -1;
+        prev = 0;
+        for (int k = 0; k < m; ++k) {
+            prev = max(prev, h[k]) + t.p[x * m + k];
+            h[k] = prev;
+        }
+        if (y >= 0) {
+            prev = 0;
+            for (int k = 0; k < m; ++k) {
+                prev = max(prev, h[k]) + t.p[y * m + k];
+                h[k] = prev;
+            }
+        }
+        leaf_offer(rs, h[m - 1], sg.child_base + c);
+    }
+}
+
+// Writes the schedule of the batch's best leaf (if it beats the pool's bound) before the
+// parents' storage is recycled by the push.  A
+// corrupt-node flag (found < 0, set by the leaf kernel) is kept for the host to report.
+__device__ inline void write_leaf_schedule(const DevTables& t, const Pool* __restrict__ pool, RoundState* rs) {
+    if (rs->found < 0) return;
+    const int32_t ub = pool->ub;
+    const int n = t.n;
+    const int nls = leaf_segments(pool, n);
+    unsigned long long inv = rs->leaf_inv;
+    unsigned long long key = ~inv;
+    int32_t* schedule = rs->schedule;
+    int32_t* found = &rs->found;
+    if (nls == 0 || inv == 0ull || (int32_t)(key >> 32) >= ub) {  // no (improving) leaf
+        *found = 0;
+        return;
+    }
+    int64_t pos = (int64_t)(key & 0xFFFFFFFFull);
+    // the leaf's segment: the first or (depth n-2 behind depth n-1) the second one
+    const int si = nls > 1 && pos >= pool->seg[1].child_base ? 1 : 0;
+    const Segment& sg = pool->seg[si];
+    const int r = n - sg.depth;
+    int64_t c = pos - sg.child_base;
+    int64_t pp = c / r;
+    int rk = (int)(c - pp * r);
+    int64_t node = sg.first + sg.step * pp;
+    const uint8_t* pre = sg.src.prefix + node * n;
+    uint64_t sm[kMaxWords] = {0, 0, 0, 0};  // scheduled jobs, from the prefix
+    for (int i = 0; i < sg.depth; ++i) {
+        schedule[i] = pre[i];
+        sm[pre[i] >> 6] |= 1ull << (pre[i] & 63);
+    }
+    int u[2] = {-1, -1}, cnt = 0;
+    for (int j = 0; j < n && cnt < 2; ++j)
+        if (!((sm[j >> 6] >> (j & 63)) & 1ull)) u[cnt++] = j;
+    schedule[sg.depth] = u[rk];
+    if (r == 2) schedule[sg.depth + 1] = u[1 - rk];
+    *found = 1;
+}
+
 }  // namespace fbb

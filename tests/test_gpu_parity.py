@@ -481,6 +481,41 @@ def test_device_planned_loop_matches_reference(instances, traces, on_host, rows,
         ctx.close()
 
 
+@pytest.mark.parametrize("persist", ["1", "0"], ids=["persistent", "graph"])
+def test_persistent_batch_matches_reference(instances, traces, persist, monkeypatch):
+    """Single-wave batches on an HBM tree run as ONE cooperative launch of the persistent K2
+    (plan, leaves, K2 with direct placement and close per round inside it, grid barriers
+    between; FBB_PERSIST=0: the conditional-graph batch): resolve and solve traces, leaf
+    rounds and schedules included, equal the reference's.  The launch count proves which
+    path ran (persistent: one launch for a whole batch)."""
+    monkeypatch.setenv("FBB_DEVICE_LOOP", "1")
+    monkeypatch.setenv("FBB_PERSIST", persist)
+    ran_persistent = False
+    for tr in traces["resolve"]:
+        inst = inst_of(instance_p(instances, tr["instance"]))
+        ctx = fbb.Context(inst)
+        if "batch=1" not in ctx.kernels() or max(tr["targets"]) > 16384:
+            ctx.close()
+            continue
+        ctx.explorer_reset(fbb.nodes_from_prefixes(inst, tr["roots"]), tr["ub"], frozen=True)
+        rounds, tim = ctx.explorer_run(tr["targets"], 1 << 20, tr["budget"], timing=True)
+        assert rounds == [tuple(r) for r in tr["rounds"]], tr["instance"]
+        if persist == "1" and len(tim) > 2:
+            assert sum(t["launches"] for t in tim) < len(tim)  # not 5 kernels per round
+            ran_persistent = True
+        ctx.close()
+    for case in traces["solve_full"]:
+        p = np.asarray(case["p"], np.int32).reshape(case["n"], case["m"])
+        ctx = fbb.Context(inst_of(p))
+        r0 = ctx.explorer_start_solve(None)
+        rounds = ctx.explorer_run([case["batch"]], 1 << 20)
+        st = ctx.explorer_state()
+        assert [r0] + rounds == [tuple(r) for r in case["rounds"]]
+        assert st["incumbent"] == case["optimum"] and st["schedule"] == case["schedule"]
+        ctx.close()
+    assert ran_persistent or persist == "0"
+
+
 # ---- >= 1 M-node traces at 50x20, 100x20, 200x20 (tests/golden/make_traces_large.py) ----------
 
 def _large_traces():
