@@ -760,8 +760,9 @@ int explorer_run_batched(fbb_ctx* ctx, const int64_t* targets, int ntargets, int
     if (done) *done = 0;
     CK(ctx->d_loop.ensure(sizeof(LoopState)), "loop state");
     CK(ctx->h_loop.ensure(sizeof(LoopState)), "loop state");
-    CK(ctx->d_pool.ensure(sizeof(Pool)), "pool");
-    CK(ctx->d_round.ensure(sizeof(RoundState)), "round state");
+    // (two of each: the persistent kernel alternates between them)
+    CK(ctx->d_pool.ensure(2 * sizeof(Pool)), "pool");
+    CK(ctx->d_round.ensure(2 * sizeof(RoundState)), "round state");
     LoopState* hl = ctx->h_loop.as<LoopState>();
     static const bool dbg = [] { const char* e = getenv("FBB_LOOP_DEBUG"); return e && e[0] == '1'; }();
     while (r < max_rounds) {
@@ -840,7 +841,10 @@ int explorer_run_batched(fbb_ctx* ctx, const int64_t* targets, int ntargets, int
         static const bool use_graph = [] { const char* e = getenv("FBB_LOOP_GRAPH"); return !(e && e[0] == '0'); }();
         static const bool loop_pdl = [] { const char* e = getenv("FBB_PDL"); return !(e && e[0] == '0'); }();
         static const bool persist = [] { const char* e = getenv("FBB_PERSIST"); return !(e && e[0] == '0'); }();
-        const bool pbk = persist && all_direct && ctx->k2.batch;
+        // the persistent kernel when the batch's pools are mostly single-wave (a round that
+        // is not comes back as stop 6 and runs host-planned)
+        const bool pbk = persist && ctx->k2.batch && hl->direct_cap > 0 &&
+                         (tmax + n) * 4 <= (int64_t)hl->direct_cap * cmax * 3;
         if (pbk) {
             // every round of the batch fits one wave: ONE cooperative launch of the
             // persistent K2 plans, runs and closes them all (expand_v2.cu, BATCH)
@@ -1008,6 +1012,16 @@ int explorer_run_batched(fbb_ctx* ctx, const int64_t* targets, int ntargets, int
                 fprintf(stderr, "[loop] grow bucket %d to %lld rows (cap %lld) in %.1f us\n", d,
                         (long long)hl->need_rows, (long long)ctx->bucket[d].cap,
                         std::chrono::duration<float, std::micro>(std::chrono::steady_clock::now() - g0).count());
+            continue;
+        }
+        if (hl->stop == 6 && r < max_rounds) {  // a round larger than one wave: host-planned
+            int64_t target = targets[r < ntargets ? r : ntargets - 1];
+            fbb_round_t rec;
+            const int rc = explorer_round(ctx, target < 1 ? 1 : target, &rec);
+            if (rc != FBB_OK) return rc;
+            if (rounds) rounds[r] = rec;
+            ++r;
+            if (done) *done = r;
             continue;
         }
         if (hl->stop == 1 || hl->stop == 2) break;

@@ -334,7 +334,7 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
         ((uint4*)s_Mq)[x] = make_uint4(0u, 0u, 0u, 0u);
 
     // one round over `pool` (the kernel's argument, or the batch's shared-memory copy)
-    auto k2_round = [&](const Pool* __restrict__ pool) {
+    auto k2_round = [&](const Pool* __restrict__ pool, RoundState* rs) {
     // the round's bound, semantics and first internal segment come from the pool
     // (written by the host, or by the device-side planner of the batched explorer loop)
     asm volatile("griddepcontrol.wait;" ::: "memory");  // the pool upload kernel (PDL)
@@ -748,7 +748,7 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
     };  // k2_round
 
     if constexpr (!BATCH) {
-        k2_round(pool_arg);
+        k2_round(pool_arg, rs);
     } else {
         // batch state: CTA 0 keeps the bucket sizes in shared memory for the whole batch;
         // every CTA copies each round's plan (written by CTA 0 during this kernel, so read
@@ -764,42 +764,56 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
             stage_buckets(ls, s_bucket, s_cap, n, tid, bd);
             for (int i = tid; i < kLoopMax; i += bd) ls->rec[i].valid = 0;  // see loop_step_kernel
         }
-        __syncthreads();
-        for (int round = 0;; ++round) {
-            if (blockIdx.x == 0) {  // CTA 0 closes and plans in its shared memory, then publishes
-                if (warp == 0) {
-                    if (round > 0) close_round(t, ls, s_pool, rs, round - 1, s_cnt, lane);
-                    __syncwarp();
-                    // nothing planned past nrounds or a stop
-                    plan_round(t, ls, s_pool, rs, round, s_cnt, LoopBuckets{s_bucket, s_cap}, lane);
+        // Rounds alternate between two (Pool, RoundState) buffers: CTA 0 closes round r and
+        // plans round r + 1 right after its own K2 chunk, while the other CTAs still write
+        // their survivors (the plan needs only the counts, final at direct_arrive), so a
+        // round costs one grid barrier plus K2's arrival count.  Round r + 1's buffers were
+        // last used by round r - 1, which every CTA left at round r's barrier.
+        const LoopBuckets bk{s_bucket, s_cap};
+        auto plan_publish = [&](int round) {  // CTA 0
+            if (warp == 0) plan_round(t, ls, s_pool, rs + (round & 1), round, s_cnt, bk, lane);
+            if (lead) {
+                if (s_pool->nseg > 0 && s_pool->nchunks > 0 && !s_pool->direct) {
+                    ls->stop = 6;  // more chunks than one wave: the host runs this round itself
+                    s_pool->nseg = 0;
                 }
-                if (lead) {
-                    if (s_pool->nseg > 0 && s_pool->nchunks > 0 && !s_pool->direct) {
-                        ls->stop = 5;  // more chunks than one wave: the host never plans such a batch
-                        s_pool->nseg = 0;
-                    }
-                    if (round < kLoopMax) ls->rec[round].tp = loop_ns();
-                }
-                __syncthreads();
-                pool_store(gpool, s_pool, s_pool->nseg, tid, bd);
+                if (round < kLoopMax) ls->rec[round].tp = loop_ns();
             }
-            batch_grid_sync(&ls->bar_count, &ls->bar_gen);
-            if (lead && round < kLoopMax) ls->rec[round].tb = loop_ns();
-            if (blockIdx.x != 0) pool_load(s_pool, gpool, __ldcg(&gpool->nseg), tid, bd);
             __syncthreads();
-            const int nseg = s_pool->nseg;
-            if (nseg == 0) break;
+            pool_store(gpool + (round & 1), s_pool, s_pool->nseg, tid, bd);
+        };
+        __syncthreads();  // CTA 0's staged bucket state
+        if (blockIdx.x == 0) plan_publish(0);
+        int round = 0;
+        for (;; ++round) {
+            Pool* gp = gpool + (round & 1);
+            RoundState* rsr = rs + (round & 1);
+            batch_grid_sync(&ls->bar_count, &ls->bar_gen);  // plan published, last survivors written
+            if (lead && round < kLoopMax) ls->rec[round].tb = loop_ns();
+            if (blockIdx.x != 0) pool_load(s_pool, gp, __ldcg(&gp->nseg), tid, bd);
+            __syncthreads();
+            if (s_pool->nseg == 0) break;
             if (s_pool->seg[0].depth >= n - 2) {
                 // leaves (search.hpp:48-55), then the best leaf's schedule before K2 recycles
                 // the leaf parents' slots
-                leaf_children(t, s_pool, rs, leaf_segments(s_pool, n));
+                leaf_children(t, s_pool, rsr, leaf_segments(s_pool, n));
                 batch_grid_sync(&ls->bar_count, &ls->bar_gen);
-                if (lead) write_leaf_schedule(t, s_pool, rs);
+                if (lead) write_leaf_schedule(t, s_pool, rsr);
                 batch_grid_sync(&ls->bar_count, &ls->bar_gen);
             }
-            k2_round(s_pool);
-            batch_grid_sync(&ls->bar_count, &ls->bar_gen);  // survivors written, counts final
+            k2_round(s_pool, rsr);
+            __syncthreads();
+            if (blockIdx.x == 0) {
+                if (warp == 0) {
+                    close_round(t, ls, s_pool, rsr, round, s_cnt, lane);
+                    // the previous round's K2 end stamp is final now (before its buffer is reset)
+                    if (lane == 0 && round > 0) ls->rec[round - 1].k2_t1 = __ldcg(&rs[(round - 1) & 1].k2_t1);
+                    __syncwarp();
+                }
+                plan_publish(round + 1);
+            }
         }
+        if (lead && round > 0 && round - 1 < kLoopMax) ls->rec[round - 1].k2_t1 = __ldcg(&rs[(round - 1) & 1].k2_t1);
         if (blockIdx.x == 0)
             for (int d = tid; d <= n; d += bd) ls->cnt[d] = s_cnt[d];
     }

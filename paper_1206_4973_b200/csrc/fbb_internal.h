@@ -285,7 +285,8 @@ struct LoopState {
     int64_t tot_bounded, budget;      // cumulative bounded count; stop when >= budget (> 0)
     int32_t incumbent, best, found, frozen;
     int32_t stop;                     // 0 running, 1 pending empty, 2 budget, 3 bucket too small,
-                                      // 4 corrupt node, 5 staging too small (never, by sizing)
+                                      // 4 corrupt node, 5 staging too small (never, by sizing),
+                                      // 6 persistent kernel: the next round is not single-wave
     int32_t need_depth;               // stop == 3: the bucket that must grow ...
     int64_t need_rows;                // ... to at least this many rows
     int32_t cmax, ppc_cap, nrounds, chunk_cap;  // chunk_cap: staging chunks available
@@ -415,6 +416,7 @@ __host__ __device__ inline int spread_ppc(const Segment* seg, int nseg, int n, i
     // search between a lower bound (every segment at the cap) and ppc_max (fits)
     int64_t lo = ceil_div(parents, blocks - nint), hi = ppc_max;
     if (lo < 1) lo = 1;
+    if (lo < hi && spread_chunks(seg, nseg, n, cmax, (int)lo) <= blocks) hi = lo;  // usual case
     while (lo < hi) {
         const int64_t mid = (lo + hi) >> 1;
         if (spread_chunks(seg, nseg, n, cmax, (int)mid) > blocks) lo = mid + 1;

@@ -90,6 +90,7 @@ __device__ __forceinline__ void plan_round(const DevTables& t, LoopState* __rest
                                            const int64_t* __restrict__ cnt, LoopBuckets bk, int lane) {
     const int n = t.n;
     int nseg = 0;
+    int64_t target = 0;
     if (lane == 0) {
         if (round < kLoopMax) ls->rec[round].t0 = loop_ns();
         pool->nseg = 0;
@@ -106,52 +107,73 @@ __device__ __forceinline__ void plan_round(const DevTables& t, LoopState* __rest
         pool->ub = ls->incumbent;
         pool->frozen = ls->frozen;
         pool->first_internal = 0;
-        if (!ls->stop && round < ls->nrounds) {
-            const int64_t target = ls->targets[round] < 1 ? 1 : ls->targets[round];
-            // fill_buffer on the sizes (deepest bucket first, LIFO, until >= target)
-            int64_t have = 0;
-            for (int d = n; d >= 0 && have < target; --d) {
-                const int64_t c = cnt[d];
-                if (c == 0) continue;
-                const int r = n - d;
-                const int64_t k = min(c, ceil_div(target - have, r));
-                Segment& sg = pool->seg[nseg++];
-                sg.src = bk.bucket[d];
-                sg.first = c - 1;
-                sg.step = -1;
-                sg.count = k;
-                sg.depth = d;
-                sg.pad = 0;
-                sg.dst_lb = nullptr;
-                have += k * r;
-            }
-            if (nseg == 0) ls->stop = 1;
-            // destinations: bucket d+1 after this round's pops (depths are distinct and
-            // descending, so only the previous segment can pop bucket d+1); all sizes
-            // checked first
-            for (int s = 0; s < nseg; ++s) {
-                Segment& sg = pool->seg[s];
-                const int d = sg.depth;
-                if (d >= n - 2) {
-                    sg.dst = NodeStore{nullptr, nullptr, nullptr};
-                    sg.dst_base = 0;
-                    continue;
-                }
-                int64_t after = cnt[d + 1];
-                if (s > 0 && pool->seg[s - 1].depth == d + 1) after -= pool->seg[s - 1].count;
-                const int64_t worst = after + sg.count * (n - d);
-                if (worst > bk.cap[d + 1]) {
-                    ls->stop = 3;
-                    ls->need_depth = d + 1;
-                    ls->need_rows = worst;
-                    nseg = 0;  // nothing of this round runs
-                    break;
-                }
+        if (!ls->stop && round < ls->nrounds) target = ls->targets[round] < 1 ? 1 : ls->targets[round];
+    }
+    target = __shfl_sync(0xFFFFFFFFu, target, 0);
+    if (target == 0) return;  // stopped, or past the batch's rounds
+    // fill_buffer on the sizes (deepest bucket first, LIFO, until >= target), a lane per
+    // bucket in passes of 32 (i = n - d, deepest first): bucket i is popped iff it is
+    // non-empty and the full contents of the deeper buckets, prefix_i = sum_{j<i} c_j r_j,
+    // stay below the target (then every deeper one was popped whole); it gives k_i =
+    // min(c_i, ceil((target - prefix_i) / r_i)) parents.  Destinations: bucket d+1 after
+    // the pops (only bucket i-1 = d+1 can have been popped) must hold the worst case.
+    int64_t have = 0, k_prev = 0;
+    int fail = -1;  // first segment whose destination is too small
+    int64_t fail_rows = 0;
+    for (int i0 = 0; i0 <= n && have < target; i0 += 32) {
+        const int i = i0 + lane, d = n - i;
+        const bool lane_ok = i <= n;
+        const int64_t c = lane_ok ? cnt[d] : 0;
+        const int r = i;
+        const int64_t capc = c * r;
+        const int64_t prefix = have + warp_excl64(capc, lane);
+        const bool take = lane_ok && c > 0 && prefix < target;
+        const int64_t k = take ? (r > 0 ? min(c, ceil_div(target - prefix, r)) : c) : 0;
+        const unsigned tk = __ballot_sync(0xFFFFFFFFu, take);
+        const int s = nseg + __popc(tk & ((1u << lane) - 1u));
+        int64_t kp = __shfl_up_sync(0xFFFFFFFFu, k, 1);  // bucket d+1's pops
+        if (lane == 0) kp = k_prev;
+        bool bad = false;
+        int64_t worst = 0;
+        if (take) {
+            Segment& sg = pool->seg[s];
+            sg.src = bk.bucket[d];
+            sg.first = c - 1;
+            sg.step = -1;
+            sg.count = k;
+            sg.depth = d;
+            sg.pad = 0;
+            sg.dst_lb = nullptr;
+            if (d >= n - 2) {
+                sg.dst = NodeStore{nullptr, nullptr, nullptr};
+                sg.dst_base = 0;
+            } else {
+                const int64_t after = cnt[d + 1] - kp;
+                worst = after + k * r;
+                bad = worst > bk.cap[d + 1];
                 sg.dst = bk.bucket[d + 1];
                 sg.dst_base = after;
             }
         }
+        const unsigned badm = __ballot_sync(0xFFFFFFFFu, bad);
+        if (badm && fail < 0) {
+            const int src = __ffs(badm) - 1;
+            fail_rows = __shfl_sync(0xFFFFFFFFu, worst, src);
+            fail = n - (i0 + src) + 1;  // the bucket that must grow: depth d + 1
+        }
+        nseg += __popc(tk);
+        have += warp_sum64(take ? k * r : 0);
+        k_prev = __shfl_sync(0xFFFFFFFFu, k, 31);
     }
+    if (lane == 0) {
+        if (nseg == 0) ls->stop = 1;
+        else if (fail >= 0) {
+            ls->stop = 3;
+            ls->need_depth = fail;
+            ls->need_rows = fail_rows;
+        }
+    }
+    if (fail >= 0) nseg = 0;  // nothing of this round runs
     nseg = __shfl_sync(0xFFFFFFFFu, nseg, 0);
     __syncwarp();
     if (nseg == 0) return;
@@ -176,6 +198,7 @@ __device__ __forceinline__ void plan_round(const DevTables& t, LoopState* __rest
         if (nint > 0 && blocks > nint && warp_chunks(pool, nseg, n, cmax, ppc_cap, lane) < blocks) {
             int64_t lo = ceil_div(parents, blocks - nint), hi = ppc_max;
             if (lo < 1) lo = 1;
+            if (lo < hi && warp_chunks(pool, nseg, n, cmax, (int)lo, lane) <= blocks) hi = lo;  // usual case
             while (lo < hi) {
                 const int64_t mid = (lo + hi) >> 1;
                 if (warp_chunks(pool, nseg, n, cmax, (int)mid, lane) > blocks) lo = mid + 1;
