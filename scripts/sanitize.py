@@ -1,6 +1,7 @@
 """Small workloads for compute-sanitizer (memcheck / racecheck / synccheck): every kernel
 path -- K1 v1/v2, K2 v2 (both occupancies), v3, generic, leaves, place, the explorer
-with its tree in HBM and in host memory, and the device-planned loop -- on inputs
+with its tree in HBM and in host memory, the device-planned loop (graph batches and the
+persistent batch kernel) -- on inputs
 small enough for the sanitizer, each checked against the oracle."""
 import os
 import sys
@@ -33,8 +34,11 @@ for n, m in [(20, 20), (20, 5), (50, 20), (100, 20), (12, 7)]:
     ctx.close()
     # direct placement (single-wave pools: K2 grid-wide count + direct bucket writes) and the
     # device-planned graph batches, in solve mode (leaf rounds, incumbent updates)
-    for dl in ("0", "1"):
+    # (FBB_PERSIST: the persistent batch kernel -- one cooperative launch per batch, grid
+    # barriers between the rounds -- or the conditional-graph batch)
+    for dl, ps in (("0", "1"), ("1", "1"), ("1", "0")):
         os.environ["FBB_DEVICE_LOOP"] = dl
+        os.environ["FBB_PERSIST"] = ps
         ctx = fbb.Context(inst)
         ctx.explorer_set_residency(False)
         ctx.explorer_start_solve(None)
