@@ -6,7 +6,8 @@ B rounds, L2 flushed between steps (untimed); rate = bounded nodes / wall clock 
 calls (host->device state upload, the rounds, the summary download included), plus the
 device-only rate from the rounds' own timings.  Prints one JSON line per (target, planner).
 
-usage: python scripts/batch_sweep.py [targets...]   (env BATCH=rounds per call, STEPS)"""
+usage: python scripts/batch_sweep.py [targets...]   (env BATCH=rounds per call, STEPS,
+PLANNERS=01 / 0 / 1)"""
 import json
 import os
 import sys
@@ -57,5 +58,5 @@ def run(T, planner):
 
 if __name__ == "__main__":
     for T in TARGETS:
-        for pl in ("0", "1"):
+        for pl in os.environ.get("PLANNERS", "01"):
             print(json.dumps(run(T, pl)), flush=True)
