@@ -281,6 +281,48 @@ def reference_arm(args, inst_name):
     print(json.dumps(line), flush=True)
 
 
+def small_pool_batches(fbb, inst, ub, dev, targets=(4096, 16384, 32768), rounds=32, calls=10):
+    """BASELINE configs[1]'s low end (the paper's 4 K-64 K pools) the way an explorer runs
+    there: K rounds per fbb_explorer_run call on the HBM tree -- device-planned, so a batch of
+    single-wave rounds is ONE cooperative launch of the persistent K2 (expand_v2.cu, BATCH).
+    Per target: a fresh context from the root, prefill until a round reaches the target, 2
+    warm-up calls, then `calls` timed calls of `rounds` rounds with the L2 flushed (256 MiB
+    write) between calls.  device = bounded / the rounds' device-clock time; wall = bounded /
+    wall clock of the calls (state upload, launch, download and sync included)."""
+    import torch
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{dev}")
+    out = {}
+    for T in targets:
+        ctx = fbb.Context(inst, dev)
+        ctx.explorer_reset(fbb.NodeBatch.root(inst), ub, frozen=True)
+        for _ in range(64):
+            r = ctx.explorer_run([T], 1)
+            if not r or r[0][2] >= T:
+                break
+        for _ in range(2):
+            ctx.explorer_run([T], rounds)
+        wall = devs = 0.0
+        bounded = nr = launches = 0
+        for c in range(calls):
+            flush.fill_(c % 7)
+            torch.cuda.synchronize()
+            w0 = time.perf_counter()
+            r, t = ctx.explorer_run([T], rounds, timing=True)
+            wall += time.perf_counter() - w0
+            devs += sum(x["round_ms"] for x in t) / 1e3
+            bounded += sum(x[2] for x in r)
+            nr += len(r)
+            launches += sum(x["launches"] for x in t)
+        ctx.close()
+        out[str(T)] = {"rounds": nr, "bounded": bounded, "device_value": bounded / devs if devs else 0.0,
+                       "wall_value": bounded / wall if wall else 0.0,
+                       "us_per_round_device": 1e6 * devs / max(1, nr),
+                       "us_per_round_wall": 1e6 * wall / max(1, nr), "gpu_launches": launches}
+    return {"unit": "bounded subproblems/s", "rounds_per_call": rounds, "calls": calls,
+            "l2": "flushed between calls (256 MiB write)", "targets": out}
+
+
 def reference_api_e2e(target, steps):
     """The same workload driven through the calls a reference C++ user makes, with the
     reference's own PendingTree of heap Nodes on the host (tests/cpp/bench_dropin.cpp, built
@@ -1011,8 +1053,10 @@ def main():
                            "event can sit between them); rounds themselves are CUDA-event timed"),
     }
     ref_api = None
+    small = None
     if not args.no_e2e and world == 1 and inst_name == "ta021" and not args.tuner:
         ref_api = reference_api_e2e(T, min(args.steps, 20))
+        small = small_pool_batches(fbb, inst, ub, dev)
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         try:
@@ -1039,7 +1083,8 @@ def main():
             "library_sync_wait": sum(t["sync_ms"] for t in timing) / max(1, len(timing)),
             "device_events": dev_ms / max(1, len(timing)),
             "l2_flush_untimed": 1e3 * flush_s / max(1, len(rounds))},
-        "e2e": e2e, "e2e_reference_api": ref_api, "roofline": roofline, "cpu_baseline": cpu,
+        "e2e": e2e, "e2e_reference_api": ref_api, "small_pool_batches": small, "roofline": roofline,
+        "cpu_baseline": cpu,
         "clocks": clocks,
         "gpu_launches": int(launches_all),
         "rounds": [list(r) for r in rounds],
