@@ -13,7 +13,7 @@ import tempfile
 
 rep, obj, pat = sys.argv[1], sys.argv[2], sys.argv[3]
 top = int(sys.argv[4]) if len(sys.argv) > 4 else 40
-out = subprocess.run(["ncu", "-i", rep, "-k", "regex:" + pat.split("<")[0], "--page", "source", "--csv", "--print-source", "sass"],
+out = subprocess.run(["ncu", "-i", rep, "-k", "regex:" + re.split(r"<|IL", pat)[0], "--page", "source", "--csv", "--print-source", "sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 hdr, data = rows[1], [r for r in rows[2:] if len(r) == len(rows[1])]
