@@ -582,42 +582,75 @@ __global__ void __launch_bounds__(kPlaceThreads) place_kernel(DevTables t, const
     if (2 * s_need <= n || !pool->host_dst) {
         copy_array(out.nodes.prefix, n, s_need, [&](int row) { return (void*)s_store[s_rc[row]].prefix; });
     } else {
-        // host buckets, mostly-used rows: whole rows, as one contiguous byte range per
-        // chunk written in aligned 16-byte stores (the host link takes ~2x more bytes/s
-        // from those than from 4-byte row-unit stores; in HBM the row form is faster);
-        // the 16-byte blocks of all the CTA's chunks form one flat index space
+        // host buckets, mostly-used rows: whole rows, in aligned 16-byte stores (the host
+        // link takes ~2x more bytes/s from those than from 4-byte row-unit stores; in HBM
+        // the row form is faster).  Consecutive chunks of one segment are contiguous in the
+        // destination, so the CTA's chunks merge into runs (usually one): partial 16-byte
+        // blocks -- written byte by byte, each a separate small write over the link -- occur
+        // only at the two ends of a run, not at every chunk boundary.  The 16-byte blocks of
+        // all runs form one flat index space.
         __shared__ int64_t s_blk[kPlaceChunks + 1];
+        __shared__ int s_run_row[kPlaceChunks + 1];  // first CTA row of each run
+        __shared__ uint8_t* s_run_dst[kPlaceChunks];
+        __shared__ int s_nrun;
         if (tid == 0) {
-            int64_t acc = 0;
+            int nr = 0;
             for (int c = 0; c < nch; ++c) {
-                s_blk[c] = acc;
-                const int64_t len = (int64_t)(s_row0[c + 1] - s_row0[c]) * n;
-                const uintptr_t d0 = (uintptr_t)(s_store[c].prefix + s_dst[c] * n);
+                uint8_t* d = s_store[c].prefix + s_dst[c] * n;
+                if (nr > 0 && d == s_run_dst[nr - 1] + (int64_t)(s_row0[c] - s_run_row[nr - 1]) * n) continue;
+                s_run_dst[nr] = d;
+                s_run_row[nr] = s_row0[c];
+                ++nr;
+            }
+            s_run_row[nr] = s_row0[nch];
+            int64_t acc = 0;
+            for (int k = 0; k < nr; ++k) {
+                s_blk[k] = acc;
+                const int64_t len = (int64_t)(s_run_row[k + 1] - s_run_row[k]) * n;
+                const uintptr_t d0 = (uintptr_t)s_run_dst[k];
                 acc += len ? (int64_t)((d0 + len - (d0 & ~(uintptr_t)15) + 15) >> 4) : 0;
             }
-            s_blk[nch] = acc;
+            s_blk[nr] = acc;
+            s_nrun = nr;
         }
         __syncthreads();
-        for (int64_t b = tid; b < s_blk[nch]; b += kPlaceThreads) {
-            int c = 0;
-            while (b >= s_blk[c + 1]) ++c;
-            const int64_t len = (int64_t)(s_row0[c + 1] - s_row0[c]) * n;
-            const uint8_t* src = out.nodes.prefix + ((c0 + c) * (int64_t)cmax) * n;
-            uint8_t* dst = s_store[c].prefix + s_dst[c] * n;
+        const int nr = s_nrun;
+        for (int64_t b = tid; b < s_blk[nr]; b += kPlaceThreads) {
+            int k = 0;
+            while (b >= s_blk[k + 1]) ++k;
+            const int64_t len = (int64_t)(s_run_row[k + 1] - s_run_row[k]) * n;
+            uint8_t* dst = s_run_dst[k];
             const uintptr_t a0 = (uintptr_t)dst & ~(uintptr_t)15;
-            const int64_t off = (int64_t)(a0 + 16 * (b - s_blk[c]) - (uintptr_t)dst);  // block in dst
+            const int64_t off = (int64_t)(a0 + 16 * (b - s_blk[k]) - (uintptr_t)dst);  // block in dst
+            // the block's bytes from the staged rows (a run's rows are not contiguous there)
+            const int64_t o0 = off < 0 ? 0 : off;
+            int row = (int)(o0 / n), col = (int)(o0 - (int64_t)row * n);
+            const uint8_t* sp = out.nodes.prefix + src_row(s_run_row[k] + row) * n;
+            uint8_t v[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                const int64_t o = off + q;
+                v[q] = 0;
+                if (o >= o0 && o < len) {
+                    v[q] = __ldg(sp + col);
+                    if (++col == n) {
+                        col = 0;
+                        ++row;
+                        if (o + 1 < len) sp = out.nodes.prefix + src_row(s_run_row[k] + row) * n;
+                    }
+                }
+            }
             if (off >= 0 && off + 16 <= len) {
                 uint32_t w[4];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const uint8_t* sp = src + off + 4 * q;
-                    w[q] = (uint32_t)__ldg(sp) | ((uint32_t)__ldg(sp + 1) << 8) |
-                           ((uint32_t)__ldg(sp + 2) << 16) | ((uint32_t)__ldg(sp + 3) << 24);
-                }
+                for (int q = 0; q < 4; ++q)
+                    w[q] = (uint32_t)v[4 * q] | ((uint32_t)v[4 * q + 1] << 8) | ((uint32_t)v[4 * q + 2] << 16) |
+                           ((uint32_t)v[4 * q + 3] << 24);
                 *(uint4*)(dst + off) = make_uint4(w[0], w[1], w[2], w[3]);
-            } else {  // a partial block at either end of the range
+            } else {  // a partial block at either end of the run
+#pragma unroll
                 for (int q = 0; q < 16; ++q)
-                    if (off + q >= 0 && off + q < len) dst[off + q] = __ldg(src + off + q);
+                    if (off + q >= 0 && off + q < len) dst[off + q] = v[q];
             }
         }
     }

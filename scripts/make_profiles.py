@@ -91,7 +91,8 @@ def bench_line(path):
 
 def main(tag):
     os.makedirs(PROF, exist_ok=True)
-    md = [f"# {tag} — measured on one B200 (gpurun), `scripts/gpu_{tag}_final.sh`", ""]
+    script = sys.argv[2] if len(sys.argv) > 2 else f"scripts/gpu_{tag}_final.sh"
+    md = [f"# {tag} — measured on one B200 (gpurun), `{script}`", ""]
     gpu = os.path.join(OUT, "gpu.txt")
     if os.path.exists(gpu):
         md += ["```", open(gpu).read().strip(), open(os.path.join(OUT, "nproc.txt")).read().strip(),
@@ -111,6 +112,17 @@ def main(tag):
                   f"{e2e:.4g} | {rf.get('k2_share_of_round', 0):.3f} | {rf.get('frac', 0):.3f} | "
                   f"{cpu if cpu is None else f'{cpu:.4g}'} |")
         shutil.copy(os.path.join(OUT, f), os.path.join(PROF, f"{tag}_{f}"))
+    d = bench_line(os.path.join(OUT, "bench.json"))
+    if d and d.get("small_pool_batches"):
+        sp = d["small_pool_batches"]
+        md += ["", f"### small pools in the default line (`small_pool_batches`: {sp['rounds_per_call']} rounds per "
+                   f"explorer call, persistent batch kernel, {sp['l2']})", "",
+               "| children per round | device bounded/s | us/round device | wall bounded/s | us/round wall | launches |",
+               "|---|---|---|---|---|---|"]
+        for T, v in sp["targets"].items():
+            md.append(f"| {T} | {v['device_value'] / 1e6:.1f} M | {v['us_per_round_device']:.1f} | "
+                      f"{v['wall_value'] / 1e6:.1f} M | {v['us_per_round_wall']:.1f} | {v['gpu_launches']} "
+                      f"for {v['rounds']} rounds |")
     header = False
     for f in ["bench_bound_ta101.json", "bench_bound_ta051.json", "bench_bound_ta021.json",
               "bench_bound_ref.json"]:
@@ -148,7 +160,9 @@ def main(tag):
                        ("prof_k2v3_ta081.ncu-rep", "K2 (v3, Ta081)"),
                        ("prof_k1v2_ta101.ncu-rep", "K1 (v2, 200x20 bound-only pool)"),
                        ("prof_k1v3_ta101.ncu-rep", "K1 (v3, 200x20 bound-only pool of 1 M nodes)"),
-                       ("prof_k1v3_ta021.ncu-rep", "K1 (v3, 20x20 bound-only pool of 2 M nodes)")]:
+                       ("prof_k1v3_ta021.ncu-rep", "K1 (v3, 20x20 bound-only pool of 2 M nodes)"),
+                       ("prof_persistent.ncu-rep", "persistent batch kernel (K2 v2, BATCH; one launch = a "
+                                                   "batch of 4 K-child Ta021 rounds)")]:
         p = os.path.join(OUT, rep)
         if os.path.exists(p):
             md += ["", f"## ncu --set full: {title}", ncu_metrics(p)]
@@ -156,6 +170,7 @@ def main(tag):
     for f, title in [("solve_ta001.json", "Ta001 solve() from the identity UB, one context"),
                      ("solve_ta001_group2.json", "Ta001 solve() over an fbb_group of 2 (GPU 0 twice)"),
                      ("exhaust_group2.json", "Ta021 exhaustion at UB 2298 over an fbb_group of 2"),
+                     ("exhaust_ta021.json", "Ta021 exhaustion at UB 2298, one context"),
                      ("bench_bound_ta101_max.json", "Ta101 K1 over a pool filling the GPU's HBM")]:
         d = bench_line(os.path.join(OUT, f))
         if not d:
