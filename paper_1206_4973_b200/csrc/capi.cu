@@ -1148,7 +1148,25 @@ fbb_ctx* fbb_create(int device, const int32_t* p, int n, int m) {
         bool generic = sel && std::string(sel) == "generic";
         // (both register-row kernels pack d as int8 and tails as 16 bits)
         if (max_tail < 0x7FFF && ctx->ht.max_abs_d <= 127 && !generic) {
-            if (k2_v2_config(ctx->dt, device, &kc)) ctx->k2 = kc;
+            if (k2_v2_config(ctx->dt, device, &kc)) {
+                ctx->k2 = kc;
+                // the variant's staged rows (expand_v2.cu prologue), for its TMA bulk copy
+                const int N = (kc.variant / 100) % 100, occ = kc.variant / 10000, n = ctx->dt.n, P = ctx->dt.P;
+                const bool dual = occ == 2 && N == 20;
+                std::vector<uint32_t> rows((size_t)N * P, N <= 32 ? 0u : 32u);
+                for (int x = 0; x < n * P; ++x) {
+                    const uint32_t e = ctx->ht.jm[x];
+                    const uint32_t j = (uint32_t)entry_job(e);
+                    rows[x] = (31u - (j & 31u)) | (j & 32u) | ((uint32_t)entry_c(e) << 8) |
+                              ((uint32_t)(dual ? entry_d(e) : -entry_d(e)) << 24);
+                }
+                if (const char* tm = getenv("FBB_TMA"); !(tm && tm[0] == '0')) {
+                    if (cudaMalloc(&ctx->dt.rowk2, rows.size() * 4) == cudaSuccess)
+                        cudaMemcpy(ctx->dt.rowk2, rows.data(), rows.size() * 4, cudaMemcpyHostToDevice);
+                    else
+                        ctx->dt.rowk2 = nullptr;
+                }
+            }
             else if (k2_v3_config(ctx->dt, device, &kc)) ctx->k2 = kc;
         }
         // a variant that could not be configured must not leave its error behind for the

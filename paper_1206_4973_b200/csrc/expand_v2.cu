@@ -318,7 +318,23 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
     //   bits 8..23 c, bits 24..31 -d (int8).  Padding positions i >= n read the top bit
     //   of U (bit 31, or 63 in the wide variant), which is 0 when padding exists.
     uint32_t* s_row = (uint32_t*)(smem + L.row);
-    for (int x = tid; x < N * P; x += bd) {
+    // DevTables::rowk2 holds exactly these words for the configured variant: one TMA bulk
+    // copy (cp.async.bulk, completion counted on an mbarrier) stages them while the CTA's
+    // threads stage p / tails and clear Mq; the per-thread repacking loop is the fallback
+    __shared__ __align__(8) uint64_t s_tma_bar;
+    const uint32_t tma_bar = (uint32_t)__cvta_generic_to_shared(&s_tma_bar);
+    const bool tma = t.rowk2 != nullptr;
+    if (tma && tid == 0) {
+        const uint32_t bytes = (uint32_t)(N * P * 4);  // a multiple of 16 (N in {20, 32, 64})
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(tma_bar) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(tma_bar), "r"(bytes) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(s_row)),
+                     "l"(t.rowk2), "r"(bytes), "r"(tma_bar)
+                     : "memory");
+    }
+    for (int x = tid; x < N * P && !tma; x += bd) {
         uint32_t v = N <= 32 ? 0u : 32u;
         if (x < n * P) {
             uint32_t e = t.jm[x];
@@ -332,6 +348,17 @@ __global__ void __launch_bounds__(192, OCC) k2_v2_kernel(DevTables t, const Pool
     const uint32_t row_sa = (uint32_t)__cvta_generic_to_shared(s_row + q);
     for (int x = tid; x < (int)((cmax + v2_dummy_rows(P)) * L.rowb / 16); x += bd)  // padding slots stay 0
         ((uint4*)s_Mq)[x] = make_uint4(0u, 0u, 0u, 0u);
+    if (tma) {  // the rows are in (the barrier's phase 0 completes with the copy's bytes)
+        __syncthreads();  // (the mbarrier's initialisation, for every thread)
+        uint32_t done = 0;
+        while (!done)
+            asm volatile(
+                "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\nselp.u32 %0, 1, 0, p;\n}"
+                : "=r"(done)
+                : "r"(tma_bar)
+                : "memory");
+        __syncthreads();
+    }
 
     // one round over `pool` (the kernel's argument, or the batch's shared-memory copy)
     auto k2_round = [&](const Pool* __restrict__ pool, RoundState* rs) {

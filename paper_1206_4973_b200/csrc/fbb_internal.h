@@ -61,6 +61,10 @@ struct DevTables {
     // zero, k1_c0 lifts every member's candidate above every non-member's.  Null unless
     // kSafeK1x2.
     uint32_t* rowk1;
+    // K2 v2's rows exactly as its prologue stages them for the configured variant (N
+    // positions, [i][q], the 16x2 two-parent scan's +d or the others' -d), so a CTA stages
+    // them with one TMA bulk copy.  Null when K2 v2 is not configured.
+    uint32_t* rowk2;
     int32_t k1_bias, k1_c0;
     // Which 16-bit intermediates are exact for this instance (build_host_tables' range
     // analysis): kSafeM16 = every M' fits int16, kSafeLcM16 = every Lc_l + M'_kl fits int16,

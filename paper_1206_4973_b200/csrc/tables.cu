@@ -212,6 +212,7 @@ void free_tables(DevTables* d) {
     cudaFree(d->rowpk);
     cudaFree(d->rowv3);
     cudaFree(d->rowk1);
+    cudaFree(d->rowk2);
     cudaFree(d->jw);
     *d = DevTables{};
 }
