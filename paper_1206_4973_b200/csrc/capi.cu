@@ -817,6 +817,10 @@ int explorer_run_batched(fbb_ctx* ctx, const int64_t* targets, int ntargets, int
         hl->spread_blocks = (ctx->k2.variant != 0 && ctx->k2.variant < 100000) ? ctx->k2.blocks : 0;
         // every pool of the batch fits one wave (worst-case chunk count): K2 places them all
         const bool all_direct = hl->direct_cap > 0 && chunks <= hl->direct_cap;
+        // the place grid covers the staging's whole chunk capacity: tied to the staging
+        // buffers, which are part of a cached graph's key (a batch of smaller pools reusing
+        // a graph captured for larger ones launches CTAs that exit at once)
+        const int64_t place_chunks = ctx->staging.cap / cmax;
         for (int i = 0; i < n; ++i) hl->schedule[i] = ctx->schedule[i];
         LoopState* dl = ctx->d_loop.as<LoopState>();
         Pool* dp = ctx->d_pool.as<Pool>();
@@ -832,7 +836,7 @@ int explorer_run_batched(fbb_ctx* ctx, const int64_t* targets, int ntargets, int
             cudaError_t e = cudaMemcpyAsync(dl, hl, offsetof(LoopState, rec), cudaMemcpyHostToDevice, st);
             for (int i = 0; i < rounds && e == cudaSuccess; ++i) {
                 if ((e = launch_loop_step(ctx->dt, dl, dp, rs, i, false, st, pdl && i > 0)) != cudaSuccess) break;
-                e = launch_round_device(ctx->dt, ctx->k2, dp, rs, out, st, pdl, !all_direct);
+                e = launch_round_device(ctx->dt, ctx->k2, dp, rs, out, st, pdl, all_direct ? 0 : place_chunks);
             }
             if (e == cudaSuccess) e = launch_loop_step(ctx->dt, dl, dp, rs, rounds, true, st, pdl);
             if (e == cudaSuccess) e = cudaMemcpyAsync(hl, dl, sizeof(LoopState), cudaMemcpyDeviceToHost, st);
@@ -914,7 +918,8 @@ int explorer_run_batched(fbb_ctx* ctx, const int64_t* targets, int ntargets, int
                     }
                     if (ce == cudaSuccess) ce = cudaStreamUpdateCaptureDependencies(bs, &inode, 1, cudaStreamSetCaptureDependencies);
                     if (ce == cudaSuccess)
-                        ce = launch_round_k2_place(ctx->dt, ctx->k2, dp, rs, out, bs, false, loop_pdl, !all_direct);
+                        ce = launch_round_k2_place(ctx->dt, ctx->k2, dp, rs, out, bs, false, loop_pdl,
+                                                   all_direct ? 0 : place_chunks);
                     cudaError_t be = cudaStreamEndCapture(bs, nullptr);
                     if (ce == cudaSuccess) ce = be;
                 }

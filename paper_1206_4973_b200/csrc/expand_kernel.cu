@@ -789,7 +789,7 @@ cudaError_t launch_round_leaves(const DevTables& t, const Pool* d_pool, RoundSta
 }
 
 cudaError_t launch_round_k2_place(const DevTables& t, const K2Config& cfg, const Pool* d_pool, RoundState* rs,
-                                  ChunkOut out, cudaStream_t stream, bool pdl_k2, bool pdl, bool place) {
+                                  ChunkOut out, cudaStream_t stream, bool pdl_k2, bool pdl, int64_t place_chunks) {
     cudaError_t e;
     if (cfg.variant >= 100000)
         e = launch_k2_v3(t, cfg, d_pool, 0, cfg.blocks, 0, 0, rs, out, stream, pdl_k2);
@@ -800,16 +800,21 @@ cudaError_t launch_round_k2_place(const DevTables& t, const K2Config& cfg, const
                                 : (cfg.jm_in_smem ? k2_internal_kernel<true, false> : k2_internal_kernel<false, false>),
                        dim3(cfg.blocks), dim3(cfg.threads), cfg.smem, stream, pdl_k2, t, d_pool, 0, cfg.cmax, 0, 0,
                        rs, out);
-    if (e != cudaSuccess || !place) return e;  // !place: every pool of the batch is placed by K2
-    return launch_pdl(place_kernel<true>, dim3(148 * 2), dim3(kPlaceThreads), (size_t)cfg.cmax * kPlaceChunks,
-                      stream, pdl, t, d_pool, cfg.cmax, rs, out, (RoundState*)nullptr);
+    if (e != cudaSuccess || place_chunks <= 0) return e;  // 0: every pool of the batch is placed by K2
+    // one CTA per group of kPlaceChunks chunks of the largest pool the staging holds (groups
+    // past a round's chunks exit at once): measured faster than a fixed grid striding over
+    // the groups (Ta021 262 K: the grid-stride place cost ~7 us more per round)
+    const int64_t blocks = (place_chunks + kPlaceChunks - 1) / kPlaceChunks;
+    return launch_pdl(place_kernel<false>, dim3((unsigned)blocks), dim3(kPlaceThreads),
+                      (size_t)cfg.cmax * kPlaceChunks, stream, pdl, t, d_pool, cfg.cmax, rs, out,
+                      (RoundState*)nullptr);
 }
 
 cudaError_t launch_round_device(const DevTables& t, const K2Config& cfg, const Pool* d_pool,
-                                RoundState* rs, ChunkOut out, cudaStream_t stream, bool pdl, bool place) {
+                                RoundState* rs, ChunkOut out, cudaStream_t stream, bool pdl, int64_t place_chunks) {
     cudaError_t e = launch_round_leaves(t, d_pool, rs, stream, pdl, pdl);
     if (e != cudaSuccess) return e;
-    return launch_round_k2_place(t, cfg, d_pool, rs, out, stream, pdl, pdl, place);
+    return launch_round_k2_place(t, cfg, d_pool, rs, out, stream, pdl, pdl, place_chunks);
 }
 
 }  // namespace fbb

@@ -313,10 +313,11 @@ cudaError_t launch_loop_step_dyn(const DevTables& t, LoopState* ls, Pool* pool, 
 // close of round - 1 (round > 0) + plan of round (!last), one single-warp kernel
 cudaError_t launch_loop_step(const DevTables& t, LoopState* ls, Pool* pool, RoundState* rs, int round,
                              bool last, cudaStream_t stream, bool pdl);
-// place == false: every pool of the batch is small enough for direct placement (K2 writes
-// the survivors itself), so the place kernel is left out
+// place_chunks: the staging's chunk capacity (the place grid covers it); 0: every pool of the
+// batch is small enough for direct placement (K2 writes the survivors itself), so the place
+// kernel is left out
 cudaError_t launch_round_device(const DevTables& t, const K2Config& cfg, const Pool* d_pool,
-                                RoundState* rs, ChunkOut out, cudaStream_t stream, bool pdl, bool place);
+                                RoundState* rs, ChunkOut out, cudaStream_t stream, bool pdl, int64_t place_chunks);
 // Load the explorer's kernels at context creation (CUDA loads kernels lazily, at first use)
 void preload_round_kernels();
 void preload_loop_kernels();
@@ -324,7 +325,7 @@ void preload_loop_kernels();
 cudaError_t launch_round_leaves(const DevTables& t, const Pool* d_pool, RoundState* rs, cudaStream_t stream,
                                 bool pdl_first, bool pdl);
 cudaError_t launch_round_k2_place(const DevTables& t, const K2Config& cfg, const Pool* d_pool, RoundState* rs,
-                                  ChunkOut out, cudaStream_t stream, bool pdl_k2, bool pdl, bool place);
+                                  ChunkOut out, cudaStream_t stream, bool pdl_k2, bool pdl, int64_t place_chunks);
 
 // Launches kern<<<grid, block, smem, st>>>(args...), as a programmatic dependent of the
 // previous kernel in the stream when pdl (the kernel must griddepcontrol.wait before it
