@@ -744,11 +744,15 @@ int explorer_round(fbb_ctx* ctx, int64_t target, fbb_round_t* rec) {
 // explorer_round.  Used when the parents can be read in place (HBM buckets, or host
 // buckets read and written through the mapping).
 bool device_loop_ok(const fbb_ctx* ctx, int64_t max_rounds) {
-    // auto: multi-round calls, on an HBM tree or a host tree.  (A host tree was host-planned
-    // until the loop kernels were preloaded at context creation: lazy loading put a graph
-    // capture into the first timed batch, and e2e swung 0.5-1.6 G/s; with it, Ta021 262 K
-    // e2e runs 1.68 G/s batched vs 1.58 G/s host-planned -- no host round trip per round)
-    const bool want = ctx->device_loop == 1 || (ctx->device_loop == -1 && max_rounds >= 2);
+    // auto: multi-round calls, on an HBM tree or a host tree of prefix-only rows.  (A host
+    // tree was host-planned until the loop kernels were preloaded at context creation:
+    // lazy loading put a graph capture into the first timed batch, and e2e swung 0.5-1.6
+    // G/s; with it, Ta021 262 K e2e runs 1.68 G/s batched vs 1.58 G/s host-planned -- no
+    // host round trip per round.  Full-row host trees (n > 32) stay host-planned: their
+    // many deep buckets grow often, each growth ends a batch, and Ta101 e2e measured 0.84
+    // G/s batched vs 0.92 host-planned.)
+    const bool want = ctx->device_loop == 1 ||
+                      (ctx->device_loop == -1 && max_rounds >= 2 && (!ctx->host_pending || ctx->compact_rows));
     return want && (!ctx->host_pending || (ctx->mapped_in && ctx->mapped_out));
 }
 
